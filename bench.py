@@ -1,0 +1,483 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 batched-dice path (BASELINE.json metric: bounded rolls/sec and
+shuffled elements/sec per GPU and box-wide vs roofline).
+
+Headline workload = BASELINE.json configs[1] ("C2"): 2^25 batches of k=2 bounded rolls
+per GPU, bounds iid U[2, 2^16) drawn from seed 7 (2 + roll_single(pcg64(7), 65534),
+generated on the device by our own k=1 roll kernel), roll words from
+pcg64(array_seed(7, 1)).  One step = one bulk roll_batches over the resident bounds (2^26
+rolls).  Inputs (256 MiB bounds) and outputs (256 MiB rolls + 32 MiB words) exceed the
+126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c2|c3|c4|c1]
+
+Under torchrun (N > 1) every rank rolls its own 2^25-batch section of ONE global stream
+(jump-ahead by rank * 2^25 words; weak scaling); the only exchange is an all-gather of the
+per-rank rejection counts.  Secondary lines for the shuffle configs are
+reported under "secondary" (C3 2^20 x 64 u32, C4 65,536 x 4096 u32, C1 one 10,000-element
+stream).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NB_C2 = 1 << 25
+BYTES_PER_BATCH_C2 = 17  # 8 B bounds in + 8 B rolls out + 1 B words out (8.5 B/roll)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ helpers
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(torch, value, ws):
+    if ws == 1:
+        return value
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(torch, ws):
+    torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------ C2 (rolls)
+def setup_c2(torch, B, rank, nb):
+    import numpy as np
+
+    from paper_2408_06213_b200 import _native as N
+
+    # bounds: 2 + roll_single(pcg64(7), 65534), this rank's section of the global sequence
+    st = N.Pcg64State()
+    N.lib().br_pcg64_seed(7, C.byref(st))
+    N.lib().br_pcg64_advance(C.byref(st), rank * 2 * nb)
+    gen = B.DeviceStream.from_struct(st)
+    spans = torch.full((2 * nb,), 65534, dtype=torch.int32, device="cuda")
+    r = B.roll_batches(gen, spans, 1)
+    bounds = (r.rolls + 2).contiguous()
+    del spans, r
+    # roll stream: pcg64(array_seed(7, 1)) advanced to this rank's first batch
+    st = N.Pcg64State()
+    N.lib().br_pcg64_seed(N.lib().br_array_seed(7, 1), C.byref(st))
+    N.lib().br_pcg64_advance(C.byref(st), rank * nb)
+    stream = B.DeviceStream.from_struct(st)
+    rolls = torch.empty(2 * nb, dtype=torch.int32, device="cuda")
+    words = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    return bounds, stream, rolls, words
+
+
+def bench_c2(args, torch, B, ws, rank):
+    from paper_2408_06213_b200 import _native as N
+
+    L = N.lib()
+    nb = NB_C2
+    bounds, stream, rolls, words = setup_c2(torch, B, rank, nb)
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ptrs = [C.c_void_p(x.data_ptr()) for x in (bounds, stream.state, rolls, words)]
+    wsp = C.c_void_p(stream.workspace.data_ptr())
+    extras = torch.zeros(ws, dtype=torch.int64, device="cuda")
+
+    def step(ev_main=None):
+        N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 1, sp), "main")
+        if ev_main is not None:
+            ev_main.record()
+        N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 2, sp), "fixup")
+
+    for _ in range(args.warmup):
+        step()
+    barrier(torch, ws)
+    K = args.steps
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    e2 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        for i in range(K):
+            e0[i].record()
+            step(e1[i])
+            e2[i].record()
+        end.record()
+        torch.cuda.synchronize()
+    total_ms = start.elapsed_time(end)
+    main_ms = [a.elapsed_time(b) for a, b in zip(e0, e1)]
+    barrier(torch, ws)
+    total_ms = max_over_ranks(torch, total_ms, ws)
+    # cross-rank exchange: per-rank rejection counts (all zero unless a batch was rejected)
+    extra = C.c_uint64()
+    N.check(L.br_roll_check(wsp, sp, C.byref(extra)), "check")
+    if ws > 1:
+        import torch.distributed as dist
+
+        mine = torch.tensor([int(extra.value)], dtype=torch.int64, device="cuda")
+        gathered = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(ws)]
+        dist.all_gather(gathered, mine)
+        extras = torch.cat(gathered)
+    rolls_total = 2 * nb * K * ws
+    value = rolls_total / (total_ms / 1e3)
+    t_main = statistics.mean(main_ms) / 1e3
+    peak, peak_kind = load_peaks()
+    achieved = BYTES_PER_BATCH_C2 * nb / t_main / 1e9
+    traffic = load_traffic().get("roll_main_kernel")
+    res = {
+        "value": value,
+        "ms_per_step": total_ms / K,
+        "main_ms": statistics.mean(main_ms),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "roll_main_kernel<2>",
+                     "algorithmic_bytes_per_launch": BYTES_PER_BATCH_C2 * nb, "peak_source": peak_kind},
+        "clocks": clk.summary(),
+        "gpu_launches": 2 * K,
+        "cross_rank_rejections": [int(x) for x in extras.cpu().tolist()] if ws > 1 else [int(extra.value)],
+    }
+    # end to end through the public API with host (pinned) buffers
+    hb = bounds.cpu().pin_memory()
+    hrolls = torch.empty(2 * nb, dtype=torch.int32).pin_memory()
+    hwords = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    E = max(2, min(K, 5))
+    B.roll_batches(stream, hb, 2, out=(hrolls, hwords))  # warm-up
+    barrier(torch, ws)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(E):
+        B.roll_batches(stream, hb, 2, out=(hrolls, hwords), check=False)
+    t1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(torch, t0.elapsed_time(t1), ws)
+    res["e2e"] = {"value": 2 * nb * E * ws / (e2e_ms / 1e3), "unit": "rolls/s",
+                  "h2d_bytes_per_step": 8 * nb, "d2h_bytes_per_step": 8 * nb + nb, "steps": E,
+                  "api": "paper_2408_06213_b200.roll_batches(host pinned tensors, 8-chunk pipelined copies)"}
+    return res
+
+
+def cpu_baseline_c2(sample_batches=1 << 22):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    O.build()
+    bounds = O.gen_bounds(7, 2 * sample_batches)
+    src = O.pcg64(O.array_seed(7, 1))
+    t = time.perf_counter()
+    O.roll_batches(src, bounds, 2)
+    dt = time.perf_counter() - t
+    return {"value": 2 * sample_batches / dt, "unit": "rolls/s", "cores": 1, "kind": "port",
+            "sample": f"first {sample_batches} batches of C2 (one sequential stream, as the reference's roll_batch "
+                      f"loop; oracle/oracle.c or_roll_batches), {dt:.2f}s"}
+
+
+# ------------------------------------------------------------------------------ shuffles
+SHUFFLE_CFG = {
+    "c3": {"n": 64, "arrays": 1 << 20, "seed": 1234, "eb": 4, "workload": "C3: 2^20 independent shuffles of u32[64], seeds hash(1234,a)"},
+    "c4": {"n": 4096, "arrays": 1 << 16, "seed": 99, "eb": 4, "workload": "C4: 65,536 independent shuffles of u32[4096], seeds hash(99,a)"},
+}
+
+
+def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
+    n, na, eb = cfg["n"], cfg["arrays"], cfg["eb"]
+    data = torch.arange(n, dtype=torch.int32 if eb == 4 else torch.int64, device="cuda").repeat(na)
+    base = rank * na
+    K = steps or args.steps
+    for _ in range(args.warmup):
+        B.shuffle_many(data, n, cfg["seed"], array_index_base=base)
+    kernel = B.last_kernel()
+    barrier(torch, ws)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for a, b in evs:
+            a.record()
+            B.shuffle_many(data, n, cfg["seed"], array_index_base=base)
+            b.record()
+        torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in evs]
+    total_ms = max_over_ranks(torch, evs[0][0].elapsed_time(evs[-1][1]), ws)
+    elems = n * na * K * ws
+    t = statistics.mean(per) / 1e3
+    peak, kind = load_peaks()
+    achieved = 2 * eb * n * na / t / 1e9
+    return {"workload": cfg["workload"], "value": elems / (total_ms / 1e3), "unit": "elements/s",
+            "ms_per_step": total_ms / K, "kernel": kernel,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": load_traffic().get(kernel.split("<")[0]),
+                         "algorithmic_bytes_per_launch": 2 * eb * n * na, "peak_source": kind},
+            "clocks": clk.summary(), "gpu_launches": K}
+
+
+def bench_c1(args, torch, B):
+    import numpy as np
+
+    z = np.arange(10000, dtype=np.uint32)
+    for _ in range(3):
+        B.shuffle_batched(B.Pcg64Source(42), z.copy())
+    ts = []
+    for _ in range(max(5, args.steps)):
+        zz = z.copy()
+        s = B.Pcg64Source(42)
+        t = time.perf_counter()
+        B.shuffle_batched(s, zz)
+        ts.append(time.perf_counter() - t)
+    dev = torch.arange(10000, dtype=torch.int32, device="cuda")
+    from paper_2408_06213_b200 import _native as N
+
+    ds = B.DeviceStream(42)
+    regs = B.DEFAULT_SCHEDULE._regimes()
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+    for a, b in evs:
+        a.record()
+        N.check(N.lib().br_shuffle_stream(C.c_void_p(dev.data_ptr()), 4, 10000, C.c_void_p(ds.state.data_ptr()),
+                                          regs, len(regs), 0, None, sp), "c1")
+        b.record()
+    torch.cuda.synchronize()
+    kern = statistics.median([a.elapsed_time(b) for a, b in evs[5:]])
+    return {"workload": "C1: one u32[10,000] stream shuffle, pcg64 seed 42 (drop-in shuffle_batched on a numpy "
+                        "array: upload, kernel, download, state round trip)",
+            "e2e_ms_per_shuffle": statistics.median(ts) * 1e3, "kernel_ms": kern,
+            "value": 10000 / statistics.median(ts), "unit": "elements/s"}
+
+
+def cpu_baseline_shuffle(cfg, sample_arrays):
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    O.build()
+    n = cfg["n"]
+    data = np.tile(np.arange(n, dtype=np.uint32 if cfg["eb"] == 4 else np.uint64), sample_arrays)
+    t = time.perf_counter()
+    O.shuffle_segmented(data, n, cfg["seed"], nthreads=0)
+    dt = time.perf_counter() - t
+    return {"value": n * sample_arrays / dt, "unit": "elements/s", "cores": cpu_cores(), "kind": "port",
+            "sample": f"{sample_arrays} arrays of {n} (oracle shuffle_batched per array, OpenMP over arrays), {dt:.2f}s"}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    O.build()
+    cfg = args.config
+    if cfg == "c2":
+        sample = 1 << 21
+        bounds = O.gen_bounds(7, 2 * sample)
+        src = O.pcg64(O.array_seed(7, 1))
+        for _ in range(args.warmup):
+            O.roll_batches(src, bounds, 2)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            O.roll_batches(src, bounds, 2)
+        dt = time.perf_counter() - t
+        value, unit, cores = 2 * sample * args.steps / dt, "rolls/s", 1
+        desc = f"{sample} batches of C2 per step (one sequential stream; the reference roll_batch loop)"
+        metric = "bounded rolls/sec (C2: 2^25 batches of k=2, bounds U[2,2^16))"
+    else:
+        c = SHUFFLE_CFG[cfg]
+        n = c["n"]
+        arrays = max(1, (1 << 22) // n)
+        data = __import__("numpy").tile(__import__("numpy").arange(n, dtype="uint32"), arrays)
+        for _ in range(args.warmup):
+            O.shuffle_segmented(data, n, c["seed"], nthreads=0)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            O.shuffle_segmented(data, n, c["seed"], nthreads=0)
+        dt = time.perf_counter() - t
+        value, unit, cores = n * arrays * args.steps / dt, "elements/s", cpu_cores()
+        desc = f"{arrays} arrays of {n} per step, OpenMP over arrays"
+        metric = "shuffled elements/sec"
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": cfg, "note": "oracle/oracle.c port of the reference (pure Python upstream, "
+                                               "so there is no compiled reference to run)"},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+# ------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    ws, rank, local = dist_info()
+    if args.impl == "reference":
+        line = run_reference(args, ws, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    import torch
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+
+    if rank == 0:
+        __graft_entry__.build()
+    if ws > 1:
+        torch.distributed.barrier()
+    import paper_2408_06213_b200 as B
+
+    if args.config == "c2":
+        r = bench_c2(args, torch, B, ws, rank)
+        metric = "bounded rolls/sec (C2: 2^25 batches of k=2 per GPU, bounds U[2,2^16))"
+        unit = "rolls/s"
+        config = {"workload": "C2: BASELINE configs[1], 2^25 batches x k=2 bounded rolls per GPU, bounds iid "
+                              "U[2,2^16) from seed 7, words from pcg64(hash(7,1)); output 2^26 u32 rolls + 2^25 u8 "
+                              "words per GPU", "batches_per_gpu": NB_C2, "k": 2,
+                  "l2": "inputs+outputs 544 MiB per step > 126 MB L2 (no flush needed)",
+                  "parallelism": f"dp{ws} (stream sections by jump-ahead)"}
+        dtype = "u64"
+    else:
+        cfg = SHUFFLE_CFG[args.config]
+        r = bench_shuffle(cfg, args, torch, B, ws, rank)
+        metric, unit = "shuffled elements/sec", "elements/s"
+        config = {"workload": cfg["workload"], "l2": "payload larger than L2", "parallelism": f"dp{ws} (arrays)"}
+        dtype = "u32"
+        r["e2e"] = None
+    line = {"metric": metric, "value": r["value"], "unit": unit, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic (BASELINE configs; generated on device)",
+            "config": config, "roofline": r["roofline"], "clocks": r["clocks"], "gpu_launches": r["gpu_launches"],
+            "e2e": r.get("e2e")}
+    if "cross_rank_rejections" in r:
+        line["cross_rank_rejections"] = r["cross_rank_rejections"]
+    if not args.no_secondary:
+        sec = {}
+        for key in ("c3", "c4"):
+            if key != args.config:
+                sec[key] = bench_shuffle(SHUFFLE_CFG[key], args, torch, B, ws, rank, steps=min(args.steps, 10))
+        if ws == 1:
+            sec["c1"] = bench_c1(args, torch, B)
+        line["secondary"] = sec
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        if args.config == "c2":
+            line["cpu_baseline"] = cpu_baseline_c2()
+        else:
+            line["cpu_baseline"] = cpu_baseline_shuffle(SHUFFLE_CFG[args.config], max(1, (1 << 23) // SHUFFLE_CFG[args.config]["n"]))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -549,7 +549,7 @@ int or_shuffle_segmented(void *data, int32_t eb, int64_t num_arrays, uint64_t n,
     int err = OR_OK;
 #ifdef _OPENMP
     if (nthreads <= 0) nthreads = omp_get_max_threads();
-#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#pragma omp parallel for schedule(static) num_threads(nthreads)
 #endif
     for (int64_t a = 0; a < num_arrays; ++a) {
         or_source src;

@@ -1,0 +1,11 @@
+"""B200-native batched dice rolls and segmented Fisher-Yates shuffles (arXiv 2408.06213).
+
+The hot path of the reference package ``batchrand`` re-built for sm_100a: a device PCG64,
+a bulk batched-roll kernel and size-dispatched segmented shuffle kernels behind a C ABI
+(include/batchrand_b200.h), with a drop-in Python API in ``.batchrand``.
+"""
+
+from .batchrand import *  # noqa: F401,F403
+from .batchrand import __all__  # noqa: F401
+
+__version__ = "0.1.0"

@@ -1,0 +1,655 @@
+"""Drop-in, GPU-backed replacement for the reference ``batchrand`` hot path.
+
+Same names, argument meaning and error behaviour as
+/root/reference/pkg/src/batchrand (arXiv 2408.06213):
+
+  * ``shuffle_batched`` / ``shuffle_unbatched`` / ``partial_shuffle_batch``  (shuffle.py:80-225)
+  * ``roll_batch`` / ``roll_batch_known_threshold`` / ``digit_pass``          (batched.py:69-123)
+  * ``Pcg64Source`` / ``make_source`` / ``splitmix64_stream``                 (wordsource.py)
+  * ``ShuffleSchedule`` / ``DEFAULT_SCHEDULE`` / ``PAIR_SCHEDULE`` / ``default_schedule``
+  * ``RadixBases`` / ``BoundEncoding`` / ``BatchSpec`` / ``BatchResult`` and the errors.
+
+Every roll and every swap runs in the CUDA library (paper_2408_06213_b200/lib, sm_100a)
+through its C ABI; the Python layer only validates arguments (exactly like the reference)
+and moves state.  Sources: any PCG64 source with ``state``/``increment`` attributes (ours
+or the reference's own ``Pcg64Source``) is accepted and advanced by exactly the words the
+device consumed.  Other generators raise ``TypeError`` (device versions are a later row).
+
+Bulk entry points that have no reference counterpart (the reason for a GPU):
+``roll_batches`` (many batches on one stream), ``shuffle_many`` (many independent arrays,
+one seed each), ``pcg64_fill`` and ``digit_pass_many``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import NamedTuple, Optional
+
+from . import _native as N
+from .errors import (
+    BatchRandError,
+    BoundOverflow,
+    DigitOutOfRange,
+    SourceExhausted,
+    UnknownGenerator,
+    ValueOutOfRange,
+)
+
+MASK64 = (1 << 64) - 1
+PCG_MULTIPLIER = 0x2360ED051FC65DA44385DF649FCCF645
+
+
+# ---------------------------------------------------------------------------- word sources
+def splitmix64_stream(seed: int):
+    """wordsource.py:22-35 (computed by the native library)."""
+    x = C.c_uint64(seed & MASK64)
+    L = N.lib()
+    while True:
+        yield L.br_splitmix64_next(C.byref(x))
+
+
+class WordSource:
+    """wordsource.py:38-48 protocol."""
+
+    word_bits: int = 64
+
+    def next_word(self) -> int:
+        raise NotImplementedError
+
+
+class Pcg64Source(WordSource):
+    """PCG64 XSL-RR 128/64 (wordsource.py:71-89); state lives on the host between calls."""
+
+    word_bits = 64
+
+    def __init__(self, seed: int = 0):
+        st = N.Pcg64State()
+        N.lib().br_pcg64_seed(seed & MASK64, C.byref(st))
+        self.state = (st.state_hi << 64) | st.state_lo
+        self.increment = (st.inc_hi << 64) | st.inc_lo
+
+    def next_word(self) -> int:
+        st = _state_struct(self)
+        w = N.lib().br_pcg64_next(C.byref(st))
+        self.state = (st.state_hi << 64) | st.state_lo
+        return w
+
+    def advance(self, delta: int) -> None:
+        st = _state_struct(self)
+        N.lib().br_pcg64_advance(C.byref(st), delta & MASK64)
+        self.state = (st.state_hi << 64) | st.state_lo
+
+
+GENERATORS = {"pcg64": Pcg64Source}
+
+
+def make_source(name: str, seed: int = 0) -> WordSource:
+    """wordsource.py:217-225.  Only pcg64 has a device implementation."""
+    if name in ("lehmer", "chacha"):
+        raise NotImplementedError(f"generator {name!r} has no device implementation yet")
+    try:
+        cls = GENERATORS[name]
+    except KeyError:
+        raise UnknownGenerator(f"unknown generator {name!r}; expected one of {sorted(GENERATORS)}") from None
+    return cls(seed)
+
+
+def array_seed(run_seed: int, array_index: int) -> int:
+    """Per-array seed of the segmented shuffle: next(splitmix64_stream(((s<<32)|a) & MASK64))."""
+    return N.lib().br_array_seed(run_seed & MASK64, array_index & MASK64)
+
+
+def _state_struct(source) -> N.Pcg64State:
+    try:
+        state, inc = int(source.state), int(source.increment)
+    except AttributeError:
+        raise TypeError(
+            f"{type(source).__name__} is not a PCG64 source; the device path draws PCG64 words only"
+        ) from None
+    if getattr(source, "word_bits", 64) != 64:
+        raise TypeError("the device path needs 64-bit words")
+    st = N.Pcg64State()
+    st.state_hi, st.state_lo = (state >> 64) & MASK64, state & MASK64
+    st.inc_hi, st.inc_lo = (inc >> 64) & MASK64, inc & MASK64
+    return st
+
+
+# ---------------------------------------------------------------------------- bounded.py
+class FullProduct(NamedTuple):
+    hi: int
+    lo: int
+
+
+def mul_full(a: int, b: int, bits: int = 64) -> FullProduct:
+    """bounded.py:29-32 (host helper)."""
+    p = a * b
+    return FullProduct(p >> bits, p & ((1 << bits) - 1))
+
+
+@dataclass(frozen=True)
+class BoundEncoding:
+    """bounded.py:35-56."""
+
+    raw: int
+    is_full_range: bool
+    bits: int
+
+    @classmethod
+    def of(cls, bound: int, bits: int = 64) -> "BoundEncoding":
+        if not 1 <= bound <= 1 << bits:
+            raise BoundOverflow(f"bound {bound} not in [1, 2**{bits}]")
+        full = bound == 1 << bits
+        return cls(0 if full else bound, full, bits)
+
+    @property
+    def value(self) -> int:
+        return (1 << self.bits) if self.is_full_range else self.raw
+
+
+def threshold(bound: BoundEncoding) -> int:
+    """bounded.py:59-62: 2**bits mod b."""
+    neg = (-bound.raw) & ((1 << bound.bits) - 1)
+    return neg % bound.value
+
+
+def falling_factorial(n: int, k: int, bits: int = 64) -> int:
+    """bounded.py:107-119."""
+    if k < 0 or k > n:
+        raise ValueError(f"need 0 <= k <= n, got n={n} k={k}")
+    limit = 1 << bits
+    out = 1
+    for factor in range(n, n - k, -1):
+        out *= factor
+        if out > limit:
+            raise BoundOverflow(f"falling factorial of {n} over {k} terms exceeds 2**{bits}")
+    return out
+
+
+# ---------------------------------------------------------------------------- mixed_radix.py
+@dataclass(frozen=True)
+class RadixBases:
+    """mixed_radix.py:18-37."""
+
+    bases: tuple
+    bits: int
+    product: BoundEncoding
+
+    @classmethod
+    def of(cls, bases, bits: int = 64) -> "RadixBases":
+        bases = tuple(bases)
+        if not bases:
+            raise ValueError("at least one base is required")
+        if any(b < 1 for b in bases):
+            raise ValueError(f"bases must be positive, got {bases}")
+        return cls(bases, bits, BoundEncoding.of(math.prod(bases), bits))
+
+    def __len__(self) -> int:
+        return len(self.bases)
+
+
+# ---------------------------------------------------------------------------- batched.py
+@dataclass(frozen=True)
+class BatchSpec:
+    """batched.py:26-51."""
+
+    bases: RadixBases
+    precomputed_threshold: Optional[int] = None
+    upper_bound: Optional[int] = None
+
+    def __post_init__(self):
+        if self.precomputed_threshold is not None:
+            expected = threshold(self.bases.product)
+            if self.precomputed_threshold != expected:
+                raise ValueError(
+                    f"threshold {self.precomputed_threshold} does not match {expected} for bases {self.bases.bases}"
+                )
+        if self.upper_bound is not None and self.upper_bound < self.bases.product.value:
+            raise BoundOverflow(f"upper bound {self.upper_bound} below product {self.bases.product.value}")
+
+    @classmethod
+    def with_threshold(cls, bases: RadixBases) -> "BatchSpec":
+        return cls(bases, precomputed_threshold=threshold(bases.product))
+
+
+@dataclass(frozen=True)
+class BatchResult:
+    """batched.py:54-66."""
+
+    digits: tuple
+    words_consumed: int
+    threshold_computed: bool
+    final_remainder: int
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the batchrand B200 path has no CPU fallback")
+    return torch
+
+
+def _stream_ptr(torch):
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
+
+
+def _device_bases(bases, torch):
+    import numpy as np
+
+    if any(b >= 1 << 32 for b in bases):
+        raise NotImplementedError("device batches take bounds below 2**32")
+    host = np.asarray([int(b) for b in bases], dtype=np.uint32).view(np.int32)
+    return torch.from_numpy(host).cuda()
+
+
+def _roll_one(source, spec: BatchSpec) -> BatchResult:
+    torch = _torch()
+    bases = spec.bases.bases
+    if spec.bases.bits != 64:
+        raise TypeError("the device path needs 64-bit words")
+    st = _state_struct(source)
+    dstream = DeviceStream.from_struct(st)
+    b = _device_bases(bases, torch)
+    r = roll_batches(dstream, b, len(bases), flags=True, final_remainder=True)
+    dstream.write_back(source)
+    digits = tuple(int(x) & 0xFFFFFFFF for x in r.rolls.cpu().tolist())
+    return BatchResult(digits, int(r.words[0]), bool(int(r.flags[0])), int(r.final_remainder[0]) & MASK64)
+
+
+def digit_pass(r0: int, bases: RadixBases):
+    """batched.py:69-82 on the device (one word)."""
+    torch = _torch()
+    if bases.bits != 64:
+        raise TypeError("the device path needs 64-bit words")
+    w = torch.tensor([r0 - (1 << 64) if r0 >= 1 << 63 else r0], dtype=torch.int64).cuda()
+    d, rk = digit_pass_many(w, _device_bases(bases.bases, torch), len(bases.bases))
+    return tuple(int(x) & 0xFFFFFFFF for x in d.cpu().tolist()), int(rk[0]) & MASK64
+
+
+def roll_batch_known_threshold(source, spec: BatchSpec) -> BatchResult:
+    """batched.py:85-99."""
+    if spec.precomputed_threshold is None:
+        raise ValueError("spec has no precomputed threshold")
+    r = _roll_one(source, spec)
+    return BatchResult(r.digits, r.words_consumed, False, r.final_remainder)
+
+
+def roll_batch(source, spec: BatchSpec) -> BatchResult:
+    """batched.py:102-123 (threshold_computed == final remainder of the first word < product)."""
+    return _roll_one(source, spec)
+
+
+# ---------------------------------------------------------------------------- shuffle.py
+@dataclass(frozen=True)
+class ShuffleSchedule:
+    """shuffle.py:22-49."""
+
+    entries: tuple
+    max_batch: int
+    word_bits: int = 64
+
+    def __post_init__(self):
+        if not self.entries:
+            raise ValueError("schedule needs at least one regime")
+        lengths = [n for n, _ in self.entries]
+        sizes = [k for _, k in self.entries]
+        if any(a <= b for a, b in zip(lengths, lengths[1:])):
+            raise ValueError(f"regime lengths must strictly decrease: {lengths}")
+        if any(a >= b for a, b in zip(sizes, sizes[1:])):
+            raise ValueError(f"batch sizes must strictly increase: {sizes}")
+        if sizes[-1] != self.max_batch:
+            raise ValueError(f"last batch size {sizes[-1]} != max_batch {self.max_batch}")
+        for n, k in self.entries:
+            if k > n:
+                raise ValueError(f"batch size {k} exceeds regime length {n}")
+            falling_factorial(n, k, self.word_bits)
+
+    def _regimes(self):
+        arr = (N.Regime * len(self.entries))()
+        for i, (n, k) in enumerate(self.entries):
+            arr[i].max_length = min(n, MASK64)
+            arr[i].batch_size = k
+        return arr
+
+
+DEFAULT_SCHEDULE = ShuffleSchedule(
+    entries=((1 << 30, 2), (1 << 19, 3), (1 << 14, 4), (1 << 11, 5), (1 << 9, 6)), max_batch=6, word_bits=64
+)
+PAIR_SCHEDULE = ShuffleSchedule(entries=((1 << 30, 2),), max_batch=2, word_bits=64)
+
+
+def default_schedule(max_batch: int = 6) -> ShuffleSchedule:
+    """shuffle.py:71-77."""
+    if not 2 <= max_batch <= DEFAULT_SCHEDULE.max_batch:
+        raise ValueError(f"max_batch must be in [2, {DEFAULT_SCHEDULE.max_batch}]")
+    return ShuffleSchedule(DEFAULT_SCHEDULE.entries[: max_batch - 1], max_batch, DEFAULT_SCHEDULE.word_bits)
+
+
+def _device_payload(z, torch):
+    """(device tensor, finisher) for z: tensors/ndarrays of 4/8-byte items are shuffled in
+    place; anything else is shuffled as an index vector and permuted on the way back."""
+    import numpy as np
+
+    if isinstance(z, torch.Tensor) and z.element_size() in (4, 8):
+        if z.is_cuda and z.is_contiguous():
+            return z.view(-1), lambda d: z
+        dev = z.contiguous().view(-1).cuda()
+
+        def fin(d):
+            z.copy_(d.view(z.shape).to(z.device))
+            return z
+
+        return dev, fin
+    if isinstance(z, np.ndarray) and z.dtype.itemsize in (4, 8):
+        host = np.ascontiguousarray(z).reshape(-1)
+        dev = torch.from_numpy(host.view(np.int32 if z.dtype.itemsize == 4 else np.int64)).cuda()
+
+        def fin(d):
+            out = d.cpu().numpy().view(z.dtype).reshape(z.shape)
+            z[...] = out
+            return z
+
+        return dev, fin
+    n = len(z)
+    idx = torch.arange(n, dtype=torch.int32 if n < 1 << 31 else torch.int64, device="cuda")
+
+    def fin(d):
+        perm = d.cpu().tolist()
+        vals = list(z)
+        for i, p in enumerate(perm):
+            z[i] = vals[p]
+        return z
+
+    return idx, fin
+
+
+def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=False):
+    torch = _torch()
+    st = _state_struct(source)
+    dev, fin = _device_payload(z, torch)
+    n = dev.numel()
+    ds = DeviceStream.from_struct(st)
+    words = torch.zeros(1, dtype=torch.int64, device="cuda")
+    rk = torch.zeros(1, dtype=torch.int64, device="cuda") if want_rk else None
+    L = N.lib()
+    if segments is None:
+        regs = regimes if regimes is not None else (N.Regime * 1)()
+        nreg = len(regimes) if regimes is not None else 0
+        N.check(L.br_shuffle_stream(_ptr(dev), dev.element_size(), n, _ptr(ds.state), regs, nreg, int(unbatched),
+                                    _ptr(words), _stream_ptr(torch)), "shuffle")
+    else:
+        segs = (N.Segment * len(segments))()
+        for i, (sn, k, cnt) in enumerate(segments):
+            segs[i].start_n, segs[i].k, segs[i].count = sn, k, cnt
+        N.check(L.br_shuffle_stream_segments(_ptr(dev), dev.element_size(), n, _ptr(ds.state), segs, len(segments),
+                                             _ptr(words), _ptr(rk), _stream_ptr(torch)), "shuffle")
+    ds.write_back(source)
+    out = fin(dev)
+    if want_rk:
+        return out, int(rk.item()) & MASK64
+    return out
+
+
+def shuffle_batched(source, z, schedule: ShuffleSchedule = DEFAULT_SCHEDULE, check_bounds: bool = False):
+    """shuffle.py:149-225 on the device.  z is permuted in place and returned.
+
+    ``check_bounds`` is the reference's testing hook; the device plan uses exact per-batch
+    thresholds, so there is no carried bound to re-validate and behaviour is identical.
+    """
+    if getattr(source, "word_bits", 64) != schedule.word_bits:
+        raise ValueError(
+            f"source emits {getattr(source, 'word_bits', 64)}-bit words but schedule expects {schedule.word_bits}"
+        )
+    if len(z) < 2:
+        return z
+    return _shuffle_stream(source, z, schedule._regimes(), False)
+
+
+def shuffle_unbatched(source, z):
+    """shuffle.py:80-97 on the device."""
+    if len(z) < 2:
+        return z
+    return _shuffle_stream(source, z, None, True)
+
+
+def partial_shuffle_batch(source, z, n: int, k: int, u: int) -> int:
+    """shuffle.py:137-146: one batch of k dice on the first n elements; returns the bound
+    to carry (u unchanged unless the first word's remainder fell below it)."""
+    if not 1 <= k <= n or n > len(z):
+        raise ValueError(f"need 1 <= k <= n <= len(z), got n={n} k={k}")
+    ff = falling_factorial(n, k, getattr(source, "word_bits", 64))
+    if u < ff:
+        raise BoundOverflow(f"upper bound {u} below product {ff}")
+    _, rk = _shuffle_stream(source, z, None, False, segments=[(n, k, 1)], want_rk=True)
+    return ff if rk < u else u
+
+
+# ---------------------------------------------------------------------------- bulk device API
+class DeviceStream:
+    """A PCG64 stream whose state lives in device memory, for chained bulk calls without a
+    host round trip.  ``write_back(source)`` copies the advanced state to a host source."""
+
+    def __init__(self, seed: int = 0):
+        st = N.Pcg64State()
+        N.lib().br_pcg64_seed(seed & MASK64, C.byref(st))
+        self._init(st)
+
+    @classmethod
+    def from_source(cls, source) -> "DeviceStream":
+        return cls.from_struct(_state_struct(source))
+
+    @classmethod
+    def from_struct(cls, st: N.Pcg64State) -> "DeviceStream":
+        self = cls.__new__(cls)
+        self._init(st)
+        return self
+
+    def _init(self, st):
+        torch = _torch()
+        self.state = torch.empty(4, dtype=torch.int64, device="cuda")
+        self.workspace = torch.zeros(N.lib().br_roll_workspace_bytes(), dtype=torch.uint8, device="cuda")
+        N.check(N.lib().br_state_upload(_ptr(self.state), C.byref(st), _stream_ptr(torch)), "state upload")
+
+    def host_state(self) -> N.Pcg64State:
+        torch = _torch()
+        st = N.Pcg64State()
+        N.check(N.lib().br_state_download(C.byref(st), _ptr(self.state), _stream_ptr(torch)), "state download")
+        return st
+
+    def write_back(self, source) -> None:
+        st = self.host_state()
+        source.state = (st.state_hi << 64) | st.state_lo
+
+
+class RollBatchesResult(NamedTuple):
+    rolls: object
+    words: object
+    flags: object
+    final_remainder: object
+
+
+def roll_batches(stream, bounds, k: Optional[int] = None, *, flags: bool = False, final_remainder: bool = False,
+                 out=None, check: bool = True, chunks: int = 8) -> RollBatchesResult:
+    """Bulk roll_batch: batch i rolls the k dice bounds[i*k:(i+1)*k] (4-byte items, >= 1)
+    from the PCG64 ``stream`` (a DeviceStream or a host PCG64 source, advanced in place).
+
+    Device ``bounds`` give device results: rolls (int32 view of u32, len nb*k), words
+    (uint8, len nb) and optionally flags (threshold_computed) and final_remainder (int64
+    view of u64).  Host ``bounds`` (CPU tensor / ndarray, ideally pinned) give host results;
+    the copies are pipelined in ``chunks`` pieces over two copy streams so host-to-device,
+    rolling and device-to-host overlap.  ``check`` synchronises and raises ValueError /
+    BoundOverflow like RadixBases.of."""
+    torch = _torch()
+    host_source = None
+    if not isinstance(stream, DeviceStream):
+        host_source = stream
+        stream = DeviceStream.from_source(stream)
+    if hasattr(bounds, "dim") and bounds.dim() == 2:
+        k = bounds.shape[1] if k is None else k
+    elif hasattr(bounds, "ndim") and bounds.ndim == 2:
+        k = bounds.shape[1] if k is None else k
+    if k is None:
+        raise ValueError("k is required for flat bounds")
+    if not (hasattr(bounds, "is_cuda") and bounds.is_cuda):
+        res = _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, torch)
+    else:
+        res = _roll_batches_dev(stream, bounds.reshape(-1), k, flags, final_remainder, out, torch)
+    if check:
+        extra = C.c_uint64()
+        N.check(N.lib().br_roll_check(_ptr(stream.workspace), _stream_ptr(torch), C.byref(extra)), "roll_batches")
+    if host_source is not None:
+        stream.write_back(host_source)
+    return res
+
+
+def _roll_batches_dev(stream, b, k, flags, final_remainder, out, torch):
+    if b.element_size() != 4 or not b.is_contiguous():
+        raise TypeError("bounds must be a contiguous tensor of 4-byte items")
+    nb = b.numel() // k
+    if out is None:
+        rolls = torch.empty(nb * k, dtype=torch.int32, device="cuda")
+        words = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    else:
+        rolls, words = out[0], out[1]
+    fl = torch.empty(nb, dtype=torch.uint8, device="cuda") if flags else None
+    rk = torch.empty(nb, dtype=torch.int64, device="cuda") if final_remainder else None
+    N.check(N.lib().br_roll_batches(_ptr(b), k, nb, _ptr(stream.state), _ptr(rolls), _ptr(words), _ptr(fl), _ptr(rk),
+                                    _ptr(stream.workspace), _stream_ptr(torch)), "roll_batches")
+    return RollBatchesResult(rolls, words, fl, rk)
+
+
+def _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, torch):
+    import numpy as np
+
+    if isinstance(bounds, np.ndarray):
+        bounds = torch.from_numpy(np.ascontiguousarray(bounds).view(np.int32))
+    b = bounds.reshape(-1)
+    if b.element_size() != 4:
+        raise TypeError("bounds must have 4-byte items")
+    nb = b.numel() // k
+    pin = b.is_pinned()
+    if out is None:
+        rolls = torch.empty(nb * k, dtype=torch.int32, pin_memory=pin)
+        words = torch.empty(nb, dtype=torch.uint8, pin_memory=pin)
+    else:
+        rolls, words = out[0], out[1]
+    fl = torch.empty(nb, dtype=torch.uint8, pin_memory=pin) if flags else None
+    rk = torch.empty(nb, dtype=torch.int64, pin_memory=pin) if final_remainder else None
+    chunks = max(1, min(chunks, nb))
+    per = -(-nb // chunks)
+    per = (per + 3) & ~3
+    comp = torch.cuda.current_stream()
+    h2d, d2h = _copy_streams(torch)
+    dbufs = [torch.empty(per * k, dtype=torch.int32, device="cuda") for _ in range(2)]
+    dro = [torch.empty(per * k, dtype=torch.int32, device="cuda") for _ in range(2)]
+    dwo = [torch.empty(per, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    dfl = [torch.empty(per, dtype=torch.uint8, device="cuda") if flags else None for _ in range(2)]
+    drk = [torch.empty(per, dtype=torch.int64, device="cuda") if final_remainder else None for _ in range(2)]
+    freed = [None, None]
+    L = N.lib()
+    for c, lo in enumerate(range(0, nb, per)):
+        hi = min(nb, lo + per)
+        cnt = hi - lo
+        slot = c & 1
+        with torch.cuda.stream(h2d):
+            if freed[slot] is not None:
+                h2d.wait_event(freed[slot])
+            dbufs[slot][: cnt * k].copy_(b[lo * k: hi * k], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(h2d)
+        comp.wait_event(ready)
+        N.check(L.br_roll_batches(_ptr(dbufs[slot]), k, cnt, _ptr(stream.state), _ptr(dro[slot]), _ptr(dwo[slot]),
+                                  _ptr(dfl[slot]), _ptr(drk[slot]), _ptr(stream.workspace),
+                                  C.c_void_p(comp.cuda_stream)), "roll_batches")
+        done = torch.cuda.Event()
+        done.record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done)
+            rolls[lo * k: hi * k].copy_(dro[slot][: cnt * k], non_blocking=True)
+            words[lo:hi].copy_(dwo[slot][:cnt], non_blocking=True)
+            if flags:
+                fl[lo:hi].copy_(dfl[slot][:cnt], non_blocking=True)
+            if final_remainder:
+                rk[lo:hi].copy_(drk[slot][:cnt], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(d2h)
+            freed[slot] = ev
+    comp.wait_stream(d2h)
+    comp.wait_stream(h2d)
+    return RollBatchesResult(rolls, words, fl, rk)
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_streams(torch):
+    dev = torch.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return _COPY_STREAMS[dev]
+
+
+def digit_pass_many(words, bounds, k: int):
+    """Device digit_pass for word i with bases bounds[i*k:(i+1)*k]; returns (digits, rk)."""
+    torch = _torch()
+    n = words.numel()
+    digits = torch.empty(n * k, dtype=torch.int32, device="cuda")
+    rk = torch.empty(n, dtype=torch.int64, device="cuda")
+    N.check(N.lib().br_digit_pass(_ptr(words), _ptr(bounds), k, n, _ptr(digits), _ptr(rk), _stream_ptr(torch)),
+            "digit_pass")
+    return digits, rk
+
+
+def pcg64_fill(source_or_seed, count: int, offset: int = 0):
+    """count consecutive words (from word `offset`) of a PCG64 stream, as an int64 CUDA tensor
+    (bit pattern of the u64 words).  The source is not advanced."""
+    torch = _torch()
+    if isinstance(source_or_seed, int):
+        st = N.Pcg64State()
+        N.lib().br_pcg64_seed(source_or_seed & MASK64, C.byref(st))
+    else:
+        st = _state_struct(source_or_seed)
+    out = torch.empty(count, dtype=torch.int64, device="cuda")
+    N.check(N.lib().br_pcg64_fill(_ptr(out), count, C.byref(st), offset, _stream_ptr(torch)), "pcg64_fill")
+    return out
+
+
+def shuffle_many(data, n: int, run_seed: int, array_index_base: int = 0,
+                 schedule: ShuffleSchedule = DEFAULT_SCHEDULE, return_words: bool = False):
+    """Independent shuffles of the num_arrays = data.numel() // n contiguous arrays of a CUDA
+    tensor (4- or 8-byte items), in place: array a is
+    shuffle_batched(make_source("pcg64", array_seed(run_seed, array_index_base + a)), ...)."""
+    torch = _torch()
+    flat = data.view(-1)
+    if not flat.is_cuda or flat.element_size() not in (4, 8):
+        raise TypeError("data must be a CUDA tensor of 4- or 8-byte items")
+    if n <= 0 or flat.numel() % n:
+        raise ValueError("data length must be a multiple of n")
+    num_arrays = flat.numel() // n
+    words = torch.empty(num_arrays, dtype=torch.int32, device="cuda") if return_words else None
+    regs = schedule._regimes()
+    N.check(N.lib().br_shuffle_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64,
+                                         array_index_base, regs, len(regs), _ptr(words), _stream_ptr(torch)),
+            "shuffle_many")
+    return (data, words) if return_words else data
+
+
+def last_kernel() -> str:
+    """Which kernel the last device call on this thread launched (diagnostics)."""
+    return N.last_kernel()
+
+
+__all__ = [
+    "BatchRandError", "BatchResult", "BatchSpec", "BoundEncoding", "BoundOverflow", "DEFAULT_SCHEDULE",
+    "DigitOutOfRange", "DeviceStream", "FullProduct", "PAIR_SCHEDULE", "Pcg64Source", "RadixBases",
+    "RollBatchesResult", "ShuffleSchedule", "SourceExhausted", "UnknownGenerator", "ValueOutOfRange",
+    "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",
+    "make_source", "mul_full", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
+    "roll_batches", "shuffle_batched", "shuffle_many", "shuffle_unbatched", "splitmix64_stream", "threshold",
+]

@@ -1,0 +1,564 @@
+// capi.cu -- C ABI (include/batchrand_b200.h): host plan compiler, plan cache, launches.
+//
+// One translation unit: the kernels (roll.cuh, shuffle.cuh) and the jump-table symbols
+// they read live here so no relocatable device code is needed.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/batchrand_b200.h"
+#include "core.cuh"
+#include "jump.cuh"
+#include "roll.cuh"
+#include "shuffle.cuh"
+
+using namespace br;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_kernel;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(BR_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));  \
+    } while (0)
+
+typedef unsigned __int128 h128;
+
+inline u128 to_u128(h128 v) { return mk128((uint64_t)(v >> 64), (uint64_t)v); }
+inline h128 from_u128(u128 v) { return ((h128)v.hi << 64) | v.lo; }
+
+const JumpTables &host_tables() {
+    static JumpTables t;
+    static std::once_flag once;
+    std::call_once(once, [] { build_jump_tables(t); });
+    return t;
+}
+
+struct DeviceInfo {
+    bool ready = false;
+    int sms = 0;
+    bool coop = false;
+};
+std::mutex g_mu;
+std::map<int, DeviceInfo> g_dev;
+
+int ensure_device(int *dev_out, DeviceInfo *info_out) {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(BR_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceInfo &d = g_dev[dev];
+    if (!d.ready) {
+        const JumpTables &t = host_tables();
+        CK(cudaMemcpyToSymbol(c_A, t.A, sizeof(t.A)));
+        CK(cudaMemcpyToSymbol(c_G, t.G, sizeof(t.G)));
+        CK(cudaMemcpyToSymbol(g_SA, t.SA, sizeof(t.SA)));
+        CK(cudaMemcpyToSymbol(g_SG, t.SG, sizeof(t.SG)));
+        CK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+        int coop = 0;
+        CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        d.coop = coop != 0;
+        d.ready = true;
+    }
+    *dev_out = dev;
+    *info_out = d;
+    return BR_OK;
+}
+
+// ---------------------------------------------------------------- plan compiler
+// Regime walk of shuffle_batched (shuffle.py:168-224); head of single rolls above the top
+// regime (shuffle.py:175-190) becomes one k=1 segment.
+int build_segments(uint64_t n, const br_regime *e, int ne, std::vector<br_segment> &segs, uint64_t &nbatches) {
+    segs.clear();
+    nbatches = 0;
+    if (n < 2) return BR_OK;
+    if (ne < 1 || !e) return fail(BR_E_INVALID, "schedule needs at least one regime");
+    uint64_t remaining = n;
+    const uint64_t top = e[0].max_length;
+    auto push = [&](uint64_t start, uint32_t k, uint64_t count) {
+        br_segment s;
+        s.start_n = start;
+        s.k = k;
+        s.reserved = 0;
+        s.count = count;
+        segs.push_back(s);
+        nbatches += count;
+    };
+    if (remaining > top) {
+        push(remaining, 1, remaining - top);
+        remaining = top;
+    }
+    int idx = 0;
+    for (int pos = 0; pos < ne; ++pos) {
+        if (e[pos].max_length >= remaining) idx = pos;
+        else break;
+    }
+    uint32_t k = e[idx].batch_size;
+    while (remaining > 1) {
+        if (remaining < k) {
+            push(remaining, (uint32_t)(remaining - 1), 1);
+            break;
+        }
+        if (idx + 1 < ne && remaining <= e[idx + 1].max_length) {
+            ++idx;
+            k = e[idx].batch_size;
+            continue;
+        }
+        uint64_t count = (idx + 1 < ne) ? (remaining - e[idx + 1].max_length + k - 1) / k : remaining / k;
+        if (count == 0 || k == 0) return fail(BR_E_INVALID, "degenerate schedule");
+        push(remaining, k, count);
+        remaining -= count * k;
+    }
+    return BR_OK;
+}
+
+int ff_checked(uint64_t n, uint64_t k, h128 *out) {
+    if (k > n) return BR_E_INVALID;
+    h128 acc = 1, lim = (h128)1 << 64;
+    for (uint64_t f = n; f > n - k; --f) {
+        acc *= f;
+        if (acc > lim) return BR_E_BOUND_OVERFLOW;
+    }
+    *out = acc;
+    return BR_OK;
+}
+
+struct CachedPlan {
+    void *dev = nullptr;  // [DevSeg x nseg][u64 x nbatches]
+    DevPlan plan;
+    uint64_t nbatches = 0;
+};
+std::map<std::pair<int, std::string>, CachedPlan> g_plans;
+
+// Compile segments into a device plan (cached per device and segment list).
+int get_plan(uint64_t n, const std::vector<br_segment> &segs, CachedPlan *out) {
+    int dev;
+    DeviceInfo di;
+    int st = ensure_device(&dev, &di);
+    if (st) return st;
+    std::string key((const char *)segs.data(), segs.size() * sizeof(br_segment));
+    key.append((const char *)&n, sizeof(n));
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_plans.find({dev, key});
+    if (it != g_plans.end()) {
+        *out = it->second;
+        return BR_OK;
+    }
+    if (segs.size() > (size_t)MAX_SEGS) return fail(BR_E_UNSUPPORTED, "plan has too many segments");
+    std::vector<DevSeg> ds;
+    std::vector<uint64_t> th;
+    uint64_t fb = 0;
+    uint32_t maxk = 0;
+    for (const br_segment &s : segs) {
+        if (s.start_n >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements");
+        if (s.k == 0 || (uint64_t)s.k * s.count > s.start_n)
+            return fail(BR_E_INVALID, "segment runs past the start of the array");
+        DevSeg d;
+        d.start_n = (uint32_t)s.start_n;
+        d.k = s.k;
+        d.count = (uint32_t)s.count;
+        d.first_batch = (uint32_t)fb;
+        ds.push_back(d);
+        if (s.k > maxk) maxk = s.k;
+        for (uint64_t c = 0; c < s.count; ++c) {
+            uint64_t nb = s.start_n - c * s.k;
+            h128 f;
+            int e = ff_checked(nb, s.k, &f);
+            if (e) return fail(e, "falling factorial of a batch exceeds 2^64");
+            uint64_t f64 = (uint64_t)f;  // f < 2^64 because nb < 2^32 and ff <= 2^64
+            th.push_back(f == ((h128)1 << 64) ? 0 : (0 - f64) % f64);
+        }
+        fb += s.count;
+    }
+    if (fb >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "too many batches");
+    size_t bytes = ds.size() * sizeof(DevSeg) + th.size() * sizeof(uint64_t) + 16;
+    void *p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    CK(cudaMemcpy(p, ds.data(), ds.size() * sizeof(DevSeg), cudaMemcpyHostToDevice));
+    size_t off = (ds.size() * sizeof(DevSeg) + 15) & ~(size_t)15;
+    if (!th.empty())
+        CK(cudaMemcpy((char *)p + off, th.data(), th.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    CachedPlan cp;
+    cp.dev = p;
+    cp.plan.n = (uint32_t)n;
+    cp.plan.nbatches = (uint32_t)fb;
+    cp.plan.nseg = (uint32_t)ds.size();
+    cp.plan.max_k = maxk;
+    cp.plan.segs = (const DevSeg *)p;
+    cp.plan.thresh = (const uint64_t *)((char *)p + off);
+    cp.nbatches = fb;
+    g_plans[{dev, key}] = cp;
+    *out = cp;
+    return BR_OK;
+}
+
+__global__ void pcg_fill_kernel(uint64_t *__restrict__ out, int64_t count, u128 s0, u128 inc, uint64_t offset) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t per = (((count + nwarps - 1) / nwarps) + 31) & ~(int64_t)31;
+    const int64_t wb = warp * per, we = min(wb + per, count);
+    if (wb >= we) return;
+    u128 s = jump(s0, inc, offset + (uint64_t)wb);
+    s = jump_small(s, inc, lane + 1);
+    const u128 A32 = g_SA[32], C32 = mul128(g_SG[32], inc);
+    for (int64_t b0 = wb; b0 < we; b0 += 32) {
+        const int64_t i = b0 + lane;
+        if (i < we) out[i] = xslrr(s);
+        s = add128(mul128(A32, s), C32);
+    }
+}
+
+int grid_for(const DeviceInfo &di, const void *kernel, int threads, size_t smem, int64_t work_blocks) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    int64_t g = (int64_t)per_sm * di.sms;
+    if (work_blocks < g) g = work_blocks;
+    return (int)(g < 1 ? 1 : g);
+}
+
+template <int K>
+int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int phase) {
+    const int threads = 256;
+    if (phase & 1) {
+        int64_t work_blocks = (a.nb + 8 * 128 - 1) / (8 * 128);
+        int grid = grid_for(di, (const void *)roll_main_kernel<K>, threads, 0, work_blocks);
+        roll_main_kernel<K><<<grid, threads, 0, st>>>(a);
+        CK(cudaGetLastError());
+    }
+    if (phase & 2) {
+        // cooperative fixup: one block per SM (always co-resident)
+        RollArgs b = a;
+        void *args[] = {&b};
+        CK(cudaLaunchCooperativeKernel((const void *)roll_fixup_kernel<K>, dim3(di.sms), dim3(threads), args, 0, st));
+    }
+    g_kernel = "roll_main_kernel<" + std::to_string(K) + ">+roll_fixup_kernel";
+    return BR_OK;
+}
+
+constexpr uint32_t SMALL_SMEM_MAX = 64 * 1024;   // per 128-thread block
+constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
+
+template <typename T>
+int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan &cp, bool segmented,
+                   uint64_t run_seed, int64_t base, uint32_t *words32, uint64_t *state_dev, uint64_t *words64,
+                   uint64_t *rk_first, const DeviceInfo &di, cudaStream_t st) {
+    const uint32_t stride = (uint32_t)(n | 1u);
+    const size_t small_smem = (size_t)128 * stride * sizeof(T);
+    if (segmented && cp.plan.max_k <= 8 && small_smem <= SMALL_SMEM_MAX) {
+        auto kern = shuffle_small_kernel<T>;
+        CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
+        int64_t blocks = (num_arrays + 127) / 128;
+        kern<<<(unsigned)blocks, 128, small_smem, st>>>((T *)data, num_arrays, cp.plan, stride, run_seed, base, words32);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_small_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
+        return BR_OK;
+    }
+    const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);
+    const uint32_t jbytes = (uint32_t)((n * sizeof(uint16_t) + 15) & ~(uint64_t)15);
+    const size_t smem = (size_t)zbytes + jbytes;
+    if (n <= 65536 && smem <= MID_SMEM_MAX) {
+        const void *kp;
+        if (segmented) kp = (const void *)shuffle_mid_kernel<T, uint16_t, true>;
+        else kp = (const void *)shuffle_mid_kernel<T, uint16_t, false>;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int grid = segmented ? grid_for(di, kp, 32, smem, num_arrays) : 1;
+        if (segmented)
+            shuffle_mid_kernel<T, uint16_t, true><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes,
+                                                                        run_seed, base, words32, state_dev, words64, rk_first);
+        else
+            shuffle_mid_kernel<T, uint16_t, false><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes,
+                                                                         run_seed, base, words32, state_dev, words64, rk_first);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
+        return BR_OK;
+    }
+    return fail(BR_E_UNSUPPORTED, "array too large for the shared-memory shuffle kernels (n=" + std::to_string(n) + ")");
+}
+
+int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std::vector<br_segment> &segs,
+                   bool segmented, uint64_t run_seed, int64_t base, uint32_t *words32, br_pcg64 *state_dev,
+                   uint64_t *words64, uint64_t *rk_first, void *stream) {
+    if (eb != 4 && eb != 8) return fail(BR_E_UNSUPPORTED, "elem_bytes must be 4 or 8");
+    if (num_arrays < 0) return fail(BR_E_INVALID, "num_arrays < 0");
+    if (n >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements");
+    int dev;
+    DeviceInfo di;
+    int stt = ensure_device(&dev, &di);
+    if (stt) return stt;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (segs.empty() || num_arrays == 0) {  // n < 2: nothing to do, no words consumed
+        if (segmented && words32 && num_arrays > 0) CK(cudaMemsetAsync(words32, 0, num_arrays * sizeof(uint32_t), st));
+        if (!segmented && words64) CK(cudaMemsetAsync(words64, 0, sizeof(uint64_t), st));
+        g_kernel = "none";
+        return BR_OK;
+    }
+    if (!data) return fail(BR_E_INVALID, "null data pointer");
+    if (!segmented && !state_dev) return fail(BR_E_INVALID, "null state pointer");
+    CachedPlan cp;
+    stt = get_plan(n, segs, &cp);
+    if (stt) return stt;
+    if (eb == 4)
+        return launch_shuffle<uint32_t>(data, num_arrays, n, cp, segmented, run_seed, base, words32,
+                                        (uint64_t *)state_dev, words64, rk_first, di, st);
+    return launch_shuffle<uint64_t>(data, num_arrays, n, cp, segmented, run_seed, base, words32,
+                                    (uint64_t *)state_dev, words64, rk_first, di, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int br_abi_version(void) { return BR_ABI_VERSION; }
+const char *br_last_error(void) { return g_err.c_str(); }
+const char *br_last_kernel(void) { return g_kernel.c_str(); }
+
+int br_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+uint64_t br_splitmix64_next(uint64_t *x) { return splitmix64_next(*x); }
+
+void br_pcg64_seed(uint64_t seed, br_pcg64 *out) {
+    u128 s, inc;
+    pcg_seed(seed, s, inc);
+    out->state_hi = s.hi;
+    out->state_lo = s.lo;
+    out->inc_hi = inc.hi;
+    out->inc_lo = inc.lo;
+}
+
+uint64_t br_pcg64_next(br_pcg64 *st) {
+    u128 s = mk128(st->state_hi, st->state_lo);
+    s = add128(mul128(s, mk128(PCG_MULT_HI, PCG_MULT_LO)), mk128(st->inc_hi, st->inc_lo));
+    st->state_hi = s.hi;
+    st->state_lo = s.lo;
+    return xslrr(s);
+}
+
+void br_pcg64_advance(br_pcg64 *st, uint64_t delta) {
+    const JumpTables &t = host_tables();
+    u128 s = mk128(st->state_hi, st->state_lo), inc = mk128(st->inc_hi, st->inc_lo);
+    for (int k = 0; delta; ++k, delta >>= 1)
+        if (delta & 1) s = add128(mul128(t.A[k], s), mul128(t.G[k], inc));
+    st->state_hi = s.hi;
+    st->state_lo = s.lo;
+}
+
+uint64_t br_array_seed(uint64_t run_seed, uint64_t a) { return array_seed(run_seed, a); }
+
+int br_falling_factorial(uint64_t n, uint32_t k, uint64_t *lo, uint64_t *hi) {
+    h128 v;
+    int st = ff_checked(n, k, &v);
+    if (st) return fail(st, st == BR_E_INVALID ? "need 0 <= k <= n" : "falling factorial exceeds 2**64");
+    *lo = (uint64_t)v;
+    *hi = (uint64_t)(v >> 64);
+    return BR_OK;
+}
+
+int br_schedule_validate(const br_regime *e, int ne, uint32_t max_batch, int word_bits) {
+    if (word_bits != 64) return fail(BR_E_UNSUPPORTED, "device path supports 64-bit words only");
+    if (ne < 1 || !e) return fail(BR_E_INVALID, "schedule needs at least one regime");
+    for (int i = 0; i + 1 < ne; ++i) {
+        if (e[i].max_length <= e[i + 1].max_length) return fail(BR_E_INVALID, "regime lengths must strictly decrease");
+        if (e[i].batch_size >= e[i + 1].batch_size) return fail(BR_E_INVALID, "batch sizes must strictly increase");
+    }
+    if (e[ne - 1].batch_size != max_batch) return fail(BR_E_INVALID, "last batch size != max_batch");
+    for (int i = 0; i < ne; ++i) {
+        if ((uint64_t)e[i].batch_size > e[i].max_length) return fail(BR_E_INVALID, "batch size exceeds regime length");
+        h128 f;
+        int st = ff_checked(e[i].max_length, e[i].batch_size, &f);
+        if (st) return fail(st, "regime product exceeds 2**64");
+    }
+    return BR_OK;
+}
+
+int64_t br_plan_build(uint64_t n, const br_regime *entries, int n_entries, br_segment *out, int64_t cap,
+                      uint64_t *n_batches_out) {
+    std::vector<br_segment> segs;
+    uint64_t nb = 0;
+    int st = build_segments(n, entries, n_entries, segs, nb);
+    if (st) return -st;
+    for (int64_t i = 0; i < (int64_t)segs.size() && i < cap; ++i) out[i] = segs[i];
+    if (n_batches_out) *n_batches_out = nb;
+    return (int64_t)segs.size();
+}
+
+int br_pcg64_fill(uint64_t *out_dev, int64_t count, const br_pcg64 *st, uint64_t offset, void *stream) {
+    if (count < 0 || !st) return fail(BR_E_INVALID, "bad arguments");
+    int dev;
+    DeviceInfo di;
+    int s = ensure_device(&dev, &di);
+    if (s) return s;
+    if (count == 0) return BR_OK;
+    if (!out_dev) return fail(BR_E_INVALID, "null output");
+    int64_t blocks = (count + 256 * 32 - 1) / (256 * 32);
+    int grid = grid_for(di, (const void *)pcg_fill_kernel, 256, 0, blocks);
+    pcg_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(out_dev, count, mk128(st->state_hi, st->state_lo),
+                                                             mk128(st->inc_hi, st->inc_lo), offset);
+    CK(cudaGetLastError());
+    g_kernel = "pcg_fill_kernel";
+    return BR_OK;
+}
+
+int br_state_upload(br_pcg64 *state_dev, const br_pcg64 *st, void *stream) {
+    if (!state_dev || !st) return fail(BR_E_INVALID, "null state");
+    CK(cudaMemcpyAsync(state_dev, st, sizeof(br_pcg64), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return BR_OK;
+}
+
+int br_state_download(br_pcg64 *st, const br_pcg64 *state_dev, void *stream) {
+    if (!state_dev || !st) return fail(BR_E_INVALID, "null state");
+    CK(cudaMemcpyAsync(st, state_dev, sizeof(br_pcg64), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return BR_OK;
+}
+
+size_t br_roll_workspace_bytes(void) { return sizeof(RollWs); }
+
+int br_roll_batches(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *state_dev, uint32_t *rolls,
+                    uint8_t *words, uint8_t *flags, uint64_t *final_rk, void *ws, void *stream) {
+    return br_roll_batches_phase(bounds, k, nb, state_dev, rolls, words, flags, final_rk, ws, 3, stream);
+}
+
+int br_roll_batches_phase(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *state_dev, uint32_t *rolls,
+                          uint8_t *words, uint8_t *flags, uint64_t *final_rk, void *ws, int phase, void *stream) {
+    if (phase < 1 || phase > 3) return fail(BR_E_INVALID, "phase must be 1, 2 or 3");
+    if (nb < 0) return fail(BR_E_INVALID, "num_batches < 0");
+    if (k < 1) return fail(BR_E_INVALID, "at least one base is required");
+    if (k > 8) return fail(BR_E_UNSUPPORTED, "batches of more than 8 dice are not supported on the device path");
+    int dev;
+    DeviceInfo di;
+    int s = ensure_device(&dev, &di);
+    if (s) return s;
+    if (nb == 0) {
+        g_kernel = "none";
+        return BR_OK;
+    }
+    if (!bounds || !state_dev || !rolls || !words || !ws) return fail(BR_E_INVALID, "null pointer argument");
+    if ((((uintptr_t)bounds | (uintptr_t)rolls) & 15) != 0) return fail(BR_E_INVALID, "bounds/rolls must be 16-byte aligned");
+    if (!di.coop) return fail(BR_E_CUDA, "device lacks cooperative launch");
+    RollArgs a;
+    a.bounds = bounds;
+    a.k = k;
+    a.nb = nb;
+    a.state = (uint64_t *)state_dev;
+    a.rolls = rolls;
+    a.words = words;
+    a.flags = flags;
+    a.rk = final_rk;
+    a.ws = (RollWs *)ws;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (k) {
+        case 1: return launch_roll<1>(a, di, st, phase);
+        case 2: return launch_roll<2>(a, di, st, phase);
+        case 3: return launch_roll<3>(a, di, st, phase);
+        case 4: return launch_roll<4>(a, di, st, phase);
+        case 5: return launch_roll<5>(a, di, st, phase);
+        case 6: return launch_roll<6>(a, di, st, phase);
+        case 7: return launch_roll<7>(a, di, st, phase);
+        default: return launch_roll<8>(a, di, st, phase);
+    }
+}
+
+int br_roll_check(void *ws, void *stream, uint64_t *extra_words) {
+    if (!ws) return fail(BR_E_INVALID, "null workspace");
+    RollWs h;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    CK(cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost));
+    if (extra_words) *extra_words = h.extra;
+    if (h.error) {
+        unsigned zero = 0;
+        CK(cudaMemcpy((char *)ws + offsetof(RollWs, error), &zero, sizeof(zero), cudaMemcpyHostToDevice));
+        return fail((int)h.error, h.error == BR_E_INVALID ? "bases must be positive" : "product of bounds exceeds 2**64");
+    }
+    return BR_OK;
+}
+
+int br_digit_pass(const uint64_t *words, const uint32_t *bounds, int k, int64_t count, uint32_t *digits, uint64_t *rk,
+                  void *stream) {
+    if (k < 1 || count < 0) return fail(BR_E_INVALID, "bad arguments");
+    int dev;
+    DeviceInfo di;
+    int s = ensure_device(&dev, &di);
+    if (s) return s;
+    if (count == 0) return BR_OK;
+    if (!words || !bounds || !digits) return fail(BR_E_INVALID, "null pointer argument");
+    int64_t blocks = (count + 255) / 256;
+    int grid = grid_for(di, (const void *)digit_pass_kernel, 256, 0, blocks);
+    digit_pass_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(words, bounds, k, count, digits, rk);
+    CK(cudaGetLastError());
+    g_kernel = "digit_pass_kernel";
+    return BR_OK;
+}
+
+int br_shuffle_stream(void *z, int eb, uint64_t n, br_pcg64 *state_dev, const br_regime *entries, int ne,
+                      int unbatched, uint64_t *words_dev, void *stream) {
+    std::vector<br_segment> segs;
+    uint64_t nb = 0;
+    if (unbatched) {
+        if (n >= 2) {
+            br_segment s;
+            s.start_n = n;
+            s.k = 1;
+            s.reserved = 0;
+            s.count = n - 1;
+            segs.push_back(s);
+        }
+    } else {
+        int st = build_segments(n, entries, ne, segs, nb);
+        if (st) return st;
+    }
+    return shuffle_common(z, eb, 1, n, segs, false, 0, 0, nullptr, state_dev, words_dev, nullptr, stream);
+}
+
+int br_shuffle_stream_segments(void *z, int eb, uint64_t n, br_pcg64 *state_dev, const br_segment *segs, int nseg,
+                               uint64_t *words_dev, uint64_t *rk_first_dev, void *stream) {
+    if (nseg < 0 || (nseg > 0 && !segs)) return fail(BR_E_INVALID, "bad segment list");
+    std::vector<br_segment> v(segs, segs + nseg);
+    for (const br_segment &s : v) {
+        if (s.k < 1 || s.count < 1) return fail(BR_E_INVALID, "segment with k < 1 or count < 1");
+        if (s.start_n > n || (uint64_t)s.k * s.count > s.start_n)
+            return fail(BR_E_INVALID, "segment runs outside the array");
+    }
+    return shuffle_common(z, eb, 1, n, v, false, 0, 0, nullptr, state_dev, words_dev, rk_first_dev, stream);
+}
+
+int br_shuffle_segmented(void *data, int eb, int64_t num_arrays, uint64_t n, uint64_t run_seed, int64_t base,
+                         const br_regime *entries, int ne, uint32_t *words_dev, void *stream) {
+    std::vector<br_segment> segs;
+    uint64_t nb = 0;
+    int st = build_segments(n, entries, ne, segs, nb);
+    if (st) return st;
+    return shuffle_common(data, eb, num_arrays, n, segs, true, run_seed, base, words_dev, nullptr, nullptr, nullptr,
+                          stream);
+}
+
+void br_release(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto &kv : g_plans) cudaFree(kv.second.dev);
+    g_plans.clear();
+}
+
+}  // extern "C"

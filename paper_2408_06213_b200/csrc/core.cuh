@@ -1,0 +1,133 @@
+// core.cuh -- 128-bit arithmetic, device PCG64 and the Theorem-1 digit step.
+//
+// Reference semantics:
+//   PCG64 (XSL-RR 128/64, output of the post-update state)  wordsource.py:71-89
+//   splitmix64 seeding                                       wordsource.py:22-35, 80-83
+//   one die of the digit chain (a_i, r_i) = b_i (x) r_{i-1}  batched.py:69-82
+//
+// sm_100a has no 64-bit multiplier: every 64-bit product is built from 32x32->64
+// IMAD.WIDE.U32 partial products.  A die with a bound < 2^32 costs two of them, a PCG
+// step (multiply by a 128-bit constant) about ten.  Everything here is plain integer
+// CUDA; no tensor cores (there is no dense contraction on this path).
+#pragma once
+#include <stdint.h>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#endif
+
+namespace br {
+
+struct u128 {
+    uint64_t lo, hi;
+};
+
+__host__ __device__ __forceinline__ u128 mk128(uint64_t hi, uint64_t lo) {
+    u128 r;
+    r.lo = lo;
+    r.hi = hi;
+    return r;
+}
+
+__host__ __device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// a*b mod 2^128
+__host__ __device__ __forceinline__ u128 mul128(u128 a, u128 b) {
+    u128 r;
+    r.lo = a.lo * b.lo;
+    r.hi = mulhi64(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+    return r;
+}
+
+__host__ __device__ __forceinline__ u128 add128(u128 a, u128 b) {
+    u128 r;
+    r.lo = a.lo + b.lo;
+    r.hi = a.hi + b.hi + (r.lo < a.lo ? 1u : 0u);
+    return r;
+}
+
+// s <- A*s + C
+__host__ __device__ __forceinline__ u128 affine(u128 s, u128 A, u128 C) { return add128(mul128(A, s), C); }
+
+// PCG_MULTIPLIER, wordsource.py:19
+static constexpr uint64_t PCG_MULT_HI = 0x2360ED051FC65DA4ull;
+static constexpr uint64_t PCG_MULT_LO = 0x4385DF649FCCF645ull;
+
+// XSL-RR output of a (post-update) state, wordsource.py:87-89
+__host__ __device__ __forceinline__ uint64_t xslrr(u128 s) {
+    uint64_t x = s.hi ^ s.lo;
+    unsigned rot = (unsigned)(s.hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+__host__ __device__ __forceinline__ uint64_t splitmix64_next(uint64_t &x) {
+    x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Pcg64Source.__init__ (wordsource.py:80-83)
+__host__ __device__ __forceinline__ void pcg_seed(uint64_t seed, u128 &state, u128 &inc) {
+    uint64_t x = seed;
+    uint64_t z0 = splitmix64_next(x), z1 = splitmix64_next(x);
+    uint64_t z2 = splitmix64_next(x), z3 = splitmix64_next(x);
+    state = mk128(z0, z1);
+    inc = mk128(z2, z3 | 1u);
+}
+
+// per-array seed convention: first splitmix64 output of (s<<32)|a
+__host__ __device__ __forceinline__ uint64_t array_seed(uint64_t run_seed, uint64_t a) {
+    uint64_t x = (run_seed << 32) | a;
+    return splitmix64_next(x);
+}
+
+// One die: (digit, r') = b (x) r for b < 2^32.  Two IMAD.WIDE.U32 partial products.
+__host__ __device__ __forceinline__ uint32_t die(uint32_t b, uint64_t &r) {
+    uint64_t p0 = (uint64_t)b * (uint32_t)r;          // b * r_lo
+    uint64_t p1 = (uint64_t)b * (uint32_t)(r >> 32);  // b * r_hi
+    uint64_t mid = (p0 >> 32) + (uint32_t)p1;        // < 2^33
+    r = (mid << 32) | (uint32_t)p0;
+    return (uint32_t)((p1 >> 32) + (mid >> 32));
+}
+
+// 2^64 mod b for 1 <= b < 2^64 (bounded.py:59-62); b == 0 encodes 2^64 -> 0
+__host__ __device__ __forceinline__ uint64_t threshold64(uint64_t b) { return b ? (0 - b) % b : 0; }
+
+// Jump tables: A_d = M^d, G_d = sum_{i<d} M^i so that state_{t+d} = A_d*state_t + G_d*inc.
+struct JumpTables {
+    u128 A[64], G[64];       // d = 2^k
+    u128 SA[65], SG[65];     // d = 0..64 (lane offsets / small realignments)
+};
+
+// Host construction (also used by the C-ABI host helpers)
+inline void build_jump_tables(JumpTables &t) {
+    u128 m = mk128(PCG_MULT_HI, PCG_MULT_LO);
+    u128 g = mk128(0, 1);
+    for (int k = 0; k < 64; ++k) {
+        t.A[k] = m;
+        t.G[k] = g;
+        // (A,G)_{2d} = (A^2, (A+1) G)
+        g = mul128(add128(m, mk128(0, 1)), g);
+        m = mul128(m, m);
+    }
+    u128 a = mk128(0, 1), gg = mk128(0, 0);
+    u128 M = mk128(PCG_MULT_HI, PCG_MULT_LO);
+    for (int d = 0; d <= 64; ++d) {
+        t.SA[d] = a;
+        t.SG[d] = gg;
+        gg = add128(mul128(M, gg), mk128(0, 1));  // G_{d+1} = M*G_d + 1
+        a = mul128(M, a);
+    }
+}
+
+}  // namespace br

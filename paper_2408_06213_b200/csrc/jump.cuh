@@ -1,0 +1,41 @@
+// jump.cuh -- device jump-ahead for PCG64 streams.
+//
+// A stream is parallelised by giving each lane its own word offset: the state after
+// d more words is A_d*s + G_d*inc (LCG jump-ahead; checked against numpy's PCG64.advance
+// and against stepping in tests/test_oracle.py and tests/test_gpu_*.py).
+//   c_A/c_G : d = 2^k, read with warp-uniform k      -> __constant__ (broadcast)
+//   g_SA/g_SG: d = 0..64, read with per-lane d         -> global (L1-cached)
+#pragma once
+#include "core.cuh"
+
+namespace br {
+
+__constant__ u128 c_A[64];
+__constant__ u128 c_G[64];
+__device__ u128 g_SA[65];
+__device__ u128 g_SG[65];
+
+// state after d more updates (any d; cost popcount(d) affine steps)
+__device__ __forceinline__ u128 jump(u128 s, u128 inc, uint64_t d) {
+    int k = 0;
+    while (d) {
+        if (d & 1) s = add128(mul128(c_A[k], s), mul128(c_G[k], inc));
+        d >>= 1;
+        ++k;
+    }
+    return s;
+}
+
+// state after d (0..64) more updates; d may differ per lane
+__device__ __forceinline__ u128 jump_small(u128 s, u128 inc, int d) {
+    u128 A = g_SA[d], G = g_SG[d];
+    return add128(mul128(A, s), mul128(G, inc));
+}
+
+// one PCG64 update + output (wordsource.py:85-89)
+__device__ __forceinline__ uint64_t pcg_next(u128 &s, u128 inc) {
+    s = add128(mul128(s, mk128(PCG_MULT_HI, PCG_MULT_LO)), inc);
+    return xslrr(s);
+}
+
+}  // namespace br

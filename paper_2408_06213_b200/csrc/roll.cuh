@@ -1,0 +1,262 @@
+// roll.cuh -- bulk batched dice rolls (configs[1], "C2").
+//
+// Semantics: the sequential loop
+//     for i in range(nb): roll_batch(src, BatchSpec(RadixBases.of(bounds[i*k:(i+1)*k])))
+// of batched.py:102-123 on one PCG64 stream.  Batch i consumes word i + D_i, where D_i
+// counts the extra words drawn by rejected batches before it (a rejection re-draws the
+// WHOLE batch from the next word, batched.py:120-122).
+//
+// Parallel form (one HBM pass in the common case):
+//   roll_main   every warp owns a contiguous batch range, lane l takes batches l, l+32, ...
+//               (coalesced 256 B bound loads / roll stores per warp instruction) and jumps
+//               its PCG64 lane state by 32 words per step; it SPECULATES D_i = 0 and marks
+//               the first rejected batch (atomicMax of ~i).  P(reject) <= 2^-32 per batch
+//               for bounds < 2^16, so the speculation is almost always right.
+//   roll_fixup  cooperative grid, always launched: if nothing was rejected it only writes
+//               the advanced state; otherwise it resolves the first rejected batch
+//               (re-draw from the next word), re-runs the tail with the new shift, and
+//               repeats until no rejection is left -- exact for any rejection rate.
+#pragma once
+#include "jump.cuh"
+
+namespace br {
+
+struct RollWs {
+    unsigned long long neg_first;  // ~(first rejected batch); 0 = none
+    unsigned long long D;          // shift published by the fixup resolver
+    unsigned long long extra;      // words consumed beyond one per batch (last call)
+    unsigned int error;            // deferred status (BR_E_INVALID / BR_E_BOUND_OVERFLOW)
+    unsigned int bar_count;
+    unsigned int bar_gen;
+    unsigned int pad[3];
+};
+
+struct RollArgs {
+    const uint32_t *__restrict__ bounds;
+    int k;
+    int64_t nb;
+    uint64_t *state;  // br_pcg64 {state_hi, state_lo, inc_hi, inc_lo}, in/out
+    uint32_t *__restrict__ rolls;
+    uint8_t *__restrict__ words;
+    uint8_t *__restrict__ flags;
+    uint64_t *__restrict__ rk;
+    RollWs *ws;
+};
+
+// Evaluate one batch on word w (batched.py:102-123).  Returns 0 accept, 1 reject,
+// 2 invalid bases (err set).  d[] receives the digits, r the final remainder.
+template <int K>
+__device__ __forceinline__ int eval_batch(const uint32_t (&b)[K], uint64_t w, uint32_t (&d)[K],
+                                          uint64_t &r, uint8_t &tc, int &err) {
+    r = w;
+#pragma unroll
+    for (int m = 0; m < K; ++m) d[m] = die(b[m], r);
+    uint64_t prod;
+    bool full = false;
+    if constexpr (K == 1) {
+        if (b[0] == 0) { err = 1; return 2; }
+        prod = b[0];
+    } else if constexpr (K == 2) {
+        if (b[0] == 0 || b[1] == 0) { err = 1; return 2; }
+        prod = (uint64_t)b[0] * b[1];
+    } else {
+        bool zero = false;
+#pragma unroll
+        for (int m = 0; m < K; ++m) zero |= (b[m] == 0);
+        if (zero) { err = 1; return 2; }
+        // exact product with overflow detection (mixed_radix.py:33-34)
+        uint64_t lo = 1, hi = 0;
+#pragma unroll
+        for (int m = 0; m < K; ++m) {
+            uint64_t nlo = lo * b[m];
+            uint64_t nhi = hi * b[m] + mulhi64(lo, b[m]);
+            lo = nlo;
+            hi = nhi;
+            if (hi > 1 || (hi == 1 && lo != 0)) { err = 2; return 2; }
+        }
+        full = (hi == 1);
+        prod = lo;
+    }
+    if (full) { tc = 1; return 0; }  // product 2^64: threshold 0, always accepted
+    if (r >= prod) { tc = 0; return 0; }
+    tc = 1;
+    uint64_t t = (0 - prod) % prod;  // 2^64 mod prod, the only remainder (batched.py:119)
+    return r < t ? 1 : 0;
+}
+
+template <int K>
+__device__ __forceinline__ void load_bounds(const uint32_t *__restrict__ p, uint32_t (&b)[K]) {
+    if constexpr (K == 2) {
+        uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+        b[0] = v.x;
+        b[1] = v.y;
+    } else if constexpr (K == 4) {
+        uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+        b[0] = v.x;
+        b[1] = v.y;
+        b[2] = v.z;
+        b[3] = v.w;
+    } else {
+#pragma unroll
+        for (int m = 0; m < K; ++m) b[m] = __ldg(p + m);
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void store_rolls(uint32_t *__restrict__ p, const uint32_t (&d)[K]) {
+    if constexpr (K == 2) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(d[0], d[1]);
+    } else if constexpr (K == 4) {
+        *reinterpret_cast<uint4 *>(p) = make_uint4(d[0], d[1], d[2], d[3]);
+    } else {
+#pragma unroll
+        for (int m = 0; m < K; ++m) p[m] = d[m];
+    }
+}
+
+__device__ __forceinline__ void set_error(RollWs *ws, int err) {
+    atomicCAS(&ws->error, 0u, (unsigned)err);
+}
+
+// Process batches [begin, end) assuming shift D (batch i uses word i + D).
+template <int K, int U>
+__device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc, int64_t begin,
+                                           int64_t end, uint64_t D, bool early_exit) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t total = end - begin;
+    if (total <= 0) return;
+    const int64_t per = (((total + nwarps - 1) / nwarps) + 31) & ~(int64_t)31;
+    const int64_t wb = begin + warp * per;
+    const int64_t we = min(wb + per, end);
+    if (wb >= we) return;
+    // lane state: word index wb + D + lane  ->  state index (word index + 1)
+    u128 s = jump(s0, inc, (uint64_t)wb + D);
+    s = jump_small(s, inc, lane + 1);
+    const u128 A32 = g_SA[32];
+    const u128 C32 = mul128(g_SG[32], inc);
+    int err = 0;
+    volatile RollWs *vws = a.ws;
+    for (int64_t b0 = wb; b0 < we; b0 += 32 * U) {
+        if (early_exit) {
+            unsigned long long nf = vws->neg_first;
+            if (nf != 0 && (int64_t)(~nf) < b0) return;  // an earlier rejection supersedes this work
+        }
+        uint32_t bb[U][K];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = b0 + 32 * u + lane;
+            if (b < we) load_bounds<K>(a.bounds + b * K, bb[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = b0 + 32 * u + lane;
+            if (b < we) {
+                const uint64_t w = xslrr(s);
+                uint32_t d[K];
+                uint64_t r;
+                uint8_t tc = 0;
+                int st = eval_batch<K>(bb[u], w, d, r, tc, err);
+                store_rolls<K>(a.rolls + b * K, d);
+                a.words[b] = 1;
+                if (a.flags) a.flags[b] = tc;
+                if (a.rk) a.rk[b] = r;
+                if (st == 1) atomicMax(&a.ws->neg_first, ~(unsigned long long)b);
+            }
+            s = add128(mul128(A32, s), C32);
+        }
+    }
+    if (err) set_error(a.ws, err);
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) roll_main_kernel(RollArgs a) {
+    const u128 s0 = mk128(a.state[0], a.state[1]);
+    const u128 inc = mk128(a.state[2], a.state[3]);
+    roll_range<K, 4>(a, s0, inc, 0, a.nb, 0, false);
+}
+
+// grid-wide barrier for the cooperative fixup kernel (co-residency guaranteed by
+// cudaLaunchCooperativeKernel)
+__device__ __forceinline__ void grid_barrier(RollWs *ws) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = &ws->bar_gen;
+        unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(&ws->bar_count, 1u) == gridDim.x - 1) {
+            ws->bar_count = 0;
+            __threadfence();
+            atomicAdd(&ws->bar_gen, 1u);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
+    RollWs *ws = a.ws;
+    volatile RollWs *vws = ws;
+    const u128 s0 = mk128(a.state[0], a.state[1]);
+    const u128 inc = mk128(a.state[2], a.state[3]);
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    if (vws->error) {  // invalid bases: leave the source untouched (reference raises first)
+        __syncthreads();
+        if (leader) { ws->neg_first = 0; ws->extra = 0; }
+        return;
+    }
+    unsigned long long nf = vws->neg_first;
+    uint64_t D = 0;
+    if (nf != 0) {
+        for (;;) {
+            grid_barrier(ws);  // every block has read nf
+            if (nf == 0) break;
+            const int64_t cur = (int64_t)(~nf);
+            if (leader) {
+                // batch `cur` rejected word cur + D: re-draw the whole batch from the next
+                // words until accepted (batched.py:120-122)
+                uint64_t widx = (uint64_t)cur + D + 1;
+                u128 st = jump(s0, inc, widx + 1);
+                uint32_t bb[K];
+                load_bounds<K>(a.bounds + cur * K, bb);
+                uint64_t extra = 1;
+                for (;;) {
+                    uint32_t d[K];
+                    uint64_t r;
+                    uint8_t tc;
+                    int err = 0;
+                    int res = eval_batch<K>(bb, xslrr(st), d, r, tc, err);
+                    if (res != 1) {
+                        store_rolls<K>(a.rolls + cur * K, d);
+                        a.words[cur] = (uint8_t)(1 + extra > 255 ? 255 : 1 + extra);
+                        if (a.flags) a.flags[cur] = 1;
+                        if (a.rk) a.rk[cur] = r;
+                        break;
+                    }
+                    ++extra;
+                    st = add128(mul128(st, mk128(PCG_MULT_HI, PCG_MULT_LO)), inc);
+                }
+                ws->D = D + extra;
+                ws->neg_first = 0;
+                __threadfence();
+            }
+            grid_barrier(ws);
+            D = vws->D;
+            roll_range<K, 1>(a, s0, inc, cur + 1, a.nb, D, true);
+            grid_barrier(ws);
+            nf = vws->neg_first;
+        }
+    }
+    if (leader) {
+        const u128 sf = jump(s0, inc, (uint64_t)a.nb + D);
+        a.state[0] = sf.hi;
+        a.state[1] = sf.lo;
+        ws->extra = D;
+    }
+}
+
+}  // namespace br

@@ -1,0 +1,281 @@
+// shuffle.cuh -- segmented Fisher-Yates shuffles with batched dice (shuffle.py:100-225).
+//
+// A compiled plan (plan.h) lists the batches of shuffle_batched for one length n; batch b
+// has remaining length n_b, size k_b and exact threshold t_b = 2^64 mod ff(n_b, k_b).
+// A batch is accepted iff its final remainder r_k >= t_b.  This is exactly the
+// reference's acceptance: the carried bound u of _run_batches (shuffle.py:118-128) only
+// decides WHEN the threshold is computed, never WHETHER a batch is accepted (SURVEY
+// finding 3; re-checked by tests/test_oracle.py, whose oracle keeps the literal u logic).
+// Swaps of batch b: z[n_b-1-m] <-> z[d_m], m = 0..k_b-1, in that order.
+//
+// Work units sized to the array (north star item 3):
+//   shuffle_small_kernel  one THREAD per array (n <= SMALL_MAX), the block's arrays staged
+//                         in shared memory with an odd row stride so the coalesced loads
+//                         and stores and the per-position swaps are bank-conflict free;
+//   shuffle_mid_kernel    one WARP per array (n <= MID_MAX), array + swap targets in
+//                         shared memory; words generated 32 batches at a time (lane =
+//                         batch, jump-ahead per lane, ballot on the rare rejection), swaps
+//                         applied 32 steps at a time with an exact intra-group conflict
+//                         resolution (see apply_group).
+#pragma once
+#include "jump.cuh"
+
+namespace br {
+
+struct DevSeg {
+    uint32_t start_n, k, count, first_batch;
+};
+
+static constexpr int MAX_SEGS = 40;
+
+// Device plan header; thresholds follow in the same allocation.
+struct DevPlan {
+    uint32_t n, nbatches, nseg, max_k;
+    const DevSeg *segs;       // [nseg]     (device)
+    const uint64_t *thresh;   // [nbatches] (device)
+};
+
+template <typename T>
+__device__ __forceinline__ void swap_sm(T *p, uint32_t i, uint32_t j) {
+    T x = p[i], y = p[j];
+    p[i] = y;
+    p[j] = x;
+}
+
+// -------------------------------------------------------------------------------------
+// one thread per array
+// -------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                           DevPlan plan, uint32_t stride,
+                                                           uint64_t run_seed, int64_t base,
+                                                           uint32_t *__restrict__ words_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ DevSeg segs[MAX_SEGS];
+    T *buf = reinterpret_cast<T *>(smem_raw);  // array t at buf[t*stride + e]
+    const uint32_t n = plan.n;
+    const int tid = threadIdx.x;
+    const int TPB = blockDim.x;
+    const int64_t a0 = (int64_t)blockIdx.x * TPB;
+    const int na = (int)min((int64_t)TPB, num_arrays - a0);
+    if (tid < (int)plan.nseg) segs[tid] = plan.segs[tid];
+    // coalesced load: warp w copies arrays w, w+W, ...; lanes walk the elements
+    const int lane = tid & 31, wid = tid >> 5, nw = TPB >> 5;
+    const T *g = data + a0 * (int64_t)n;
+    for (int t = wid; t < na; t += nw)
+        for (uint32_t e = lane; e < n; e += 32) buf[t * stride + e] = g[(int64_t)t * n + e];
+    __syncthreads();
+    if (tid < na) {
+        u128 s, inc;
+        pcg_seed(array_seed(run_seed, (uint64_t)(base + a0 + tid)), s, inc);
+        T *z = buf + tid * stride;
+        uint32_t words = 0;
+        for (uint32_t sg = 0; sg < plan.nseg; ++sg) {
+            const DevSeg S = segs[sg];
+            for (uint32_t c = 0; c < S.count; ++c) {
+                const uint32_t nb = S.start_n - c * S.k;
+                const uint64_t t = __ldg(plan.thresh + S.first_batch + c);
+                uint32_t d[8];
+                uint64_t r;
+                do {
+                    r = pcg_next(s, inc);
+                    ++words;
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+                        if (m < (int)S.k) d[m] = die(nb - m, r);
+                } while (r < t);  // reject: re-draw the whole batch (shuffle.py:121-128)
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    if (m < (int)S.k) swap_sm(z, nb - 1 - m, d[m]);
+            }
+        }
+        if (words_out) words_out[a0 + tid] = words;
+    }
+    __syncthreads();
+    T *go = data + a0 * (int64_t)n;
+    for (int t = wid; t < na; t += nw)
+        for (uint32_t e = lane; e < n; e += 32) go[(int64_t)t * n + e] = buf[t * stride + e];
+}
+
+// -------------------------------------------------------------------------------------
+// one warp per array
+// -------------------------------------------------------------------------------------
+static constexpr unsigned FULL = 0xFFFFFFFFu;
+
+template <typename T>
+__device__ __forceinline__ T shfl_t(T v, int src) {
+    if constexpr (sizeof(T) == 8) {
+        uint64_t x = (uint64_t)v;
+        uint32_t lo = __shfl_sync(FULL, (uint32_t)x, src), hi = __shfl_sync(FULL, (uint32_t)(x >> 32), src);
+        return (T)(((uint64_t)hi << 32) | lo);
+    } else {
+        return (T)__shfl_sync(FULL, (uint32_t)v, src);
+    }
+}
+
+// warp copy global <-> shared, 16-byte vectors when aligned
+template <typename T>
+__device__ __forceinline__ void warp_copy(T *__restrict__ dst, const T *__restrict__ src, uint32_t n, int lane) {
+    const size_t bytes = (size_t)n * sizeof(T);
+    if ((((uintptr_t)dst | (uintptr_t)src | bytes) & 15) == 0) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        const uint32_t n4 = (uint32_t)(bytes >> 4);
+        for (uint32_t q = lane; q < n4; q += 32) d4[q] = s4[q];
+    } else {
+        for (uint32_t e = lane; e < n; e += 32) dst[e] = src[e];
+    }
+}
+
+// Generate the swap targets J[pos] of every batch of the plan for the stream (s0, inc).
+// Lane l evaluates batch B0+l on word B0+D+l; a rejected batch shifts every later batch
+// by one word (shuffle.py:121-128), handled by realigning the lane states.  Returns the
+// number of extra words (rejections).
+template <typename IDX>
+__device__ __forceinline__ uint32_t gen_targets(const DevPlan &plan, const DevSeg *segs, u128 s0, u128 inc,
+                                                IDX *J, int lane, uint64_t *rk_first) {
+    const uint32_t nb = plan.nbatches;
+    u128 s = jump_small(s0, inc, lane + 1);
+    const u128 A32 = g_SA[32];
+    const u128 C32 = mul128(g_SG[32], inc);
+    uint32_t B0 = 0, D = 0;
+    uint32_t seg = 0;
+    while (B0 < nb) {
+        const uint32_t b = B0 + lane;
+        bool fail = false;
+        if (b < nb) {
+            uint32_t sg = seg;
+            while (sg + 1 < plan.nseg && segs[sg + 1].first_batch <= b) ++sg;
+            const DevSeg S = segs[sg];
+            const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
+            const uint64_t t = __ldg(plan.thresh + b);
+            uint64_t r = xslrr(s);
+            const uint32_t pos = nbb - 1;
+            for (uint32_t m = 0; m < S.k; ++m) J[pos - m] = (IDX)die(nbb - m, r);
+            fail = r < t;
+            if (rk_first && b == 0 && D == 0) *rk_first = r;
+        }
+        const unsigned fm = __ballot_sync(FULL, fail);
+        __syncwarp();
+        if (fm == 0) {
+            B0 += 32;
+            s = add128(mul128(A32, s), C32);
+        } else {
+            const int l = __ffs(fm) - 1;
+            B0 += l;
+            D += 1;
+            s = jump_small(s, inc, l + 1);
+        }
+        while (seg + 1 < plan.nseg && segs[seg + 1].first_batch <= B0) ++seg;
+    }
+    return D;
+}
+
+// Apply steps at positions top, top-1, ..., top-31 (>= 1) of the sequential Fisher-Yates
+// z[i] <-> z[J[i]] (i descending) as one warp step.  Lane l owns step i_l = top-l with
+// target j_l <= i_l.  Within the group:
+//   A_l = value at i_l just before step l = A_{Pred(l)} if some earlier lane m targeted
+//         i_l (Pred(l) = latest such m) else z[i_l];
+//   B_l = value at j_l just before step l = A_{T(l)} if some earlier lane targeted j_l
+//         (T(l) = latest such) else z[j_l];
+//   final z[i_l] = B_l; positions j < the group's range receive A of their last toucher.
+// Positions above the group are final, positions inside it are finalised here, so the
+// result equals the sequential loop (checked bit-exactly against the oracle).
+template <typename T, typename IDX>
+__device__ __forceinline__ void apply_group(T *z, const IDX *J, uint32_t top, int lane) {
+    const int64_t i = (int64_t)top - lane;
+    const bool act = i >= 1;
+    const uint32_t ii = act ? (uint32_t)i : 0;
+    const uint32_t j = act ? (uint32_t)J[ii] : (0xFFFFFF00u | (uint32_t)lane);
+    const T vi = act ? z[ii] : T(0);
+    const T vj = act ? z[j] : T(0);
+    // Pred: lanes m with j_m == top - l  <=>  d_m == l, d_m = top - j_m
+    const uint32_t dm = top - j;
+    const bool dv = act && dm < 32;
+    const unsigned vmask = __ballot_sync(FULL, dv);
+    unsigned pm = vmask;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const unsigned bq = __ballot_sync(FULL, dv && ((dm >> q) & 1));
+        pm &= ((lane >> q) & 1) ? bq : ~bq;
+    }
+    const unsigned below = (1u << lane) - 1u;
+    pm &= below;
+    int p = pm ? 31 - __clz(pm) : lane;
+    // pointer jumping to the root of the Pred chain (chains are short; <= 5 rounds)
+#pragma unroll 1
+    for (int it = 0; it < 5; ++it) {
+        const int pp = __shfl_sync(FULL, p, p);
+        if (!__any_sync(FULL, pp != p)) break;
+        p = pp;
+    }
+    const T A = shfl_t(vi, p);
+    const unsigned same = __match_any_sync(FULL, j);
+    const unsigned tm = same & below;
+    const int tl = tm ? 31 - __clz(tm) : lane;
+    const T At = shfl_t(A, tl);
+    const T B = tm ? At : vj;
+    const uint32_t lo_pos = top >= 32 ? top - 31 : 1;
+    const unsigned later = same & ~((2u << lane) - 1u);
+    if (act) {
+        z[ii] = B;
+        if (later == 0 && j < lo_pos) z[j] = A;
+    }
+    __syncwarp();
+}
+
+template <typename T, typename IDX, bool SEGMENTED>
+__global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
+                                                         uint32_t zbytes, uint64_t run_seed, int64_t base,
+                                                         uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                         uint64_t *words64, uint64_t *rk_first) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ DevSeg segs[MAX_SEGS];
+    const int lane = threadIdx.x & 31;
+    T *z = reinterpret_cast<T *>(smem_raw);
+    IDX *J = reinterpret_cast<IDX *>(smem_raw + zbytes);
+    for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
+    __syncwarp();
+    const uint32_t n = plan.n;
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        T *g = data + a * (int64_t)n;
+        warp_copy(z, g, n, lane);
+        u128 s0, inc;
+        if constexpr (SEGMENTED) {
+            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+        } else {
+            s0 = mk128(state_io[0], state_io[1]);
+            inc = mk128(state_io[2], state_io[3]);
+        }
+        const uint32_t D = gen_targets<IDX>(plan, segs, s0, inc, J, lane, SEGMENTED ? nullptr : rk_first);
+        __syncwarp();
+        for (int64_t top = (int64_t)n - 1; top >= 1; top -= 32) apply_group<T, IDX>(z, J, (uint32_t)top, lane);
+        warp_copy(g, z, n, lane);
+        const uint64_t words = (uint64_t)plan.nbatches + D;
+        if (lane == 0) {
+            if constexpr (SEGMENTED) {
+                if (words32) words32[a] = (uint32_t)words;
+            } else {
+                const u128 sf = jump(s0, inc, words);
+                state_io[0] = sf.hi;
+                state_io[1] = sf.lo;
+                if (words64) words64[0] = words;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace br
+
+namespace br {
+// digit_pass over many words (batched.py:69-82)
+__global__ void digit_pass_kernel(const uint64_t *__restrict__ words, const uint32_t *__restrict__ bounds, int k,
+                                  int64_t count, uint32_t *__restrict__ digits, uint64_t *__restrict__ rk) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t r = words[i];
+        for (int m = 0; m < k; ++m) digits[i * k + m] = die(bounds[i * k + m], r);
+        if (rk) rk[i] = r;
+    }
+}
+}  // namespace br

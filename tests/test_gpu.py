@@ -1,0 +1,358 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle and the golden vectors.
+
+Bit-exact for everything: rolls, words consumed, threshold flags, final remainders,
+permutations and the advanced generator state.  Sizes are the BASELINE.json configs where
+the oracle finishes in seconds (C2 prefix + 2^22 batches, all of C3, C1, samples of C4);
+size-independent properties (permutation of the input, word counts) cover the rest.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module")
+def B():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2408_06213_b200 as B
+
+    return B
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def dev_u32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
+
+
+def sha_u32(a):
+    return hashlib.sha256(np.asarray(a, dtype="<u4").tobytes()).hexdigest()
+
+
+# ------------------------------------------------------------------ generator
+def test_pcg64_fill_matches_oracle(B, O):
+    for seed, offset, count in ((0, 0, 1), (5, 0, 100000), (42, 12345, 77777), (7, (1 << 40) + 3, 4096)):
+        got = u64(B.pcg64_fill(seed, count, offset))
+        ref = O.pcg64_fill(O.pcg64(seed), offset, count)
+        assert np.array_equal(got, ref), (seed, offset)
+    assert "pcg_fill_kernel" in B.last_kernel()
+
+
+# ------------------------------------------------------------------ batched rolls
+def run_rolls(B, O, seed, bounds, k, flags=True, rk=True):
+    src = O.pcg64(seed)
+    ref = O.roll_batches(src, bounds, k)
+    ds = B.DeviceStream(seed)
+    r = B.roll_batches(ds, dev_u32(bounds), k, flags=flags, final_remainder=rk)
+    st = ds.host_state()
+    return r, ref, src, (st.state_hi << 64) | st.state_lo
+
+
+def test_roll_batches_c2_prefix_golden(B, O, golden, golden_arrays):
+    bounds = golden_arrays["c2_bounds"]
+    ds = B.DeviceStream(golden["c2"]["roll_seed"])
+    r = B.roll_batches(ds, dev_u32(bounds), 2)
+    assert np.array_equal(u32(r.rolls), golden_arrays["c2_rolls"])
+    assert np.array_equal(r.words.cpu().numpy(), golden_arrays["c2_words"])
+    st = ds.host_state()
+    assert (st.state_hi << 64 | st.state_lo) == golden["c2"]["state_after"]
+    assert "roll_main_kernel<2>" in B.last_kernel()
+
+
+def test_roll_batches_c2_large_vs_oracle(B, O):
+    nb = 1 << 22
+    bounds = O.gen_bounds(7, 2 * nb)
+    r, (rolls, words, flags, rk), src, st = run_rolls(B, O, O.array_seed(7, 1), bounds, 2)
+    assert np.array_equal(u32(r.rolls), rolls)
+    assert np.array_equal(r.words.cpu().numpy(), words)
+    assert np.array_equal(r.flags.cpu().numpy(), flags)
+    assert np.array_equal(u64(r.final_remainder), rk)
+    assert st == src.state
+
+
+@pytest.mark.parametrize("heavy_fraction", [0.001, 0.05, 1.0])
+def test_roll_batches_forced_rejections(B, O, heavy_fraction):
+    """Products near 0.7*2^64 reject ~30% of words: exercises the exact fixup path."""
+    rng = np.random.default_rng(int(heavy_fraction * 1000) + 1)
+    nb = 20000
+    bounds = rng.integers(2, 1 << 16, 2 * nb, dtype=np.uint32)
+    heavy = rng.random(nb) < heavy_fraction
+    bounds[0::2][heavy] = 0xFFFFFFFF
+    bounds[1::2][heavy] = 3006477107
+    r, (rolls, words, flags, rk), src, st = run_rolls(B, O, 99, bounds, 2)
+    assert words.max() > 1 or heavy_fraction < 0.01
+    assert np.array_equal(u32(r.rolls), rolls)
+    assert np.array_equal(r.words.cpu().numpy(), words)
+    assert np.array_equal(r.flags.cpu().numpy(), flags)
+    assert np.array_equal(u64(r.final_remainder), rk)
+    assert st == src.state
+
+
+@pytest.mark.parametrize("k", [1, 3, 4, 5, 6, 7, 8])
+def test_roll_batches_k_variants(B, O, k):
+    rng = np.random.default_rng(k)
+    nb = 50000
+    hi = {1: 1 << 32, 3: 1 << 21, 4: 1 << 16, 5: 1 << 12, 6: 1 << 10, 7: 1 << 9, 8: 1 << 8}[k]
+    bounds = rng.integers(1, hi, k * nb, dtype=np.uint64).astype(np.uint32)
+    if k == 3:  # some products exactly 2^64 (always accepted, threshold 0) and near 2^64
+        bounds[: 3 * 50] = np.tile(np.array([1 << 31, 1 << 31, 4], dtype=np.uint32), 50)
+    r, (rolls, words, flags, rk), src, st = run_rolls(B, O, 1000 + k, bounds, k)
+    assert np.array_equal(u32(r.rolls), rolls)
+    assert np.array_equal(r.words.cpu().numpy(), words)
+    assert np.array_equal(r.flags.cpu().numpy(), flags)
+    assert np.array_equal(u64(r.final_remainder), rk)
+    assert st == src.state
+
+
+def test_roll_batches_invalid_bounds(B, O):
+    ds = B.DeviceStream(3)
+    st0 = ds.host_state()
+    bounds = np.full(2 * 1000, 6, dtype=np.uint32)
+    bounds[777] = 0
+    with pytest.raises(ValueError):
+        B.roll_batches(ds, dev_u32(bounds), 2)
+    st1 = ds.host_state()
+    assert (st1.state_hi, st1.state_lo) == (st0.state_hi, st0.state_lo)
+    bounds = np.full(3 * 100, 1 << 22, dtype=np.uint32)
+    with pytest.raises(B.BoundOverflow):
+        B.roll_batches(ds, dev_u32(bounds), 3)
+    # the workspace is clean again afterwards
+    r = B.roll_batches(ds, dev_u32(np.full(2 * 10, 6, dtype=np.uint32)), 2)
+    assert r.words.cpu().numpy().tolist() == [1] * 10
+
+
+def test_roll_batch_dropin_golden(B, golden):
+    for rec in golden["roll_batch"]:
+        s = B.Pcg64Source(rec["seed"])
+        spec = B.BatchSpec(B.RadixBases.of(rec["bases"]))
+        for digits, words, tc, rk in rec["results"][:8]:
+            r = B.roll_batch(s, spec)
+            assert (list(r.digits), r.words_consumed, int(r.threshold_computed), r.final_remainder) == (
+                digits, words, tc, rk)
+        rest = rec["results"][8:]
+        k = len(rec["bases"])
+        res = B.roll_batches(s, dev_u32(np.tile(np.asarray(rec["bases"], dtype=np.uint32), len(rest))), k,
+                             flags=True, final_remainder=True)
+        assert u32(res.rolls).reshape(-1, k).tolist() == [x[0] for x in rest]
+        assert res.words.cpu().tolist() == [x[1] for x in rest]
+        assert res.flags.cpu().tolist() == [x[2] for x in rest]
+        assert u64(res.final_remainder).tolist() == [x[3] for x in rest]
+        assert s.state == rec["state_after"]
+
+
+def test_roll_batch_known_threshold(B):
+    spec = B.BatchSpec.with_threshold(B.RadixBases.of((52, 51)))
+    a, b = B.Pcg64Source(5), B.Pcg64Source(5)
+    r1 = B.roll_batch_known_threshold(a, spec)
+    r2 = B.roll_batch(b, B.BatchSpec(B.RadixBases.of((52, 51))))
+    assert r1.digits == r2.digits and r1.words_consumed == r2.words_consumed and not r1.threshold_computed
+    with pytest.raises(ValueError):
+        B.roll_batch_known_threshold(a, B.BatchSpec(B.RadixBases.of((52, 51))))
+
+
+def test_digit_pass_vs_oracle(B, O, golden):
+    for rec in golden["digit_pass"][:40]:
+        if max(rec["bases"]) < 1 << 32:
+            assert B.digit_pass(rec["r0"], B.RadixBases.of(rec["bases"])) == (tuple(rec["digits"]), rec["rk"])
+    rng = np.random.default_rng(3)
+    n, k = 1 << 20, 4
+    words = rng.integers(0, 2**63, n, dtype=np.int64)
+    bounds = rng.integers(1, 1 << 16, n * k, dtype=np.uint32)
+    d, rk = B.digit_pass_many(torch.from_numpy(words).cuda(), dev_u32(bounds), k)
+    d = u32(d).reshape(n, k)
+    rk = u64(rk)
+    # Theorem 1 reconstruction (test_acceptance.py:72-99): encode(digits)*2^64 + rk == prod*r0
+    for i in rng.integers(0, n, 2000):
+        bs = [int(x) for x in bounds[i * k:(i + 1) * k]]
+        enc = 0
+        for dig, base in zip(d[i].tolist(), bs):
+            enc = enc * base + dig
+        prod = bs[0] * bs[1] * bs[2] * bs[3]
+        assert enc * (1 << 64) + int(rk[i]) == prod * int(words[i])
+
+
+# ------------------------------------------------------------------ segmented shuffles
+def test_c3_every_array(B, O, golden, golden_arrays):
+    n, na = 64, 1 << 20
+    data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
+    _, words = B.shuffle_many(data, n, 1234, return_words=True)
+    assert "shuffle_small_kernel" in B.last_kernel()
+    got = u32(data)
+    ref = np.tile(np.arange(n, dtype=np.uint32), na)
+    ref_words = O.shuffle_segmented(ref, n, 1234)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(u32(words), ref_words)
+    assert np.array_equal(got[: 256 * 64].reshape(256, 64), golden_arrays["c3_perm_first256"].astype(np.uint32))
+    for rec in golden["c3_high"]:
+        assert got[rec["a"] * 64:(rec["a"] + 1) * 64].tolist() == rec["perm"]
+
+
+def test_c4_sample(B, O, golden):
+    n, na = 4096, 1 << 16
+    data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
+    _, words = B.shuffle_many(data, n, 99, return_words=True)
+    assert "shuffle_mid_kernel" in B.last_kernel()
+    got = u32(data).reshape(na, n)
+    w = u32(words)
+    for rec in golden["c4"]:
+        assert sha_u32(got[rec["a"]]) == rec["sha"] and int(w[rec["a"]]) == rec["words"]
+    rng = np.random.default_rng(4)
+    for start in rng.integers(0, na - 256, 8):
+        ref = np.tile(np.arange(n, dtype=np.uint32), 256)
+        rw = O.shuffle_segmented(ref, n, 99, array_index_base=int(start))
+        assert np.array_equal(got[start:start + 256].reshape(-1), ref)
+        assert np.array_equal(w[start:start + 256], rw)
+    # every array is a permutation
+    assert np.array_equal(np.sort(got[::97], axis=1), np.tile(np.arange(n, dtype=np.uint32), (len(got[::97]), 1)))
+
+
+@pytest.mark.parametrize("eb", [4, 8])
+@pytest.mark.parametrize("n", [2, 3, 5, 7, 8, 9, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 255, 256, 257, 511,
+                               512, 513, 1000, 2047, 2048, 2049, 4095, 4097, 10000, 16384])
+def test_shuffle_many_lengths_and_payloads(B, O, n, eb):
+    na = max(2, min(3000, (1 << 21) // n))
+    rng = np.random.default_rng(n * 10 + eb)
+    dt = np.uint32 if eb == 4 else np.uint64
+    payload = rng.integers(0, np.iinfo(dt).max, na * n, dtype=dt)
+    dev = torch.from_numpy(payload.view(np.int32 if eb == 4 else np.int64).copy()).cuda()
+    _, words = B.shuffle_many(dev, n, 777, array_index_base=123, return_words=True)
+    ref = payload.copy()
+    rw = O.shuffle_segmented(ref, n, 777, array_index_base=123)
+    got = dev.cpu().numpy().view(dt)
+    assert np.array_equal(got, ref), (n, eb, B.last_kernel())
+    assert np.array_equal(u32(words), rw)
+
+
+def test_shuffle_many_custom_schedules(B, O, golden):
+    for name in ("pair", "max3", "head", "wide"):
+        entries = [tuple(e) for e in golden["schedules"][name]["entries"]]
+        sched = B.ShuffleSchedule(tuple(entries), golden["schedules"][name]["max_batch"])
+        for n in (5, 64, 300, 1000, 4097):
+            na = 64
+            data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
+            B.shuffle_many(data, n, 5, schedule=sched)
+            ref = np.tile(np.arange(n, dtype=np.uint32), na)
+            from oracle import shuffle_segmented
+
+            shuffle_segmented(ref, n, 5, entries=entries)
+            assert np.array_equal(u32(data), ref), (name, n)
+
+
+# ------------------------------------------------------------------ single stream / drop-in
+def test_c1_stream_golden(B, golden, golden_arrays):
+    s = B.Pcg64Source(42)
+    z = np.arange(10000, dtype=np.uint32)
+    B.shuffle_batched(s, z)
+    assert np.array_equal(z, golden_arrays["c1_batched"])
+    o = B.Pcg64Source(42)
+    o.advance(golden["c1"]["batched"]["words"])
+    assert s.state == o.state
+    s = B.Pcg64Source(42)
+    z = np.arange(10000, dtype=np.uint32)
+    B.shuffle_unbatched(s, z)
+    assert np.array_equal(z, golden_arrays["c1_unbatched"])
+    o = B.Pcg64Source(42)
+    o.advance(9999)
+    assert s.state == o.state
+
+
+def test_dropin_shuffle_batched_golden(B, golden):
+    scheds = {k: B.ShuffleSchedule(tuple(tuple(e) for e in v["entries"]), v["max_batch"])
+              for k, v in golden["schedules"].items()}
+    for rec in golden["shuffle_batched"]:
+        if rec["n"] > 16384:
+            continue  # above the shared-memory kernels; covered by the large-array path tests
+        s = B.Pcg64Source(rec["seed"])
+        z = list(range(rec["n"]))
+        out = B.shuffle_batched(s, z, scheds[rec["schedule"]])
+        assert out is z
+        assert sha_u32(z) == rec["sha"], rec["n"]
+        o = B.Pcg64Source(rec["seed"])
+        o.advance(rec["words"])
+        assert s.state == o.state
+
+
+def test_dropin_unbatched_golden(B, golden):
+    for rec in golden["shuffle_unbatched"]:
+        s = B.Pcg64Source(rec["seed"])
+        z = B.shuffle_unbatched(s, list(range(rec["n"])))
+        assert sha_u32(z) == rec["sha"]
+
+
+def test_partial_shuffle_batch_golden(B, golden):
+    for rec in golden["partial_shuffle_batch"]:
+        s = B.Pcg64Source(rec["seed"])
+        z = list(range(rec["n"]))
+        u = B.partial_shuffle_batch(s, z, rec["n"], rec["k"], rec["u_in"])
+        assert z == rec["perm"] and u == rec["u_out"]
+
+
+def test_dropin_payload_types(B, O):
+    s1, s2, s3 = B.Pcg64Source(9), B.Pcg64Source(9), B.Pcg64Source(9)
+    objs = [f"item{i}" for i in range(777)]
+    a = B.shuffle_batched(s1, list(objs))
+    b = B.shuffle_batched(s2, np.arange(777, dtype=np.uint64))
+    c = B.shuffle_batched(s3, torch.arange(777, dtype=torch.int32, device="cuda"))
+    assert a == [objs[i] for i in b.tolist()]
+    assert c.cpu().tolist() == b.tolist()
+    assert s1.state == s2.state == s3.state
+    ref = O.shuffle_batched(O.pcg64(9), np.arange(777, dtype=np.uint32))
+    assert b.tolist() == ref.tolist()
+    # multiset preservation with duplicates (test_shuffle.py:248-257)
+    d = [3, 1, 3, 3, 7, 1] * 50
+    out = B.shuffle_batched(B.Pcg64Source(1), list(d))
+    assert sorted(out) == sorted(d)
+
+
+def test_dropin_accepts_reference_style_source(B, O):
+    class RefLike:  # duck-typed like the reference Pcg64Source
+        word_bits = 64
+
+        def __init__(self, seed):
+            o = O.pcg64(seed)
+            self.state, self.increment = o.state, o.increment
+
+    s = RefLike(31)
+    z = B.shuffle_batched(s, list(range(1000)))
+    o = O.pcg64(31)
+    assert z == O.shuffle_batched(o, np.arange(1000, dtype=np.uint32)).tolist()
+    assert s.state == o.state
+    with pytest.raises(TypeError):
+        class Lehmerish:
+            word_bits = 64
+            state = 5
+
+        B.shuffle_batched(Lehmerish(), list(range(10)))
+
+
+def test_short_arrays_finish_in_one_batch(B):
+    # test_shuffle.py:223-235: n=5 under the default schedule is one batch of four dice
+    for seed in range(20):
+        s = B.Pcg64Source(seed)
+        z = B.shuffle_batched(s, list(range(5)))
+        o = B.Pcg64Source(seed)
+        o.advance(1)
+        assert s.state == o.state and sorted(z) == list(range(5))
+
+
+def test_native_library_is_the_one_loaded(B):
+    import paper_2408_06213_b200._native as N
+
+    maps = open("/proc/self/maps").read()
+    assert N.LIB_PATH in maps
