@@ -652,4 +652,5 @@ __all__ = [
     "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",
     "make_source", "mul_full", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
     "roll_batches", "shuffle_batched", "shuffle_many", "shuffle_unbatched", "splitmix64_stream", "threshold",
+    "last_kernel",
 ]

@@ -198,6 +198,12 @@ int get_plan(uint64_t n, const std::vector<br_segment> &segs, CachedPlan *out) {
     cp.plan.nbatches = (uint32_t)fb;
     cp.plan.nseg = (uint32_t)ds.size();
     cp.plan.max_k = maxk;
+    {
+        uint64_t steps = 0;
+        for (const br_segment &sg : segs) steps += (uint64_t)sg.k * sg.count;
+        cp.plan.lo = (uint32_t)(n > steps ? n - steps : 0);
+        cp.plan.pad = 0;
+    }
     cp.plan.segs = (const DevSeg *)p;
     cp.plan.thresh = (const uint64_t *)((char *)p + off);
     cp.nbatches = fb;
@@ -278,12 +284,13 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         else kp = (const void *)shuffle_mid_kernel<T, uint16_t, false>;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int grid = segmented ? grid_for(di, kp, 32, smem, num_arrays) : 1;
+        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
         if (segmented)
             shuffle_mid_kernel<T, uint16_t, true><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes,
-                                                                        run_seed, base, words32, state_dev, words64, rk_first);
+                                                                        run_seed, base, words32, state_dev, words64, rk_first, use_tma);
         else
             shuffle_mid_kernel<T, uint16_t, false><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes,
-                                                                         run_seed, base, words32, state_dev, words64, rk_first);
+                                                                         run_seed, base, words32, state_dev, words64, rk_first, use_tma);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;

@@ -138,16 +138,23 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
     const u128 C32 = mul128(g_SG[32], inc);
     int err = 0;
     volatile RollWs *vws = a.ws;
+    // software pipeline: the bounds of the next U*32 batches are in flight while the
+    // current ones are rolled
+    uint32_t cur[U][K], nxt[U][K];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t b = wb + 32 * u + lane;
+        if (b < we) load_bounds<K>(a.bounds + b * K, cur[u]);
+    }
     for (int64_t b0 = wb; b0 < we; b0 += 32 * U) {
         if (early_exit) {
             unsigned long long nf = vws->neg_first;
             if (nf != 0 && (int64_t)(~nf) < b0) return;  // an earlier rejection supersedes this work
         }
-        uint32_t bb[U][K];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t b = b0 + 32 * u + lane;
-            if (b < we) load_bounds<K>(a.bounds + b * K, bb[u]);
+            const int64_t b = b0 + 32 * (U + u) + lane;
+            if (b < we) load_bounds<K>(a.bounds + b * K, nxt[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -157,7 +164,7 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
                 uint32_t d[K];
                 uint64_t r;
                 uint8_t tc = 0;
-                int st = eval_batch<K>(bb[u], w, d, r, tc, err);
+                int st = eval_batch<K>(cur[u], w, d, r, tc, err);
                 store_rolls<K>(a.rolls + b * K, d);
                 a.words[b] = 1;
                 if (a.flags) a.flags[b] = tc;
@@ -166,6 +173,10 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
             }
             s = add128(mul128(A32, s), C32);
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < K; ++m) cur[u][m] = nxt[u][m];
     }
     if (err) set_error(a.ws, err);
 }

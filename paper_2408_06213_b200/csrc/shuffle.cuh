@@ -19,6 +19,7 @@
 //                         resolution (see apply_group).
 #pragma once
 #include "jump.cuh"
+#include "tma.cuh"
 
 namespace br {
 
@@ -31,6 +32,8 @@ static constexpr int MAX_SEGS = 40;
 // Device plan header; thresholds follow in the same allocation.
 struct DevPlan {
     uint32_t n, nbatches, nseg, max_k;
+    uint32_t lo;              // lowest position that has a step (0 or 1 for full plans)
+    uint32_t pad;
     const DevSeg *segs;       // [nseg]     (device)
     const uint64_t *thresh;   // [nbatches] (device)
 };
@@ -59,11 +62,30 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
     const int64_t a0 = (int64_t)blockIdx.x * TPB;
     const int na = (int)min((int64_t)TPB, num_arrays - a0);
     if (tid < (int)plan.nseg) segs[tid] = plan.segs[tid];
-    // coalesced load: warp w copies arrays w, w+W, ...; lanes walk the elements
-    const int lane = tid & 31, wid = tid >> 5, nw = TPB >> 5;
-    const T *g = data + a0 * (int64_t)n;
-    for (int t = wid; t < na; t += nw)
-        for (uint32_t e = lane; e < n; e += 32) buf[t * stride + e] = g[(int64_t)t * n + e];
+    // coalesced staged load: warp w copies its own 32 arrays (the ones its lanes shuffle),
+    // U loads in flight per lane before the shared-memory stores
+    const int lane = tid & 31, wid = tid >> 5;
+    const int t0 = wid * 32;
+    const int tcount = max(0, min(32, na - t0));
+    const uint32_t chunks = (n + 31) / 32;
+    const uint32_t items = (uint32_t)tcount * chunks;
+    const T *g = data + (a0 + t0) * (int64_t)n;
+    constexpr int U = 8;
+    for (uint32_t i0 = 0; i0 < items; i0 += U) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t it = i0 + u;
+            const uint32_t t = it / chunks, e = (it - t * chunks) * 32 + lane;
+            if (it < items && e < n) v[u] = g[(int64_t)t * n + e];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t it = i0 + u;
+            const uint32_t t = it / chunks, e = (it - t * chunks) * 32 + lane;
+            if (it < items && e < n) buf[(t0 + t) * stride + e] = v[u];
+        }
+    }
     __syncthreads();
     if (tid < na) {
         u128 s, inc;
@@ -91,10 +113,16 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
         }
         if (words_out) words_out[a0 + tid] = words;
     }
-    __syncthreads();
-    T *go = data + a0 * (int64_t)n;
-    for (int t = wid; t < na; t += nw)
-        for (uint32_t e = lane; e < n; e += 32) go[(int64_t)t * n + e] = buf[t * stride + e];
+    __syncwarp();
+    T *go = data + (a0 + t0) * (int64_t)n;
+    for (uint32_t i0 = 0; i0 < items; i0 += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t it = i0 + u;
+            const uint32_t t = it / chunks, e = (it - t * chunks) * 32 + lane;
+            if (it < items && e < n) go[(int64_t)t * n + e] = buf[(t0 + t) * stride + e];
+        }
+    }
 }
 
 // -------------------------------------------------------------------------------------
@@ -113,17 +141,23 @@ __device__ __forceinline__ T shfl_t(T v, int src) {
     }
 }
 
-// warp copy global <-> shared, 16-byte vectors when aligned
+// warp copy (fallback when the array is not 16-byte sized/aligned for the bulk engine):
+// U independent loads in flight per lane before the stores
 template <typename T>
 __device__ __forceinline__ void warp_copy(T *__restrict__ dst, const T *__restrict__ src, uint32_t n, int lane) {
-    const size_t bytes = (size_t)n * sizeof(T);
-    if ((((uintptr_t)dst | (uintptr_t)src | bytes) & 15) == 0) {
-        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-        const uint32_t n4 = (uint32_t)(bytes >> 4);
-        for (uint32_t q = lane; q < n4; q += 32) d4[q] = s4[q];
-    } else {
-        for (uint32_t e = lane; e < n; e += 32) dst[e] = src[e];
+    constexpr int U = 8;
+    for (uint32_t e0 = 0; e0 < n; e0 += 32 * U) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + 32 * u + lane;
+            if (e < n) v[u] = src[e];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + 32 * u + lane;
+            if (e < n) dst[e] = v[u];
+        }
     }
 }
 
@@ -182,9 +216,9 @@ __device__ __forceinline__ uint32_t gen_targets(const DevPlan &plan, const DevSe
 // Positions above the group are final, positions inside it are finalised here, so the
 // result equals the sequential loop (checked bit-exactly against the oracle).
 template <typename T, typename IDX>
-__device__ __forceinline__ void apply_group(T *z, const IDX *J, uint32_t top, int lane) {
+__device__ __forceinline__ void apply_group(T *z, const IDX *J, uint32_t top, uint32_t lim, int lane) {
     const int64_t i = (int64_t)top - lane;
-    const bool act = i >= 1;
+    const bool act = i >= (int64_t)lim;
     const uint32_t ii = act ? (uint32_t)i : 0;
     const uint32_t j = act ? (uint32_t)J[ii] : (0xFFFFFF00u | (uint32_t)lane);
     const T vi = act ? z[ii] : T(0);
@@ -215,7 +249,7 @@ __device__ __forceinline__ void apply_group(T *z, const IDX *J, uint32_t top, in
     const int tl = tm ? 31 - __clz(tm) : lane;
     const T At = shfl_t(A, tl);
     const T B = tm ? At : vj;
-    const uint32_t lo_pos = top >= 32 ? top - 31 : 1;
+    const uint32_t lo_pos = top >= lim + 31 ? top - 31 : lim;
     const unsigned later = same & ~((2u << lane) - 1u);
     if (act) {
         z[ii] = B;
@@ -228,18 +262,32 @@ template <typename T, typename IDX, bool SEGMENTED>
 __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
                                                          uint32_t zbytes, uint64_t run_seed, int64_t base,
                                                          uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                         uint64_t *words64, uint64_t *rk_first) {
+                                                         uint64_t *words64, uint64_t *rk_first, int use_tma) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevSeg segs[MAX_SEGS];
+    __shared__ __align__(8) uint64_t bar;
     const int lane = threadIdx.x & 31;
     T *z = reinterpret_cast<T *>(smem_raw);
     IDX *J = reinterpret_cast<IDX *>(smem_raw + zbytes);
     for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
+    if (use_tma && lane == 0) mbar_init(&bar, 1);
     __syncwarp();
     const uint32_t n = plan.n;
+    const uint32_t bytes = n * (uint32_t)sizeof(T);
+    const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
+    uint32_t parity = 0;
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         T *g = data + a * (int64_t)n;
-        warp_copy(z, g, n, lane);
+        if (use_tma) {
+            if (lane == 0) {
+                bulk_wait_read();  // the previous array's bulk store has read z
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bar, bytes);
+                bulk_load(z, g, bytes, &bar);
+            }
+        } else {
+            warp_copy(z, g, n, lane);
+        }
         u128 s0, inc;
         if constexpr (SEGMENTED) {
             pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
@@ -247,10 +295,23 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
         }
+        // swap targets are generated while the payload streams in
         const uint32_t D = gen_targets<IDX>(plan, segs, s0, inc, J, lane, SEGMENTED ? nullptr : rk_first);
+        if (use_tma) {
+            mbar_wait(&bar, parity);
+            parity ^= 1u;
+        }
         __syncwarp();
-        for (int64_t top = (int64_t)n - 1; top >= 1; top -= 32) apply_group<T, IDX>(z, J, (uint32_t)top, lane);
-        warp_copy(g, z, n, lane);
+        for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= 32)
+            apply_group<T, IDX>(z, J, (uint32_t)top, lim, lane);
+        if (use_tma) {
+            if (lane == 0) {
+                fence_proxy_async();
+                bulk_store(g, z, bytes);
+            }
+        } else {
+            warp_copy(g, z, n, lane);
+        }
         const uint64_t words = (uint64_t)plan.nbatches + D;
         if (lane == 0) {
             if constexpr (SEGMENTED) {
@@ -264,6 +325,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         }
         __syncwarp();
     }
+    if (use_tma && lane == 0) bulk_wait_all();
 }
 
 }  // namespace br
