@@ -106,6 +106,8 @@ class ClockSampler:
 
 def soak(torch, fn, seconds=0.3):
     """Run the step back to back until the clocks have ramped (part of the warm-up)."""
+    if os.environ.get("BENCH_NO_SOAK"):
+        return
     t = time.perf_counter()
     while time.perf_counter() - t < seconds:
         for _ in range(8):
