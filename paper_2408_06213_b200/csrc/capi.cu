@@ -225,7 +225,7 @@ __global__ void pcg_fill_kernel(uint64_t *__restrict__ out, int64_t count, u128 
     for (int64_t b0 = wb; b0 < we; b0 += 32) {
         const int64_t i = b0 + lane;
         if (i < we) out[i] = xslrr(s);
-        s = add128(mul128(A32, s), C32);
+        s = mad128(s, A32, C32);
     }
 }
 
@@ -242,9 +242,20 @@ template <int K>
 int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int phase) {
     const int threads = 256;
     if (phase & 1) {
-        int64_t work_blocks = (a.nb + 8 * 128 - 1) / (8 * 128);
-        int grid = grid_for(di, (const void *)roll_main_kernel<K>, threads, 0, work_blocks);
-        roll_main_kernel<K><<<grid, threads, 0, st>>>(a);
+        int64_t work_blocks = (a.nb + 8 * 512 - 1) / (8 * 512);
+        if constexpr (K <= 2) {
+            const void *kp = a.flags ? (a.rk ? (const void *)roll_fast_kernel<K, true, true>
+                                             : (const void *)roll_fast_kernel<K, true, false>)
+                                     : (a.rk ? (const void *)roll_fast_kernel<K, false, true>
+                                             : (const void *)roll_fast_kernel<K, false, false>);
+            int grid = grid_for(di, kp, threads, 0, work_blocks);
+            RollArgs b = a;
+            void *args[] = {&b};
+            CK(cudaLaunchKernel(kp, dim3(grid), dim3(threads), args, 0, st));
+        } else {
+            int grid = grid_for(di, (const void *)roll_main_kernel<K>, threads, 0, work_blocks);
+            roll_main_kernel<K><<<grid, threads, 0, st>>>(a);
+        }
         CK(cudaGetLastError());
     }
     if (phase & 2) {
@@ -253,7 +264,7 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
         void *args[] = {&b};
         CK(cudaLaunchCooperativeKernel((const void *)roll_fixup_kernel<K>, dim3(di.sms), dim3(threads), args, 0, st));
     }
-    g_kernel = "roll_main_kernel<" + std::to_string(K) + ">+roll_fixup_kernel";
+    g_kernel = std::string(K <= 2 ? "roll_fast_kernel<" : "roll_main_kernel<") + std::to_string(K) + ">+roll_fixup_kernel";
     return BR_OK;
 }
 

@@ -54,8 +54,44 @@ __host__ __device__ __forceinline__ u128 add128(u128 a, u128 b) {
     return r;
 }
 
+// s*a + c mod 2^128.  On the device: one 16-instruction multiply-add carry chain over
+// 32-bit limbs (10 low and 6 high partial products, the addend folded into the chain).
+__host__ __device__ __forceinline__ u128 mad128(u128 s, u128 a, u128 c) {
+#ifdef __CUDA_ARCH__
+    const uint32_t s0 = (uint32_t)s.lo, s1 = (uint32_t)(s.lo >> 32), s2 = (uint32_t)s.hi, s3 = (uint32_t)(s.hi >> 32);
+    const uint32_t a0 = (uint32_t)a.lo, a1 = (uint32_t)(a.lo >> 32), a2 = (uint32_t)a.hi, a3 = (uint32_t)(a.hi >> 32);
+    const uint32_t c0 = (uint32_t)c.lo, c1 = (uint32_t)(c.lo >> 32), c2 = (uint32_t)c.hi, c3 = (uint32_t)(c.hi >> 32);
+    uint32_t r0, r1, r2, r3;
+    asm("mad.lo.cc.u32 %0, %4, %8, %12;\n\t"
+        "madc.lo.cc.u32 %1, %4, %9, %13;\n\t"
+        "madc.lo.cc.u32 %2, %4, %10, %14;\n\t"
+        "madc.lo.u32 %3, %4, %11, %15;\n\t"
+        "mad.hi.cc.u32 %1, %4, %8, %1;\n\t"
+        "madc.hi.cc.u32 %2, %4, %9, %2;\n\t"
+        "madc.hi.u32 %3, %4, %10, %3;\n\t"
+        "mad.lo.cc.u32 %1, %5, %8, %1;\n\t"
+        "madc.lo.cc.u32 %2, %5, %9, %2;\n\t"
+        "madc.lo.u32 %3, %5, %10, %3;\n\t"
+        "mad.hi.cc.u32 %2, %5, %8, %2;\n\t"
+        "madc.hi.u32 %3, %5, %9, %3;\n\t"
+        "mad.lo.cc.u32 %2, %6, %8, %2;\n\t"
+        "madc.lo.u32 %3, %6, %9, %3;\n\t"
+        "mad.hi.u32 %3, %6, %8, %3;\n\t"
+        "mad.lo.u32 %3, %7, %8, %3;"
+        : "=&r"(r0), "=&r"(r1), "=&r"(r2), "=&r"(r3)
+        : "r"(s0), "r"(s1), "r"(s2), "r"(s3), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(c0), "r"(c1), "r"(c2),
+          "r"(c3));
+    u128 r;
+    r.lo = ((uint64_t)r1 << 32) | r0;
+    r.hi = ((uint64_t)r3 << 32) | r2;
+    return r;
+#else
+    return add128(mul128(s, a), c);
+#endif
+}
+
 // s <- A*s + C
-__host__ __device__ __forceinline__ u128 affine(u128 s, u128 A, u128 C) { return add128(mul128(A, s), C); }
+__host__ __device__ __forceinline__ u128 affine(u128 s, u128 A, u128 C) { return mad128(s, A, C); }
 
 // PCG_MULTIPLIER, wordsource.py:19
 static constexpr uint64_t PCG_MULT_HI = 0x2360ED051FC65DA4ull;
@@ -63,9 +99,18 @@ static constexpr uint64_t PCG_MULT_LO = 0x4385DF649FCCF645ull;
 
 // XSL-RR output of a (post-update) state, wordsource.py:87-89
 __host__ __device__ __forceinline__ uint64_t xslrr(u128 s) {
+#ifdef __CUDA_ARCH__
+    // rotate right by the top 6 bits with two funnel shifts (swap halves for rot >= 32)
+    const uint32_t xl = (uint32_t)s.hi ^ (uint32_t)s.lo, xh = (uint32_t)(s.hi >> 32) ^ (uint32_t)(s.lo >> 32);
+    const uint32_t rot = (uint32_t)(s.hi >> 58);
+    const bool sw = rot & 32u;
+    const uint32_t a = sw ? xh : xl, b = sw ? xl : xh;
+    return ((uint64_t)__funnelshift_r(b, a, rot) << 32) | __funnelshift_r(a, b, rot);
+#else
     uint64_t x = s.hi ^ s.lo;
     unsigned rot = (unsigned)(s.hi >> 58);
     return (x >> rot) | (x << ((64u - rot) & 63u));
+#endif
 }
 
 __host__ __device__ __forceinline__ uint64_t splitmix64_next(uint64_t &x) {
@@ -92,12 +137,13 @@ __host__ __device__ __forceinline__ uint64_t array_seed(uint64_t run_seed, uint6
 }
 
 // One die: (digit, r') = b (x) r for b < 2^32.  Two IMAD.WIDE.U32 partial products.
+// The carry of b*r_lo is absorbed as the 64-bit addend of the second IMAD.WIDE:
+// b*r_hi + (b*r_lo >> 32) < 2^64, so (digit, r') = (p1 >> 32, p1_lo : p0_lo).
 __host__ __device__ __forceinline__ uint32_t die(uint32_t b, uint64_t &r) {
-    uint64_t p0 = (uint64_t)b * (uint32_t)r;          // b * r_lo
-    uint64_t p1 = (uint64_t)b * (uint32_t)(r >> 32);  // b * r_hi
-    uint64_t mid = (p0 >> 32) + (uint32_t)p1;        // < 2^33
-    r = (mid << 32) | (uint32_t)p0;
-    return (uint32_t)((p1 >> 32) + (mid >> 32));
+    const uint64_t p0 = (uint64_t)b * (uint32_t)r;
+    const uint64_t p1 = (uint64_t)b * (uint32_t)(r >> 32) + (p0 >> 32);
+    r = (p1 << 32) | (uint32_t)p0;
+    return (uint32_t)(p1 >> 32);
 }
 
 // 2^64 mod b for 1 <= b < 2^64 (bounded.py:59-62); b == 0 encodes 2^64 -> 0

@@ -19,7 +19,7 @@ __device__ u128 g_SG[65];
 __device__ __forceinline__ u128 jump(u128 s, u128 inc, uint64_t d) {
     int k = 0;
     while (d) {
-        if (d & 1) s = add128(mul128(c_A[k], s), mul128(c_G[k], inc));
+        if (d & 1) s = mad128(s, c_A[k], mul128(c_G[k], inc));
         d >>= 1;
         ++k;
     }
@@ -29,12 +29,12 @@ __device__ __forceinline__ u128 jump(u128 s, u128 inc, uint64_t d) {
 // state after d (0..64) more updates; d may differ per lane
 __device__ __forceinline__ u128 jump_small(u128 s, u128 inc, int d) {
     u128 A = g_SA[d], G = g_SG[d];
-    return add128(mul128(A, s), mul128(G, inc));
+    return mad128(s, A, mul128(G, inc));
 }
 
 // one PCG64 update + output (wordsource.py:85-89)
 __device__ __forceinline__ uint64_t pcg_next(u128 &s, u128 inc) {
-    s = add128(mul128(s, mk128(PCG_MULT_HI, PCG_MULT_LO)), inc);
+    s = mad128(s, mk128(PCG_MULT_HI, PCG_MULT_LO), inc);
     return xslrr(s);
 }
 

@@ -171,7 +171,7 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
                 if (a.rk) a.rk[b] = r;
                 if (st == 1) atomicMax(&a.ws->neg_first, ~(unsigned long long)b);
             }
-            s = add128(mul128(A32, s), C32);
+            s = mad128(s, A32, C32);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -186,6 +186,96 @@ __global__ void __launch_bounds__(256) roll_main_kernel(RollArgs a) {
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
     roll_range<K, 4>(a, s0, inc, 0, a.nb, 0, false);
+}
+
+
+// Rare path of the fast kernel, out of line: zero bounds, and batches whose final
+// remainder fell below the product (threshold needed; P < 2^-32 per batch for C2).
+__device__ __noinline__ void roll_slow(RollWs *ws, uint8_t *flags, int64_t b, uint64_t r, uint64_t prod) {
+    if (prod == 0) {
+        set_error(ws, 1);  // a zero bound (mixed_radix.py:31-32: bases must be positive)
+        return;
+    }
+    if (flags) flags[b] = 1;
+    const uint64_t t = (0 - prod) % prod;
+    if (r < t) atomicMax(&ws->neg_first, ~(unsigned long long)b);
+}
+
+// Main kernel for k <= 2 (the C2 shape): every lane moves 16 bytes of bounds per load
+// (VB = 4/K batches), four loads in flight, and rolls 16 bytes / words VB bytes per store.
+// Lane l of sub-step u owns batches base + 32*VB*u + VB*l + v (v < VB); its words come
+// from VB consecutive PCG steps, the lane state then jumps 32*VB words.
+template <int K, bool FLAGS, bool RK>
+__global__ void __launch_bounds__(256, 3) roll_fast_kernel(RollArgs a) {
+    static_assert(K == 1 || K == 2, "fast path is for k <= 2");
+    constexpr int VB = 4 / K;
+    constexpr int U = 4;
+    constexpr int64_t CH = 32 * VB * U;
+    const u128 s0 = mk128(a.state[0], a.state[1]);
+    const u128 inc = mk128(a.state[2], a.state[3]);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nchunks = a.nb / CH;
+    const int64_t cpw = (nchunks + nwarps - 1) / nwarps;
+    const int64_t c0 = warp * cpw, c1 = min(c0 + cpw, nchunks);
+    const u128 M = mk128(PCG_MULT_HI, PCG_MULT_LO);
+    if (c0 < c1) {
+        const int64_t wb = c0 * CH;
+        u128 s = jump(s0, inc, (uint64_t)wb);
+        s = jump_small(s, inc, VB * lane + 1);
+        const u128 AJ = g_SA[32 * VB];
+        const u128 CJ = mul128(g_SG[32 * VB], inc);
+        const uint4 *bp = reinterpret_cast<const uint4 *>(a.bounds + wb * K) + lane;
+        uint4 *rp = reinterpret_cast<uint4 *>(a.rolls + wb * K) + lane;
+        uint8_t *wp = a.words + wb + VB * lane;
+        uint4 cur[U], nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = __ldg(bp + 32 * u);
+        for (int64_t c = c0; c < c1; ++c) {
+            if (c + 1 < c1) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) nxt[u] = __ldg(bp + 32 * (U + u));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t bb[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
+                uint32_t dd[4];
+                u128 st = s;
+                const int64_t b0 = wb + (c - c0) * CH + 32 * VB * u + VB * lane;
+#pragma unroll
+                for (int v = 0; v < VB; ++v) {
+                    uint64_t r = xslrr(st);
+                    uint64_t prod;
+                    if constexpr (K == 2) {
+                        dd[2 * v] = die(bb[2 * v], r);
+                        dd[2 * v + 1] = die(bb[2 * v + 1], r);
+                        prod = (uint64_t)bb[2 * v] * bb[2 * v + 1];
+                    } else {
+                        dd[v] = die(bb[v], r);
+                        prod = bb[v];
+                    }
+                    if constexpr (FLAGS) a.flags[b0 + v] = r < prod;
+                    if constexpr (RK) a.rk[b0 + v] = r;
+                    if (__builtin_expect(r < prod || prod == 0, 0)) roll_slow(a.ws, a.flags, b0 + v, r, prod);
+                    if (v + 1 < VB) st = mad128(st, M, inc);
+                }
+                rp[32 * u] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+                if constexpr (VB == 2)
+                    *reinterpret_cast<uint16_t *>(wp + 32 * VB * u) = 0x0101;
+                else
+                    *reinterpret_cast<uint32_t *>(wp + 32 * VB * u) = 0x01010101u;
+                s = mad128(s, AJ, CJ);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+            bp += 32 * U;
+            rp += 32 * U;
+            wp += CH;
+        }
+    }
+    // the last partial chunk (< CH batches) with the generic per-batch path
+    if (nchunks * CH < a.nb) roll_range<K, 1>(a, s0, inc, nchunks * CH, a.nb, 0, false);
 }
 
 // grid-wide barrier for the cooperative fixup kernel (co-residency guaranteed by
@@ -249,7 +339,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
                         break;
                     }
                     ++extra;
-                    st = add128(mul128(st, mk128(PCG_MULT_HI, PCG_MULT_LO)), inc);
+                    st = mad128(st, mk128(PCG_MULT_HI, PCG_MULT_LO), inc);
                 }
                 ws->D = D + extra;
                 ws->neg_first = 0;

@@ -193,7 +193,7 @@ __device__ __forceinline__ uint32_t gen_targets(const DevPlan &plan, const DevSe
         __syncwarp();
         if (fm == 0) {
             B0 += 32;
-            s = add128(mul128(A32, s), C32);
+            s = mad128(s, A32, C32);
         } else {
             const int l = __ffs(fm) - 1;
             B0 += l;
