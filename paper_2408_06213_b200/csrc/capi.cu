@@ -281,7 +281,11 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         auto kern = shuffle_small_kernel<T>;
         CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
         int64_t blocks = (num_arrays + 127) / 128;
-        kern<<<(unsigned)blocks, 128, small_smem, st>>>((T *)data, num_arrays, cp.plan, stride, run_seed, base, words32);
+        // q / n == umulhi(q, ceil(2^32 / n)) exactly for q < 2^32 / n (spans are < 2^16 elements)
+        const uint32_t magic = (uint32_t)((((uint64_t)1 << 32) + n - 1) / n);
+        const int vec_ok = ((n * sizeof(T)) % 16 == 0 && ((uintptr_t)data & 15) == 0) ? 1 : 0;
+        kern<<<(unsigned)blocks, 128, small_smem, st>>>((T *)data, num_arrays, cp.plan, stride, magic, vec_ok, run_seed,
+                                                        base, words32);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_small_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;

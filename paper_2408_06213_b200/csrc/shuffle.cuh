@@ -48,44 +48,124 @@ __device__ __forceinline__ void swap_sm(T *p, uint32_t i, uint32_t j) {
 // -------------------------------------------------------------------------------------
 // one thread per array
 // -------------------------------------------------------------------------------------
+// Run `count` consecutive batches of K dice (the first at remaining length nb) on one
+// thread's array z (row of the block's shared buffer).  Fully unrolled per K.
+template <int K, typename T>
+__device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count, const uint64_t *thresh, u128 &s,
+                                              u128 inc, uint32_t &words) {
+    for (uint32_t c = 0; c < count; ++c, nb -= K) {
+        const uint64_t t = __ldg(thresh + c);
+        uint32_t d[K];
+        uint64_t r;
+        do {
+            r = pcg_next(s, inc);
+            ++words;
+#pragma unroll
+            for (int m = 0; m < K; ++m) d[m] = die(nb - m, r);
+        } while (r < t);  // reject: re-draw the whole batch (shuffle.py:121-128)
+#pragma unroll
+        for (int m = 0; m < K; ++m) swap_sm(z, nb - 1 - m, d[m]);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void small_segment_any(T *z, uint32_t k, uint32_t nb, uint32_t count,
+                                                  const uint64_t *thresh, u128 &s, u128 inc, uint32_t &words) {
+    switch (k) {
+        case 1: small_segment<1>(z, nb, count, thresh, s, inc, words); break;
+        case 2: small_segment<2>(z, nb, count, thresh, s, inc, words); break;
+        case 3: small_segment<3>(z, nb, count, thresh, s, inc, words); break;
+        case 4: small_segment<4>(z, nb, count, thresh, s, inc, words); break;
+        case 5: small_segment<5>(z, nb, count, thresh, s, inc, words); break;
+        case 6: small_segment<6>(z, nb, count, thresh, s, inc, words); break;
+        case 7: small_segment<7>(z, nb, count, thresh, s, inc, words); break;
+        default: small_segment<8>(z, nb, count, thresh, s, inc, words); break;
+    }
+}
+
+// Shared-memory layout: array t of the block at buf[t*stride + e], stride odd, so a warp's
+// lanes touching the same position of 32 different arrays hit 32 different banks, and the
+// coalesced copies (lanes = consecutive elements of one array) are conflict free too.
+// Copies move the warp's own 32 arrays (a contiguous 32*n span) in 16-byte pieces when n
+// is a multiple of 16/sizeof(T), else element by element; q / n uses a magic multiplier.
+template <typename T>
+__device__ __forceinline__ void small_copy(T *buf, T *g, uint32_t span, uint32_t n, uint32_t stride, uint32_t t0,
+                                           uint32_t magic, int lane, bool to_smem, bool vec_ok) {
+    constexpr uint32_t V = 16 / sizeof(T);
+    constexpr int U = 4;
+    if (vec_ok) {
+        const uint32_t nv = span / V;
+        for (uint32_t q0 = 0; q0 < nv; q0 += 32 * U) {
+            uint4 v[U];
+            if (to_smem) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + 32 * u + lane;
+                    if (q < nv) v[u] = reinterpret_cast<const uint4 *>(g)[q];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                if (q < nv) {
+                    const uint32_t e0 = q * V;
+                    const uint32_t t = __umulhi(e0, magic);
+                    T *row = buf + (t0 + t) * stride + (e0 - t * n);
+                    T *vv = reinterpret_cast<T *>(&v[u]);
+                    if (to_smem) {
+#pragma unroll
+                        for (int x = 0; x < (int)V; ++x) row[x] = vv[x];
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < (int)V; ++x) vv[x] = row[x];
+                        reinterpret_cast<uint4 *>(g)[q] = v[u];
+                    }
+                }
+            }
+        }
+    } else {
+        for (uint32_t q0 = 0; q0 < span; q0 += 32 * U) {
+            T v[U];
+            if (to_smem) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + 32 * u + lane;
+                    if (q < span) v[u] = g[q];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                if (q < span) {
+                    const uint32_t t = __umulhi(q, magic);
+                    T *p = buf + (t0 + t) * stride + (q - t * n);
+                    if (to_smem) *p = v[u];
+                    else g[q] = *p;
+                }
+            }
+        }
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data, int64_t num_arrays,
-                                                           DevPlan plan, uint32_t stride,
-                                                           uint64_t run_seed, int64_t base,
+                                                           DevPlan plan, uint32_t stride, uint32_t magic,
+                                                           int vec_ok, uint64_t run_seed, int64_t base,
                                                            uint32_t *__restrict__ words_out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevSeg segs[MAX_SEGS];
-    T *buf = reinterpret_cast<T *>(smem_raw);  // array t at buf[t*stride + e]
+    T *buf = reinterpret_cast<T *>(smem_raw);
     const uint32_t n = plan.n;
     const int tid = threadIdx.x;
-    const int TPB = blockDim.x;
-    const int64_t a0 = (int64_t)blockIdx.x * TPB;
-    const int na = (int)min((int64_t)TPB, num_arrays - a0);
+    const int64_t a0 = (int64_t)blockIdx.x * blockDim.x;
+    const int na = (int)min((int64_t)blockDim.x, num_arrays - a0);
     if (tid < (int)plan.nseg) segs[tid] = plan.segs[tid];
-    // coalesced staged load: warp w copies its own 32 arrays (the ones its lanes shuffle),
-    // U loads in flight per lane before the shared-memory stores
+    // each warp stages exactly the 32 arrays its lanes shuffle
     const int lane = tid & 31, wid = tid >> 5;
-    const int t0 = wid * 32;
-    const int tcount = max(0, min(32, na - t0));
-    const uint32_t chunks = (n + 31) / 32;
-    const uint32_t items = (uint32_t)tcount * chunks;
-    const T *g = data + (a0 + t0) * (int64_t)n;
-    constexpr int U = 8;
-    for (uint32_t i0 = 0; i0 < items; i0 += U) {
-        T v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t it = i0 + u;
-            const uint32_t t = it / chunks, e = (it - t * chunks) * 32 + lane;
-            if (it < items && e < n) v[u] = g[(int64_t)t * n + e];
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t it = i0 + u;
-            const uint32_t t = it / chunks, e = (it - t * chunks) * 32 + lane;
-            if (it < items && e < n) buf[(t0 + t) * stride + e] = v[u];
-        }
-    }
+    const uint32_t t0 = wid * 32;
+    const int tcount = max(0, min(32, na - (int)t0));
+    T *g = data + (a0 + t0) * (int64_t)n;
+    small_copy<T>(buf, g, (uint32_t)tcount * n, n, stride, t0, magic, lane, true, vec_ok != 0);
     __syncthreads();
     if (tid < na) {
         u128 s, inc;
@@ -94,35 +174,12 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
         uint32_t words = 0;
         for (uint32_t sg = 0; sg < plan.nseg; ++sg) {
             const DevSeg S = segs[sg];
-            for (uint32_t c = 0; c < S.count; ++c) {
-                const uint32_t nb = S.start_n - c * S.k;
-                const uint64_t t = __ldg(plan.thresh + S.first_batch + c);
-                uint32_t d[8];
-                uint64_t r;
-                do {
-                    r = pcg_next(s, inc);
-                    ++words;
-#pragma unroll
-                    for (int m = 0; m < 8; ++m)
-                        if (m < (int)S.k) d[m] = die(nb - m, r);
-                } while (r < t);  // reject: re-draw the whole batch (shuffle.py:121-128)
-#pragma unroll
-                for (int m = 0; m < 8; ++m)
-                    if (m < (int)S.k) swap_sm(z, nb - 1 - m, d[m]);
-            }
+            small_segment_any<T>(z, S.k, S.start_n, S.count, plan.thresh + S.first_batch, s, inc, words);
         }
         if (words_out) words_out[a0 + tid] = words;
     }
     __syncwarp();
-    T *go = data + (a0 + t0) * (int64_t)n;
-    for (uint32_t i0 = 0; i0 < items; i0 += U) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t it = i0 + u;
-            const uint32_t t = it / chunks, e = (it - t * chunks) * 32 + lane;
-            if (it < items && e < n) go[(int64_t)t * n + e] = buf[(t0 + t) * stride + e];
-        }
-    }
+    small_copy<T>(buf, g, (uint32_t)tcount * n, n, stride, t0, magic, lane, false, vec_ok != 0);
 }
 
 // -------------------------------------------------------------------------------------
@@ -205,29 +262,35 @@ __device__ __forceinline__ uint32_t gen_targets(const DevPlan &plan, const DevSe
     return D;
 }
 
-// Apply steps at positions top, top-1, ..., top-31 (>= 1) of the sequential Fisher-Yates
-// z[i] <-> z[J[i]] (i descending) as one warp step.  Lane l owns step i_l = top-l with
-// target j_l <= i_l.  Within the group:
+// Apply the steps at positions top, top-1, ..., top-31 (>= lim) of the sequential
+// Fisher-Yates z[i] <-> z[J[i]] (i descending) as one warp step.  Lane l owns step
+// i_l = top-l with target j_l <= i_l.  Within the group:
 //   A_l = value at i_l just before step l = A_{Pred(l)} if some earlier lane m targeted
 //         i_l (Pred(l) = latest such m) else z[i_l];
 //   B_l = value at j_l just before step l = A_{T(l)} if some earlier lane targeted j_l
 //         (T(l) = latest such) else z[j_l];
-//   final z[i_l] = B_l; positions j < the group's range receive A of their last toucher.
-// Positions above the group are final, positions inside it are finalised here, so the
+//   final z[i_l] = B_l; positions below the group receive A of their last toucher.
+// Positions above the group are final and positions inside it are finalised here, so the
 // result equals the sequential loop (checked bit-exactly against the oracle).
-template <typename T, typename IDX>
-__device__ __forceinline__ void apply_group(T *z, const IDX *J, uint32_t top, uint32_t lim, int lane) {
+// GroupMeta holds everything that depends only on the targets; it is computed for the next
+// group while the current group's shared-memory loads are in flight.
+struct GroupMeta {
+    uint32_t i, j;
+    int root, tl;
+    bool act, tm, wb;
+};
+
+template <typename IDX>
+__device__ __forceinline__ GroupMeta group_meta(const IDX *J, uint32_t top, uint32_t lim, int lane) {
+    GroupMeta g;
     const int64_t i = (int64_t)top - lane;
-    const bool act = i >= (int64_t)lim;
-    const uint32_t ii = act ? (uint32_t)i : 0;
-    const uint32_t j = act ? (uint32_t)J[ii] : (0xFFFFFF00u | (uint32_t)lane);
-    const T vi = act ? z[ii] : T(0);
-    const T vj = act ? z[j] : T(0);
+    g.act = i >= (int64_t)lim;
+    g.i = g.act ? (uint32_t)i : 0;
+    g.j = g.act ? (uint32_t)J[g.i] : (0xFFFFFF00u | (uint32_t)lane);
     // Pred: lanes m with j_m == top - l  <=>  d_m == l, d_m = top - j_m
-    const uint32_t dm = top - j;
-    const bool dv = act && dm < 32;
-    const unsigned vmask = __ballot_sync(FULL, dv);
-    unsigned pm = vmask;
+    const uint32_t dm = top - g.j;
+    const bool dv = g.act && dm < 32;
+    unsigned pm = __ballot_sync(FULL, dv);
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
         const unsigned bq = __ballot_sync(FULL, dv && ((dm >> q) & 1));
@@ -236,26 +299,47 @@ __device__ __forceinline__ void apply_group(T *z, const IDX *J, uint32_t top, ui
     const unsigned below = (1u << lane) - 1u;
     pm &= below;
     int p = pm ? 31 - __clz(pm) : lane;
-    // pointer jumping to the root of the Pred chain (chains are short; <= 5 rounds)
 #pragma unroll 1
-    for (int it = 0; it < 5; ++it) {
+    for (int it = 0; it < 5; ++it) {  // pointer jumping to the root of the Pred chain
         const int pp = __shfl_sync(FULL, p, p);
         if (!__any_sync(FULL, pp != p)) break;
         p = pp;
     }
-    const T A = shfl_t(vi, p);
-    const unsigned same = __match_any_sync(FULL, j);
+    g.root = p;
+    const unsigned same = __match_any_sync(FULL, g.j);
     const unsigned tm = same & below;
-    const int tl = tm ? 31 - __clz(tm) : lane;
-    const T At = shfl_t(A, tl);
-    const T B = tm ? At : vj;
+    g.tm = tm != 0;
+    g.tl = tm ? 31 - __clz(tm) : lane;
     const uint32_t lo_pos = top >= lim + 31 ? top - 31 : lim;
     const unsigned later = same & ~((2u << lane) - 1u);
-    if (act) {
-        z[ii] = B;
-        if (later == 0 && j < lo_pos) z[j] = A;
+    g.wb = g.act && later == 0 && g.j < lo_pos;
+    return g;
+}
+
+template <typename T, typename IDX>
+__device__ __forceinline__ void apply_all(T *z, const IDX *J, uint32_t n, uint32_t lim, int lane) {
+    if (n < 1 || n - 1 < lim) return;
+    int64_t top = (int64_t)n - 1;
+    GroupMeta cur = group_meta<IDX>(J, (uint32_t)top, lim, lane);
+    for (;;) {
+        const T vi = cur.act ? z[cur.i] : T(0);
+        const T vj = cur.act ? z[cur.j] : T(0);
+        const int64_t ntop = top - 32;
+        const bool more = ntop >= (int64_t)lim;
+        GroupMeta nxt;
+        if (more) nxt = group_meta<IDX>(J, (uint32_t)ntop, lim, lane);
+        const T A = shfl_t(vi, cur.root);
+        const T At = shfl_t(A, cur.tl);
+        const T B = cur.tm ? At : vj;
+        if (cur.act) {
+            z[cur.i] = B;
+            if (cur.wb) z[cur.j] = A;
+        }
+        __syncwarp();
+        if (!more) break;
+        cur = nxt;
+        top = ntop;
     }
-    __syncwarp();
 }
 
 template <typename T, typename IDX, bool SEGMENTED>
@@ -302,8 +386,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
             parity ^= 1u;
         }
         __syncwarp();
-        for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= 32)
-            apply_group<T, IDX>(z, J, (uint32_t)top, lim, lane);
+        apply_all<T, IDX>(z, J, n, lim, lane);
         if (use_tma) {
             if (lane == 0) {
                 fence_proxy_async();
