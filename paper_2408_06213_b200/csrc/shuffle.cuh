@@ -280,8 +280,19 @@ struct GroupMeta {
     bool act, tm, wb;
 };
 
+// Lanes whose j equals this lane's j, from one ballot per bit of j (jbits = bit length of
+// n-1).  Replaces __match_any_sync, which is throughput-bound on sm_100.
+__device__ __forceinline__ unsigned match_bits(uint32_t j, bool act, int jbits) {
+    unsigned eq = __ballot_sync(FULL, act);
+    for (int q = 0; q < jbits; ++q) {
+        const unsigned bq = __ballot_sync(FULL, (j >> q) & 1u);
+        eq &= ((j >> q) & 1u) ? bq : ~bq;
+    }
+    return eq;
+}
+
 template <typename IDX>
-__device__ __forceinline__ GroupMeta group_meta(const IDX *J, uint32_t top, uint32_t lim, int lane) {
+__device__ __forceinline__ GroupMeta group_meta(const IDX *J, uint32_t top, uint32_t lim, int lane, int jbits) {
     GroupMeta g;
     const int64_t i = (int64_t)top - lane;
     g.act = i >= (int64_t)lim;
@@ -306,7 +317,7 @@ __device__ __forceinline__ GroupMeta group_meta(const IDX *J, uint32_t top, uint
         p = pp;
     }
     g.root = p;
-    const unsigned same = __match_any_sync(FULL, g.j);
+    const unsigned same = match_bits(g.j, g.act, jbits);
     const unsigned tm = same & below;
     g.tm = tm != 0;
     g.tl = tm ? 31 - __clz(tm) : lane;
@@ -319,15 +330,16 @@ __device__ __forceinline__ GroupMeta group_meta(const IDX *J, uint32_t top, uint
 template <typename T, typename IDX>
 __device__ __forceinline__ void apply_all(T *z, const IDX *J, uint32_t n, uint32_t lim, int lane) {
     if (n < 1 || n - 1 < lim) return;
+    const int jbits = 32 - __clz(n - 1);
     int64_t top = (int64_t)n - 1;
-    GroupMeta cur = group_meta<IDX>(J, (uint32_t)top, lim, lane);
+    GroupMeta cur = group_meta<IDX>(J, (uint32_t)top, lim, lane, jbits);
     for (;;) {
         const T vi = cur.act ? z[cur.i] : T(0);
         const T vj = cur.act ? z[cur.j] : T(0);
         const int64_t ntop = top - 32;
         const bool more = ntop >= (int64_t)lim;
         GroupMeta nxt;
-        if (more) nxt = group_meta<IDX>(J, (uint32_t)ntop, lim, lane);
+        if (more) nxt = group_meta<IDX>(J, (uint32_t)ntop, lim, lane, jbits);
         const T A = shfl_t(vi, cur.root);
         const T At = shfl_t(A, cur.tl);
         const T B = cur.tm ? At : vj;
