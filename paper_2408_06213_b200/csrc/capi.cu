@@ -291,21 +291,21 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         return BR_OK;
     }
     const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);
-    const uint32_t jbytes = (uint32_t)((n * sizeof(uint16_t) + 15) & ~(uint64_t)15);
-    const size_t smem = (size_t)zbytes + jbytes;
-    if (n <= 65536 && smem <= MID_SMEM_MAX) {
+    const uint32_t hbytes = (uint32_t)((n + 15) & ~(uint64_t)15);  // lane-id table indexed by target
+    const size_t smem = (size_t)zbytes + hbytes;
+    if (n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 30) {
         const void *kp;
-        if (segmented) kp = (const void *)shuffle_mid_kernel<T, uint16_t, true>;
-        else kp = (const void *)shuffle_mid_kernel<T, uint16_t, false>;
+        if (segmented) kp = (const void *)shuffle_mid_kernel<T, true>;
+        else kp = (const void *)shuffle_mid_kernel<T, false>;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int grid = segmented ? grid_for(di, kp, 32, smem, num_arrays) : 1;
         const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
         if (segmented)
-            shuffle_mid_kernel<T, uint16_t, true><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes,
-                                                                        run_seed, base, words32, state_dev, words64, rk_first, use_tma);
+            shuffle_mid_kernel<T, true><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
+                                                                words32, state_dev, words64, rk_first, use_tma);
         else
-            shuffle_mid_kernel<T, uint16_t, false><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes,
-                                                                         run_seed, base, words32, state_dev, words64, rk_first, use_tma);
+            shuffle_mid_kernel<T, false><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
+                                                                 words32, state_dev, words64, rk_first, use_tma);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;

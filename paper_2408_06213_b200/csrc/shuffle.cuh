@@ -218,48 +218,67 @@ __device__ __forceinline__ void warp_copy(T *__restrict__ dst, const T *__restri
     }
 }
 
-// Generate the swap targets J[pos] of every batch of the plan for the stream (s0, inc).
-// Lane l evaluates batch B0+l on word B0+D+l; a rejected batch shifts every later batch
-// by one word (shuffle.py:121-128), handled by realigning the lane states.  Returns the
-// number of extra words (rejections).
-template <typename IDX>
-__device__ __forceinline__ uint32_t gen_targets(const DevPlan &plan, const DevSeg *segs, u128 s0, u128 inc,
-                                                IDX *J, int lane, uint64_t *rk_first) {
+// Word/target generator of one array for the warp-per-array kernel.  Lane l evaluates
+// batch B0+l on word B0+D+l; a rejected batch shifts every later batch by one word
+// (shuffle.py:121-128), handled by realigning the lane states.  Targets are written into a
+// ring indexed by position (RING entries), just ahead of the groups that consume them.
+static constexpr uint32_t RING = 1024;
+
+struct GenState {
+    u128 s, inc, A32, C32;
+    uint32_t B0, D, seg, frontier;  // frontier: lowest position whose target is committed
+};
+
+__device__ __forceinline__ void gen_init(GenState &g, u128 s0, u128 inc, uint32_t n, int lane) {
+    g.inc = inc;
+    g.s = jump_small(s0, inc, lane + 1);
+    g.A32 = g_SA[32];
+    g.C32 = mul128(g_SG[32], inc);
+    g.B0 = 0;
+    g.D = 0;
+    g.seg = 0;
+    g.frontier = n;
+}
+
+// One generation step: 32 batches evaluated, the accepted prefix committed.
+__device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const DevSeg *segs, uint16_t *ring,
+                                         int lane, uint64_t *rk_first) {
     const uint32_t nb = plan.nbatches;
-    u128 s = jump_small(s0, inc, lane + 1);
-    const u128 A32 = g_SA[32];
-    const u128 C32 = mul128(g_SG[32], inc);
-    uint32_t B0 = 0, D = 0;
-    uint32_t seg = 0;
-    while (B0 < nb) {
-        const uint32_t b = B0 + lane;
-        bool fail = false;
-        if (b < nb) {
-            uint32_t sg = seg;
-            while (sg + 1 < plan.nseg && segs[sg + 1].first_batch <= b) ++sg;
-            const DevSeg S = segs[sg];
-            const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
-            const uint64_t t = __ldg(plan.thresh + b);
-            uint64_t r = xslrr(s);
-            const uint32_t pos = nbb - 1;
-            for (uint32_t m = 0; m < S.k; ++m) J[pos - m] = (IDX)die(nbb - m, r);
-            fail = r < t;
-            if (rk_first && b == 0 && D == 0) *rk_first = r;
-        }
-        const unsigned fm = __ballot_sync(FULL, fail);
-        __syncwarp();
-        if (fm == 0) {
-            B0 += 32;
-            s = mad128(s, A32, C32);
-        } else {
-            const int l = __ffs(fm) - 1;
-            B0 += l;
-            D += 1;
-            s = jump_small(s, inc, l + 1);
-        }
-        while (seg + 1 < plan.nseg && segs[seg + 1].first_batch <= B0) ++seg;
+    const uint32_t b = g.B0 + lane;
+    bool fail = false;
+    uint32_t low = 0xFFFFFFFFu;  // lowest position this lane's batch covers
+    if (b < nb) {
+        uint32_t sg = g.seg;
+        while (sg + 1 < plan.nseg && segs[sg + 1].first_batch <= b) ++sg;
+        const DevSeg S = segs[sg];
+        const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
+        const uint64_t t = __ldg(plan.thresh + b);
+        uint64_t r = xslrr(g.s);
+        const uint32_t pos = nbb - 1;
+        for (uint32_t m = 0; m < S.k; ++m) ring[(pos - m) & (RING - 1)] = (uint16_t)die(nbb - m, r);
+        low = nbb - S.k;
+        fail = r < t;
+        if (rk_first && b == 0 && g.D == 0) *rk_first = r;
     }
-    return D;
+    const unsigned fm = __ballot_sync(FULL, fail);
+    const unsigned active = __ballot_sync(FULL, b < nb);
+    // committed lanes: all active ones, or those before the first rejection
+    const unsigned commit = fm ? (active & ((fm & (0u - fm)) - 1u)) : active;
+    if (commit) {
+        const int lastc = 31 - __clz(commit);
+        g.frontier = __shfl_sync(FULL, low, lastc);
+    }
+    __syncwarp();
+    if (fm == 0) {
+        g.B0 += 32;
+        g.s = mad128(g.s, g.A32, g.C32);
+    } else {
+        const int l = __ffs(fm) - 1;
+        g.B0 += l;
+        g.D += 1;
+        g.s = jump_small(g.s, g.inc, l + 1);
+    }
+    while (g.seg + 1 < plan.nseg && segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
 }
 
 // Apply the steps at positions top, top-1, ..., top-31 (>= lim) of the sequential
@@ -272,35 +291,36 @@ __device__ __forceinline__ uint32_t gen_targets(const DevPlan &plan, const DevSe
 //   final z[i_l] = B_l; positions below the group receive A of their last toucher.
 // Positions above the group are final and positions inside it are finalised here, so the
 // result equals the sequential loop (checked bit-exactly against the oracle).
-// GroupMeta holds everything that depends only on the targets; it is computed for the next
-// group while the current group's shared-memory loads are in flight.
-struct GroupMeta {
-    uint32_t i, j;
-    int root, tl;
-    bool act, tm, wb;
-};
-
-// Lanes whose j equals this lane's j, from one ballot per bit of j (jbits = bit length of
-// n-1).  Replaces __match_any_sync, which is throughput-bound on sm_100.
-__device__ __forceinline__ unsigned match_bits(uint32_t j, bool act, int jbits) {
-    unsigned eq = __ballot_sync(FULL, act);
-    for (int q = 0; q < jbits; ++q) {
-        const unsigned bq = __ballot_sync(FULL, (j >> q) & 1u);
-        eq &= ((j >> q) & 1u) ? bq : ~bq;
+// Most groups have neither an in-group target (one vote) nor a repeated target (exact
+// check through the per-array lane-id table H indexed by target): they take the direct
+// path.  The rest resolve Pred chains with ballots + pointer jumping and T with a
+// radix ballot over the bits of j.
+template <typename T>
+__device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t *H, uint32_t top, uint32_t lim,
+                                            int jbits, int lane) {
+    const int64_t i64 = (int64_t)top - lane;
+    const bool act = i64 >= (int64_t)lim;
+    const uint32_t i = act ? (uint32_t)i64 : 0;
+    const uint32_t j = act ? (uint32_t)ring[i & (RING - 1)] : 0;
+    const T vi = act ? z[i] : T(0);
+    const T vj = act ? z[j] : T(0);
+    const uint32_t lo_pos = top >= lim + 31 ? top - 31 : lim;
+    if (act) H[j] = (uint8_t)lane;
+    const bool inrange = act && j >= lo_pos && j < i;
+    __syncwarp();
+    const bool dupl = act && H[j] != (uint8_t)lane;
+    const unsigned flags = __ballot_sync(FULL, inrange) | __ballot_sync(FULL, dupl);
+    if (flags == 0) {  // direct path: independent swaps
+        if (act) {
+            z[i] = vj;
+            z[j] = vi;
+        }
+        __syncwarp();
+        return;
     }
-    return eq;
-}
-
-template <typename IDX>
-__device__ __forceinline__ GroupMeta group_meta(const IDX *J, uint32_t top, uint32_t lim, int lane, int jbits) {
-    GroupMeta g;
-    const int64_t i = (int64_t)top - lane;
-    g.act = i >= (int64_t)lim;
-    g.i = g.act ? (uint32_t)i : 0;
-    g.j = g.act ? (uint32_t)J[g.i] : (0xFFFFFF00u | (uint32_t)lane);
     // Pred: lanes m with j_m == top - l  <=>  d_m == l, d_m = top - j_m
-    const uint32_t dm = top - g.j;
-    const bool dv = g.act && dm < 32;
+    const uint32_t dm = top - j;
+    const bool dv = act && dm < 32;
     unsigned pm = __ballot_sync(FULL, dv);
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
@@ -316,61 +336,48 @@ __device__ __forceinline__ GroupMeta group_meta(const IDX *J, uint32_t top, uint
         if (!__any_sync(FULL, pp != p)) break;
         p = pp;
     }
-    g.root = p;
-    const unsigned same = match_bits(g.j, g.act, jbits);
-    const unsigned tm = same & below;
-    g.tm = tm != 0;
-    g.tl = tm ? 31 - __clz(tm) : lane;
-    const uint32_t lo_pos = top >= lim + 31 ? top - 31 : lim;
-    const unsigned later = same & ~((2u << lane) - 1u);
-    g.wb = g.act && later == 0 && g.j < lo_pos;
-    return g;
-}
-
-template <typename T, typename IDX>
-__device__ __forceinline__ void apply_all(T *z, const IDX *J, uint32_t n, uint32_t lim, int lane) {
-    if (n < 1 || n - 1 < lim) return;
-    const int jbits = 32 - __clz(n - 1);
-    int64_t top = (int64_t)n - 1;
-    GroupMeta cur = group_meta<IDX>(J, (uint32_t)top, lim, lane, jbits);
-    for (;;) {
-        const T vi = cur.act ? z[cur.i] : T(0);
-        const T vj = cur.act ? z[cur.j] : T(0);
-        const int64_t ntop = top - 32;
-        const bool more = ntop >= (int64_t)lim;
-        GroupMeta nxt;
-        if (more) nxt = group_meta<IDX>(J, (uint32_t)ntop, lim, lane, jbits);
-        const T A = shfl_t(vi, cur.root);
-        const T At = shfl_t(A, cur.tl);
-        const T B = cur.tm ? At : vj;
-        if (cur.act) {
-            z[cur.i] = B;
-            if (cur.wb) z[cur.j] = A;
+    const T A = shfl_t(vi, p);
+    // lanes sharing j (radix ballot; only groups with a repeated target need it)
+    unsigned same = 1u << lane;
+    if (__any_sync(FULL, dupl)) {
+        same = __ballot_sync(FULL, act);
+#pragma unroll 1
+        for (int q = 0; q < jbits; ++q) {
+            const unsigned bq = __ballot_sync(FULL, (j >> q) & 1u);
+            same &= ((j >> q) & 1u) ? bq : ~bq;
         }
-        __syncwarp();
-        if (!more) break;
-        cur = nxt;
-        top = ntop;
+        if (!act) same = 1u << lane;
     }
+    const unsigned tm = same & below;
+    const T At = shfl_t(A, tm ? 31 - __clz(tm) : lane);
+    const T B = tm ? At : vj;
+    const unsigned later = same & ~((2u << lane) - 1u);
+    if (act) {
+        z[i] = B;
+        if (later == 0 && j < lo_pos) z[j] = A;
+    }
+    __syncwarp();
 }
 
-template <typename T, typename IDX, bool SEGMENTED>
+template <typename T, bool SEGMENTED>
 __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
                                                          uint32_t zbytes, uint64_t run_seed, int64_t base,
                                                          uint32_t *__restrict__ words32, uint64_t *state_io,
                                                          uint64_t *words64, uint64_t *rk_first, int use_tma) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevSeg segs[MAX_SEGS];
+    __shared__ __align__(16) uint16_t ring[RING];
     __shared__ __align__(8) uint64_t bar;
     const int lane = threadIdx.x & 31;
     T *z = reinterpret_cast<T *>(smem_raw);
-    IDX *J = reinterpret_cast<IDX *>(smem_raw + zbytes);
+    uint8_t *H = smem_raw + zbytes;
     for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
     if (use_tma && lane == 0) mbar_init(&bar, 1);
     __syncwarp();
     const uint32_t n = plan.n;
     const uint32_t bytes = n * (uint32_t)sizeof(T);
     const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
+    const int jbits = n > 1 ? 32 - __clz(n - 1) : 1;
     uint32_t parity = 0;
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         T *g = data + a * (int64_t)n;
@@ -391,14 +398,23 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
         }
-        // swap targets are generated while the payload streams in
-        const uint32_t D = gen_targets<IDX>(plan, segs, s0, inc, J, lane, SEGMENTED ? nullptr : rk_first);
+        GenState gs;
+        gen_init(gs, s0, inc, n, lane);
+        uint64_t *rkf = SEGMENTED ? nullptr : rk_first;
+        // the first targets are generated while the payload streams in
+        if (plan.nbatches) gen_step(gs, plan, segs, ring, lane, rkf);
         if (use_tma) {
             mbar_wait(&bar, parity);
             parity ^= 1u;
         }
         __syncwarp();
-        apply_all<T, IDX>(z, J, n, lim, lane);
+        for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= 32) {
+            const uint32_t need = top >= (int64_t)lim + 31 ? (uint32_t)top - 31 : lim;
+            while (gs.frontier > need && gs.B0 < plan.nbatches) gen_step(gs, plan, segs, ring, lane, rkf);
+            apply_group<T>(z, ring, H, (uint32_t)top, lim, jbits, lane);
+        }
+        // finish the word accounting (a trailing rejection can follow the last position)
+        while (gs.B0 < plan.nbatches) gen_step(gs, plan, segs, ring, lane, rkf);
         if (use_tma) {
             if (lane == 0) {
                 fence_proxy_async();
@@ -407,7 +423,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         } else {
             warp_copy(g, z, n, lane);
         }
-        const uint64_t words = (uint64_t)plan.nbatches + D;
+        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
         if (lane == 0) {
             if constexpr (SEGMENTED) {
                 if (words32) words32[a] = (uint32_t)words;
