@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -310,7 +311,31 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
     }
-    return fail(BR_E_UNSUPPORTED, "array too large for the shared-memory shuffle kernels (n=" + std::to_string(n) + ")");
+    // large arrays: targets (u32 per position) into stream-ordered scratch, then the apply
+    {
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(num_arrays, (int64_t)((1ull << 31) / (n * 4))));
+        uint32_t *J = nullptr;
+        CK(cudaMallocAsync((void **)&J, (size_t)chunk * n * sizeof(uint32_t), st));
+        for (int64_t a0 = 0; a0 < num_arrays; a0 += chunk) {
+            const int64_t na = std::min(chunk, num_arrays - a0);
+            const int grid_gen = (int)std::min<int64_t>(na, (int64_t)di.sms * 16);
+            if (segmented)
+                shuffle_large_gen_kernel<true><<<grid_gen, 32, 0, st>>>(na, cp.plan, run_seed, base + a0, J,
+                                                                         words32 ? words32 + a0 : nullptr, state_dev,
+                                                                         words64, rk_first);
+            else
+                shuffle_large_gen_kernel<false><<<1, 32, 0, st>>>(1, cp.plan, run_seed, base, J, nullptr, state_dev,
+                                                                   words64, rk_first);
+            const uint32_t lim = cp.plan.lo > 1 ? cp.plan.lo : 1;
+            shuffle_large_apply_kernel<T><<<(int)std::min<int64_t>(na, (int64_t)di.sms * 16), 32, 0, st>>>(
+                (T *)data + a0 * (int64_t)n, na, (uint32_t)n, lim, J);
+            CK(cudaGetLastError());
+        }
+        CK(cudaFreeAsync(J, st));
+        g_kernel = std::string("shuffle_large_gen_kernel+shuffle_large_apply_kernel<u") + std::to_string(8 * sizeof(T)) +
+                   ">";
+        return BR_OK;
+    }
 }
 
 int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std::vector<br_segment> &segs,

@@ -241,8 +241,9 @@ __device__ __forceinline__ void gen_init(GenState &g, u128 s0, u128 inc, uint32_
 }
 
 // One generation step: 32 batches evaluated, the accepted prefix committed.
-__device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const DevSeg *segs, uint16_t *ring,
-                                         int lane, uint64_t *rk_first) {
+template <typename Sink>
+__device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const DevSeg *segs, Sink sink, int lane,
+                                         uint64_t *rk_first) {
     const uint32_t nb = plan.nbatches;
     const uint32_t b = g.B0 + lane;
     bool fail = false;
@@ -255,7 +256,7 @@ __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const
         const uint64_t t = __ldg(plan.thresh + b);
         uint64_t r = xslrr(g.s);
         const uint32_t pos = nbb - 1;
-        for (uint32_t m = 0; m < S.k; ++m) ring[(pos - m) & (RING - 1)] = (uint16_t)die(nbb - m, r);
+        for (uint32_t m = 0; m < S.k; ++m) sink(pos - m, die(nbb - m, r));
         low = nbb - S.k;
         fail = r < t;
         if (rk_first && b == 0 && g.D == 0) *rk_first = r;
@@ -402,7 +403,9 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         gen_init(gs, s0, inc, n, lane);
         uint64_t *rkf = SEGMENTED ? nullptr : rk_first;
         // the first targets are generated while the payload streams in
-        if (plan.nbatches) gen_step(gs, plan, segs, ring, lane, rkf);
+        uint16_t *ringp = ring;
+        auto sink = [ringp](uint32_t pos, uint32_t v) { ringp[pos & (RING - 1)] = (uint16_t)v; };
+        if (plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
         if (use_tma) {
             mbar_wait(&bar, parity);
             parity ^= 1u;
@@ -410,11 +413,11 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         __syncwarp();
         for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= 32) {
             const uint32_t need = top >= (int64_t)lim + 31 ? (uint32_t)top - 31 : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) gen_step(gs, plan, segs, ring, lane, rkf);
+            while (gs.frontier > need && gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
             apply_group<T>(z, ring, H, (uint32_t)top, lim, jbits, lane);
         }
         // finish the word accounting (a trailing rejection can follow the last position)
-        while (gs.B0 < plan.nbatches) gen_step(gs, plan, segs, ring, lane, rkf);
+        while (gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
         if (use_tma) {
             if (lane == 0) {
                 fence_proxy_async();
@@ -437,6 +440,104 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         __syncwarp();
     }
     if (use_tma && lane == 0) bulk_wait_all();
+}
+
+
+// -------------------------------------------------------------------------------------
+// arrays larger than shared memory: targets into a global buffer, then warp-group apply
+// on the array in global memory
+// -------------------------------------------------------------------------------------
+template <bool SEGMENTED>
+__global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_arrays, DevPlan plan, uint64_t run_seed,
+                                                               int64_t base, uint32_t *__restrict__ J,
+                                                               uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                               uint64_t *words64, uint64_t *rk_first) {
+    __shared__ DevSeg segs[MAX_SEGS];
+    const int lane = threadIdx.x & 31;
+    for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
+    __syncwarp();
+    const uint32_t n = plan.n;
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        uint32_t *Ja = J + a * (int64_t)n;
+        u128 s0, inc;
+        if constexpr (SEGMENTED) {
+            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+        } else {
+            s0 = mk128(state_io[0], state_io[1]);
+            inc = mk128(state_io[2], state_io[3]);
+        }
+        GenState gs;
+        gen_init(gs, s0, inc, n, lane);
+        auto sink = [Ja](uint32_t pos, uint32_t v) { Ja[pos] = v; };
+        uint64_t *rkf = SEGMENTED ? nullptr : rk_first;
+        while (gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
+        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
+        if (lane == 0) {
+            if constexpr (SEGMENTED) {
+                if (words32) words32[a] = (uint32_t)words;
+            } else {
+                const u128 sf = jump(s0, inc, words);
+                state_io[0] = sf.hi;
+                state_io[1] = sf.lo;
+                if (words64) words64[0] = words;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Same group resolution as apply_group, on global memory (no lane-id table: repeated
+// targets are found with __match_any_sync).
+template <typename T>
+__device__ __forceinline__ void apply_group_global(T *z, const uint32_t *J, uint32_t top, uint32_t lim, int lane) {
+    const int64_t i64 = (int64_t)top - lane;
+    const bool act = i64 >= (int64_t)lim;
+    const uint32_t i = act ? (uint32_t)i64 : 0;
+    const uint32_t j = act ? __ldg(J + i) : (0xFFFFFFE0u | (uint32_t)lane);
+    const T vi = act ? z[i] : T(0);
+    const T vj = act ? z[j] : T(0);
+    const uint32_t lo_pos = top >= lim + 31 ? top - 31 : lim;
+    const uint32_t dm = top - j;
+    const bool dv = act && dm < 32;
+    unsigned pm = __ballot_sync(FULL, dv);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const unsigned bq = __ballot_sync(FULL, dv && ((dm >> q) & 1));
+        pm &= ((lane >> q) & 1) ? bq : ~bq;
+    }
+    const unsigned below = (1u << lane) - 1u;
+    pm &= below;
+    int p = pm ? 31 - __clz(pm) : lane;
+#pragma unroll 1
+    for (int it = 0; it < 5; ++it) {
+        const int pp = __shfl_sync(FULL, p, p);
+        if (!__any_sync(FULL, pp != p)) break;
+        p = pp;
+    }
+    const T A = shfl_t(vi, p);
+    const unsigned same = __match_any_sync(FULL, j);
+    const unsigned tm = same & below;
+    const T At = shfl_t(A, tm ? 31 - __clz(tm) : lane);
+    const T B = tm ? At : vj;
+    const unsigned later = same & ~((2u << lane) - 1u);
+    if (act) {
+        z[i] = B;
+        if (later == 0 && j < lo_pos) z[j] = A;
+    }
+    __syncwarp();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32) shuffle_large_apply_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                 uint32_t n, uint32_t lim,
+                                                                 const uint32_t *__restrict__ J) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        T *z = data + a * (int64_t)n;
+        const uint32_t *Ja = J + a * (int64_t)n;
+        for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= 32)
+            apply_group_global<T>(z, Ja, (uint32_t)top, lim, lane);
+    }
 }
 
 }  // namespace br

@@ -276,8 +276,6 @@ def test_dropin_shuffle_batched_golden(B, golden):
     scheds = {k: B.ShuffleSchedule(tuple(tuple(e) for e in v["entries"]), v["max_batch"])
               for k, v in golden["schedules"].items()}
     for rec in golden["shuffle_batched"]:
-        if rec["n"] > 16384:
-            continue  # above the shared-memory kernels; covered by the large-array path tests
         s = B.Pcg64Source(rec["seed"])
         z = list(range(rec["n"]))
         out = B.shuffle_batched(s, z, scheds[rec["schedule"]])
@@ -356,3 +354,42 @@ def test_native_library_is_the_one_loaded(B):
 
     maps = open("/proc/self/maps").read()
     assert N.LIB_PATH in maps
+
+
+# ------------------------------------------------------------------ large arrays (global-memory path)
+def test_c5_sample_vs_golden_and_oracle(B, O, golden):
+    n, na = 1 << 20, 8
+    payload = O.pcg64_fill(O.pcg64(5), 0, n * na)  # C5 payload convention: words of pcg64(5)
+    dev = torch.from_numpy(payload.view(np.int64).copy()).cuda()
+    _, words = B.shuffle_many(dev, n, 5, return_words=True)
+    assert "shuffle_large" in B.last_kernel()
+    got = dev.cpu().numpy().view(np.uint64)
+    ref = payload.copy()
+    rw = O.shuffle_segmented(ref, n, 5)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(u32(words), rw)
+    # golden (reference-run) index permutations of arrays 0 and 255
+    for rec in golden["c5"]:
+        idx = torch.arange(n, dtype=torch.int32, device="cuda")
+        _, w = B.shuffle_many(idx, n, 5, array_index_base=rec["a"], return_words=True)
+        assert sha_u32(u32(idx)) == rec["sha"] and int(u32(w)[0]) == rec["words"]
+
+
+@pytest.mark.parametrize("n", [16385, 20000, 65536, 100003, 1 << 18])
+def test_large_stream_and_segmented_vs_oracle(B, O, n):
+    s = B.Pcg64Source(n)
+    z = np.arange(n, dtype=np.uint32)
+    B.shuffle_batched(s, z)
+    o = O.pcg64(n)
+    ref = O.shuffle_batched(o, np.arange(n, dtype=np.uint32))
+    assert np.array_equal(z, ref) and s.state == o.state
+    s = B.Pcg64Source(n + 1)
+    z = np.arange(n, dtype=np.uint64)
+    B.shuffle_unbatched(s, z)
+    o = O.pcg64(n + 1)
+    assert np.array_equal(z, O.shuffle_unbatched(o, np.arange(n, dtype=np.uint64))) and s.state == o.state
+    data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(3)
+    _, w = B.shuffle_many(data, n, 11, array_index_base=7, return_words=True)
+    ref = np.tile(np.arange(n, dtype=np.uint32), 3)
+    rw = O.shuffle_segmented(ref, n, 11, array_index_base=7)
+    assert np.array_equal(u32(data), ref) and np.array_equal(u32(w), rw)
