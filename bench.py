@@ -281,13 +281,17 @@ def cpu_baseline_c2(sample_batches=1 << 22):
 SHUFFLE_CFG = {
     "c3": {"n": 64, "arrays": 1 << 20, "seed": 1234, "eb": 4, "workload": "C3: 2^20 independent shuffles of u32[64], seeds hash(1234,a)"},
     "c4": {"n": 4096, "arrays": 1 << 16, "seed": 99, "eb": 4, "workload": "C4: 65,536 independent shuffles of u32[4096], seeds hash(99,a)"},
+    "c5": {"n": 1 << 20, "arrays": 256, "seed": 5, "eb": 8, "workload": "C5: 256 independent shuffles of u64[2^20] (payload = words of pcg64(5)), seeds hash(5,a), HBM-resident"},
 }
 
 
 def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
     n, na, eb = cfg["n"], cfg["arrays"], cfg["eb"]
-    data = torch.arange(n, dtype=torch.int32 if eb == 4 else torch.int64, device="cuda").repeat(na)
     base = rank * na
+    if eb == 8:  # payload: consecutive words of pcg64(seed) (this rank's section)
+        data = B.pcg64_fill(cfg["seed"], n * na, offset=base * n)
+    else:
+        data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
     K = steps or args.steps
     for _ in range(args.warmup):
         B.shuffle_many(data, n, cfg["seed"], array_index_base=base)
@@ -356,6 +360,8 @@ def cpu_baseline_shuffle(cfg, sample_arrays):
 
     O.build()
     n = cfg["n"]
+    if cfg["eb"] == 8:
+        sample_arrays = max(sample_arrays, cpu_cores())
     data = np.tile(np.arange(n, dtype=np.uint32 if cfg["eb"] == 4 else np.uint64), sample_arrays)
     t = time.perf_counter()
     O.shuffle_segmented(data, n, cfg["seed"], nthreads=0)
@@ -390,7 +396,11 @@ def run_reference(args, ws, rank):
         c = SHUFFLE_CFG[cfg]
         n = c["n"]
         arrays = max(1, (1 << 22) // n)
-        data = __import__("numpy").tile(__import__("numpy").arange(n, dtype="uint32"), arrays)
+        if c["eb"] == 8:
+            arrays = max(arrays, cpu_cores())
+            data = O.pcg64_fill(O.pcg64(c["seed"]), 0, n * arrays)
+        else:
+            data = __import__("numpy").tile(__import__("numpy").arange(n, dtype="uint32"), arrays)
         for _ in range(args.warmup):
             O.shuffle_segmented(data, n, c["seed"], nthreads=0)
         t = time.perf_counter()
@@ -417,7 +427,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -469,9 +479,10 @@ def main():
         line["cross_rank_rejections"] = r["cross_rank_rejections"]
     if not args.no_secondary:
         sec = {}
-        for key in ("c3", "c4"):
+        for key in ("c3", "c4", "c5"):
             if key != args.config:
-                sec[key] = bench_shuffle(SHUFFLE_CFG[key], args, torch, B, ws, rank, steps=min(args.steps, 10))
+                sec[key] = bench_shuffle(SHUFFLE_CFG[key], args, torch, B, ws, rank,
+                                         steps=min(args.steps, 3 if key == "c5" else 10))
         if ws == 1:
             sec["c1"] = bench_c1(args, torch, B)
         line["secondary"] = sec
