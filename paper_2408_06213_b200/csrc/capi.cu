@@ -260,10 +260,29 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
         CK(cudaGetLastError());
     }
     if (phase & 2) {
-        // cooperative fixup: one block per SM (always co-resident)
+        // cooperative fixup (one block per SM, always co-resident), launched as a programmatic
+        // dependent of the main kernel so its launch latency overlaps the main kernel's tail
         RollArgs b = a;
         void *args[] = {&b};
-        CK(cudaLaunchCooperativeKernel((const void *)roll_fixup_kernel<K>, dim3(di.sms), dim3(threads), args, 0, st));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(di.sms);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute attrs[2];
+        attrs[0].id = cudaLaunchAttributeCooperative;
+        attrs[0].val.cooperative = 1;
+        attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attrs;
+        cfg.numAttrs = (phase & 1) ? 2 : 1;
+        cudaError_t e = cudaLaunchKernelExC(&cfg, (const void *)roll_fixup_kernel<K>, args);
+        if (e != cudaSuccess && cfg.numAttrs == 2) {  // PDL + cooperative refused: plain cooperative launch
+            cudaGetLastError();
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelExC(&cfg, (const void *)roll_fixup_kernel<K>, args);
+        }
+        if (e != cudaSuccess) return fail(BR_E_CUDA, std::string("fixup launch: ") + cudaGetErrorString(e));
     }
     g_kernel = std::string(K <= 2 ? "roll_fast_kernel<" : "roll_main_kernel<") + std::to_string(K) + ">+roll_fixup_kernel";
     return BR_OK;

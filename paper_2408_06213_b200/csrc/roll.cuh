@@ -29,7 +29,13 @@ struct RollWs {
     unsigned int bar_count;
     unsigned int bar_gen;
     unsigned int pad[3];
+    unsigned long long final_hi, final_lo;  // state after nb words (no-rejection case), by the main kernel
 };
+
+// Programmatic dependent launch: the main kernel lets the fixup kernel be scheduled early;
+// the fixup waits for the main grid's completion (and memory) before reading anything.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 struct RollArgs {
     const uint32_t *__restrict__ bounds;
@@ -181,10 +187,21 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
     if (err) set_error(a.ws, err);
 }
 
+// state after nb words, for the fixup kernel's no-rejection case (one lane of the grid)
+__device__ __forceinline__ void publish_final(const RollArgs &a, u128 s0, u128 inc) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const u128 sf = jump(s0, inc, (uint64_t)a.nb);
+        a.ws->final_hi = sf.hi;
+        a.ws->final_lo = sf.lo;
+    }
+}
+
 template <int K>
 __global__ void __launch_bounds__(256) roll_main_kernel(RollArgs a) {
+    pdl_launch_dependents();
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
+    publish_final(a, s0, inc);
     roll_range<K, 4>(a, s0, inc, 0, a.nb, 0, false);
 }
 
@@ -212,8 +229,10 @@ __global__ void __launch_bounds__(256, 3) roll_fast_kernel(RollArgs a) {
     static_assert(32 * VB <= 128, "jump table covers 128 words");
     constexpr int U = 4;
     constexpr int64_t CH = 32 * VB * U;
+    pdl_launch_dependents();
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
+    publish_final(a, s0, inc);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -301,6 +320,7 @@ __device__ __forceinline__ void grid_barrier(RollWs *ws) {
 
 template <int K>
 __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
+    pdl_wait();
     RollWs *ws = a.ws;
     volatile RollWs *vws = ws;
     const u128 s0 = mk128(a.state[0], a.state[1]);
@@ -354,9 +374,14 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
         }
     }
     if (leader) {
-        const u128 sf = jump(s0, inc, (uint64_t)a.nb + D);
-        a.state[0] = sf.hi;
-        a.state[1] = sf.lo;
+        if (D == 0) {
+            a.state[0] = vws->final_hi;
+            a.state[1] = vws->final_lo;
+        } else {
+            const u128 sf = jump(s0, inc, (uint64_t)a.nb + D);
+            a.state[0] = sf.hi;
+            a.state[1] = sf.lo;
+        }
         ws->extra = D;
     }
 }
