@@ -186,31 +186,33 @@ def bench_c2(args, torch, B, ws, rank):
     wsp = C.c_void_p(stream.workspace.data_ptr())
     extras = torch.zeros(ws, dtype=torch.int64, device="cuda")
 
-    def step(ev_main=None):
-        N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 1, sp), "main")
-        if ev_main is not None:
-            ev_main.record()
-        N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 2, sp), "fixup")
+    def step():  # production call: main kernel + PDL-launched fixup (br_roll_batches)
+        N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 3, sp), "roll")
 
     for _ in range(args.warmup):
         step()
     soak(torch, step)
     barrier(torch, ws)
     K = args.steps
-    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    e2 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     with ClockSampler(torch.cuda.current_device()) as clk:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record()
         for i in range(K):
-            e0[i].record()
-            step(e1[i])
-            e2[i].record()
+            step()
         end.record()
         torch.cuda.synchronize()
     total_ms = start.elapsed_time(end)
+    # dominant kernel alone: the same K steps issued as two phases with CUDA events around
+    # the main kernel (roll_fast_kernel) on the launching stream
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    for i in range(K):
+        e0[i].record()
+        N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 1, sp), "main")
+        e1[i].record()
+        N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 2, sp), "fixup")
+    torch.cuda.synchronize()
     main_ms = [a.elapsed_time(b) for a, b in zip(e0, e1)]
     barrier(torch, ws)
     total_ms = max_over_ranks(torch, total_ms, ws)
@@ -229,13 +231,13 @@ def bench_c2(args, torch, B, ws, rank):
     t_main = statistics.mean(main_ms) / 1e3
     peak, peak_kind = load_peaks()
     achieved = BYTES_PER_BATCH_C2 * nb / t_main / 1e9
-    traffic = load_traffic().get("roll_main_kernel")
+    traffic = load_traffic().get("roll_fast_kernel")
     res = {
         "value": value,
         "ms_per_step": total_ms / K,
         "main_ms": statistics.mean(main_ms),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "roll_main_kernel<2>",
+                     "traffic": traffic, "kernel": "roll_fast_kernel<2>",
                      "algorithmic_bytes_per_launch": BYTES_PER_BATCH_C2 * nb, "peak_source": peak_kind},
         "clocks": clk.summary(),
         "gpu_launches": 2 * K,
