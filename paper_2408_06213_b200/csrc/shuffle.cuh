@@ -297,8 +297,8 @@ __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const
 // path.  The rest resolve Pred chains with ballots + pointer jumping and T with a
 // radix ballot over the bits of j.
 template <typename T>
-__device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t *H, uint32_t top, uint32_t lim,
-                                            int jbits, int lane) {
+__device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t *H, int8_t *P, uint32_t top,
+                                            uint32_t lim, int jbits, int lane) {
     const int64_t i64 = (int64_t)top - lane;
     const bool act = i64 >= (int64_t)lim;
     const uint32_t i = act ? (uint32_t)i64 : 0;
@@ -306,10 +306,13 @@ __device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t 
     const T vi = act ? z[i] : T(0);
     const T vj = act ? z[j] : T(0);
     const uint32_t lo_pos = top >= lim + 31 ? top - 31 : lim;
+    // round 1: every lane claims H[j]; the survivor of a repeated target is arbitrary
     if (act) H[j] = (uint8_t)lane;
+    P[lane] = -1;
     const bool inrange = act && j >= lo_pos && j < i;
     __syncwarp();
-    const bool dupl = act && H[j] != (uint8_t)lane;
+    const uint32_t w = act ? H[j] : (uint32_t)lane;
+    const bool dupl = w != (uint32_t)lane;
     const unsigned flags = __ballot_sync(FULL, inrange) | __ballot_sync(FULL, dupl);
     if (flags == 0) {  // direct path: independent swaps
         if (act) {
@@ -319,18 +322,36 @@ __device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t 
         __syncwarp();
         return;
     }
-    // Pred: lanes m with j_m == top - l  <=>  d_m == l, d_m = top - j_m
-    const uint32_t dm = top - j;
-    const bool dv = act && dm < 32;
-    unsigned pm = __ballot_sync(FULL, dv);
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-        const unsigned bq = __ballot_sync(FULL, dv && ((dm >> q) & 1));
-        pm &= ((lane >> q) & 1) ? bq : ~bq;
+    // round 2: the losers of round 1 announce themselves; the round-1 survivor learns its
+    // partner.  A loser that is overwritten again means three or more lanes share j.
+    unsigned same = 1u << lane;
+    if (__any_sync(FULL, dupl)) {
+        __syncwarp();
+        if (dupl) H[j] = (uint8_t)lane;
+        __syncwarp();
+        const uint32_t h2 = act ? H[j] : (uint32_t)lane;
+        const uint32_t partner = dupl ? w : h2;
+        const bool triple = dupl && h2 != (uint32_t)lane;
+        if (__any_sync(FULL, triple)) {  // rare: radix ballot over the bits of j
+            same = __ballot_sync(FULL, act);
+#pragma unroll 1
+            for (int q = 0; q < jbits; ++q) {
+                const unsigned bq = __ballot_sync(FULL, (j >> q) & 1u);
+                same &= ((j >> q) & 1u) ? bq : ~bq;
+            }
+            if (!act) same = 1u << lane;
+        } else {
+            same |= (1u << partner);
+        }
     }
     const unsigned below = (1u << lane) - 1u;
-    pm &= below;
-    int p = pm ? 31 - __clz(pm) : lane;
+    const unsigned tm = same & below;
+    const unsigned later = same & ~((2u << lane) - 1u);
+    // Pred(l): the last earlier lane whose target is i_l (unique writer: the last toucher of j)
+    if (inrange && later == 0) P[top - j] = (int8_t)lane;
+    __syncwarp();
+    int p = P[lane];
+    p = p >= 0 ? p : lane;
 #pragma unroll 1
     for (int it = 0; it < 5; ++it) {  // pointer jumping to the root of the Pred chain
         const int pp = __shfl_sync(FULL, p, p);
@@ -338,21 +359,8 @@ __device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t 
         p = pp;
     }
     const T A = shfl_t(vi, p);
-    // lanes sharing j (radix ballot; only groups with a repeated target need it)
-    unsigned same = 1u << lane;
-    if (__any_sync(FULL, dupl)) {
-        same = __ballot_sync(FULL, act);
-#pragma unroll 1
-        for (int q = 0; q < jbits; ++q) {
-            const unsigned bq = __ballot_sync(FULL, (j >> q) & 1u);
-            same &= ((j >> q) & 1u) ? bq : ~bq;
-        }
-        if (!act) same = 1u << lane;
-    }
-    const unsigned tm = same & below;
     const T At = shfl_t(A, tm ? 31 - __clz(tm) : lane);
     const T B = tm ? At : vj;
-    const unsigned later = same & ~((2u << lane) - 1u);
     if (act) {
         z[i] = B;
         if (later == 0 && j < lo_pos) z[j] = A;
@@ -368,6 +376,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevSeg segs[MAX_SEGS];
     __shared__ __align__(16) uint16_t ring[RING];
+    __shared__ int8_t predslot[32];
     __shared__ __align__(8) uint64_t bar;
     const int lane = threadIdx.x & 31;
     T *z = reinterpret_cast<T *>(smem_raw);
@@ -414,7 +423,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= 32) {
             const uint32_t need = top >= (int64_t)lim + 31 ? (uint32_t)top - 31 : lim;
             while (gs.frontier > need && gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
-            apply_group<T>(z, ring, H, (uint32_t)top, lim, jbits, lane);
+            apply_group<T>(z, ring, H, predslot, (uint32_t)top, lim, jbits, lane);
         }
         // finish the word accounting (a trailing rejection can follow the last position)
         while (gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
