@@ -313,6 +313,19 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);
     const uint32_t hbytes = (uint32_t)((n + 15) & ~(uint64_t)15);  // lane-id table indexed by target
     const size_t smem = (size_t)zbytes + hbytes;
+    if (n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 14) {
+        constexpr int W = 4;
+        const void *kp = (const void *)shuffle_cta_kernel<T, W>;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int grid = segmented ? grid_for(di, kp, 32 * W, smem, num_arrays) : 1;
+        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+        shuffle_cta_kernel<T, W><<<grid, 32 * W, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
+                                                           words32, state_dev, words64, rk_first, use_tma,
+                                                           segmented ? 1 : 0);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_cta_kernel<u") + std::to_string(8 * sizeof(T)) + ",4>";
+        return BR_OK;
+    }
     if (n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 30) {
         const void *kp;
         if (segmented) kp = (const void *)shuffle_mid_kernel<T, true>;

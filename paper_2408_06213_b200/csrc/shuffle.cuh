@@ -296,13 +296,13 @@ __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const
 // check through the per-array lane-id table H indexed by target): they take the direct
 // path.  The rest resolve Pred chains with ballots + pointer jumping and T with a
 // radix ballot over the bits of j.
-template <typename T>
+template <typename T, uint32_t RSIZE = RING>
 __device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t *H, int8_t *P, uint32_t top,
                                             uint32_t lim, int jbits, int lane) {
     const int64_t i64 = (int64_t)top - lane;
     const bool act = i64 >= (int64_t)lim;
     const uint32_t i = act ? (uint32_t)i64 : 0;
-    const uint32_t j = act ? (uint32_t)ring[i & (RING - 1)] : 0;
+    const uint32_t j = act ? (uint32_t)ring[i & (RSIZE - 1)] : 0;
     const T vi = act ? z[i] : T(0);
     const T vj = act ? z[j] : T(0);
     const uint32_t lo_pos = top >= lim + 31 ? top - 31 : lim;
@@ -451,6 +451,242 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
     if (use_tma && lane == 0) bulk_wait_all();
 }
 
+
+// -------------------------------------------------------------------------------------
+// one CTA (W warps) per array: groups of G = 32*W steps
+// -------------------------------------------------------------------------------------
+// Same resolution as apply_group, done across the CTA through shared memory and barriers:
+// the serial chain per array is n/G groups instead of n/32, and W warps share the target
+// generation.  Groups with three or more lanes on one target, and the bottom of the array
+// (where such groups are common), fall back to warp groups run by warp 0.
+static constexpr uint32_t CRING = 2048;
+
+template <typename T, int W>
+struct CtaShared {
+    DevSeg segs[MAX_SEGS];
+    uint16_t ring[CRING];
+    int16_t P[32 * W];
+    T VI[32 * W];
+    T AV[32 * W];
+    uint32_t fmin;
+    uint32_t frontier[2];
+    uint64_t bar;
+};
+
+template <int W>
+struct CtaGen {
+    u128 s, inc, AJ, CJ;
+    uint32_t B0, D, seg, frontier, parity;
+};
+
+template <typename T, int W>
+__device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, CtaShared<T, W> &sh, int L,
+                                             uint64_t *rk_first) {
+    constexpr int G = 32 * W;
+    const uint32_t nb = plan.nbatches;
+    const uint32_t b = g.B0 + L;
+    bool fail = false;
+    uint32_t low = 0xFFFFFFFFu;
+    if (b < nb) {
+        uint32_t sg = g.seg;
+        while (sg + 1 < plan.nseg && sh.segs[sg + 1].first_batch <= b) ++sg;
+        const DevSeg S = sh.segs[sg];
+        const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
+        const uint64_t t = __ldg(plan.thresh + b);
+        uint64_t r = xslrr(g.s);
+        const uint32_t pos = nbb - 1;
+        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (CRING - 1)] = (uint16_t)die(nbb - m, r);
+        low = nbb - S.k;
+        fail = r < t;
+        if (rk_first && b == 0 && g.D == 0) *rk_first = r;
+    }
+    const uint32_t nact = nb - g.B0 < (uint32_t)G ? nb - g.B0 : (uint32_t)G;
+    const uint32_t par = g.parity;
+    g.parity ^= 1u;
+    if (L == (int)nact - 1) sh.frontier[par] = low;  // frontier if nothing is rejected
+    if (!__syncthreads_or(fail)) {
+        g.frontier = sh.frontier[par];
+        g.B0 += G;
+        g.s = mad128(g.s, g.AJ, g.CJ);
+    } else {  // rare: find the first rejected lane, commit the lanes before it
+        if (L == 0) sh.fmin = G;
+        __syncthreads();
+        if (fail) atomicMin(&sh.fmin, (uint32_t)L);
+        __syncthreads();
+        const uint32_t f = sh.fmin;
+        if (f > 0 && L == (int)f - 1) sh.frontier[par] = low;
+        __syncthreads();
+        if (f > 0) g.frontier = sh.frontier[par];
+        g.B0 += f;
+        g.D += 1;
+        g.s = jump_small(g.s, g.inc, (int)f + 1);
+        __syncthreads();  // fmin / frontier reuse
+    }
+    while (g.seg + 1 < plan.nseg && sh.segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
+}
+
+// returns false if the group must be redone with warp groups (three+ lanes on a target)
+template <typename T, int W>
+__device__ __forceinline__ bool apply_group_cta(T *z, uint8_t *H, CtaShared<T, W> &sh, uint32_t top, uint32_t lim,
+                                                int L) {
+    constexpr int G = 32 * W;
+    const int64_t i64 = (int64_t)top - L;
+    const bool act = i64 >= (int64_t)lim;
+    const uint32_t i = act ? (uint32_t)i64 : 0;
+    const uint32_t j = act ? (uint32_t)sh.ring[i & (CRING - 1)] : 0;
+    const T vi = act ? z[i] : T(0);
+    const T vj = act ? z[j] : T(0);
+    const uint32_t lo_pos = top >= lim + (G - 1) ? top - (G - 1) : lim;
+    sh.VI[L] = vi;
+    sh.P[L] = -1;
+    if (act) H[j] = (uint8_t)L;
+    const bool inrange = act && j >= lo_pos && j < i;
+    __syncthreads();
+    const uint32_t w = act ? H[j] : (uint32_t)L;
+    const bool dupl = w != (uint32_t)L;
+    if (!__syncthreads_or(dupl || inrange)) {  // direct path
+        if (act) {
+            z[i] = vj;
+            z[j] = vi;
+        }
+        __syncthreads();
+        return true;
+    }
+    int partner = L;
+    if (__syncthreads_or(dupl)) {
+        if (dupl) H[j] = (uint8_t)L;
+        __syncthreads();
+        const uint32_t h2 = act ? H[j] : (uint32_t)L;
+        partner = dupl ? (int)w : (int)h2;
+        const bool triple = dupl && h2 != (uint32_t)L;
+        if (__syncthreads_or(triple)) return false;
+    }
+    const int tl = partner < L ? partner : -1;
+    const bool later = partner > L;
+    if (inrange && !later) sh.P[top - j] = (int16_t)L;
+    __syncthreads();
+    int p = sh.P[L];
+    p = p >= 0 ? p : L;
+    // pointer jumping to the root of the Pred chain (P holds the chain links)
+    for (;;) {
+        const int pp = sh.P[p];
+        const int np = pp >= 0 ? pp : p;
+        if (!__syncthreads_or(np != p)) break;
+        p = np;
+    }
+    const T A = sh.VI[p];
+    sh.AV[L] = A;
+    __syncthreads();
+    const T B = tl >= 0 ? sh.AV[tl] : vj;
+    if (act) {
+        z[i] = B;
+        if (!later && j < lo_pos) z[j] = A;
+    }
+    __syncthreads();
+    return true;
+}
+
+template <typename T, int W>
+__global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
+                                                             uint32_t zbytes, uint64_t run_seed, int64_t base,
+                                                             uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                             uint64_t *words64, uint64_t *rk_first, int use_tma,
+                                                             int segmented) {
+    constexpr int G = 32 * W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ CtaShared<T, W> sh;
+    const int L = threadIdx.x;
+    const int lane = L & 31, warp = L >> 5;
+    T *z = reinterpret_cast<T *>(smem_raw);
+    uint8_t *H = smem_raw + zbytes;
+    for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
+    if (use_tma && L == 0) mbar_init(&sh.bar, 1);
+    __syncthreads();
+    const uint32_t n = plan.n;
+    const uint32_t bytes = n * (uint32_t)sizeof(T);
+    const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
+    const int jbits = n > 1 ? 32 - __clz(n - 1) : 1;
+    const uint32_t warp_below = 4 * G;  // below this position warp groups do the apply
+    uint32_t parity = 0;
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        T *g = data + a * (int64_t)n;
+        if (use_tma) {
+            if (L == 0) {
+                bulk_wait_read();
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&sh.bar, bytes);
+                bulk_load(z, g, bytes, &sh.bar);
+            }
+        } else {
+            for (uint32_t e = L; e < n; e += G) z[e] = g[e];
+        }
+        u128 s0, inc;
+        if (segmented) {
+            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+        } else {
+            s0 = mk128(state_io[0], state_io[1]);
+            inc = mk128(state_io[2], state_io[3]);
+        }
+        CtaGen<W> gs;
+        gs.inc = inc;
+        gs.s = jump_small(s0, inc, L + 1);
+        gs.AJ = g_SA[G];
+        gs.CJ = mul128(g_SG[G], inc);
+        gs.B0 = 0;
+        gs.D = 0;
+        gs.seg = 0;
+        gs.frontier = n;
+        gs.parity = 0;
+        uint64_t *rkf = segmented ? nullptr : rk_first;
+        if (plan.nbatches) cta_gen_step<T, W>(gs, plan, sh, L, rkf);
+        if (use_tma) {
+            mbar_wait(&sh.bar, parity);
+            parity ^= 1u;
+        }
+        __syncthreads();
+        int64_t top = (int64_t)n - 1;
+        for (; top >= (int64_t)lim && top >= (int64_t)warp_below; top -= G) {
+            const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
+            while (gs.frontier > need && gs.B0 < plan.nbatches) cta_gen_step<T, W>(gs, plan, sh, L, rkf);
+            if (!apply_group_cta<T, W>(z, H, sh, (uint32_t)top, lim, L)) {
+                // three or more lanes share a target: redo this group as W warp groups, in order
+                for (int w = 0; w < W; ++w) {
+                    const int64_t t2 = top - 32 * w;
+                    if (warp == 0 && t2 >= (int64_t)lim)
+                        apply_group<T, CRING>(z, sh.ring, H, reinterpret_cast<int8_t *>(sh.P), (uint32_t)t2, lim, jbits, lane);
+                    __syncthreads();
+                }
+            }
+        }
+        // bottom of the array: all remaining targets, then warp groups by warp 0
+        while (gs.B0 < plan.nbatches) cta_gen_step<T, W>(gs, plan, sh, L, rkf);
+        if (warp == 0)
+            for (; top >= (int64_t)lim; top -= 32)
+                apply_group<T, CRING>(z, sh.ring, H, reinterpret_cast<int8_t *>(sh.P), (uint32_t)top, lim, jbits, lane);
+        __syncthreads();
+        if (use_tma) {
+            if (L == 0) {
+                fence_proxy_async();
+                bulk_store(g, z, bytes);
+            }
+        } else {
+            for (uint32_t e = L; e < n; e += G) g[e] = z[e];
+        }
+        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
+        if (L == 0) {
+            if (segmented) {
+                if (words32) words32[a] = (uint32_t)words;
+            } else {
+                const u128 sf = jump(s0, inc, words);
+                state_io[0] = sf.hi;
+                state_io[1] = sf.lo;
+                if (words64) words64[0] = words;
+            }
+        }
+        __syncthreads();
+    }
+    if (use_tma && L == 0) bulk_wait_all();
+}
 
 // -------------------------------------------------------------------------------------
 // arrays larger than shared memory: targets into a global buffer, then warp-group apply
