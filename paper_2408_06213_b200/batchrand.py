@@ -154,6 +154,34 @@ def threshold(bound: BoundEncoding) -> int:
     return neg % bound.value
 
 
+class RollOutcome(NamedTuple):
+    """bounded.py:65-70."""
+
+    value: int
+    words_consumed: int
+    remainder_ops: int
+
+
+def roll_single_traced(source, bound) -> RollOutcome:
+    """bounded.py:73-99 on the device: a single Lemire roll is a k=1 batch (same acceptance
+    rule, lo >= 2^64 mod b); remainder_ops = 1 iff the first low word fell below b."""
+    if isinstance(bound, BoundEncoding):
+        bits, b = bound.bits, bound.value
+    else:
+        bits, b = getattr(source, "word_bits", 64), bound
+        if not 1 <= b <= 1 << bits:
+            raise BoundOverflow(f"bound {b} not in [1, 2**{bits}]")
+    if bits != 64:
+        raise TypeError("the device path needs 64-bit words")
+    r = _roll_one(source, BatchSpec(RadixBases.of((b,), 64)))
+    return RollOutcome(r.digits[0], r.words_consumed, int(r.threshold_computed))
+
+
+def roll_single(source, bound) -> int:
+    """bounded.py:102-104."""
+    return roll_single_traced(source, bound).value
+
+
 def falling_factorial(n: int, k: int, bits: int = 64) -> int:
     """bounded.py:107-119."""
     if k < 0 or k > n:
@@ -647,6 +675,7 @@ def last_kernel() -> str:
 
 __all__ = [
     "BatchRandError", "BatchResult", "BatchSpec", "BoundEncoding", "BoundOverflow", "DEFAULT_SCHEDULE",
+    "RollOutcome", "roll_single", "roll_single_traced",
     "DigitOutOfRange", "DeviceStream", "FullProduct", "PAIR_SCHEDULE", "Pcg64Source", "RadixBases",
     "RollBatchesResult", "ShuffleSchedule", "SourceExhausted", "UnknownGenerator", "ValueOutOfRange",
     "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",

@@ -393,3 +393,15 @@ def test_large_stream_and_segmented_vs_oracle(B, O, n):
     ref = np.tile(np.arange(n, dtype=np.uint32), 3)
     rw = O.shuffle_segmented(ref, n, 11, array_index_base=7)
     assert np.array_equal(u32(data), ref) and np.array_equal(u32(w), rw)
+
+
+def test_roll_single_dropin(B, O):  # bounded.py:73-104 via the k=1 batch kernel
+    for seed, bound in ((1, 6), (2, 52), (3, (1 << 32) - 1), (4, 3 << 30), (5, 1)):
+        s, o = B.Pcg64Source(seed), O.pcg64(seed)
+        for _ in range(20):
+            v, w, ro = O.roll_single(o, bound)
+            r = B.roll_single_traced(s, bound)
+            assert (r.value, r.words_consumed, r.remainder_ops) == (v, w, ro)
+        assert s.state == o.state
+    with pytest.raises(B.BoundOverflow):
+        B.roll_single(B.Pcg64Source(1), 0)
