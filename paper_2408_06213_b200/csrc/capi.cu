@@ -296,15 +296,16 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
                    uint64_t run_seed, int64_t base, uint32_t *words32, uint64_t *state_dev, uint64_t *words64,
                    uint64_t *rk_first, const DeviceInfo &di, cudaStream_t st) {
     const uint32_t stride = (uint32_t)(n | 1u);
-    const size_t small_smem = (size_t)128 * stride * sizeof(T);
-    if (segmented && cp.plan.max_k <= 8 && small_smem <= SMALL_SMEM_MAX) {
+    const int tpb = 64;  // 2 warps: many small blocks per SM overlap their load/compute/store phases
+    const size_t small_smem = (size_t)tpb * stride * sizeof(T);
+    if (segmented && cp.plan.max_k <= 8 && small_smem <= SMALL_SMEM_MAX / 2) {
         auto kern = shuffle_small_kernel<T>;
         CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
-        int64_t blocks = (num_arrays + 127) / 128;
+        int64_t blocks = (num_arrays + tpb - 1) / tpb;
         // q / n == umulhi(q, ceil(2^32 / n)) exactly for q < 2^32 / n (spans are < 2^16 elements)
         const uint32_t magic = (uint32_t)((((uint64_t)1 << 32) + n - 1) / n);
         const int vec_ok = ((n * sizeof(T)) % 16 == 0 && ((uintptr_t)data & 15) == 0) ? 1 : 0;
-        kern<<<(unsigned)blocks, 128, small_smem, st>>>((T *)data, num_arrays, cp.plan, stride, magic, vec_ok, run_seed,
+        kern<<<(unsigned)blocks, tpb, small_smem, st>>>((T *)data, num_arrays, cp.plan, stride, magic, vec_ok, run_seed,
                                                         base, words32);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_small_kernel<u") + std::to_string(8 * sizeof(T)) + ">";

@@ -92,7 +92,7 @@ template <typename T>
 __device__ __forceinline__ void small_copy(T *buf, T *g, uint32_t span, uint32_t n, uint32_t stride, uint32_t t0,
                                            uint32_t magic, int lane, bool to_smem, bool vec_ok) {
     constexpr uint32_t V = 16 / sizeof(T);
-    constexpr int U = 4;
+    constexpr int U = 16;  // a warp's whole 8 KB span (n=64 u32) in flight at once
     if (vec_ok) {
         const uint32_t nv = span / V;
         for (uint32_t q0 = 0; q0 < nv; q0 += 32 * U) {
