@@ -290,6 +290,9 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
 
 constexpr uint32_t SMALL_SMEM_MAX = 64 * 1024;   // per 128-thread block
 constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
+#ifndef LARGE_W
+#define LARGE_W 8
+#endif
 
 template <typename T>
 int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan &cp, bool segmented,
@@ -344,7 +347,19 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
     }
-    // large arrays: targets (u32 per position) into stream-ordered scratch, then the apply
+    // large arrays: one CTA per array, targets generated in-CTA, array in global memory
+    if ((uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= CRING) {
+        constexpr int W = LARGE_W;
+        const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
+        shuffle_cta_large_kernel<T, W><<<grid, 32 * W, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base,
+                                                                  words32, state_dev, words64, rk_first,
+                                                                  segmented ? 1 : 0);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_cta_large_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
+                   std::to_string(W) + ">";
+        return BR_OK;
+    }
+    // large arrays, exotic schedules: targets (u32 per position) into scratch, then warp-group apply
     {
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(num_arrays, (int64_t)((1ull << 31) / (n * 4))));
         uint32_t *J = nullptr;

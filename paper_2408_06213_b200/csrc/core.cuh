@@ -152,7 +152,7 @@ __host__ __device__ __forceinline__ uint64_t threshold64(uint64_t b) { return b 
 // Jump tables: A_d = M^d, G_d = sum_{i<d} M^i so that state_{t+d} = A_d*state_t + G_d*inc.
 struct JumpTables {
     u128 A[64], G[64];       // d = 2^k
-    u128 SA[129], SG[129];   // d = 0..128 (lane offsets / small realignments)
+    u128 SA[257], SG[257];   // d = 0..256 (lane offsets / small realignments)
 };
 
 // Host construction (also used by the C-ABI host helpers)
@@ -168,7 +168,7 @@ inline void build_jump_tables(JumpTables &t) {
     }
     u128 a = mk128(0, 1), gg = mk128(0, 0);
     u128 M = mk128(PCG_MULT_HI, PCG_MULT_LO);
-    for (int d = 0; d <= 128; ++d) {
+    for (int d = 0; d <= 256; ++d) {
         t.SA[d] = a;
         t.SG[d] = gg;
         gg = add128(mul128(M, gg), mk128(0, 1));  // G_{d+1} = M*G_d + 1

@@ -226,7 +226,7 @@ template <int K, bool FLAGS, bool RK>
 __global__ void __launch_bounds__(256, 3) roll_fast_kernel(RollArgs a) {
     static_assert(K == 1 || K == 2, "fast path is for k <= 2");
     constexpr int VB = 4 / K;
-    static_assert(32 * VB <= 128, "jump table covers 128 words");
+    static_assert(32 * VB <= 256, "jump table covers 256 words");
     constexpr int U = 4;
     constexpr int64_t CH = 32 * VB * U;
     pdl_launch_dependents();

@@ -92,7 +92,7 @@ template <typename T>
 __device__ __forceinline__ void small_copy(T *buf, T *g, uint32_t span, uint32_t n, uint32_t stride, uint32_t t0,
                                            uint32_t magic, int lane, bool to_smem, bool vec_ok) {
     constexpr uint32_t V = 16 / sizeof(T);
-    constexpr int U = 16;  // a warp's whole 8 KB span (n=64 u32) in flight at once
+    constexpr int U = 8;  // half a warp span (n=64 u32) in flight per round
     if (vec_ok) {
         const uint32_t nv = span / V;
         for (uint32_t q0 = 0; q0 < nv; q0 += 32 * U) {
@@ -461,10 +461,10 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
 // (where such groups are common), fall back to warp groups run by warp 0.
 static constexpr uint32_t CRING = 2048;
 
-template <typename T, int W>
+template <typename T, int W, typename RT = uint16_t>
 struct CtaShared {
     DevSeg segs[MAX_SEGS];
-    uint16_t ring[CRING];
+    RT ring[CRING];
     int16_t P[32 * W];
     T VI[32 * W];
     T AV[32 * W];
@@ -479,8 +479,8 @@ struct CtaGen {
     uint32_t B0, D, seg, frontier, parity;
 };
 
-template <typename T, int W>
-__device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, CtaShared<T, W> &sh, int L,
+template <typename T, int W, typename RT>
+__device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, CtaShared<T, W, RT> &sh, int L,
                                              uint64_t *rk_first) {
     constexpr int G = 32 * W;
     const uint32_t nb = plan.nbatches;
@@ -495,7 +495,7 @@ __device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, 
         const uint64_t t = __ldg(plan.thresh + b);
         uint64_t r = xslrr(g.s);
         const uint32_t pos = nbb - 1;
-        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (CRING - 1)] = (uint16_t)die(nbb - m, r);
+        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (CRING - 1)] = (RT)die(nbb - m, r);
         low = nbb - S.k;
         fail = r < t;
         if (rk_first && b == 0 && g.D == 0) *rk_first = r;
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
         gs.frontier = n;
         gs.parity = 0;
         uint64_t *rkf = segmented ? nullptr : rk_first;
-        if (plan.nbatches) cta_gen_step<T, W>(gs, plan, sh, L, rkf);
+        if (plan.nbatches) cta_gen_step<T, W, uint16_t>(gs, plan, sh, L, rkf);
         if (use_tma) {
             mbar_wait(&sh.bar, parity);
             parity ^= 1u;
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
         int64_t top = (int64_t)n - 1;
         for (; top >= (int64_t)lim && top >= (int64_t)warp_below; top -= G) {
             const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) cta_gen_step<T, W>(gs, plan, sh, L, rkf);
+            while (gs.frontier > need && gs.B0 < plan.nbatches) cta_gen_step<T, W, uint16_t>(gs, plan, sh, L, rkf);
             if (!apply_group_cta<T, W>(z, H, sh, (uint32_t)top, lim, L)) {
                 // three or more lanes share a target: redo this group as W warp groups, in order
                 for (int w = 0; w < W; ++w) {
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
             }
         }
         // bottom of the array: all remaining targets, then warp groups by warp 0
-        while (gs.B0 < plan.nbatches) cta_gen_step<T, W>(gs, plan, sh, L, rkf);
+        while (gs.B0 < plan.nbatches) cta_gen_step<T, W, uint16_t>(gs, plan, sh, L, rkf);
         if (warp == 0)
             for (; top >= (int64_t)lim; top -= 32)
                 apply_group<T, CRING>(z, sh.ring, H, reinterpret_cast<int8_t *>(sh.P), (uint32_t)top, lim, jbits, lane);
@@ -686,6 +686,132 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
         __syncthreads();
     }
     if (use_tma && L == 0) bulk_wait_all();
+}
+
+// -------------------------------------------------------------------------------------
+// arrays in global memory: one CTA (W warps) per array, groups of G = 32*W steps
+// -------------------------------------------------------------------------------------
+// Targets are generated in-CTA into a u32 ring (no global target buffer).  Repeated
+// targets are found exactly with one ballot per bit of j in every warp; lane L combines the
+// W*jbits masks through shared memory, which yields T(L) and "later" for any multiplicity.
+template <typename T, int W>
+__device__ __forceinline__ void apply_group_cta_global(T *z, CtaShared<T, W, uint32_t> &sh, unsigned (*Bm)[33],
+                                                       uint32_t top, uint32_t lim, int jbits, int L) {
+    constexpr int G = 32 * W;
+    const int lane = L & 31, warp = L >> 5;
+    const int64_t i64 = (int64_t)top - L;
+    const bool act = i64 >= (int64_t)lim;
+    const uint32_t i = act ? (uint32_t)i64 : 0;
+    const uint32_t j = act ? sh.ring[i & (CRING - 1)] : 0;
+    const T vi = act ? z[i] : T(0);
+    const T vj = act ? z[j] : T(0);
+    const uint32_t lo_pos = top >= lim + (G - 1) ? top - (G - 1) : lim;
+    const bool inrange = act && j >= lo_pos && j < i;
+    // per-warp bit ballots of j (and the active mask in slot 32)
+    for (int q = 0; q < jbits; ++q) {
+        const unsigned bq = __ballot_sync(FULL, (j >> q) & 1u);
+        if (lane == 0) Bm[warp * 32 + q][0] = bq;
+    }
+    const unsigned am = __ballot_sync(FULL, act);
+    if (lane == 0) Bm[warp * 32][32] = am;
+    sh.P[L] = -1;
+    sh.VI[L] = vi;
+    __syncthreads();
+    int tl = -1;
+    bool later = false;
+    if (act) {
+        for (int w = W - 1; w >= 0; --w) {
+            unsigned eq = Bm[w * 32][32];
+            for (int q = 0; q < jbits; ++q) {
+                const unsigned bq = Bm[w * 32 + q][0];
+                eq &= ((j >> q) & 1u) ? bq : ~bq;
+            }
+            if (w == warp) {
+                const unsigned below = (1u << lane) - 1u;
+                if (eq & ~below & ~(1u << lane)) later = true;
+                eq &= below;
+            } else if (w > warp) {
+                if (eq) later = true;
+                eq = 0;
+            }
+            if (tl < 0 && eq) tl = w * 32 + 31 - __clz(eq);
+        }
+    }
+    if (inrange && !later) sh.P[top - j] = (int16_t)L;
+    __syncthreads();
+    int p = sh.P[L];
+    p = p >= 0 ? p : L;
+    for (;;) {
+        const int pp = sh.P[p];
+        const int np = pp >= 0 ? pp : p;
+        if (!__syncthreads_or(np != p)) break;
+        p = np;
+    }
+    const T A = sh.VI[p];
+    sh.AV[L] = A;
+    __syncthreads();
+    const T B = tl >= 0 ? sh.AV[tl] : vj;
+    if (act) {
+        z[i] = B;
+        if (!later && j < lo_pos) z[j] = A;
+    }
+    __syncthreads();
+}
+
+template <typename T, int W>
+__global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                   DevPlan plan, uint64_t run_seed, int64_t base,
+                                                                   uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                                   uint64_t *words64, uint64_t *rk_first,
+                                                                   int segmented) {
+    constexpr int G = 32 * W;
+    __shared__ CtaShared<T, W, uint32_t> sh;
+    __shared__ unsigned Bm[32 * W][33];
+    const int L = threadIdx.x;
+    for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
+    __syncthreads();
+    const uint32_t n = plan.n;
+    const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
+    const int jbits = n > 1 ? 32 - __clz(n - 1) : 1;
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        T *z = data + a * (int64_t)n;
+        u128 s0, inc;
+        if (segmented) {
+            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+        } else {
+            s0 = mk128(state_io[0], state_io[1]);
+            inc = mk128(state_io[2], state_io[3]);
+        }
+        CtaGen<W> gs;
+        gs.inc = inc;
+        gs.s = jump_small(s0, inc, L + 1);
+        gs.AJ = g_SA[G];
+        gs.CJ = mul128(g_SG[G], inc);
+        gs.B0 = 0;
+        gs.D = 0;
+        gs.seg = 0;
+        gs.frontier = n;
+        gs.parity = 0;
+        uint64_t *rkf = segmented ? nullptr : rk_first;
+        for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= G) {
+            const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
+            while (gs.frontier > need && gs.B0 < plan.nbatches) cta_gen_step<T, W, uint32_t>(gs, plan, sh, L, rkf);
+            apply_group_cta_global<T, W>(z, sh, Bm, (uint32_t)top, lim, jbits, L);
+        }
+        while (gs.B0 < plan.nbatches) cta_gen_step<T, W, uint32_t>(gs, plan, sh, L, rkf);
+        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
+        if (L == 0) {
+            if (segmented) {
+                if (words32) words32[a] = (uint32_t)words;
+            } else {
+                const u128 sf = jump(s0, inc, words);
+                state_io[0] = sf.hi;
+                state_io[1] = sf.lo;
+                if (words64) words64[0] = words;
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // -------------------------------------------------------------------------------------

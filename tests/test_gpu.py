@@ -362,7 +362,7 @@ def test_c5_sample_vs_golden_and_oracle(B, O, golden):
     payload = O.pcg64_fill(O.pcg64(5), 0, n * na)  # C5 payload convention: words of pcg64(5)
     dev = torch.from_numpy(payload.view(np.int64).copy()).cuda()
     _, words = B.shuffle_many(dev, n, 5, return_words=True)
-    assert "shuffle_large" in B.last_kernel()
+    assert "shuffle_cta_large" in B.last_kernel()
     got = dev.cpu().numpy().view(np.uint64)
     ref = payload.copy()
     rw = O.shuffle_segmented(ref, n, 5)
