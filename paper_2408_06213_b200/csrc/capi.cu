@@ -348,7 +348,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         return BR_OK;
     }
     // large arrays: one CTA per array, targets generated in-CTA, array in global memory
-    if ((uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= CRING) {
+    if ((uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= LRING) {
         constexpr int W = LARGE_W;
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
         shuffle_cta_large_kernel<T, W><<<grid, 32 * W, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base,

@@ -694,47 +694,56 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
 // Targets are generated in-CTA into a u32 ring (no global target buffer).  Repeated
 // targets are found exactly with one ballot per bit of j in every warp; lane L combines the
 // W*jbits masks through shared memory, which yields T(L) and "later" for any multiplicity.
+static constexpr uint32_t LRING = 4096;  // u32 target ring of the large kernel
+static constexpr int HBITS = 11;          // 2048-slot lane-chain hash per group
+
 template <typename T, int W>
-__device__ __forceinline__ void apply_group_cta_global(T *z, CtaShared<T, W, uint32_t> &sh, unsigned (*Bm)[33],
-                                                       uint32_t top, uint32_t lim, int jbits, int L) {
+struct LargeShared {
+    DevSeg segs[MAX_SEGS];
+    uint32_t ring[LRING];
+    uint32_t ht[1 << HBITS];  // (group tag << 16) | (lane + 1) of the last lane hashed here
+    int16_t nxt[32 * W];      // previous lane in the same slot (-1: none)
+    uint32_t jv[32 * W];
+    int16_t P[32 * W];
+    T VI[32 * W];
+    T AV[32 * W];
+    uint32_t fmin;
+    uint32_t frontier[2];
+};
+
+template <typename T, int W>
+__device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W> &sh, uint32_t tag, uint32_t top,
+                                                       uint32_t lim, int L) {
     constexpr int G = 32 * W;
-    const int lane = L & 31, warp = L >> 5;
     const int64_t i64 = (int64_t)top - L;
     const bool act = i64 >= (int64_t)lim;
     const uint32_t i = act ? (uint32_t)i64 : 0;
-    const uint32_t j = act ? sh.ring[i & (CRING - 1)] : 0;
+    const uint32_t j = act ? sh.ring[i & (LRING - 1)] : 0;
     const T vi = act ? z[i] : T(0);
     const T vj = act ? z[j] : T(0);
     const uint32_t lo_pos = top >= lim + (G - 1) ? top - (G - 1) : lim;
     const bool inrange = act && j >= lo_pos && j < i;
-    // per-warp bit ballots of j (and the active mask in slot 32)
-    for (int q = 0; q < jbits; ++q) {
-        const unsigned bq = __ballot_sync(FULL, (j >> q) & 1u);
-        if (lane == 0) Bm[warp * 32 + q][0] = bq;
+    // lanes with equal targets meet in a hash slot; each slot keeps a chain of its lanes
+    const uint32_t h = (j * 2654435761u) >> (32 - HBITS);
+    int16_t link = -1;
+    if (act) {
+        const uint32_t old = atomicExch(&sh.ht[h], (tag << 16) | (uint32_t)(L + 1));
+        if ((old >> 16) == tag) link = (int16_t)((old & 0xFFFFu) - 1);
     }
-    const unsigned am = __ballot_sync(FULL, act);
-    if (lane == 0) Bm[warp * 32][32] = am;
+    sh.nxt[L] = link;
+    sh.jv[L] = j;
     sh.P[L] = -1;
     sh.VI[L] = vi;
     __syncthreads();
     int tl = -1;
     bool later = false;
     if (act) {
-        for (int w = W - 1; w >= 0; --w) {
-            unsigned eq = Bm[w * 32][32];
-            for (int q = 0; q < jbits; ++q) {
-                const unsigned bq = Bm[w * 32 + q][0];
-                eq &= ((j >> q) & 1u) ? bq : ~bq;
+        const uint32_t head = sh.ht[h];
+        for (int t = (int)(head & 0xFFFFu) - 1; t >= 0; t = sh.nxt[t]) {
+            if (t != L && sh.jv[t] == j) {
+                if (t < L) tl = t > tl ? t : tl;
+                else later = true;
             }
-            if (w == warp) {
-                const unsigned below = (1u << lane) - 1u;
-                if (eq & ~below & ~(1u << lane)) later = true;
-                eq &= below;
-            } else if (w > warp) {
-                if (eq) later = true;
-                eq = 0;
-            }
-            if (tl < 0 && eq) tl = w * 32 + 31 - __clz(eq);
         }
     }
     if (inrange && !later) sh.P[top - j] = (int16_t)L;
@@ -759,20 +768,66 @@ __device__ __forceinline__ void apply_group_cta_global(T *z, CtaShared<T, W, uin
 }
 
 template <typename T, int W>
+__device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan, LargeShared<T, W> &sh, int L,
+                                               uint64_t *rk_first) {
+    constexpr int G = 32 * W;
+    const uint32_t nb = plan.nbatches;
+    const uint32_t b = g.B0 + L;
+    bool fail = false;
+    uint32_t low = 0xFFFFFFFFu;
+    if (b < nb) {
+        uint32_t sg = g.seg;
+        while (sg + 1 < plan.nseg && sh.segs[sg + 1].first_batch <= b) ++sg;
+        const DevSeg S = sh.segs[sg];
+        const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
+        const uint64_t t = __ldg(plan.thresh + b);
+        uint64_t r = xslrr(g.s);
+        const uint32_t pos = nbb - 1;
+        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (LRING - 1)] = die(nbb - m, r);
+        low = nbb - S.k;
+        fail = r < t;
+        if (rk_first && b == 0 && g.D == 0) *rk_first = r;
+    }
+    const uint32_t nact = nb - g.B0 < (uint32_t)G ? nb - g.B0 : (uint32_t)G;
+    const uint32_t par = g.parity;
+    g.parity ^= 1u;
+    if (L == (int)nact - 1) sh.frontier[par] = low;
+    if (!__syncthreads_or(fail)) {
+        g.frontier = sh.frontier[par];
+        g.B0 += G;
+        g.s = mad128(g.s, g.AJ, g.CJ);
+    } else {
+        if (L == 0) sh.fmin = G;
+        __syncthreads();
+        if (fail) atomicMin(&sh.fmin, (uint32_t)L);
+        __syncthreads();
+        const uint32_t f = sh.fmin;
+        if (f > 0 && L == (int)f - 1) sh.frontier[par] = low;
+        __syncthreads();
+        if (f > 0) g.frontier = sh.frontier[par];
+        g.B0 += f;
+        g.D += 1;
+        g.s = jump_small(g.s, g.inc, (int)f + 1);
+        __syncthreads();
+    }
+    while (g.seg + 1 < plan.nseg && sh.segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
+}
+
+template <typename T, int W>
 __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict__ data, int64_t num_arrays,
                                                                    DevPlan plan, uint64_t run_seed, int64_t base,
                                                                    uint32_t *__restrict__ words32, uint64_t *state_io,
                                                                    uint64_t *words64, uint64_t *rk_first,
                                                                    int segmented) {
     constexpr int G = 32 * W;
-    __shared__ CtaShared<T, W, uint32_t> sh;
-    __shared__ unsigned Bm[32 * W][33];
+    __shared__ LargeShared<T, W> sh;
     const int L = threadIdx.x;
     for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
+    for (uint32_t q = L; q < (1u << HBITS); q += G) sh.ht[q] = 0;
     __syncthreads();
+    uint32_t tag = 0;
     const uint32_t n = plan.n;
     const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
-    const int jbits = n > 1 ? 32 - __clz(n - 1) : 1;
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         T *z = data + a * (int64_t)n;
         u128 s0, inc;
@@ -795,10 +850,16 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
         uint64_t *rkf = segmented ? nullptr : rk_first;
         for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= G) {
             const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) cta_gen_step<T, W, uint32_t>(gs, plan, sh, L, rkf);
-            apply_group_cta_global<T, W>(z, sh, Bm, (uint32_t)top, lim, jbits, L);
+            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step<T, W>(gs, plan, sh, L, rkf);
+            tag = (tag + 1) & 0xFFFFu;
+            if (tag == 0) {  // tag wrap: clear the slots (every 65535 groups)
+                for (uint32_t q = L; q < (1u << HBITS); q += G) sh.ht[q] = 0;
+                tag = 1;
+                __syncthreads();
+            }
+            apply_group_cta_global<T, W>(z, sh, tag, (uint32_t)top, lim, L);
         }
-        while (gs.B0 < plan.nbatches) cta_gen_step<T, W, uint32_t>(gs, plan, sh, L, rkf);
+        while (gs.B0 < plan.nbatches) large_gen_step<T, W>(gs, plan, sh, L, rkf);
         const uint64_t words = (uint64_t)plan.nbatches + gs.D;
         if (L == 0) {
             if (segmented) {
