@@ -293,6 +293,9 @@ constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 #ifndef LARGE_W
 #define LARGE_W 8
 #endif
+#ifndef CTA_W
+#define CTA_W 4
+#endif
 
 template <typename T>
 int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan &cp, bool segmented,
@@ -317,17 +320,19 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);
     const uint32_t hbytes = (uint32_t)((n + 15) & ~(uint64_t)15);  // lane-id table indexed by target
     const size_t smem = (size_t)zbytes + hbytes;
-    if (n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 14) {
-        constexpr int W = 4;
-        const void *kp = (const void *)shuffle_cta_kernel<T, W>;
-        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int grid = segmented ? grid_for(di, kp, 32 * W, smem, num_arrays) : 1;
+    const size_t csmem = (size_t)zbytes;  // payload only; the rest is static
+    if (n < 65536 && csmem <= MID_SMEM_MAX && (uint64_t)cp.plan.max_k * 32 * CTA_W + 32 * CTA_W <= CRING) {
+        constexpr int W = CTA_W;
+        const void *kp = (const void *)shuffle_cta_hash_kernel<T, W>;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+        int grid = segmented ? grid_for(di, kp, 32 * W, csmem, num_arrays) : 1;
         const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
-        shuffle_cta_kernel<T, W><<<grid, 32 * W, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
-                                                           words32, state_dev, words64, rk_first, use_tma,
-                                                           segmented ? 1 : 0);
+        shuffle_cta_hash_kernel<T, W><<<grid, 32 * W, csmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base,
+                                                                 words32, state_dev, words64, rk_first, use_tma,
+                                                                 segmented ? 1 : 0);
         CK(cudaGetLastError());
-        g_kernel = std::string("shuffle_cta_kernel<u") + std::to_string(8 * sizeof(T)) + ",4>";
+        g_kernel = std::string("shuffle_cta_hash_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
+                   std::to_string(W) + ">";
         return BR_OK;
     }
     if (n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 30) {

@@ -697,11 +697,11 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
 static constexpr uint32_t LRING = 4096;  // u32 target ring of the large kernel
 static constexpr int HBITS = 11;          // 2048-slot lane-chain hash per group
 
-template <typename T, int W>
+template <typename T, int W, typename RT = uint32_t, uint32_t RS = LRING, int HB = HBITS>
 struct LargeShared {
     DevSeg segs[MAX_SEGS];
-    uint32_t ring[LRING];
-    uint32_t ht[1 << HBITS];  // (group tag << 16) | (lane + 1) of the last lane hashed here
+    RT ring[RS];
+    uint32_t ht[1 << HB];  // (group tag << 16) | (lane + 1) of the last lane hashed here
     int16_t nxt[32 * W];      // previous lane in the same slot (-1: none)
     uint32_t jv[32 * W];
     int16_t P[32 * W];
@@ -711,20 +711,20 @@ struct LargeShared {
     uint32_t frontier[2];
 };
 
-template <typename T, int W>
-__device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W> &sh, uint32_t tag, uint32_t top,
-                                                       uint32_t lim, int L) {
+template <typename T, int W, typename RT, uint32_t RS, int HB>
+__device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W, RT, RS, HB> &sh, uint32_t tag,
+                                                       uint32_t top, uint32_t lim, int L) {
     constexpr int G = 32 * W;
     const int64_t i64 = (int64_t)top - L;
     const bool act = i64 >= (int64_t)lim;
     const uint32_t i = act ? (uint32_t)i64 : 0;
-    const uint32_t j = act ? sh.ring[i & (LRING - 1)] : 0;
+    const uint32_t j = act ? (uint32_t)sh.ring[i & (RS - 1)] : 0;
     const T vi = act ? z[i] : T(0);
     const T vj = act ? z[j] : T(0);
     const uint32_t lo_pos = top >= lim + (G - 1) ? top - (G - 1) : lim;
     const bool inrange = act && j >= lo_pos && j < i;
     // lanes with equal targets meet in a hash slot; each slot keeps a chain of its lanes
-    const uint32_t h = (j * 2654435761u) >> (32 - HBITS);
+    const uint32_t h = (j * 2654435761u) >> (32 - HB);
     int16_t link = -1;
     if (act) {
         const uint32_t old = atomicExch(&sh.ht[h], (tag << 16) | (uint32_t)(L + 1));
@@ -767,9 +767,9 @@ __device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W> &
     __syncthreads();
 }
 
-template <typename T, int W>
-__device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan, LargeShared<T, W> &sh, int L,
-                                               uint64_t *rk_first) {
+template <typename T, int W, typename RT, uint32_t RS, int HB>
+__device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan, LargeShared<T, W, RT, RS, HB> &sh,
+                                               int L, uint64_t *rk_first) {
     constexpr int G = 32 * W;
     const uint32_t nb = plan.nbatches;
     const uint32_t b = g.B0 + L;
@@ -783,7 +783,7 @@ __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan
         const uint64_t t = __ldg(plan.thresh + b);
         uint64_t r = xslrr(g.s);
         const uint32_t pos = nbb - 1;
-        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (LRING - 1)] = die(nbb - m, r);
+        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (RS - 1)] = (RT)die(nbb - m, r);
         low = nbb - S.k;
         fail = r < t;
         if (rk_first && b == 0 && g.D == 0) *rk_first = r;
@@ -850,16 +850,16 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
         uint64_t *rkf = segmented ? nullptr : rk_first;
         for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= G) {
             const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step<T, W>(gs, plan, sh, L, rkf);
+            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
             tag = (tag + 1) & 0xFFFFu;
             if (tag == 0) {  // tag wrap: clear the slots (every 65535 groups)
                 for (uint32_t q = L; q < (1u << HBITS); q += G) sh.ht[q] = 0;
                 tag = 1;
                 __syncthreads();
             }
-            apply_group_cta_global<T, W>(z, sh, tag, (uint32_t)top, lim, L);
+            apply_group_cta_global(z, sh, tag, (uint32_t)top, lim, L);
         }
-        while (gs.B0 < plan.nbatches) large_gen_step<T, W>(gs, plan, sh, L, rkf);
+        while (gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
         const uint64_t words = (uint64_t)plan.nbatches + gs.D;
         if (L == 0) {
             if (segmented) {
@@ -873,6 +873,101 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
         }
         __syncthreads();
     }
+}
+
+// Shared-memory-resident arrays with the same hashed CTA groups: payload moved by TMA bulk
+// copies, targets in a u16 ring, 1024-slot lane-chain hash.
+template <typename T, int W>
+__global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                  DevPlan plan, uint64_t run_seed, int64_t base,
+                                                                  uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                                  uint64_t *words64, uint64_t *rk_first, int use_tma,
+                                                                  int segmented) {
+    constexpr int G = 32 * W;
+    constexpr int HB = 10;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ LargeShared<T, W, uint16_t, CRING, HB> sh;
+    __shared__ __align__(8) uint64_t bar;
+    const int L = threadIdx.x;
+    T *z = reinterpret_cast<T *>(smem_raw);
+    for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
+    for (uint32_t q = L; q < (1u << HB); q += G) sh.ht[q] = 0;
+    if (use_tma && L == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    const uint32_t n = plan.n;
+    const uint32_t bytes = n * (uint32_t)sizeof(T);
+    const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
+    uint32_t parity = 0, tag = 0;
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        T *g = data + a * (int64_t)n;
+        if (use_tma) {
+            if (L == 0) {
+                bulk_wait_read();
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bar, bytes);
+                bulk_load(z, g, bytes, &bar);
+            }
+        } else {
+            for (uint32_t e = L; e < n; e += G) z[e] = g[e];
+        }
+        u128 s0, inc;
+        if (segmented) {
+            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+        } else {
+            s0 = mk128(state_io[0], state_io[1]);
+            inc = mk128(state_io[2], state_io[3]);
+        }
+        CtaGen<W> gs;
+        gs.inc = inc;
+        gs.s = jump_small(s0, inc, L + 1);
+        gs.AJ = g_SA[G];
+        gs.CJ = mul128(g_SG[G], inc);
+        gs.B0 = 0;
+        gs.D = 0;
+        gs.seg = 0;
+        gs.frontier = n;
+        gs.parity = 0;
+        uint64_t *rkf = segmented ? nullptr : rk_first;
+        if (plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);  // overlaps the payload load
+        if (use_tma) {
+            mbar_wait(&bar, parity);
+            parity ^= 1u;
+        }
+        __syncthreads();
+        for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= G) {
+            const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
+            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
+            tag = (tag + 1) & 0xFFFFu;
+            if (tag == 0) {
+                for (uint32_t q = L; q < (1u << HB); q += G) sh.ht[q] = 0;
+                tag = 1;
+                __syncthreads();
+            }
+            apply_group_cta_global(z, sh, tag, (uint32_t)top, lim, L);
+        }
+        while (gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
+        if (use_tma) {
+            if (L == 0) {
+                fence_proxy_async();
+                bulk_store(g, z, bytes);
+            }
+        } else {
+            for (uint32_t e = L; e < n; e += G) g[e] = z[e];
+        }
+        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
+        if (L == 0) {
+            if (segmented) {
+                if (words32) words32[a] = (uint32_t)words;
+            } else {
+                const u128 sf = jump(s0, inc, words);
+                state_io[0] = sf.hi;
+                state_io[1] = sf.lo;
+                if (words64) words64[0] = words;
+            }
+        }
+        __syncthreads();
+    }
+    if (use_tma && L == 0) bulk_wait_all();
 }
 
 // -------------------------------------------------------------------------------------
