@@ -222,12 +222,65 @@ __device__ __noinline__ void roll_slow(RollWs *ws, uint8_t *flags, int64_t b, ui
 // (VB = 4/K batches), four loads in flight, and rolls 16 bytes / words VB bytes per store.
 // Lane l of sub-step u owns batches base + 32*VB*u + VB*l + v (v < VB); its words come
 // from VB consecutive PCG steps, the lane state then jumps 32*VB words.
+#ifndef ROLL_U
+#define ROLL_U 8
+#endif
+#ifndef ROLL_MINB
+#define ROLL_MINB 2
+#endif
+#ifndef ROLL_LB
+#define ROLL_LB 16
+#endif
+
+// LB bytes of consecutive u32 per lane.  32-byte lanes use Blackwell's 256-bit
+// LDG/STG (LDG.E.NA.EFL2.256) with L1 no-allocate / L2 evict-first: bounds are read once and
+// rolls written once, so neither should displace anything in L2.
+template <int LB>
+struct Vec {
+    uint32_t v[LB / 4];
+};
+
+template <int LB>
+__device__ __forceinline__ Vec<LB> ld_vec(const uint32_t *p) {
+    Vec<LB> r;
+    if constexpr (LB == 32) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                       "=r"(r.v[6]), "=r"(r.v[7])
+                     : "l"(p));
+    } else {
+        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p));
+        r.v[0] = x.x;
+        r.v[1] = x.y;
+        r.v[2] = x.z;
+        r.v[3] = x.w;
+    }
+    return r;
+}
+
+template <int LB>
+__device__ __forceinline__ void st_vec(uint32_t *p, const Vec<LB> &r) {
+    if constexpr (LB == 32) {
+        asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                     "r"(r.v[0]), "r"(r.v[1]), "r"(r.v[2]), "r"(r.v[3]), "r"(r.v[4]), "r"(r.v[5]), "r"(r.v[6]),
+                     "r"(r.v[7])
+                     : "memory");
+    } else {
+        *reinterpret_cast<uint4 *>(p) = make_uint4(r.v[0], r.v[1], r.v[2], r.v[3]);
+    }
+}
+
+// Main kernel for k <= 2 (the C2 shape): every lane moves LB bytes of bounds per load
+// (VB = LB/(4K) batches), U loads in flight, and rolls LB bytes / words VB bytes per store.
+// Lane l of sub-step u owns batches base + 32*VB*u + VB*l + v (v < VB); its words come
+// from VB consecutive PCG steps, the lane state then jumps 32*VB words.
 template <int K, bool FLAGS, bool RK>
-__global__ void __launch_bounds__(256, 3) roll_fast_kernel(RollArgs a) {
+__global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     static_assert(K == 1 || K == 2, "fast path is for k <= 2");
-    constexpr int VB = 4 / K;
+    constexpr int LB = ROLL_LB;
+    constexpr int VB = LB / (4 * K);
     static_assert(32 * VB <= 256, "jump table covers 256 words");
-    constexpr int U = 4;
+    constexpr int U = ROLL_U;
     constexpr int64_t CH = 32 * VB * U;
     pdl_launch_dependents();
     const u128 s0 = mk128(a.state[0], a.state[1]);
@@ -246,21 +299,21 @@ __global__ void __launch_bounds__(256, 3) roll_fast_kernel(RollArgs a) {
         s = jump_small(s, inc, VB * lane + 1);
         const u128 AJ = g_SA[32 * VB];
         const u128 CJ = mul128(g_SG[32 * VB], inc);
-        const uint4 *bp = reinterpret_cast<const uint4 *>(a.bounds + wb * K) + lane;
-        uint4 *rp = reinterpret_cast<uint4 *>(a.rolls + wb * K) + lane;
+        const uint32_t *bp = a.bounds + (wb + VB * lane) * K;
+        uint32_t *rp = a.rolls + (wb + VB * lane) * K;
         uint8_t *wp = a.words + wb + VB * lane;
-        uint4 cur[U], nxt[U];
+        constexpr int STEP = 32 * VB * K;  // u32 per sub-step
+        Vec<LB> cur[U], nxt[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) cur[u] = __ldg(bp + 32 * u);
+        for (int u = 0; u < U; ++u) cur[u] = ld_vec<LB>(bp + STEP * u);
         for (int64_t c = c0; c < c1; ++c) {
             if (c + 1 < c1) {
 #pragma unroll
-                for (int u = 0; u < U; ++u) nxt[u] = __ldg(bp + 32 * (U + u));
+                for (int u = 0; u < U; ++u) nxt[u] = ld_vec<LB>(bp + STEP * (U + u));
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const uint32_t bb[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
-                uint32_t dd[4];
+                Vec<LB> dd;
                 u128 st = s;
                 const int64_t b0 = wb + (c - c0) * CH + 32 * VB * u + VB * lane;
 #pragma unroll
@@ -268,29 +321,31 @@ __global__ void __launch_bounds__(256, 3) roll_fast_kernel(RollArgs a) {
                     uint64_t r = xslrr(st);
                     uint64_t prod;
                     if constexpr (K == 2) {
-                        dd[2 * v] = die(bb[2 * v], r);
-                        dd[2 * v + 1] = die(bb[2 * v + 1], r);
-                        prod = (uint64_t)bb[2 * v] * bb[2 * v + 1];
+                        dd.v[2 * v] = die(cur[u].v[2 * v], r);
+                        dd.v[2 * v + 1] = die(cur[u].v[2 * v + 1], r);
+                        prod = (uint64_t)cur[u].v[2 * v] * cur[u].v[2 * v + 1];
                     } else {
-                        dd[v] = die(bb[v], r);
-                        prod = bb[v];
+                        dd.v[v] = die(cur[u].v[v], r);
+                        prod = cur[u].v[v];
                     }
                     if constexpr (FLAGS) a.flags[b0 + v] = r < prod;
                     if constexpr (RK) a.rk[b0 + v] = r;
                     if (__builtin_expect(r < prod || prod == 0, 0)) roll_slow(a.ws, a.flags, b0 + v, r, prod);
                     if (v + 1 < VB) st = mad128(st, M, inc);
                 }
-                rp[32 * u] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+                st_vec<LB>(rp + STEP * u, dd);
                 if constexpr (VB == 2)
                     *reinterpret_cast<uint16_t *>(wp + 32 * VB * u) = 0x0101;
-                else
+                else if constexpr (VB == 4)
                     *reinterpret_cast<uint32_t *>(wp + 32 * VB * u) = 0x01010101u;
+                else
+                    *reinterpret_cast<uint2 *>(wp + 32 * VB * u) = make_uint2(0x01010101u, 0x01010101u);
                 s = mad128(s, AJ, CJ);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-            bp += 32 * U;
-            rp += 32 * U;
+            bp += STEP * U;
+            rp += STEP * U;
             wp += CH;
         }
     }
