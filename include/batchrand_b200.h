@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define BR_ABI_VERSION 1
+#define BR_ABI_VERSION 2
 
 /* Status codes.  Python mapping (errors.py:4-37): */
 #define BR_OK 0
@@ -41,7 +41,9 @@ extern "C" {
 #define BR_E_CUDA 4           /* RuntimeError (CUDA error / no device) */
 #define BR_E_UNSUPPORTED 5    /* TypeError/NotImplementedError (size or source not handled) */
 
-/* PCG64 state: 128-bit LCG state and odd increment (wordsource.py:80-83). */
+/* Generator state.  PCG64 (wordsource.py:71-89): 128-bit LCG state and ODD increment.
+ * Lehmer128 (wordsource.py:51-67): 128-bit odd state, increment 0 -- an increment of 0 is
+ * how every entry point below tells a Lehmer stream from a PCG64 stream. */
 typedef struct br_pcg64 {
     uint64_t state_hi, state_lo;
     uint64_t inc_hi, inc_lo;
@@ -73,7 +75,9 @@ int br_device_count(void);
 uint64_t br_splitmix64_next(uint64_t *x);
 /* wordsource.py:80-83 Pcg64Source.__init__ */
 void br_pcg64_seed(uint64_t seed, br_pcg64 *out);
-/* wordsource.py:85-89 Pcg64Source.next_word */
+/* wordsource.py:61-63 LehmerSource.__init__ (increment 0) */
+void br_lehmer_seed(uint64_t seed, br_pcg64 *out);
+/* wordsource.py:85-89 Pcg64Source.next_word / :65-67 LehmerSource.next_word */
 uint64_t br_pcg64_next(br_pcg64 *st);
 /* O(log d) jump-ahead by `delta` words (numpy PCG64.advance semantics) */
 void br_pcg64_advance(br_pcg64 *st, uint64_t delta);
@@ -149,12 +153,13 @@ int br_shuffle_stream_segments(void *z_dev, int elem_bytes, uint64_t n, br_pcg64
                                uint64_t *rk_first_dev, void *stream);
 /* Many independent shuffles: array a (0 <= a < num_arrays) of n elements at
  * data_dev + a*n*elem_bytes is shuffled in place by
- *     shuffle_batched(make_source("pcg64", br_array_seed(run_seed, array_index_base + a)), z)
+ *     shuffle_batched(make_source(G, br_array_seed(run_seed, array_index_base + a)), z)
+ * with G = "pcg64" (generator 0) or "lehmer" (generator 1).
  * array_index_base lets shards of one job run on different GPUs with no exchange.
  * words_dev (may be NULL) receives words consumed per array (u32). */
 int br_shuffle_segmented(void *data_dev, int elem_bytes, int64_t num_arrays, uint64_t n,
                          uint64_t run_seed, int64_t array_index_base, const br_regime *entries,
-                         int n_entries, uint32_t *words_dev, void *stream);
+                         int n_entries, int generator, uint32_t *words_dev, void *stream);
 
 /* Kernel-selection report for the last device call on this thread (diagnostics). */
 const char *br_last_kernel(void);

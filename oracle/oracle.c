@@ -546,6 +546,14 @@ int or_shuffle_segmented(void *data, int32_t eb, int64_t num_arrays, uint64_t n,
                          uint64_t run_seed, int64_t base, const uint64_t *lengths,
                          const uint32_t *sizes, int32_t nent, uint32_t *words_out,
                          int32_t nthreads, int32_t unbatched) {
+    return or_shuffle_segmented_gen(data, eb, num_arrays, n, run_seed, base, lengths, sizes, nent,
+                                    words_out, nthreads, unbatched, 0);
+}
+
+int or_shuffle_segmented_gen(void *data, int32_t eb, int64_t num_arrays, uint64_t n,
+                             uint64_t run_seed, int64_t base, const uint64_t *lengths,
+                             const uint32_t *sizes, int32_t nent, uint32_t *words_out,
+                             int32_t nthreads, int32_t unbatched, int32_t generator) {
     int err = OR_OK;
 #ifdef _OPENMP
     if (nthreads <= 0) nthreads = omp_get_max_threads();
@@ -553,7 +561,10 @@ int or_shuffle_segmented(void *data, int32_t eb, int64_t num_arrays, uint64_t n,
 #endif
     for (int64_t a = 0; a < num_arrays; ++a) {
         or_source src;
-        or_source_pcg64(&src, or_array_seed(run_seed, (uint64_t)(base + a)));
+        if (generator == 1)
+            or_source_lehmer(&src, or_array_seed(run_seed, (uint64_t)(base + a)));
+        else
+            or_source_pcg64(&src, or_array_seed(run_seed, (uint64_t)(base + a)));
         unsigned char *z = (unsigned char *)data + (size_t)a * n * eb;
         int st = unbatched ? or_shuffle_unbatched(&src, z, eb, n)
                            : or_shuffle_batched(&src, z, eb, n, lengths, sizes, nent, 64, 0);

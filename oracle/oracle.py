@@ -102,6 +102,7 @@ def lib():
             "or_roll_batches": (C.c_int, [P(Source), vp, i32, i64, vp, vp, vp, vp]),
             "or_gen_bounds": (C.c_int, [P(Source), vp, i64, u64, u64]),
             "or_shuffle_segmented": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, vp, i32, vp, i32, i32]),
+            "or_shuffle_segmented_gen": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, vp, i32, vp, i32, i32, i32]),
             "or_pcg64_fill": (None, [P(Source), u64, vp, i64]),
         }
         for name, (res, args) in sig.items():
@@ -285,13 +286,14 @@ def shuffle_trace(n: int, entries=DEFAULT_ENTRIES, bits=64):
 
 
 def shuffle_segmented(data: np.ndarray, n: int, run_seed: int, array_index_base: int = 0,
-                      entries=DEFAULT_ENTRIES, nthreads: int = 0, unbatched: bool = False):
+                      entries=DEFAULT_ENTRIES, nthreads: int = 0, unbatched: bool = False, generator: str = "pcg64"):
     """Shuffle data (num_arrays*n elements, in place) like the device segmented shuffle."""
     assert data.flags.c_contiguous
     num_arrays = data.size // n
     lengths, sizes = _sched(entries)
     wds = np.empty(num_arrays, dtype=np.uint32)
-    _check(lib().or_shuffle_segmented(_ptr(data), data.dtype.itemsize, num_arrays, n, run_seed & MASK64,
-                                      array_index_base, _ptr(lengths), _ptr(sizes), len(entries), _ptr(wds),
-                                      nthreads, int(unbatched)), "shuffle_segmented")
+    _check(lib().or_shuffle_segmented_gen(_ptr(data), data.dtype.itemsize, num_arrays, n, run_seed & MASK64,
+                                          array_index_base, _ptr(lengths), _ptr(sizes), len(entries), _ptr(wds),
+                                          nthreads, int(unbatched), {"pcg64": 0, "lehmer": 1}[generator]),
+           "shuffle_segmented")
     return wds

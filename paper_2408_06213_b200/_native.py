@@ -40,6 +40,7 @@ PROTOTYPES = {
     "br_device_count": (C.c_int, []),
     "br_splitmix64_next": (u64, [P(u64)]),
     "br_pcg64_seed": (None, [u64, P(Pcg64State)]),
+    "br_lehmer_seed": (None, [u64, P(Pcg64State)]),
     "br_pcg64_next": (u64, [P(Pcg64State)]),
     "br_pcg64_advance": (None, [P(Pcg64State), u64]),
     "br_array_seed": (u64, [u64, u64]),
@@ -56,7 +57,7 @@ PROTOTYPES = {
     "br_digit_pass": (C.c_int, [vp, vp, C.c_int, i64, vp, vp, vp]),
     "br_shuffle_stream": (C.c_int, [vp, C.c_int, u64, vp, P(Regime), C.c_int, C.c_int, vp, vp]),
     "br_shuffle_stream_segments": (C.c_int, [vp, C.c_int, u64, vp, P(Segment), C.c_int, vp, vp, vp]),
-    "br_shuffle_segmented": (C.c_int, [vp, C.c_int, i64, u64, u64, i64, P(Regime), C.c_int, vp, vp]),
+    "br_shuffle_segmented": (C.c_int, [vp, C.c_int, i64, u64, u64, i64, P(Regime), C.c_int, C.c_int, vp, vp]),
     "br_release": (None, []),
 }
 

@@ -82,13 +82,32 @@ class Pcg64Source(WordSource):
         self.state = (st.state_hi << 64) | st.state_lo
 
 
-GENERATORS = {"pcg64": Pcg64Source}
+class LehmerSource(WordSource):
+    """128-bit multiplicative generator, output = top 64 bits (wordsource.py:51-67).  On the
+    device a Lehmer stream is a generator state with increment 0."""
+
+    word_bits = 64
+
+    def __init__(self, seed: int = 0):
+        st = N.Pcg64State()
+        N.lib().br_lehmer_seed(seed & MASK64, C.byref(st))
+        self.state = (st.state_hi << 64) | st.state_lo
+
+    def next_word(self) -> int:
+        st = _state_struct(self)
+        w = N.lib().br_pcg64_next(C.byref(st))
+        self.state = (st.state_hi << 64) | st.state_lo
+        return w
+
+
+GENERATORS = {"pcg64": Pcg64Source, "lehmer": LehmerSource}
+_GENERATOR_IDS = {"pcg64": 0, "lehmer": 1}
 
 
 def make_source(name: str, seed: int = 0) -> WordSource:
-    """wordsource.py:217-225.  Only pcg64 has a device implementation."""
-    if name in ("lehmer", "chacha"):
-        raise NotImplementedError(f"generator {name!r} has no device implementation yet")
+    """wordsource.py:217-225.  pcg64 and lehmer have device implementations."""
+    if name == "chacha":
+        raise NotImplementedError("generator 'chacha' has no device implementation yet")
     try:
         cls = GENERATORS[name]
     except KeyError:
@@ -101,12 +120,19 @@ def array_seed(run_seed: int, array_index: int) -> int:
     return N.lib().br_array_seed(run_seed & MASK64, array_index & MASK64)
 
 
+def _is_lehmer(source) -> bool:
+    return not hasattr(source, "increment") and hasattr(source, "state") and "lehmer" in type(source).__name__.lower()
+
+
 def _state_struct(source) -> N.Pcg64State:
     try:
-        state, inc = int(source.state), int(source.increment)
+        if _is_lehmer(source):  # reference LehmerSource or ours: state only, increment 0
+            state, inc = int(source.state), 0
+        else:
+            state, inc = int(source.state), int(source.increment)
     except AttributeError:
         raise TypeError(
-            f"{type(source).__name__} is not a PCG64 source; the device path draws PCG64 words only"
+            f"{type(source).__name__} is not a PCG64 or Lehmer source; the device path draws those words only"
         ) from None
     if getattr(source, "word_bits", 64) != 64:
         raise TypeError("the device path needs 64-bit words")
@@ -463,9 +489,14 @@ class DeviceStream:
     """A PCG64 stream whose state lives in device memory, for chained bulk calls without a
     host round trip.  ``write_back(source)`` copies the advanced state to a host source."""
 
-    def __init__(self, seed: int = 0):
+    def __init__(self, seed: int = 0, generator: str = "pcg64"):
         st = N.Pcg64State()
-        N.lib().br_pcg64_seed(seed & MASK64, C.byref(st))
+        if generator == "lehmer":
+            N.lib().br_lehmer_seed(seed & MASK64, C.byref(st))
+        elif generator == "pcg64":
+            N.lib().br_pcg64_seed(seed & MASK64, C.byref(st))
+        else:
+            raise UnknownGenerator(f"no device generator {generator!r}")
         self._init(st)
 
     @classmethod
@@ -634,13 +665,16 @@ def digit_pass_many(words, bounds, k: int):
     return digits, rk
 
 
-def pcg64_fill(source_or_seed, count: int, offset: int = 0):
-    """count consecutive words (from word `offset`) of a PCG64 stream, as an int64 CUDA tensor
-    (bit pattern of the u64 words).  The source is not advanced."""
+def pcg64_fill(source_or_seed, count: int, offset: int = 0, generator: str = "pcg64"):
+    """count consecutive words (from word `offset`) of a PCG64 (or Lehmer) stream, as an int64
+    CUDA tensor (bit pattern of the u64 words).  The source is not advanced."""
     torch = _torch()
     if isinstance(source_or_seed, int):
         st = N.Pcg64State()
-        N.lib().br_pcg64_seed(source_or_seed & MASK64, C.byref(st))
+        if generator == "lehmer":
+            N.lib().br_lehmer_seed(source_or_seed & MASK64, C.byref(st))
+        else:
+            N.lib().br_pcg64_seed(source_or_seed & MASK64, C.byref(st))
     else:
         st = _state_struct(source_or_seed)
     out = torch.empty(count, dtype=torch.int64, device="cuda")
@@ -649,10 +683,14 @@ def pcg64_fill(source_or_seed, count: int, offset: int = 0):
 
 
 def shuffle_many(data, n: int, run_seed: int, array_index_base: int = 0,
-                 schedule: ShuffleSchedule = DEFAULT_SCHEDULE, return_words: bool = False):
+                 schedule: ShuffleSchedule = DEFAULT_SCHEDULE, return_words: bool = False,
+                 generator: str = "pcg64"):
     """Independent shuffles of the num_arrays = data.numel() // n contiguous arrays of a CUDA
     tensor (4- or 8-byte items), in place: array a is
-    shuffle_batched(make_source("pcg64", array_seed(run_seed, array_index_base + a)), ...)."""
+    shuffle_batched(make_source(generator, array_seed(run_seed, array_index_base + a)), ...)
+    with generator "pcg64" or "lehmer"."""
+    if generator not in _GENERATOR_IDS:
+        raise UnknownGenerator(f"no device generator {generator!r}")
     torch = _torch()
     flat = data.view(-1)
     if not flat.is_cuda or flat.element_size() not in (4, 8):
@@ -663,7 +701,8 @@ def shuffle_many(data, n: int, run_seed: int, array_index_base: int = 0,
     words = torch.empty(num_arrays, dtype=torch.int32, device="cuda") if return_words else None
     regs = schedule._regimes()
     N.check(N.lib().br_shuffle_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64,
-                                         array_index_base, regs, len(regs), _ptr(words), _stream_ptr(torch)),
+                                         array_index_base, regs, len(regs), _GENERATOR_IDS[generator], _ptr(words),
+                                         _stream_ptr(torch)),
             "shuffle_many")
     return (data, words) if return_words else data
 
@@ -679,7 +718,7 @@ __all__ = [
     "DigitOutOfRange", "DeviceStream", "FullProduct", "PAIR_SCHEDULE", "Pcg64Source", "RadixBases",
     "RollBatchesResult", "ShuffleSchedule", "SourceExhausted", "UnknownGenerator", "ValueOutOfRange",
     "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",
-    "make_source", "mul_full", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
+    "make_source", "mul_full", "LehmerSource", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
     "roll_batches", "shuffle_batched", "shuffle_many", "shuffle_unbatched", "splitmix64_stream", "threshold",
     "last_kernel",
 ]

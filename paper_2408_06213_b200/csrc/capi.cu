@@ -69,6 +69,8 @@ int ensure_device(int *dev_out, DeviceInfo *info_out) {
         CK(cudaMemcpyToSymbol(c_G, t.G, sizeof(t.G)));
         CK(cudaMemcpyToSymbol(g_SA, t.SA, sizeof(t.SA)));
         CK(cudaMemcpyToSymbol(g_SG, t.SG, sizeof(t.SG)));
+        CK(cudaMemcpyToSymbol(c_LA, t.LA, sizeof(t.LA)));
+        CK(cudaMemcpyToSymbol(g_LSA, t.LSA, sizeof(t.LSA)));
         CK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
         int coop = 0;
         CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
@@ -220,12 +222,13 @@ __global__ void pcg_fill_kernel(uint64_t *__restrict__ out, int64_t count, u128 
     const int64_t per = (((count + nwarps - 1) / nwarps) + 31) & ~(int64_t)31;
     const int64_t wb = warp * per, we = min(wb + per, count);
     if (wb >= we) return;
-    u128 s = jump(s0, inc, offset + (uint64_t)wb);
-    s = jump_small(s, inc, lane + 1);
-    const u128 A32 = g_SA[32], C32 = mul128(g_SG[32], inc);
+    const bool lh = is_lehmer(inc);
+    u128 s = gen_jump(s0, inc, offset + (uint64_t)wb, lh);
+    s = gen_jump_small(s, inc, lane + 1, lh);
+    const u128 A32 = gen_SA(lh, 32), C32 = mul128(g_SG[32], inc);
     for (int64_t b0 = wb; b0 < we; b0 += 32) {
         const int64_t i = b0 + lane;
-        if (i < we) out[i] = xslrr(s);
+        if (i < we) out[i] = gen_out(s, lh);
         s = mad128(s, A32, C32);
     }
 }
@@ -300,7 +303,7 @@ constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 template <typename T>
 int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan &cp, bool segmented,
                    uint64_t run_seed, int64_t base, uint32_t *words32, uint64_t *state_dev, uint64_t *words64,
-                   uint64_t *rk_first, const DeviceInfo &di, cudaStream_t st) {
+                   uint64_t *rk_first, int gen, const DeviceInfo &di, cudaStream_t st) {
     const uint32_t stride = (uint32_t)(n | 1u);
     const int tpb = 64;  // 2 warps: many small blocks per SM overlap their load/compute/store phases
     const size_t small_smem = (size_t)tpb * stride * sizeof(T);
@@ -312,7 +315,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         const uint32_t magic = (uint32_t)((((uint64_t)1 << 32) + n - 1) / n);
         const int vec_ok = ((n * sizeof(T)) % 16 == 0 && ((uintptr_t)data & 15) == 0) ? 1 : 0;
         kern<<<(unsigned)blocks, tpb, small_smem, st>>>((T *)data, num_arrays, cp.plan, stride, magic, vec_ok, run_seed,
-                                                        base, words32);
+                                                        base, words32, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_small_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
@@ -329,7 +332,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
         shuffle_cta_hash_kernel<T, W><<<grid, 32 * W, csmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base,
                                                                  words32, state_dev, words64, rk_first, use_tma,
-                                                                 segmented ? 1 : 0);
+                                                                 segmented ? 1 : 0, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_cta_hash_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
                    std::to_string(W) + ">";
@@ -344,10 +347,10 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
         if (segmented)
             shuffle_mid_kernel<T, true><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
-                                                                words32, state_dev, words64, rk_first, use_tma);
+                                                                words32, state_dev, words64, rk_first, use_tma, gen);
         else
             shuffle_mid_kernel<T, false><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
-                                                                 words32, state_dev, words64, rk_first, use_tma);
+                                                                 words32, state_dev, words64, rk_first, use_tma, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
@@ -358,7 +361,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
         shuffle_cta_large_kernel<T, W><<<grid, 32 * W, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base,
                                                                   words32, state_dev, words64, rk_first,
-                                                                  segmented ? 1 : 0);
+                                                                  segmented ? 1 : 0, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_cta_large_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
                    std::to_string(W) + ">";
@@ -375,10 +378,10 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
             if (segmented)
                 shuffle_large_gen_kernel<true><<<grid_gen, 32, 0, st>>>(na, cp.plan, run_seed, base + a0, J,
                                                                          words32 ? words32 + a0 : nullptr, state_dev,
-                                                                         words64, rk_first);
+                                                                         words64, rk_first, gen);
             else
                 shuffle_large_gen_kernel<false><<<1, 32, 0, st>>>(1, cp.plan, run_seed, base, J, nullptr, state_dev,
-                                                                   words64, rk_first);
+                                                                   words64, rk_first, gen);
             const uint32_t lim = cp.plan.lo > 1 ? cp.plan.lo : 1;
             shuffle_large_apply_kernel<T><<<(int)std::min<int64_t>(na, (int64_t)di.sms * 16), 32, 0, st>>>(
                 (T *)data + a0 * (int64_t)n, na, (uint32_t)n, lim, J);
@@ -393,7 +396,8 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
 
 int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std::vector<br_segment> &segs,
                    bool segmented, uint64_t run_seed, int64_t base, uint32_t *words32, br_pcg64 *state_dev,
-                   uint64_t *words64, uint64_t *rk_first, void *stream) {
+                   uint64_t *words64, uint64_t *rk_first, int gen, void *stream) {
+    if (gen != 0 && gen != 1) return fail(BR_E_UNSUPPORTED, "generator must be 0 (pcg64) or 1 (lehmer)");
     if (eb != 4 && eb != 8) return fail(BR_E_UNSUPPORTED, "elem_bytes must be 4 or 8");
     if (num_arrays < 0) return fail(BR_E_INVALID, "num_arrays < 0");
     if (n >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements");
@@ -415,9 +419,9 @@ int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std
     if (stt) return stt;
     if (eb == 4)
         return launch_shuffle<uint32_t>(data, num_arrays, n, cp, segmented, run_seed, base, words32,
-                                        (uint64_t *)state_dev, words64, rk_first, di, st);
+                                        (uint64_t *)state_dev, words64, rk_first, gen, di, st);
     return launch_shuffle<uint64_t>(data, num_arrays, n, cp, segmented, run_seed, base, words32,
-                                    (uint64_t *)state_dev, words64, rk_first, di, st);
+                                    (uint64_t *)state_dev, words64, rk_first, gen, di, st);
 }
 
 }  // namespace
@@ -448,19 +452,30 @@ void br_pcg64_seed(uint64_t seed, br_pcg64 *out) {
     out->inc_lo = inc.lo;
 }
 
+void br_lehmer_seed(uint64_t seed, br_pcg64 *out) {
+    u128 s, inc;
+    lehmer_seed(seed, s, inc);
+    out->state_hi = s.hi;
+    out->state_lo = s.lo;
+    out->inc_hi = inc.hi;
+    out->inc_lo = inc.lo;
+}
+
 uint64_t br_pcg64_next(br_pcg64 *st) {
     u128 s = mk128(st->state_hi, st->state_lo);
-    s = add128(mul128(s, mk128(PCG_MULT_HI, PCG_MULT_LO)), mk128(st->inc_hi, st->inc_lo));
+    const bool lh = (st->inc_hi | st->inc_lo) == 0;
+    s = add128(mul128(s, lh ? mk128(0, LEHMER_MULT) : mk128(PCG_MULT_HI, PCG_MULT_LO)), mk128(st->inc_hi, st->inc_lo));
     st->state_hi = s.hi;
     st->state_lo = s.lo;
-    return xslrr(s);
+    return lh ? s.hi : xslrr(s);
 }
 
 void br_pcg64_advance(br_pcg64 *st, uint64_t delta) {
     const JumpTables &t = host_tables();
     u128 s = mk128(st->state_hi, st->state_lo), inc = mk128(st->inc_hi, st->inc_lo);
+    const bool lh = (inc.hi | inc.lo) == 0;
     for (int k = 0; delta; ++k, delta >>= 1)
-        if (delta & 1) s = add128(mul128(t.A[k], s), mul128(t.G[k], inc));
+        if (delta & 1) s = add128(mul128(lh ? t.LA[k] : t.A[k], s), mul128(t.G[k], inc));
     st->state_hi = s.hi;
     st->state_lo = s.lo;
 }
@@ -630,7 +645,7 @@ int br_shuffle_stream(void *z, int eb, uint64_t n, br_pcg64 *state_dev, const br
         int st = build_segments(n, entries, ne, segs, nb);
         if (st) return st;
     }
-    return shuffle_common(z, eb, 1, n, segs, false, 0, 0, nullptr, state_dev, words_dev, nullptr, stream);
+    return shuffle_common(z, eb, 1, n, segs, false, 0, 0, nullptr, state_dev, words_dev, nullptr, 0, stream);
 }
 
 int br_shuffle_stream_segments(void *z, int eb, uint64_t n, br_pcg64 *state_dev, const br_segment *segs, int nseg,
@@ -642,17 +657,17 @@ int br_shuffle_stream_segments(void *z, int eb, uint64_t n, br_pcg64 *state_dev,
         if (s.start_n > n || (uint64_t)s.k * s.count > s.start_n)
             return fail(BR_E_INVALID, "segment runs outside the array");
     }
-    return shuffle_common(z, eb, 1, n, v, false, 0, 0, nullptr, state_dev, words_dev, rk_first_dev, stream);
+    return shuffle_common(z, eb, 1, n, v, false, 0, 0, nullptr, state_dev, words_dev, rk_first_dev, 0, stream);
 }
 
 int br_shuffle_segmented(void *data, int eb, int64_t num_arrays, uint64_t n, uint64_t run_seed, int64_t base,
-                         const br_regime *entries, int ne, uint32_t *words_dev, void *stream) {
+                         const br_regime *entries, int ne, int generator, uint32_t *words_dev, void *stream) {
     std::vector<br_segment> segs;
     uint64_t nb = 0;
     int st = build_segments(n, entries, ne, segs, nb);
     if (st) return st;
     return shuffle_common(data, eb, num_arrays, n, segs, true, run_seed, base, words_dev, nullptr, nullptr, nullptr,
-                          stream);
+                          generator, stream);
 }
 
 void br_release(void) {

@@ -96,6 +96,8 @@ __host__ __device__ __forceinline__ u128 affine(u128 s, u128 A, u128 C) { return
 // PCG_MULTIPLIER, wordsource.py:19
 static constexpr uint64_t PCG_MULT_HI = 0x2360ED051FC65DA4ull;
 static constexpr uint64_t PCG_MULT_LO = 0x4385DF649FCCF645ull;
+// LEHMER_MULTIPLIER, wordsource.py:18 (128-bit multiplicative generator, output = top 64 bits)
+static constexpr uint64_t LEHMER_MULT = 0xDA942042E4DD58B5ull;
 
 // XSL-RR output of a (post-update) state, wordsource.py:87-89
 __host__ __device__ __forceinline__ uint64_t xslrr(u128 s) {
@@ -130,6 +132,15 @@ __host__ __device__ __forceinline__ void pcg_seed(uint64_t seed, u128 &state, u1
     inc = mk128(z2, z3 | 1u);
 }
 
+// LehmerSource.__init__ (wordsource.py:61-63); the increment is 0, which is how a Lehmer
+// stream is told apart from a PCG64 stream (whose increment is always odd)
+__host__ __device__ __forceinline__ void lehmer_seed(uint64_t seed, u128 &state, u128 &inc) {
+    uint64_t x = seed;
+    uint64_t z0 = splitmix64_next(x), z1 = splitmix64_next(x);
+    state = mk128(z0, z1 | 1u);
+    inc = mk128(0, 0);
+}
+
 // per-array seed convention: first splitmix64 output of (s<<32)|a
 __host__ __device__ __forceinline__ uint64_t array_seed(uint64_t run_seed, uint64_t a) {
     uint64_t x = (run_seed << 32) | a;
@@ -153,6 +164,7 @@ __host__ __device__ __forceinline__ uint64_t threshold64(uint64_t b) { return b 
 struct JumpTables {
     u128 A[64], G[64];       // d = 2^k
     u128 SA[257], SG[257];   // d = 0..256 (lane offsets / small realignments)
+    u128 LA[64], LSA[257];   // Lehmer: multiplier powers M_L^(2^k), M_L^d
 };
 
 // Host construction (also used by the C-ABI host helpers)
@@ -165,6 +177,16 @@ inline void build_jump_tables(JumpTables &t) {
         // (A,G)_{2d} = (A^2, (A+1) G)
         g = mul128(add128(m, mk128(0, 1)), g);
         m = mul128(m, m);
+    }
+    u128 lm = mk128(0, LEHMER_MULT);
+    for (int k = 0; k < 64; ++k) {
+        t.LA[k] = lm;
+        lm = mul128(lm, lm);
+    }
+    u128 la = mk128(0, 1);
+    for (int d = 0; d <= 256; ++d) {
+        t.LSA[d] = la;
+        la = mul128(mk128(0, LEHMER_MULT), la);
     }
     u128 a = mk128(0, 1), gg = mk128(0, 0);
     u128 M = mk128(PCG_MULT_HI, PCG_MULT_LO);

@@ -12,8 +12,10 @@ namespace br {
 
 __constant__ u128 c_A[64];
 __constant__ u128 c_G[64];
+__constant__ u128 c_LA[64];
 __device__ u128 g_SA[257];
 __device__ u128 g_SG[257];
+__device__ u128 g_LSA[257];
 
 // state after d more updates (any d; cost popcount(d) affine steps)
 __device__ __forceinline__ u128 jump(u128 s, u128 inc, uint64_t d) {
@@ -38,4 +40,44 @@ __device__ __forceinline__ uint64_t pcg_next(u128 &s, u128 inc) {
     return xslrr(s);
 }
 
+}  // namespace br
+
+namespace br {
+// ---- generator-generic forms: `lh` selects Lehmer128 (increment 0) instead of PCG64.
+// Every additive term carries the increment, so for Lehmer it vanishes and only the
+// multiplier tables differ.
+__device__ __forceinline__ bool is_lehmer(u128 inc) { return (inc.hi | inc.lo) == 0; }
+
+__device__ __forceinline__ u128 gen_mult(bool lh) {
+    return lh ? mk128(0, LEHMER_MULT) : mk128(PCG_MULT_HI, PCG_MULT_LO);
+}
+
+// output of a post-update state: XSL-RR (wordsource.py:87-89) or the top 64 bits (:65-67)
+__device__ __forceinline__ uint64_t gen_out(u128 s, bool lh) { return lh ? s.hi : xslrr(s); }
+
+__device__ __forceinline__ uint64_t gen_next(u128 &s, u128 inc, bool lh) {
+    s = mad128(s, gen_mult(lh), inc);
+    return gen_out(s, lh);
+}
+
+__device__ __forceinline__ u128 gen_jump(u128 s, u128 inc, uint64_t d, bool lh) {
+    int k = 0;
+    while (d) {
+        if (d & 1) s = mad128(s, lh ? c_LA[k] : c_A[k], mul128(c_G[k], inc));
+        d >>= 1;
+        ++k;
+    }
+    return s;
+}
+
+__device__ __forceinline__ u128 gen_jump_small(u128 s, u128 inc, int d, bool lh) {
+    return mad128(s, lh ? g_LSA[d] : g_SA[d], mul128(g_SG[d], inc));
+}
+
+__device__ __forceinline__ u128 gen_SA(bool lh, int d) { return lh ? g_LSA[d] : g_SA[d]; }
+
+__device__ __forceinline__ void gen_seed(uint64_t seed, u128 &s, u128 &inc, bool lh) {
+    if (lh) lehmer_seed(seed, s, inc);
+    else pcg_seed(seed, s, inc);
+}
 }  // namespace br

@@ -128,6 +128,7 @@ __device__ __forceinline__ void set_error(RollWs *ws, int err) {
 template <int K, int U>
 __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc, int64_t begin,
                                            int64_t end, uint64_t D, bool early_exit) {
+    const bool lh = is_lehmer(inc);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -138,9 +139,9 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
     const int64_t we = min(wb + per, end);
     if (wb >= we) return;
     // lane state: word index wb + D + lane  ->  state index (word index + 1)
-    u128 s = jump(s0, inc, (uint64_t)wb + D);
-    s = jump_small(s, inc, lane + 1);
-    const u128 A32 = g_SA[32];
+    u128 s = gen_jump(s0, inc, (uint64_t)wb + D, lh);
+    s = gen_jump_small(s, inc, lane + 1, lh);
+    const u128 A32 = gen_SA(lh, 32);
     const u128 C32 = mul128(g_SG[32], inc);
     int err = 0;
     volatile RollWs *vws = a.ws;
@@ -166,7 +167,7 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
         for (int u = 0; u < U; ++u) {
             const int64_t b = b0 + 32 * u + lane;
             if (b < we) {
-                const uint64_t w = xslrr(s);
+                const uint64_t w = gen_out(s, lh);
                 uint32_t d[K];
                 uint64_t r;
                 uint8_t tc = 0;
@@ -189,8 +190,9 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
 
 // state after nb words, for the fixup kernel's no-rejection case (one lane of the grid)
 __device__ __forceinline__ void publish_final(const RollArgs &a, u128 s0, u128 inc) {
+    const bool lh = is_lehmer(inc);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const u128 sf = jump(s0, inc, (uint64_t)a.nb);
+        const u128 sf = gen_jump(s0, inc, (uint64_t)a.nb, lh);
         a.ws->final_hi = sf.hi;
         a.ws->final_lo = sf.lo;
     }
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     pdl_launch_dependents();
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
+    const bool lh = is_lehmer(inc);
     publish_final(a, s0, inc);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -292,12 +295,12 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     const int64_t nchunks = a.nb / CH;
     const int64_t cpw = (nchunks + nwarps - 1) / nwarps;
     const int64_t c0 = warp * cpw, c1 = min(c0 + cpw, nchunks);
-    const u128 M = mk128(PCG_MULT_HI, PCG_MULT_LO);
+    const u128 M = gen_mult(lh);
     if (c0 < c1) {
         const int64_t wb = c0 * CH;
-        u128 s = jump(s0, inc, (uint64_t)wb);
-        s = jump_small(s, inc, VB * lane + 1);
-        const u128 AJ = g_SA[32 * VB];
+        u128 s = gen_jump(s0, inc, (uint64_t)wb, lh);
+        s = gen_jump_small(s, inc, VB * lane + 1, lh);
+        const u128 AJ = gen_SA(lh, 32 * VB);
         const u128 CJ = mul128(g_SG[32 * VB], inc);
         const uint32_t *bp = a.bounds + (wb + VB * lane) * K;
         uint32_t *rp = a.rolls + (wb + VB * lane) * K;
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
                 const int64_t b0 = wb + (c - c0) * CH + 32 * VB * u + VB * lane;
 #pragma unroll
                 for (int v = 0; v < VB; ++v) {
-                    uint64_t r = xslrr(st);
+                    uint64_t r = gen_out(st, lh);
                     uint64_t prod;
                     if constexpr (K == 2) {
                         dd.v[2 * v] = die(cur[u].v[2 * v], r);
@@ -380,6 +383,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
     volatile RollWs *vws = ws;
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
+    const bool lh = is_lehmer(inc);
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     if (vws->error) {  // invalid bases: leave the source untouched (reference raises first)
         __syncthreads();
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
                 // batch `cur` rejected word cur + D: re-draw the whole batch from the next
                 // words until accepted (batched.py:120-122)
                 uint64_t widx = (uint64_t)cur + D + 1;
-                u128 st = jump(s0, inc, widx + 1);
+                u128 st = gen_jump(s0, inc, widx + 1, lh);
                 uint32_t bb[K];
                 load_bounds<K>(a.bounds + cur * K, bb);
                 uint64_t extra = 1;
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
                     uint64_t r;
                     uint8_t tc;
                     int err = 0;
-                    int res = eval_batch<K>(bb, xslrr(st), d, r, tc, err);
+                    int res = eval_batch<K>(bb, gen_out(st, lh), d, r, tc, err);
                     if (res != 1) {
                         store_rolls<K>(a.rolls + cur * K, d);
                         a.words[cur] = (uint8_t)(1 + extra > 255 ? 255 : 1 + extra);
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
                         break;
                     }
                     ++extra;
-                    st = mad128(st, mk128(PCG_MULT_HI, PCG_MULT_LO), inc);
+                    st = mad128(st, gen_mult(lh), inc);
                 }
                 ws->D = D + extra;
                 ws->neg_first = 0;
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
             a.state[0] = vws->final_hi;
             a.state[1] = vws->final_lo;
         } else {
-            const u128 sf = jump(s0, inc, (uint64_t)a.nb + D);
+            const u128 sf = gen_jump(s0, inc, (uint64_t)a.nb + D, lh);
             a.state[0] = sf.hi;
             a.state[1] = sf.lo;
         }

@@ -52,13 +52,13 @@ __device__ __forceinline__ void swap_sm(T *p, uint32_t i, uint32_t j) {
 // thread's array z (row of the block's shared buffer).  Fully unrolled per K.
 template <int K, typename T>
 __device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count, const uint64_t *thresh, u128 &s,
-                                              u128 inc, uint32_t &words) {
+                                              u128 inc, uint32_t &words, bool lh) {
     for (uint32_t c = 0; c < count; ++c, nb -= K) {
         const uint64_t t = __ldg(thresh + c);
         uint32_t d[K];
         uint64_t r;
         do {
-            r = pcg_next(s, inc);
+            r = gen_next(s, inc, lh);
             ++words;
 #pragma unroll
             for (int m = 0; m < K; ++m) d[m] = die(nb - m, r);
@@ -70,16 +70,17 @@ __device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count,
 
 template <typename T>
 __device__ __forceinline__ void small_segment_any(T *z, uint32_t k, uint32_t nb, uint32_t count,
-                                                  const uint64_t *thresh, u128 &s, u128 inc, uint32_t &words) {
+                                                  const uint64_t *thresh, u128 &s, u128 inc, uint32_t &words,
+                                                  bool lh) {
     switch (k) {
-        case 1: small_segment<1>(z, nb, count, thresh, s, inc, words); break;
-        case 2: small_segment<2>(z, nb, count, thresh, s, inc, words); break;
-        case 3: small_segment<3>(z, nb, count, thresh, s, inc, words); break;
-        case 4: small_segment<4>(z, nb, count, thresh, s, inc, words); break;
-        case 5: small_segment<5>(z, nb, count, thresh, s, inc, words); break;
-        case 6: small_segment<6>(z, nb, count, thresh, s, inc, words); break;
-        case 7: small_segment<7>(z, nb, count, thresh, s, inc, words); break;
-        default: small_segment<8>(z, nb, count, thresh, s, inc, words); break;
+        case 1: small_segment<1>(z, nb, count, thresh, s, inc, words, lh); break;
+        case 2: small_segment<2>(z, nb, count, thresh, s, inc, words, lh); break;
+        case 3: small_segment<3>(z, nb, count, thresh, s, inc, words, lh); break;
+        case 4: small_segment<4>(z, nb, count, thresh, s, inc, words, lh); break;
+        case 5: small_segment<5>(z, nb, count, thresh, s, inc, words, lh); break;
+        case 6: small_segment<6>(z, nb, count, thresh, s, inc, words, lh); break;
+        case 7: small_segment<7>(z, nb, count, thresh, s, inc, words, lh); break;
+        default: small_segment<8>(z, nb, count, thresh, s, inc, words, lh); break;
     }
 }
 
@@ -151,7 +152,7 @@ template <typename T>
 __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data, int64_t num_arrays,
                                                            DevPlan plan, uint32_t stride, uint32_t magic,
                                                            int vec_ok, uint64_t run_seed, int64_t base,
-                                                           uint32_t *__restrict__ words_out) {
+                                                           uint32_t *__restrict__ words_out, int gen) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevSeg segs[MAX_SEGS];
     T *buf = reinterpret_cast<T *>(smem_raw);
@@ -169,12 +170,13 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
     __syncthreads();
     if (tid < na) {
         u128 s, inc;
-        pcg_seed(array_seed(run_seed, (uint64_t)(base + a0 + tid)), s, inc);
+        const bool lh = gen != 0;
+        gen_seed(array_seed(run_seed, (uint64_t)(base + a0 + tid)), s, inc, lh);
         T *z = buf + tid * stride;
         uint32_t words = 0;
         for (uint32_t sg = 0; sg < plan.nseg; ++sg) {
             const DevSeg S = segs[sg];
-            small_segment_any<T>(z, S.k, S.start_n, S.count, plan.thresh + S.first_batch, s, inc, words);
+            small_segment_any<T>(z, S.k, S.start_n, S.count, plan.thresh + S.first_batch, s, inc, words, lh);
         }
         if (words_out) words_out[a0 + tid] = words;
     }
@@ -230,9 +232,10 @@ struct GenState {
 };
 
 __device__ __forceinline__ void gen_init(GenState &g, u128 s0, u128 inc, uint32_t n, int lane) {
+    const bool lh = is_lehmer(inc);
     g.inc = inc;
-    g.s = jump_small(s0, inc, lane + 1);
-    g.A32 = g_SA[32];
+    g.s = gen_jump_small(s0, inc, lane + 1, lh);
+    g.A32 = gen_SA(lh, 32);
     g.C32 = mul128(g_SG[32], inc);
     g.B0 = 0;
     g.D = 0;
@@ -244,6 +247,7 @@ __device__ __forceinline__ void gen_init(GenState &g, u128 s0, u128 inc, uint32_
 template <typename Sink>
 __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const DevSeg *segs, Sink sink, int lane,
                                          uint64_t *rk_first) {
+    const bool lh = is_lehmer(g.inc);
     const uint32_t nb = plan.nbatches;
     const uint32_t b = g.B0 + lane;
     bool fail = false;
@@ -254,7 +258,7 @@ __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const
         const DevSeg S = segs[sg];
         const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
         const uint64_t t = __ldg(plan.thresh + b);
-        uint64_t r = xslrr(g.s);
+        uint64_t r = gen_out(g.s, lh);
         const uint32_t pos = nbb - 1;
         for (uint32_t m = 0; m < S.k; ++m) sink(pos - m, die(nbb - m, r));
         low = nbb - S.k;
@@ -277,7 +281,7 @@ __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const
         const int l = __ffs(fm) - 1;
         g.B0 += l;
         g.D += 1;
-        g.s = jump_small(g.s, g.inc, l + 1);
+        g.s = gen_jump_small(g.s, g.inc, l + 1, lh);
     }
     while (g.seg + 1 < plan.nseg && segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
 }
@@ -372,7 +376,7 @@ template <typename T, bool SEGMENTED>
 __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
                                                          uint32_t zbytes, uint64_t run_seed, int64_t base,
                                                          uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                         uint64_t *words64, uint64_t *rk_first, int use_tma) {
+                                                         uint64_t *words64, uint64_t *rk_first, int use_tma, int gen) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevSeg segs[MAX_SEGS];
     __shared__ __align__(16) uint16_t ring[RING];
@@ -402,11 +406,14 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
             warp_copy(z, g, n, lane);
         }
         u128 s0, inc;
+        bool lh;
         if constexpr (SEGMENTED) {
-            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+            lh = gen != 0;
+            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
         } else {
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
+            lh = is_lehmer(inc);
         }
         GenState gs;
         gen_init(gs, s0, inc, n, lane);
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
             if constexpr (SEGMENTED) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = jump(s0, inc, words);
+                const u128 sf = gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -482,6 +489,7 @@ struct CtaGen {
 template <typename T, int W, typename RT>
 __device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, CtaShared<T, W, RT> &sh, int L,
                                              uint64_t *rk_first) {
+    const bool lh = is_lehmer(g.inc);
     constexpr int G = 32 * W;
     const uint32_t nb = plan.nbatches;
     const uint32_t b = g.B0 + L;
@@ -493,7 +501,7 @@ __device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, 
         const DevSeg S = sh.segs[sg];
         const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
         const uint64_t t = __ldg(plan.thresh + b);
-        uint64_t r = xslrr(g.s);
+        uint64_t r = gen_out(g.s, lh);
         const uint32_t pos = nbb - 1;
         for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (CRING - 1)] = (RT)die(nbb - m, r);
         low = nbb - S.k;
@@ -519,7 +527,7 @@ __device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, 
         if (f > 0) g.frontier = sh.frontier[par];
         g.B0 += f;
         g.D += 1;
-        g.s = jump_small(g.s, g.inc, (int)f + 1);
+        g.s = gen_jump_small(g.s, g.inc, (int)f + 1, lh);
         __syncthreads();  // fmin / frontier reuse
     }
     while (g.seg + 1 < plan.nseg && sh.segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
@@ -591,7 +599,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
                                                              uint32_t zbytes, uint64_t run_seed, int64_t base,
                                                              uint32_t *__restrict__ words32, uint64_t *state_io,
                                                              uint64_t *words64, uint64_t *rk_first, int use_tma,
-                                                             int segmented) {
+                                                             int segmented, int gen) {
     constexpr int G = 32 * W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CtaShared<T, W> sh;
@@ -621,16 +629,19 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
             for (uint32_t e = L; e < n; e += G) z[e] = g[e];
         }
         u128 s0, inc;
+        bool lh;
         if (segmented) {
-            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+            lh = gen != 0;
+            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
         } else {
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
+            lh = is_lehmer(inc);
         }
         CtaGen<W> gs;
         gs.inc = inc;
-        gs.s = jump_small(s0, inc, L + 1);
-        gs.AJ = g_SA[G];
+        gs.s = gen_jump_small(s0, inc, L + 1, lh);
+        gs.AJ = gen_SA(lh, G);
         gs.CJ = mul128(g_SG[G], inc);
         gs.B0 = 0;
         gs.D = 0;
@@ -677,7 +688,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ dat
             if (segmented) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = jump(s0, inc, words);
+                const u128 sf = gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -770,6 +781,7 @@ __device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W, R
 template <typename T, int W, typename RT, uint32_t RS, int HB>
 __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan, LargeShared<T, W, RT, RS, HB> &sh,
                                                int L, uint64_t *rk_first) {
+    const bool lh = is_lehmer(g.inc);
     constexpr int G = 32 * W;
     const uint32_t nb = plan.nbatches;
     const uint32_t b = g.B0 + L;
@@ -781,7 +793,7 @@ __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan
         const DevSeg S = sh.segs[sg];
         const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
         const uint64_t t = __ldg(plan.thresh + b);
-        uint64_t r = xslrr(g.s);
+        uint64_t r = gen_out(g.s, lh);
         const uint32_t pos = nbb - 1;
         for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (RS - 1)] = (RT)die(nbb - m, r);
         low = nbb - S.k;
@@ -807,7 +819,7 @@ __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan
         if (f > 0) g.frontier = sh.frontier[par];
         g.B0 += f;
         g.D += 1;
-        g.s = jump_small(g.s, g.inc, (int)f + 1);
+        g.s = gen_jump_small(g.s, g.inc, (int)f + 1, lh);
         __syncthreads();
     }
     while (g.seg + 1 < plan.nseg && sh.segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
@@ -818,7 +830,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
                                                                    DevPlan plan, uint64_t run_seed, int64_t base,
                                                                    uint32_t *__restrict__ words32, uint64_t *state_io,
                                                                    uint64_t *words64, uint64_t *rk_first,
-                                                                   int segmented) {
+                                                                   int segmented, int gen) {
     constexpr int G = 32 * W;
     __shared__ LargeShared<T, W> sh;
     const int L = threadIdx.x;
@@ -831,16 +843,19 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         T *z = data + a * (int64_t)n;
         u128 s0, inc;
+        bool lh;
         if (segmented) {
-            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+            lh = gen != 0;
+            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
         } else {
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
+            lh = is_lehmer(inc);
         }
         CtaGen<W> gs;
         gs.inc = inc;
-        gs.s = jump_small(s0, inc, L + 1);
-        gs.AJ = g_SA[G];
+        gs.s = gen_jump_small(s0, inc, L + 1, lh);
+        gs.AJ = gen_SA(lh, G);
         gs.CJ = mul128(g_SG[G], inc);
         gs.B0 = 0;
         gs.D = 0;
@@ -865,7 +880,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
             if (segmented) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = jump(s0, inc, words);
+                const u128 sf = gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -882,7 +897,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
                                                                   DevPlan plan, uint64_t run_seed, int64_t base,
                                                                   uint32_t *__restrict__ words32, uint64_t *state_io,
                                                                   uint64_t *words64, uint64_t *rk_first, int use_tma,
-                                                                  int segmented) {
+                                                                  int segmented, int gen) {
     constexpr int G = 32 * W;
     constexpr int HB = 10;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -911,16 +926,19 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
             for (uint32_t e = L; e < n; e += G) z[e] = g[e];
         }
         u128 s0, inc;
+        bool lh;
         if (segmented) {
-            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+            lh = gen != 0;
+            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
         } else {
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
+            lh = is_lehmer(inc);
         }
         CtaGen<W> gs;
         gs.inc = inc;
-        gs.s = jump_small(s0, inc, L + 1);
-        gs.AJ = g_SA[G];
+        gs.s = gen_jump_small(s0, inc, L + 1, lh);
+        gs.AJ = gen_SA(lh, G);
         gs.CJ = mul128(g_SG[G], inc);
         gs.B0 = 0;
         gs.D = 0;
@@ -959,7 +977,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
             if (segmented) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = jump(s0, inc, words);
+                const u128 sf = gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -978,7 +996,7 @@ template <bool SEGMENTED>
 __global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_arrays, DevPlan plan, uint64_t run_seed,
                                                                int64_t base, uint32_t *__restrict__ J,
                                                                uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                               uint64_t *words64, uint64_t *rk_first) {
+                                                               uint64_t *words64, uint64_t *rk_first, int gen) {
     __shared__ DevSeg segs[MAX_SEGS];
     const int lane = threadIdx.x & 31;
     for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
@@ -987,11 +1005,14 @@ __global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_array
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         uint32_t *Ja = J + a * (int64_t)n;
         u128 s0, inc;
+        bool lh;
         if constexpr (SEGMENTED) {
-            pcg_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc);
+            lh = gen != 0;
+            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
         } else {
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
+            lh = is_lehmer(inc);
         }
         GenState gs;
         gen_init(gs, s0, inc, n, lane);
@@ -1003,7 +1024,7 @@ __global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_array
             if constexpr (SEGMENTED) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = jump(s0, inc, words);
+                const u128 sf = gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;

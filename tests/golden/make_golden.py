@@ -220,6 +220,36 @@ def main():
             pb.append({"n": n, "k": k, "seed": seed, "u_in": u, "u_out": u2, "perm": z})
     out["partial_shuffle_batch"] = pb
 
+    # Lehmer128 (wordsource.py:51-67) through the same hot path
+    lsh = []
+    for n in (2, 3, 5, 64, 100, 1000, 4096, 10000, 70000):
+        for name in ("default", "pair"):
+            seed = rng.getrandbits(64)
+            src = CountingSource(R.make_source("lehmer", seed))
+            z = R.shuffle_batched(src, list(range(n)), scheds[name])
+            lsh.append({"n": n, "schedule": name, "seed": seed, "words": src.count, "sha": sha_u32(z)})
+    src = CountingSource(R.LehmerSource(31337))
+    R.shuffle_batched(src, list(range(1000)))
+    out["lehmer_31337_n1000_words"] = src.count
+    out["shuffle_batched_lehmer"] = lsh
+    lun = []
+    for n in (2, 17, 1000, 5000):
+        seed = rng.getrandbits(64)
+        src = CountingSource(R.make_source("lehmer", seed))
+        z = R.shuffle_unbatched(src, list(range(n)))
+        lun.append({"n": n, "seed": seed, "words": src.count, "sha": sha_u32(z)})
+    out["shuffle_unbatched_lehmer"] = lun
+    lrb = []
+    for seed, bases in ((31, (6, 5)), (32, (2**32 - 1, 2**31 + 11)), (33, (1 << 16, 3, 5))):
+        src = R.make_source("lehmer", seed)
+        spec = R.BatchSpec(R.RadixBases.of(bases, 64))
+        res = []
+        for _ in range(48):
+            r = R.roll_batch(src, spec)
+            res.append([list(r.digits), r.words_consumed, int(r.threshold_computed), r.final_remainder])
+        lrb.append({"seed": seed, "bases": list(bases), "results": res, "state_after": src.state})
+    out["roll_batch_lehmer"] = lrb
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)

@@ -42,7 +42,7 @@ def test_struct_layouts(N):
     assert C.sizeof(N.Pcg64State) == 32
     assert C.sizeof(N.Regime) == 16
     assert C.sizeof(N.Segment) == 24
-    assert N.lib().br_abi_version() == 1
+    assert N.lib().br_abi_version() == 2
 
 
 def test_host_generator_helpers_match_oracle(N, O, golden):
@@ -154,3 +154,16 @@ def test_host_source_matches_oracle(O):
     assert (s.state, s.increment) == (o.state, o.increment)
     assert [s.next_word() for _ in range(10)] == O.words(o, 10)
     assert [next(g) for g in [B.splitmix64_stream(7)] for _ in range(3)] == O.splitmix64(7, 3)
+
+
+def test_host_lehmer_matches_golden(N, golden):
+    import paper_2408_06213_b200 as B
+
+    L = N.lib()
+    for rec in golden["lehmer"]:
+        st = N.Pcg64State()
+        L.br_lehmer_seed(rec["seed"], C.byref(st))
+        assert (st.state_hi << 64 | st.state_lo) == rec["state"] and st.inc_hi == st.inc_lo == 0
+        assert [L.br_pcg64_next(C.byref(st)) for _ in range(8)] == rec["words"]
+        s = B.make_source("lehmer", rec["seed"])
+        assert [s.next_word() for _ in range(8)] == rec["words"]

@@ -405,3 +405,66 @@ def test_roll_single_dropin(B, O):  # bounded.py:73-104 via the k=1 batch kernel
         assert s.state == o.state
     with pytest.raises(B.BoundOverflow):
         B.roll_single(B.Pcg64Source(1), 0)
+
+
+# ------------------------------------------------------------------ Lehmer128
+def test_lehmer_fill_and_dropin_shuffles(B, O, golden):
+    got = u64(B.pcg64_fill(77, 5000, 123, generator="lehmer"))
+    o = O.lehmer(77)
+    O.words(o, 123)
+    assert got.tolist() == O.words(o, 5000)
+    scheds = {k: B.ShuffleSchedule(tuple(tuple(e) for e in v["entries"]), v["max_batch"])
+              for k, v in golden["schedules"].items()}
+    for rec in golden["shuffle_batched_lehmer"]:
+        s = B.LehmerSource(rec["seed"])
+        z = np.arange(rec["n"], dtype=np.uint32)
+        B.shuffle_batched(s, z, scheds[rec["schedule"]])
+        o = O.lehmer(rec["seed"])
+        O.shuffle_batched(o, np.arange(rec["n"], dtype=np.uint32), [tuple(e) for e in golden["schedules"][rec["schedule"]]["entries"]])
+        assert sha_u32(z) == rec["sha"] and s.state == o.state, rec["n"]
+    for rec in golden["shuffle_unbatched_lehmer"]:
+        s = B.LehmerSource(rec["seed"])
+        z = B.shuffle_unbatched(s, list(range(rec["n"])))
+        assert sha_u32(z) == rec["sha"]
+    # test_shuffle.py:154-161 word budget on the reference's own Lehmer seed
+    s = B.LehmerSource(31337)
+    B.shuffle_batched(s, list(range(1000)))
+    o = O.lehmer(31337)
+    O.words(o, golden["lehmer_31337_n1000_words"])
+    assert s.state == o.state
+
+
+@pytest.mark.parametrize("n,eb", [(64, 4), (100, 8), (4096, 4), (20000, 8), (70000, 4)])
+def test_lehmer_segmented(B, O, n, eb):
+    na = max(2, min(500, (1 << 20) // n))
+    dt = np.uint32 if eb == 4 else np.uint64
+    payload = np.arange(n * na, dtype=dt)
+    dev = torch.from_numpy(payload.view(np.int32 if eb == 4 else np.int64).copy()).cuda()
+    _, w = B.shuffle_many(dev, n, 4242, array_index_base=9, return_words=True, generator="lehmer")
+    ref = payload.copy()
+    rw = O.shuffle_segmented(ref, n, 4242, array_index_base=9, generator="lehmer")
+    assert np.array_equal(dev.cpu().numpy().view(dt), ref), B.last_kernel()
+    assert np.array_equal(u32(w), rw)
+
+
+def test_lehmer_rolls(B, O, golden):
+    for rec in golden["roll_batch_lehmer"]:
+        s = B.LehmerSource(rec["seed"])
+        k = len(rec["bases"])
+        res = B.roll_batches(s, dev_u32(np.tile(np.asarray(rec["bases"], dtype=np.uint32), len(rec["results"]))), k,
+                             flags=True, final_remainder=True)
+        assert u32(res.rolls).reshape(-1, k).tolist() == [x[0] for x in rec["results"]]
+        assert res.words.cpu().tolist() == [x[1] for x in rec["results"]]
+        assert u64(res.final_remainder).tolist() == [x[3] for x in rec["results"]]
+        assert s.state == rec["state_after"]
+    nb = 300000
+    bounds = O.gen_bounds(8, 2 * nb)
+    bounds[:1000:2] = 0xFFFFFFFF
+    bounds[1:1000:2] = 3006477107
+    src = O.lehmer(5)
+    rolls, words, _, _ = O.roll_batches(src, bounds, 2)
+    ds = B.DeviceStream(5, generator="lehmer")
+    r = B.roll_batches(ds, dev_u32(bounds), 2)
+    st = ds.host_state()
+    assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words)
+    assert (st.state_hi << 64 | st.state_lo) == src.state
