@@ -332,11 +332,11 @@ def test_dropin_accepts_reference_style_source(B, O):
     assert z == O.shuffle_batched(o, np.arange(1000, dtype=np.uint32)).tolist()
     assert s.state == o.state
     with pytest.raises(TypeError):
-        class Lehmerish:
+        class Mystery:  # neither a PCG64 (state+increment) nor a Lehmer source
             word_bits = 64
             state = 5
 
-        B.shuffle_batched(Lehmerish(), list(range(10)))
+        B.shuffle_batched(Mystery(), list(range(10)))
 
 
 def test_short_arrays_finish_in_one_batch(B):
