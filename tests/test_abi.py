@@ -167,3 +167,19 @@ def test_host_lehmer_matches_golden(N, golden):
         assert [L.br_pcg64_next(C.byref(st)) for _ in range(8)] == rec["words"]
         s = B.make_source("lehmer", rec["seed"])
         assert [s.next_word() for _ in range(8)] == rec["words"]
+
+
+def test_cli_parser_and_csv_schema():
+    """The device CLI keeps the reference's CSV schema (cli.py:27) and argument surface."""
+    import io
+
+    from paper_2408_06213_b200 import cli
+
+    assert cli.CSV_HEADER == "algorithm,generator,n,avg_ns_per_element,min_ns_per_element"
+    args = cli.build_parser().parse_args(["bench", "--sizes", "64,128", "--algorithms", "shuffle_6_b200"])
+    assert args.sizes == (64, 128) and args.algorithms == ("shuffle_6_b200",)
+    buf = io.StringIO()
+    cli.write_csv([("shuffle_6_b200", "pcg64", 64, 12.5, 11.25)], buf)
+    assert buf.getvalue().splitlines() == [cli.CSV_HEADER, "shuffle_6_b200,pcg64,64,12.500,11.250"]
+    with pytest.raises(SystemExit):
+        cli.build_parser().parse_args(["bench", "--sizes", "1"])

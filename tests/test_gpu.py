@@ -468,3 +468,23 @@ def test_lehmer_rolls(B, O, golden):
     st = ds.host_state()
     assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words)
     assert (st.state_hi << 64 | st.state_lo) == src.state
+
+
+def test_cli_bench_and_shuffle(B, O, tmp_path):
+    import io
+    import contextlib
+
+    from paper_2408_06213_b200 import cli
+
+    recs = cli.bench("pcg64", (64, 4096), ("shuffle_6_b200", "many_6_b200"), budget_ns=200_000)
+    assert [(r[0], r[2]) for r in recs] == [("shuffle_6_b200", 64), ("shuffle_6_b200", 4096),
+                                            ("many_6_b200", 64), ("many_6_b200", 4096)]
+    assert all(r[3] >= r[4] > 0 for r in recs)
+    inp = tmp_path / "lines.txt"
+    inp.write_text("\n".join(f"line{i}" for i in range(500)) + "\n")
+    out = io.StringIO()
+    with contextlib.redirect_stdout(out):
+        assert cli.main(["shuffle", str(inp), "--seed", "7"]) == 0
+    got = out.getvalue().splitlines()
+    perm = O.shuffle_batched(O.pcg64(7), np.arange(500, dtype=np.uint32)).tolist()
+    assert got == [f"line{p}" for p in perm]
