@@ -69,6 +69,69 @@ void or_source_fixed(or_source *s, const uint64_t *words, int64_t n, int32_t bit
     s->nwords = n;
 }
 
+/* wordsource.py:92-99 round pattern and constants */
+static const int CHACHA_IDX[8][4] = {{0, 4, 8, 12}, {1, 5, 9, 13}, {2, 6, 10, 14}, {3, 7, 11, 15},
+                                     {0, 5, 10, 15}, {1, 6, 11, 12}, {2, 7, 8, 13}, {3, 4, 9, 14}};
+static inline uint32_t rotl32(uint32_t v, int r) { return (v << r) | (v >> (32 - r)); }
+
+/* wordsource.py:102-133 chacha_block */
+void or_chacha_block(const uint32_t key[8], uint64_t counter, uint64_t nonce, uint32_t out[16]) {
+    uint32_t init[16] = {0x61707865u, 0x3320646Eu, 0x79622D32u, 0x6B206574u};
+    for (int i = 0; i < 8; ++i) init[4 + i] = key[i];
+    init[12] = (uint32_t)counter;
+    init[13] = (uint32_t)(counter >> 32);
+    init[14] = (uint32_t)nonce;
+    init[15] = (uint32_t)(nonce >> 32);
+    uint32_t x[16];
+    memcpy(x, init, sizeof x);
+    for (int r = 0; r < 10; ++r) {
+        for (int q = 0; q < 8; ++q) {
+            const int a = CHACHA_IDX[q][0], b = CHACHA_IDX[q][1], c = CHACHA_IDX[q][2], d = CHACHA_IDX[q][3];
+            x[a] += x[b]; x[d] = rotl32(x[d] ^ x[a], 16);
+            x[c] += x[d]; x[b] = rotl32(x[b] ^ x[c], 12);
+            x[a] += x[b]; x[d] = rotl32(x[d] ^ x[a], 8);
+            x[c] += x[d]; x[b] = rotl32(x[b] ^ x[c], 7);
+        }
+    }
+    for (int i = 0; i < 16; ++i) out[i] = x[i] + init[i];
+}
+
+/* wordsource.py:147-153 ChaChaSource.__init__ */
+void or_source_chacha(or_source *s, uint64_t seed) {
+    memset(s, 0, sizeof(*s));
+    s->kind = 3;
+    s->word_bits = 64;
+    uint64_t x = seed;
+    for (int i = 0; i < 4; ++i) {
+        uint64_t c = or_splitmix64_next(&x);
+        s->key[2 * i] = (uint32_t)c;
+        s->key[2 * i + 1] = (uint32_t)(c >> 32);
+    }
+    s->nonce = or_splitmix64_next(&x);
+    s->counter = 0;
+    s->pos = 16;
+}
+
+/* position arithmetic on the ChaCha source: the next word is word pos/2 of the buffered
+ * block counter-1, or word 0 of block `counter` when the buffer is empty.  Skipping delta
+ * words lands on block (P + delta) / 8 with the same refill rule as next_word. */
+void or_chacha_advance(or_source *s, uint64_t delta) {
+    /* absolute word position mod 2^67, as (block, word) */
+    uint64_t blk = s->pos == 16 ? s->counter : s->counter - 1;
+    uint64_t w = s->pos == 16 ? 0 : (uint64_t)(s->pos / 2);
+    uint64_t t = w + (delta & 7);
+    blk += (delta >> 3) + (t >> 3);
+    w = t & 7;
+    if (w == 0) {
+        s->counter = blk;
+        s->pos = 16;
+    } else {
+        or_chacha_block(s->key, blk, s->nonce, s->buf);
+        s->counter = blk + 1;
+        s->pos = (int32_t)(2 * w);
+    }
+}
+
 int or_next_word(or_source *s, uint64_t *w) {
     if (s->kind == 0) {
         /* wordsource.py:85-89 Pcg64Source.next_word: update, then XSL-RR of the new state */
@@ -85,6 +148,15 @@ int or_next_word(or_source *s, uint64_t *w) {
         s->state_hi = (uint64_t)(st >> 64);
         s->state_lo = (uint64_t)st;
         *w = s->state_hi;
+    } else if (s->kind == 3) {
+        /* wordsource.py:155-164 ChaChaSource.next_word */
+        if (s->pos == 16) {
+            or_chacha_block(s->key, s->counter, s->nonce, s->buf);
+            s->counter += 1;
+            s->pos = 0;
+        }
+        *w = (uint64_t)s->buf[s->pos] | ((uint64_t)s->buf[s->pos + 1] << 32);
+        s->pos += 2;
     } else {
         /* wordsource.py:202-207 FixedSequenceSource.next_word */
         if (s->cursor >= s->nwords) return OR_E_EXHAUSTED;
@@ -561,7 +633,9 @@ int or_shuffle_segmented_gen(void *data, int32_t eb, int64_t num_arrays, uint64_
 #endif
     for (int64_t a = 0; a < num_arrays; ++a) {
         or_source src;
-        if (generator == 1)
+        if (generator == 2)
+            or_source_chacha(&src, or_array_seed(run_seed, (uint64_t)(base + a)));
+        else if (generator == 1)
             or_source_lehmer(&src, or_array_seed(run_seed, (uint64_t)(base + a)));
         else
             or_source_pcg64(&src, or_array_seed(run_seed, (uint64_t)(base + a)));
@@ -583,7 +657,10 @@ void or_pcg64_fill(const or_source *s0, uint64_t offset, uint64_t *out, int64_t 
 #endif
     for (int64_t c = 0; c < nch; ++c) {
         or_source s = *s0;
-        or_pcg64_advance(&s, offset + (uint64_t)(c * CH));
+        if (s.kind == 3)
+            or_chacha_advance(&s, offset + (uint64_t)(c * CH));
+        else
+            or_pcg64_advance(&s, offset + (uint64_t)(c * CH));
         int64_t end = (c + 1) * CH < count ? (c + 1) * CH : count;
         for (int64_t i = c * CH; i < end; ++i) or_next_word(&s, &out[i]);
     }

@@ -44,6 +44,11 @@ class Source(C.Structure):
         ("nwords", C.c_int64),
         ("cursor", C.c_int64),
         ("drawn", C.c_int64),
+        ("key", C.c_uint32 * 8),
+        ("nonce", C.c_uint64),
+        ("counter", C.c_uint64),
+        ("pos", C.c_int32),
+        ("buf", C.c_uint32 * 16),
     ]
 
     @property
@@ -104,6 +109,9 @@ def lib():
             "or_shuffle_segmented": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, vp, i32, vp, i32, i32]),
             "or_shuffle_segmented_gen": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, vp, i32, vp, i32, i32, i32]),
             "or_pcg64_fill": (None, [P(Source), u64, vp, i64]),
+            "or_chacha_block": (None, [vp, u64, u64, vp]),
+            "or_source_chacha": (None, [P(Source), u64]),
+            "or_chacha_advance": (None, [P(Source), u64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -146,6 +154,27 @@ def lehmer(seed: int) -> Source:
     return s
 
 
+def chacha(seed: int) -> Source:
+    s = Source()
+    lib().or_source_chacha(C.byref(s), seed & MASK64)
+    return s
+
+
+def chacha_block(key_words, counter: int, nonce: int) -> list[int]:
+    key = np.asarray(key_words, dtype=np.uint32)
+    out = np.zeros(16, dtype=np.uint32)
+    lib().or_chacha_block(_ptr(key), counter & MASK64, nonce & MASK64, _ptr(out))
+    return out.tolist()
+
+
+def chacha_position(s: Source) -> int:
+    """Absolute word position of a ChaCha source's next word (block*8 + word)."""
+    return s.counter * 8 if s.pos == 16 else (s.counter - 1) * 8 + s.pos // 2
+
+
+GENERATOR_MAKERS = {"pcg64": pcg64, "lehmer": lehmer, "chacha": chacha}
+
+
 def fixed(words, bits: int = 64) -> Source:
     arr = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
     s = Source()
@@ -165,7 +194,10 @@ def words(s: Source, count: int) -> list[int]:
 
 
 def advance(s: Source, delta: int) -> None:
-    lib().or_pcg64_advance(C.byref(s), delta & MASK64)
+    if s.kind == 3:
+        lib().or_chacha_advance(C.byref(s), delta & MASK64)
+    else:
+        lib().or_pcg64_advance(C.byref(s), delta & MASK64)
 
 
 def array_seed(run_seed: int, a: int) -> int:
@@ -294,6 +326,6 @@ def shuffle_segmented(data: np.ndarray, n: int, run_seed: int, array_index_base:
     wds = np.empty(num_arrays, dtype=np.uint32)
     _check(lib().or_shuffle_segmented_gen(_ptr(data), data.dtype.itemsize, num_arrays, n, run_seed & MASK64,
                                           array_index_base, _ptr(lengths), _ptr(sizes), len(entries), _ptr(wds),
-                                          nthreads, int(unbatched), {"pcg64": 0, "lehmer": 1}[generator]),
+                                          nthreads, int(unbatched), {"pcg64": 0, "lehmer": 1, "chacha": 2}[generator]),
            "shuffle_segmented")
     return wds

@@ -23,6 +23,7 @@ one seed each), ``pcg64_fill`` and ``digit_pass_many``.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import math
 from dataclasses import dataclass
 from typing import NamedTuple, Optional
@@ -423,14 +424,33 @@ def _device_payload(z, torch):
     return idx, fin
 
 
+_TLS = threading.local()
+
+
+def _call_scratch(torch):
+    """Per-thread, per-device 8-word device scratch (state, words, rk) reused by the
+    single-array calls; every such call ends with a synchronising state download, so the
+    scratch is free again when the next call on this thread starts."""
+    dev = torch.cuda.current_device()
+    cache = getattr(_TLS, "scratch", None)
+    if cache is None:
+        cache = _TLS.scratch = {}
+    t = cache.get(dev)
+    if t is None:
+        t = cache[dev] = torch.zeros(8, dtype=torch.int64, device="cuda")
+    return t
+
+
 def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=False):
     torch = _torch()
     st = _state_struct(source)
     dev, fin = _device_payload(z, torch)
     n = dev.numel()
-    ds = DeviceStream.from_struct(st)
-    words = torch.zeros(1, dtype=torch.int64, device="cuda")
-    rk = torch.zeros(1, dtype=torch.int64, device="cuda") if want_rk else None
+    scratch = _call_scratch(torch)
+    ds = DeviceStream.__new__(DeviceStream)
+    ds._init(st, scratch[0:4])
+    words = scratch[4:5]
+    rk = scratch[5:6] if want_rk else None
     L = N.lib()
     if segments is None:
         regs = regimes if regimes is not None else (N.Regime * 1)()
@@ -509,11 +529,19 @@ class DeviceStream:
         self._init(st)
         return self
 
-    def _init(self, st):
+    def _init(self, st, state=None):
         torch = _torch()
-        self.state = torch.empty(4, dtype=torch.int64, device="cuda")
-        self.workspace = torch.zeros(N.lib().br_roll_workspace_bytes(), dtype=torch.uint8, device="cuda")
+        self.state = torch.empty(4, dtype=torch.int64, device="cuda") if state is None else state
+        self._workspace = None
         N.check(N.lib().br_state_upload(_ptr(self.state), C.byref(st), _stream_ptr(torch)), "state upload")
+
+    @property
+    def workspace(self):
+        """Roll-kernel workspace (rejection bookkeeping), allocated on first bulk roll."""
+        if self._workspace is None:
+            torch = _torch()
+            self._workspace = torch.zeros(N.lib().br_roll_workspace_bytes(), dtype=torch.uint8, device="cuda")
+        return self._workspace
 
     def host_state(self) -> N.Pcg64State:
         torch = _torch()

@@ -250,6 +250,47 @@ def main():
         lrb.append({"seed": seed, "bases": list(bases), "results": res, "state_after": src.state})
     out["roll_batch_lehmer"] = lrb
 
+    # ChaCha20 keystream (wordsource.py:102-164) through the same hot path
+    out["chacha"] = []
+    for seed in (0, 1, 3, 42, 12345, MASK64):
+        src = R.make_source("chacha", seed)
+        out["chacha"].append({"seed": seed, "key": list(src.key_words), "nonce": src.nonce,
+                              "words": [src.next_word() for _ in range(20)]})
+    rfc_key = tuple(int.from_bytes(bytes(range(32))[i:i + 4], "little") for i in range(0, 32, 4))
+    out["chacha_block_rfc8439"] = {"key": list(rfc_key), "counter": (0x09000000 << 32) | 1, "nonce": 0x4A000000,
+                                   "block": list(R.chacha_block(rfc_key, (0x09000000 << 32) | 1, 0x4A000000))}
+    csh = []
+    for n in (2, 3, 5, 64, 100, 1000, 4096, 10000, 70000):
+        for name in ("default", "pair", "max3"):
+            seed = rng.getrandbits(64)
+            pre = rng.randrange(0, 9)  # start mid-block: words already drawn from the source
+            src = R.make_source("chacha", seed)
+            for _ in range(pre):
+                src.next_word()
+            cs = CountingSource(src)
+            z = R.shuffle_batched(cs, list(range(n)), scheds[name])
+            csh.append({"n": n, "schedule": name, "seed": seed, "pre": pre, "words": cs.count, "sha": sha_u32(z),
+                        "counter_after": src.counter, "pos_after": src._pos})
+    out["shuffle_batched_chacha"] = csh
+    cun = []
+    for n in (2, 17, 1000, 5000):
+        seed = rng.getrandbits(64)
+        src = CountingSource(R.make_source("chacha", seed))
+        z = R.shuffle_unbatched(src, list(range(n)))
+        cun.append({"n": n, "seed": seed, "words": src.count, "sha": sha_u32(z)})
+    out["shuffle_unbatched_chacha"] = cun
+    crb = []
+    for seed, bases in ((41, (6, 5)), (42, (2**32 - 1, 2**31 + 11)), (43, (1 << 16, 3, 5)), (44, (7,))):
+        src = R.make_source("chacha", seed)
+        spec = R.BatchSpec(R.RadixBases.of(bases, 64))
+        res = []
+        for _ in range(48):
+            r = R.roll_batch(src, spec)
+            res.append([list(r.digits), r.words_consumed, int(r.threshold_computed), r.final_remainder])
+        crb.append({"seed": seed, "bases": list(bases), "results": res, "counter_after": src.counter,
+                    "pos_after": src._pos})
+    out["roll_batch_chacha"] = crb
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
