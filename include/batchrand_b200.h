@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define BR_ABI_VERSION 2
+#define BR_ABI_VERSION 3
 
 /* Status codes.  Python mapping (errors.py:4-37): */
 #define BR_OK 0
@@ -48,6 +48,20 @@ typedef struct br_pcg64 {
     uint64_t state_hi, state_lo;
     uint64_t inc_hi, inc_lo;
 } br_pcg64;
+
+/* ChaCha20 keystream (wordsource.py:136-164): a br_pcg64 head followed by the key.
+ *   head.state = absolute position of the next word (ChaChaSource: counter*8 when the
+ *                buffer is empty, else (counter-1)*8 + _pos/2); the next word is 64-bit
+ *                word (position % 8) of block (position / 8) mod 2^64
+ *   head.inc_hi = nonce, head.inc_lo = BR_CHACHA_TAG (even and non-zero, so no PCG64 or
+ *                Lehmer state carries it)
+ * Every entry point taking a br_pcg64* (host or device) reads the 64-byte br_chacha when
+ * it sees the tag, so a ChaCha state buffer must be a whole br_chacha. */
+#define BR_CHACHA_TAG 2
+typedef struct br_chacha {
+    br_pcg64 head;
+    uint32_t key[8];
+} br_chacha;
 
 /* One regime of a ShuffleSchedule: (max_length, batch_size) (shuffle.py:22-30). */
 typedef struct br_regime {
@@ -77,9 +91,12 @@ uint64_t br_splitmix64_next(uint64_t *x);
 void br_pcg64_seed(uint64_t seed, br_pcg64 *out);
 /* wordsource.py:61-63 LehmerSource.__init__ (increment 0) */
 void br_lehmer_seed(uint64_t seed, br_pcg64 *out);
-/* wordsource.py:85-89 Pcg64Source.next_word / :65-67 LehmerSource.next_word */
+/* wordsource.py:147-153 ChaChaSource.__init__ (position 0) */
+void br_chacha_seed(uint64_t seed, br_chacha *out);
+/* wordsource.py:85-89 Pcg64Source.next_word / :65-67 LehmerSource.next_word /
+ * :155-164 ChaChaSource.next_word (any of the three, told apart by the increment) */
 uint64_t br_pcg64_next(br_pcg64 *st);
-/* O(log d) jump-ahead by `delta` words (numpy PCG64.advance semantics) */
+/* O(log d) jump-ahead by `delta` words (numpy PCG64.advance semantics; ChaCha: position + d) */
 void br_pcg64_advance(br_pcg64 *st, uint64_t delta);
 /* Per-array seed convention: first splitmix64 output of ((run_seed << 32) | a) mod 2^64 */
 uint64_t br_array_seed(uint64_t run_seed, uint64_t array_index);
@@ -99,8 +116,9 @@ int64_t br_plan_build(uint64_t n, const br_regime *entries, int n_entries, br_se
 /* out_dev[i] = word (offset + i) of the stream `st` (host struct, not modified). */
 int br_pcg64_fill(uint64_t *out_dev, int64_t count, const br_pcg64 *st, uint64_t offset,
                   void *stream);
-/* Copy a host state to/from device memory on `stream` (the host copy is synchronous for
- * br_state_download: it synchronises `stream`). */
+/* Copy a host state to/from device memory on `stream` (both synchronise `stream`).  Upload
+ * copies a whole br_chacha for a ChaCha state; download copies the 32-byte head (the key
+ * never changes). */
 int br_state_upload(br_pcg64 *state_dev, const br_pcg64 *st, void *stream);
 int br_state_download(br_pcg64 *st, const br_pcg64 *state_dev, void *stream);
 
@@ -110,7 +128,8 @@ int br_state_download(br_pcg64 *st, const br_pcg64 *state_dev, void *stream);
  *       r = roll_batch(src, BatchSpec(RadixBases.of(bounds[i*k:(i+1)*k])))
  *       rolls[i*k:(i+1)*k] = r.digits; words[i] = min(r.words_consumed, 255)
  *       flags[i] = r.threshold_computed; final_rk[i] = r.final_remainder
- * with src the PCG64 stream in *state_dev (advanced in place by the words consumed).
+ * with src the stream in *state_dev (PCG64, Lehmer or ChaCha; advanced in place by the
+ * words consumed).
  * bounds are u32 (>= 1); flags_dev / final_rk_dev may be NULL.  `workspace_dev` is
  * br_roll_workspace_bytes() of zero-initialised device memory, reusable across calls on
  * one stream (calls sharing a workspace must be stream-ordered).  Invalid bounds (a zero
@@ -139,7 +158,8 @@ int br_digit_pass(const uint64_t *words_dev, const uint32_t *bounds_dev, int k, 
 
 /* ---------------------------------------------------------------- device: shuffles */
 /* shuffle.py:149-225 shuffle_batched(src, z, schedule) on one device array of n elements
- * (elem_bytes 4 or 8), src = the PCG64 stream in *state_dev (advanced in place).
+ * (elem_bytes 4 or 8), src = the stream in *state_dev (PCG64, Lehmer or ChaCha; advanced
+ * in place).
  * unbatched != 0 runs shuffle.py:80-97 shuffle_unbatched instead (schedule ignored).
  * words_dev (may be NULL) receives the words consumed (u64). */
 int br_shuffle_stream(void *z_dev, int elem_bytes, uint64_t n, br_pcg64 *state_dev,
@@ -154,7 +174,7 @@ int br_shuffle_stream_segments(void *z_dev, int elem_bytes, uint64_t n, br_pcg64
 /* Many independent shuffles: array a (0 <= a < num_arrays) of n elements at
  * data_dev + a*n*elem_bytes is shuffled in place by
  *     shuffle_batched(make_source(G, br_array_seed(run_seed, array_index_base + a)), z)
- * with G = "pcg64" (generator 0) or "lehmer" (generator 1).
+ * with G = "pcg64" (generator 0), "lehmer" (generator 1) or "chacha" (generator 2).
  * array_index_base lets shards of one job run on different GPUs with no exchange.
  * words_dev (may be NULL) receives words consumed per array (u32). */
 int br_shuffle_segmented(void *data_dev, int elem_bytes, int64_t num_arrays, uint64_t n,

@@ -13,7 +13,8 @@ import os
 from .errors import BoundOverflow, SourceExhausted
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libbatchrand_b200.so")
+# BR_LIB overrides the library path (A/B timing of two builds; tools/ only)
+LIB_PATH = os.environ.get("BR_LIB") or os.path.join(HERE, "lib", "libbatchrand_b200.so")
 
 BR_OK, BR_E_INVALID, BR_E_BOUND_OVERFLOW, BR_E_EXHAUSTED, BR_E_CUDA, BR_E_UNSUPPORTED = range(6)
 
@@ -22,6 +23,15 @@ u64, u32, i32, i64, vp, sz = C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_v
 
 class Pcg64State(C.Structure):
     _fields_ = [("state_hi", u64), ("state_lo", u64), ("inc_hi", u64), ("inc_lo", u64)]
+
+
+class ChachaState(Pcg64State):
+    """br_chacha: the br_pcg64 head (position, nonce, tag) followed by the 8 key words."""
+
+    _fields_ = [("key", u32 * 8)]
+
+
+BR_CHACHA_TAG = 2
 
 
 class Regime(C.Structure):
@@ -41,6 +51,7 @@ PROTOTYPES = {
     "br_splitmix64_next": (u64, [P(u64)]),
     "br_pcg64_seed": (None, [u64, P(Pcg64State)]),
     "br_lehmer_seed": (None, [u64, P(Pcg64State)]),
+    "br_chacha_seed": (None, [u64, P(ChachaState)]),
     "br_pcg64_next": (u64, [P(Pcg64State)]),
     "br_pcg64_advance": (None, [P(Pcg64State), u64]),
     "br_array_seed": (u64, [u64, u64]),
@@ -78,6 +89,8 @@ def lib():
             )
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in PROTOTYPES.items():
+            if os.environ.get("BR_LIB") and not hasattr(L, name):
+                continue  # an older build under A/B test
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -101,14 +101,75 @@ class LehmerSource(WordSource):
         return w
 
 
-GENERATORS = {"pcg64": Pcg64Source, "lehmer": LehmerSource}
-_GENERATOR_IDS = {"pcg64": 0, "lehmer": 1}
+class ChaChaSource(WordSource):
+    """ChaCha20 keystream consumed as 64-bit words (wordsource.py:136-164), with the
+    reference's fields (key_words, nonce, counter, _buffer, _pos).  On the device a ChaCha
+    stream is a position plus key and nonce (br_chacha); blocks are computed by the native
+    library."""
+
+    word_bits = 64
+
+    def __init__(self, seed: int = 0):
+        st = N.ChachaState()
+        N.lib().br_chacha_seed(seed & MASK64, C.byref(st))
+        self.key_words = tuple(int(k) for k in st.key)
+        self.nonce = st.inc_hi
+        self.counter = 0
+        self._buffer = [0] * 16
+        self._pos = 16  # empty; filled on first use
+
+    def next_word(self) -> int:
+        pos = self._pos
+        if pos == 16:
+            self._buffer = _chacha_block_words(self.key_words, self.nonce, self.counter)
+            self.counter = (self.counter + 1) & MASK64
+            pos = 0
+        self._pos = pos + 2
+        return self._buffer[pos] | (self._buffer[pos + 1] << 32)
+
+
+def _chacha_block_words(key_words, nonce: int, block: int) -> list:
+    """The 16 keystream u32 of one block (wordsource.py:102-133), from the native library."""
+    st = N.ChachaState()
+    st.state_hi, st.state_lo = block >> 61, (block << 3) & MASK64
+    st.inc_hi, st.inc_lo = nonce & MASK64, N.BR_CHACHA_TAG
+    for i, k in enumerate(key_words):
+        st.key[i] = k
+    out = []
+    for _ in range(8):
+        w = N.lib().br_pcg64_next(C.byref(st))
+        out += [w & 0xFFFFFFFF, w >> 32]
+    return out
+
+
+def _is_chacha(source) -> bool:
+    return all(hasattr(source, a) for a in ("key_words", "nonce", "counter", "_pos"))
+
+
+def _chacha_position(source) -> int:
+    """Absolute position of the next word: counter*8 with an empty buffer, else the
+    buffered block (counter-1) and word _pos/2 (wordsource.py:155-164)."""
+    if source._pos == 16:
+        return int(source.counter) * 8
+    return ((int(source.counter) - 1) & MASK64) * 8 + source._pos // 2
+
+
+def _chacha_set_position(source, p: int) -> None:
+    p &= (1 << 67) - 1
+    blk, q = p >> 3, p & 7
+    if q == 0:
+        source.counter, source._pos = blk, 16
+    else:
+        source._buffer = _chacha_block_words(source.key_words, source.nonce, blk)
+        source.counter, source._pos = (blk + 1) & MASK64, 2 * q
+
+
+GENERATORS = {"pcg64": Pcg64Source, "lehmer": LehmerSource, "chacha": ChaChaSource}
+_GENERATOR_IDS = {"pcg64": 0, "lehmer": 1, "chacha": 2}
 
 
 def make_source(name: str, seed: int = 0) -> WordSource:
-    """wordsource.py:217-225.  pcg64 and lehmer have device implementations."""
-    if name == "chacha":
-        raise NotImplementedError("generator 'chacha' has no device implementation yet")
+    """wordsource.py:217-225.  Every named generator has a device implementation."""
     try:
         cls = GENERATORS[name]
     except KeyError:
@@ -126,6 +187,16 @@ def _is_lehmer(source) -> bool:
 
 
 def _state_struct(source) -> N.Pcg64State:
+    if getattr(source, "word_bits", 64) != 64:
+        raise TypeError("the device path needs 64-bit words")
+    if _is_chacha(source):
+        st = N.ChachaState()
+        p = _chacha_position(source)
+        st.state_hi, st.state_lo = p >> 64, p & MASK64
+        st.inc_hi, st.inc_lo = int(source.nonce) & MASK64, N.BR_CHACHA_TAG
+        for i, k in enumerate(source.key_words):
+            st.key[i] = int(k)
+        return st
     try:
         if _is_lehmer(source):  # reference LehmerSource or ours: state only, increment 0
             state, inc = int(source.state), 0
@@ -133,10 +204,8 @@ def _state_struct(source) -> N.Pcg64State:
             state, inc = int(source.state), int(source.increment)
     except AttributeError:
         raise TypeError(
-            f"{type(source).__name__} is not a PCG64 or Lehmer source; the device path draws those words only"
+            f"{type(source).__name__} is not a PCG64, Lehmer or ChaCha source; the device path draws those words only"
         ) from None
-    if getattr(source, "word_bits", 64) != 64:
-        raise TypeError("the device path needs 64-bit words")
     st = N.Pcg64State()
     st.state_hi, st.state_lo = (state >> 64) & MASK64, state & MASK64
     st.inc_hi, st.inc_lo = (inc >> 64) & MASK64, inc & MASK64
@@ -428,7 +497,7 @@ _TLS = threading.local()
 
 
 def _call_scratch(torch):
-    """Per-thread, per-device 8-word device scratch (state, words, rk) reused by the
+    """Per-thread, per-device 16-word device scratch (state, words, rk) reused by the
     single-array calls; every such call ends with a synchronising state download, so the
     scratch is free again when the next call on this thread starts."""
     dev = torch.cuda.current_device()
@@ -437,7 +506,7 @@ def _call_scratch(torch):
         cache = _TLS.scratch = {}
     t = cache.get(dev)
     if t is None:
-        t = cache[dev] = torch.zeros(8, dtype=torch.int64, device="cuda")
+        t = cache[dev] = torch.zeros(16, dtype=torch.int64, device="cuda")
     return t
 
 
@@ -448,9 +517,9 @@ def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=
     n = dev.numel()
     scratch = _call_scratch(torch)
     ds = DeviceStream.__new__(DeviceStream)
-    ds._init(st, scratch[0:4])
-    words = scratch[4:5]
-    rk = scratch[5:6] if want_rk else None
+    ds._init(st, scratch[0:8])
+    words = scratch[8:9]
+    rk = scratch[9:10] if want_rk else None
     L = N.lib()
     if segments is None:
         regs = regimes if regimes is not None else (N.Regime * 1)()
@@ -515,6 +584,9 @@ class DeviceStream:
             N.lib().br_lehmer_seed(seed & MASK64, C.byref(st))
         elif generator == "pcg64":
             N.lib().br_pcg64_seed(seed & MASK64, C.byref(st))
+        elif generator == "chacha":
+            st = N.ChachaState()
+            N.lib().br_chacha_seed(seed & MASK64, C.byref(st))
         else:
             raise UnknownGenerator(f"no device generator {generator!r}")
         self._init(st)
@@ -531,7 +603,8 @@ class DeviceStream:
 
     def _init(self, st, state=None):
         torch = _torch()
-        self.state = torch.empty(4, dtype=torch.int64, device="cuda") if state is None else state
+        # 8 words: a br_pcg64 head, then the ChaCha key (unused by PCG64 / Lehmer)
+        self.state = torch.empty(8, dtype=torch.int64, device="cuda") if state is None else state
         self._workspace = None
         N.check(N.lib().br_state_upload(_ptr(self.state), C.byref(st), _stream_ptr(torch)), "state upload")
 
@@ -551,7 +624,10 @@ class DeviceStream:
 
     def write_back(self, source) -> None:
         st = self.host_state()
-        source.state = (st.state_hi << 64) | st.state_lo
+        if _is_chacha(source):
+            _chacha_set_position(source, (st.state_hi << 64) | st.state_lo)
+        else:
+            source.state = (st.state_hi << 64) | st.state_lo
 
 
 class RollBatchesResult(NamedTuple):
@@ -694,15 +770,20 @@ def digit_pass_many(words, bounds, k: int):
 
 
 def pcg64_fill(source_or_seed, count: int, offset: int = 0, generator: str = "pcg64"):
-    """count consecutive words (from word `offset`) of a PCG64 (or Lehmer) stream, as an int64
-    CUDA tensor (bit pattern of the u64 words).  The source is not advanced."""
+    """count consecutive words (from word `offset`) of a PCG64, Lehmer or ChaCha stream, as an
+    int64 CUDA tensor (bit pattern of the u64 words).  The source is not advanced."""
     torch = _torch()
     if isinstance(source_or_seed, int):
         st = N.Pcg64State()
         if generator == "lehmer":
             N.lib().br_lehmer_seed(source_or_seed & MASK64, C.byref(st))
-        else:
+        elif generator == "chacha":
+            st = N.ChachaState()
+            N.lib().br_chacha_seed(source_or_seed & MASK64, C.byref(st))
+        elif generator == "pcg64":
             N.lib().br_pcg64_seed(source_or_seed & MASK64, C.byref(st))
+        else:
+            raise UnknownGenerator(f"no device generator {generator!r}")
     else:
         st = _state_struct(source_or_seed)
     out = torch.empty(count, dtype=torch.int64, device="cuda")
@@ -716,7 +797,7 @@ def shuffle_many(data, n: int, run_seed: int, array_index_base: int = 0,
     """Independent shuffles of the num_arrays = data.numel() // n contiguous arrays of a CUDA
     tensor (4- or 8-byte items), in place: array a is
     shuffle_batched(make_source(generator, array_seed(run_seed, array_index_base + a)), ...)
-    with generator "pcg64" or "lehmer"."""
+    with generator "pcg64", "lehmer" or "chacha"."""
     if generator not in _GENERATOR_IDS:
         raise UnknownGenerator(f"no device generator {generator!r}")
     torch = _torch()
@@ -746,7 +827,7 @@ __all__ = [
     "DigitOutOfRange", "DeviceStream", "FullProduct", "PAIR_SCHEDULE", "Pcg64Source", "RadixBases",
     "RollBatchesResult", "ShuffleSchedule", "SourceExhausted", "UnknownGenerator", "ValueOutOfRange",
     "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",
-    "make_source", "mul_full", "LehmerSource", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
+    "make_source", "mul_full", "LehmerSource", "ChaChaSource", "GENERATORS", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
     "roll_batches", "shuffle_batched", "shuffle_many", "shuffle_unbatched", "splitmix64_stream", "threshold",
     "last_kernel",
 ]

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/batchrand_b200.h"
+#include "chacha.cuh"
 #include "core.cuh"
 #include "jump.cuh"
 #include "roll.cuh"
@@ -233,6 +234,34 @@ __global__ void pcg_fill_kernel(uint64_t *__restrict__ out, int64_t count, u128 
     }
 }
 
+// ChaCha keystream words: thread t computes block (P0 + offset)/8 + t and writes the
+// words of it that fall in [0, count).
+__global__ void cha_fill_kernel(uint64_t *__restrict__ out, int64_t count, ChaKey K, u128 p0) {
+    const uint32_t q0 = (uint32_t)(p0.lo & 7);  // word of the first block that is out[0]
+    const int64_t nblk = ((int64_t)q0 + count + 7) >> 3;
+    const uint64_t blk0 = cha_block_of(p0);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nblk; t += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t b[16];
+        chacha_block(K, blk0 + (uint64_t)t, b);
+        const int64_t i0 = t * 8 - q0;  // out index of word 0 of this block
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t i = i0 + q;
+            if (i >= 0 && i < count) out[i] = ((uint64_t)b[2 * q + 1] << 32) | b[2 * q];
+        }
+    }
+}
+
+inline bool host_is_chacha(const br_pcg64 *st) { return st->inc_lo == CHACHA_TAG; }
+
+inline ChaKey host_cha_key(const br_pcg64 *st) {
+    const br_chacha *c = reinterpret_cast<const br_chacha *>(st);
+    ChaKey K;
+    for (int i = 0; i < 8; ++i) K.k[i] = c->key[i];
+    K.nonce = st->inc_hi;
+    return K;
+}
+
 int grid_for(const DeviceInfo &di, const void *kernel, int threads, size_t smem, int64_t work_blocks) {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
@@ -308,7 +337,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     const int tpb = 64;  // 2 warps: many small blocks per SM overlap their load/compute/store phases
     const size_t small_smem = (size_t)tpb * stride * sizeof(T);
     if (segmented && cp.plan.max_k <= 8 && small_smem <= SMALL_SMEM_MAX / 2) {
-        auto kern = shuffle_small_kernel<T>;
+        auto kern = gen == 2 ? shuffle_small_kernel<T, true> : shuffle_small_kernel<T, false>;
         CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
         int64_t blocks = (num_arrays + tpb - 1) / tpb;
         // q / n == umulhi(q, ceil(2^32 / n)) exactly for q < 2^32 / n (spans are < 2^16 elements)
@@ -326,31 +355,28 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     const size_t csmem = (size_t)zbytes;  // payload only; the rest is static
     if (n < 65536 && csmem <= MID_SMEM_MAX && (uint64_t)cp.plan.max_k * 32 * CTA_W + 32 * CTA_W <= CRING) {
         constexpr int W = CTA_W;
-        const void *kp = (const void *)shuffle_cta_hash_kernel<T, W>;
+        auto kern = !segmented ? shuffle_cta_hash_kernel<T, W, 2>
+                               : (gen == 2 ? shuffle_cta_hash_kernel<T, W, 1> : shuffle_cta_hash_kernel<T, W, 0>);
+        const void *kp = (const void *)kern;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
         int grid = segmented ? grid_for(di, kp, 32 * W, csmem, num_arrays) : 1;
         const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
-        shuffle_cta_hash_kernel<T, W><<<grid, 32 * W, csmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base,
-                                                                 words32, state_dev, words64, rk_first, use_tma,
-                                                                 segmented ? 1 : 0, gen);
+        kern<<<grid, 32 * W, csmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
+                                          rk_first, use_tma, segmented ? 1 : 0, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_cta_hash_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
                    std::to_string(W) + ">";
         return BR_OK;
     }
     if (n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 30) {
-        const void *kp;
-        if (segmented) kp = (const void *)shuffle_mid_kernel<T, true>;
-        else kp = (const void *)shuffle_mid_kernel<T, false>;
+        auto kern = !segmented ? shuffle_mid_kernel<T, false, 2>
+                               : (gen == 2 ? shuffle_mid_kernel<T, true, 1> : shuffle_mid_kernel<T, true, 0>);
+        const void *kp = (const void *)kern;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int grid = segmented ? grid_for(di, kp, 32, smem, num_arrays) : 1;
         const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
-        if (segmented)
-            shuffle_mid_kernel<T, true><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
-                                                                words32, state_dev, words64, rk_first, use_tma, gen);
-        else
-            shuffle_mid_kernel<T, false><<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base,
-                                                                 words32, state_dev, words64, rk_first, use_tma, gen);
+        kern<<<grid, 32, smem, st>>>((T *)data, num_arrays, cp.plan, zbytes, run_seed, base, words32, state_dev,
+                                     words64, rk_first, use_tma, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
@@ -359,9 +385,10 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     if ((uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= LRING) {
         constexpr int W = LARGE_W;
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
-        shuffle_cta_large_kernel<T, W><<<grid, 32 * W, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base,
-                                                                  words32, state_dev, words64, rk_first,
-                                                                  segmented ? 1 : 0, gen);
+        auto kern = !segmented ? shuffle_cta_large_kernel<T, W, 2>
+                               : (gen == 2 ? shuffle_cta_large_kernel<T, W, 1> : shuffle_cta_large_kernel<T, W, 0>);
+        kern<<<grid, 32 * W, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
+                                      rk_first, segmented ? 1 : 0, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_cta_large_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
                    std::to_string(W) + ">";
@@ -375,13 +402,14 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         for (int64_t a0 = 0; a0 < num_arrays; a0 += chunk) {
             const int64_t na = std::min(chunk, num_arrays - a0);
             const int grid_gen = (int)std::min<int64_t>(na, (int64_t)di.sms * 16);
-            if (segmented)
-                shuffle_large_gen_kernel<true><<<grid_gen, 32, 0, st>>>(na, cp.plan, run_seed, base + a0, J,
-                                                                         words32 ? words32 + a0 : nullptr, state_dev,
-                                                                         words64, rk_first, gen);
-            else
-                shuffle_large_gen_kernel<false><<<1, 32, 0, st>>>(1, cp.plan, run_seed, base, J, nullptr, state_dev,
-                                                                   words64, rk_first, gen);
+            if (segmented) {
+                auto kern = gen == 2 ? shuffle_large_gen_kernel<true, 1> : shuffle_large_gen_kernel<true, 0>;
+                kern<<<grid_gen, 32, 0, st>>>(na, cp.plan, run_seed, base + a0, J, words32 ? words32 + a0 : nullptr,
+                                              state_dev, words64, rk_first, gen);
+            } else {
+                shuffle_large_gen_kernel<false, 2><<<1, 32, 0, st>>>(1, cp.plan, run_seed, base, J, nullptr,
+                                                                      state_dev, words64, rk_first, gen);
+            }
             const uint32_t lim = cp.plan.lo > 1 ? cp.plan.lo : 1;
             shuffle_large_apply_kernel<T><<<(int)std::min<int64_t>(na, (int64_t)di.sms * 16), 32, 0, st>>>(
                 (T *)data + a0 * (int64_t)n, na, (uint32_t)n, lim, J);
@@ -397,7 +425,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
 int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std::vector<br_segment> &segs,
                    bool segmented, uint64_t run_seed, int64_t base, uint32_t *words32, br_pcg64 *state_dev,
                    uint64_t *words64, uint64_t *rk_first, int gen, void *stream) {
-    if (gen != 0 && gen != 1) return fail(BR_E_UNSUPPORTED, "generator must be 0 (pcg64) or 1 (lehmer)");
+    if (gen < 0 || gen > 2) return fail(BR_E_UNSUPPORTED, "generator must be 0 (pcg64), 1 (lehmer) or 2 (chacha)");
     if (eb != 4 && eb != 8) return fail(BR_E_UNSUPPORTED, "elem_bytes must be 4 or 8");
     if (num_arrays < 0) return fail(BR_E_INVALID, "num_arrays < 0");
     if (n >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements");
@@ -461,7 +489,23 @@ void br_lehmer_seed(uint64_t seed, br_pcg64 *out) {
     out->inc_lo = inc.lo;
 }
 
+void br_chacha_seed(uint64_t seed, br_chacha *out) {
+    ChaKey K;
+    chacha_seed(seed, K);
+    out->head.state_hi = 0;
+    out->head.state_lo = 0;
+    out->head.inc_hi = K.nonce;
+    out->head.inc_lo = CHACHA_TAG;
+    for (int i = 0; i < 8; ++i) out->key[i] = K.k[i];
+}
+
 uint64_t br_pcg64_next(br_pcg64 *st) {
+    if (host_is_chacha(st)) {
+        const u128 s = add128(mk128(st->state_hi, st->state_lo), mk128(0, 1));
+        st->state_hi = s.hi;
+        st->state_lo = s.lo;
+        return cha_out(host_cha_key(st), s);
+    }
     u128 s = mk128(st->state_hi, st->state_lo);
     const bool lh = (st->inc_hi | st->inc_lo) == 0;
     s = add128(mul128(s, lh ? mk128(0, LEHMER_MULT) : mk128(PCG_MULT_HI, PCG_MULT_LO)), mk128(st->inc_hi, st->inc_lo));
@@ -471,6 +515,12 @@ uint64_t br_pcg64_next(br_pcg64 *st) {
 }
 
 void br_pcg64_advance(br_pcg64 *st, uint64_t delta) {
+    if (host_is_chacha(st)) {
+        const u128 s = add128(mk128(st->state_hi, st->state_lo), mk128(0, delta));
+        st->state_hi = s.hi;
+        st->state_lo = s.lo;
+        return;
+    }
     const JumpTables &t = host_tables();
     u128 s = mk128(st->state_hi, st->state_lo), inc = mk128(st->inc_hi, st->inc_lo);
     const bool lh = (inc.hi | inc.lo) == 0;
@@ -527,6 +577,15 @@ int br_pcg64_fill(uint64_t *out_dev, int64_t count, const br_pcg64 *st, uint64_t
     if (s) return s;
     if (count == 0) return BR_OK;
     if (!out_dev) return fail(BR_E_INVALID, "null output");
+    if (host_is_chacha(st)) {
+        const u128 p0 = add128(mk128(st->state_hi, st->state_lo), mk128(0, offset));
+        const int64_t nblk = (int64_t)((p0.lo & 7) + (uint64_t)count + 7) >> 3;
+        int grid = grid_for(di, (const void *)cha_fill_kernel, 256, 0, (nblk + 255) / 256);
+        cha_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(out_dev, count, host_cha_key(st), p0);
+        CK(cudaGetLastError());
+        g_kernel = "cha_fill_kernel";
+        return BR_OK;
+    }
     int64_t blocks = (count + 256 * 32 - 1) / (256 * 32);
     int grid = grid_for(di, (const void *)pcg_fill_kernel, 256, 0, blocks);
     pcg_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(out_dev, count, mk128(st->state_hi, st->state_lo),
@@ -538,7 +597,8 @@ int br_pcg64_fill(uint64_t *out_dev, int64_t count, const br_pcg64 *st, uint64_t
 
 int br_state_upload(br_pcg64 *state_dev, const br_pcg64 *st, void *stream) {
     if (!state_dev || !st) return fail(BR_E_INVALID, "null state");
-    CK(cudaMemcpyAsync(state_dev, st, sizeof(br_pcg64), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    const size_t bytes = host_is_chacha(st) ? sizeof(br_chacha) : sizeof(br_pcg64);
+    CK(cudaMemcpyAsync(state_dev, st, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     return BR_OK;
 }

@@ -17,6 +17,7 @@
 //               (re-draw from the next word), re-runs the tail with the new shift, and
 //               repeats until no rejection is left -- exact for any rejection rate.
 #pragma once
+#include "chacha.cuh"
 #include "jump.cuh"
 
 namespace br {
@@ -198,9 +199,69 @@ __device__ __forceinline__ void publish_final(const RollArgs &a, u128 s0, u128 i
     }
 }
 
+// ---- ChaCha streams.  Only the device state says which generator a stream is (tag in
+// inc_lo, key after the head), so every roll kernel checks it and branches here.  Warp w
+// owns a contiguous batch range; lane l of a sub-step takes batch b0 + l, whose word
+// (position s0 + b + D) comes from the warp's 256-word keystream window.
+template <int K>
+__device__ __forceinline__ void roll_range_cha(const RollArgs &a, u128 s0, int64_t begin, int64_t end, uint64_t D,
+                                               bool early_exit, uint64_t *win) {
+    const ChaKey ck = cha_key_of_state(a.state);
+    const uint32_t lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t total = end - begin;
+    if (total <= 0) return;
+    const int64_t per = (((total + nwarps - 1) / nwarps) + 31) & ~(int64_t)31;
+    const int64_t wb = begin + warp * per;
+    const int64_t we = min(wb + per, end);
+    if (wb >= we) return;  // warp-uniform
+    u128 W0 = cha_win_unset(cha_add(s0, (uint64_t)wb + D));
+    int err = 0;
+    volatile RollWs *vws = a.ws;
+    for (int64_t b0 = wb; b0 < we; b0 += 32) {
+        if (early_exit) {  // warp-uniform decision: the window refill is warp-collective
+            unsigned long long nf = lane == 0 ? vws->neg_first : 0ull;
+            nf = __shfl_sync(0xFFFFFFFFu, nf, 0);
+            if (nf != 0 && (int64_t)(~nf) < b0) break;
+        }
+        const int64_t b = b0 + lane;
+        const uint64_t w = cha_warp_word(win, ck, W0, cha_add(s0, (uint64_t)b + D), lane);
+        if (b < we) {
+            uint32_t bb[K], d[K];
+            load_bounds<K>(a.bounds + b * K, bb);
+            uint64_t r;
+            uint8_t tc = 0;
+            const int st = eval_batch<K>(bb, w, d, r, tc, err);
+            store_rolls<K>(a.rolls + b * K, d);
+            a.words[b] = 1;
+            if (a.flags) a.flags[b] = tc;
+            if (a.rk) a.rk[b] = r;
+            if (st == 1) atomicMax(&a.ws->neg_first, ~(unsigned long long)b);
+        }
+    }
+    if (err) set_error(a.ws, err);
+}
+
+// speculative main pass of a ChaCha stream: run by the (cooperative) fixup kernel itself,
+// so the PCG64 main kernels only carry a one-compare early exit
+template <int K>
+__device__ __forceinline__ void roll_cha_main(const RollArgs &a, uint64_t *win) {
+    const u128 s0 = mk128(a.state[0], a.state[1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const u128 sf = cha_add(s0, (uint64_t)a.nb);
+        a.ws->final_hi = sf.hi;
+        a.ws->final_lo = sf.lo;
+    }
+    roll_range_cha<K>(a, s0, 0, a.nb, 0, false, win);
+}
+
+__device__ __forceinline__ bool roll_is_chacha(const RollArgs &a) { return a.state[3] == CHACHA_TAG; }
+
 template <int K>
 __global__ void __launch_bounds__(256) roll_main_kernel(RollArgs a) {
     pdl_launch_dependents();
+    if (roll_is_chacha(a)) return;  // the fixup kernel rolls ChaCha streams
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
     publish_final(a, s0, inc);
@@ -285,6 +346,7 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     constexpr int U = ROLL_U;
     constexpr int64_t CH = 32 * VB * U;
     pdl_launch_dependents();
+    if (roll_is_chacha(a)) return;  // the fixup kernel rolls ChaCha streams
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
     const bool lh = is_lehmer(inc);
@@ -376,9 +438,8 @@ __device__ __forceinline__ void grid_barrier(RollWs *ws) {
     __syncthreads();
 }
 
-template <int K>
-__global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
-    pdl_wait();
+template <int K, bool CHA>
+__device__ __forceinline__ void roll_fixup_body(const RollArgs &a, uint64_t *win) {
     RollWs *ws = a.ws;
     volatile RollWs *vws = ws;
     const u128 s0 = mk128(a.state[0], a.state[1]);
@@ -401,16 +462,21 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
                 // batch `cur` rejected word cur + D: re-draw the whole batch from the next
                 // words until accepted (batched.py:120-122)
                 uint64_t widx = (uint64_t)cur + D + 1;
-                u128 st = gen_jump(s0, inc, widx + 1, lh);
+                u128 st = CHA ? cha_add(s0, widx + 1) : gen_jump(s0, inc, widx + 1, lh);
                 uint32_t bb[K];
                 load_bounds<K>(a.bounds + cur * K, bb);
                 uint64_t extra = 1;
+                ChaKey ck;
+                ChaCursor cc;
+                cc.valid = false;
+                if constexpr (CHA) ck = cha_key_of_state(a.state);
                 for (;;) {
                     uint32_t d[K];
                     uint64_t r;
                     uint8_t tc;
                     int err = 0;
-                    int res = eval_batch<K>(bb, gen_out(st, lh), d, r, tc, err);
+                    const uint64_t w = CHA ? cha_out_cached(ck, cc, st) : gen_out(st, lh);
+                    int res = eval_batch<K>(bb, w, d, r, tc, err);
                     if (res != 1) {
                         store_rolls<K>(a.rolls + cur * K, d);
                         a.words[cur] = (uint8_t)(1 + extra > 255 ? 255 : 1 + extra);
@@ -419,7 +485,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
                         break;
                     }
                     ++extra;
-                    st = mad128(st, gen_mult(lh), inc);
+                    st = CHA ? cha_add(st, 1) : mad128(st, gen_mult(lh), inc);
                 }
                 ws->D = D + extra;
                 ws->neg_first = 0;
@@ -427,7 +493,8 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
             }
             grid_barrier(ws);
             D = vws->D;
-            roll_range<K, 1>(a, s0, inc, cur + 1, a.nb, D, true);
+            if constexpr (CHA) roll_range_cha<K>(a, s0, cur + 1, a.nb, D, true, win);
+            else roll_range<K, 1>(a, s0, inc, cur + 1, a.nb, D, true);
             grid_barrier(ws);
             nf = vws->neg_first;
         }
@@ -437,11 +504,25 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
             a.state[0] = vws->final_hi;
             a.state[1] = vws->final_lo;
         } else {
-            const u128 sf = gen_jump(s0, inc, (uint64_t)a.nb + D, lh);
+            const u128 sf = CHA ? cha_add(s0, (uint64_t)a.nb + D) : gen_jump(s0, inc, (uint64_t)a.nb + D, lh);
             a.state[0] = sf.hi;
             a.state[1] = sf.lo;
         }
         ws->extra = D;
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
+    pdl_wait();
+    __shared__ __align__(16) uint64_t win[8][256];
+    if (roll_is_chacha(a)) {
+        uint64_t *w = win[(threadIdx.x >> 5) & 7];
+        roll_cha_main<K>(a, w);
+        grid_barrier(a.ws);
+        roll_fixup_body<K, true>(a, w);
+    } else {
+        roll_fixup_body<K, false>(a, nullptr);
     }
 }
 

@@ -18,6 +18,7 @@
 //                         applied 32 steps at a time with an exact intra-group conflict
 //                         resolution (see apply_group).
 #pragma once
+#include "chacha.cuh"
 #include "jump.cuh"
 #include "tma.cuh"
 
@@ -50,15 +51,21 @@ __device__ __forceinline__ void swap_sm(T *p, uint32_t i, uint32_t j) {
 // -------------------------------------------------------------------------------------
 // Run `count` consecutive batches of K dice (the first at remaining length nb) on one
 // thread's array z (row of the block's shared buffer).  Fully unrolled per K.
-template <int K, typename T>
+template <int K, typename T, bool CHA>
 __device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count, const uint64_t *thresh, u128 &s,
-                                              u128 inc, uint32_t &words, bool lh) {
+                                              u128 inc, uint32_t &words, bool lh, const ChaKey &ck,
+                                              ChaCursor &cur) {
     for (uint32_t c = 0; c < count; ++c, nb -= K) {
         const uint64_t t = __ldg(thresh + c);
         uint32_t d[K];
         uint64_t r;
         do {
-            r = gen_next(s, inc, lh);
+            if constexpr (CHA) {
+                s = cha_add(s, 1);
+                r = cha_out_cached(ck, cur, s);
+            } else {
+                r = gen_next(s, inc, lh);
+            }
             ++words;
 #pragma unroll
             for (int m = 0; m < K; ++m) d[m] = die(nb - m, r);
@@ -68,19 +75,19 @@ __device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count,
     }
 }
 
-template <typename T>
+template <typename T, bool CHA>
 __device__ __forceinline__ void small_segment_any(T *z, uint32_t k, uint32_t nb, uint32_t count,
                                                   const uint64_t *thresh, u128 &s, u128 inc, uint32_t &words,
-                                                  bool lh) {
+                                                  bool lh, const ChaKey &ck, ChaCursor &cur) {
     switch (k) {
-        case 1: small_segment<1>(z, nb, count, thresh, s, inc, words, lh); break;
-        case 2: small_segment<2>(z, nb, count, thresh, s, inc, words, lh); break;
-        case 3: small_segment<3>(z, nb, count, thresh, s, inc, words, lh); break;
-        case 4: small_segment<4>(z, nb, count, thresh, s, inc, words, lh); break;
-        case 5: small_segment<5>(z, nb, count, thresh, s, inc, words, lh); break;
-        case 6: small_segment<6>(z, nb, count, thresh, s, inc, words, lh); break;
-        case 7: small_segment<7>(z, nb, count, thresh, s, inc, words, lh); break;
-        default: small_segment<8>(z, nb, count, thresh, s, inc, words, lh); break;
+        case 1: small_segment<1, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        case 2: small_segment<2, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        case 3: small_segment<3, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        case 4: small_segment<4, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        case 5: small_segment<5, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        case 6: small_segment<6, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        case 7: small_segment<7, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        default: small_segment<8, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
     }
 }
 
@@ -148,7 +155,7 @@ __device__ __forceinline__ void small_copy(T *buf, T *g, uint32_t span, uint32_t
     }
 }
 
-template <typename T>
+template <typename T, bool CHA>
 __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data, int64_t num_arrays,
                                                            DevPlan plan, uint32_t stride, uint32_t magic,
                                                            int vec_ok, uint64_t run_seed, int64_t base,
@@ -170,13 +177,24 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
     __syncthreads();
     if (tid < na) {
         u128 s, inc;
-        const bool lh = gen != 0;
-        gen_seed(array_seed(run_seed, (uint64_t)(base + a0 + tid)), s, inc, lh);
+        const bool lh = gen == 1;
+        ChaKey ck;
+        ChaCursor cur;
+        cur.valid = false;
+        const uint64_t seed = array_seed(run_seed, (uint64_t)(base + a0 + tid));
+        if constexpr (CHA) {
+            chacha_seed(seed, ck);
+            s = mk128(0, 0);
+            inc = mk128(ck.nonce, CHACHA_TAG);
+        } else {
+            gen_seed(seed, s, inc, lh);
+        }
         T *z = buf + tid * stride;
         uint32_t words = 0;
         for (uint32_t sg = 0; sg < plan.nseg; ++sg) {
             const DevSeg S = segs[sg];
-            small_segment_any<T>(z, S.k, S.start_n, S.count, plan.thresh + S.first_batch, s, inc, words, lh);
+            small_segment_any<T, CHA>(z, S.k, S.start_n, S.count, plan.thresh + S.first_batch, s, inc, words, lh,
+                                      ck, cur);
         }
         if (words_out) words_out[a0 + tid] = words;
     }
@@ -228,15 +246,22 @@ static constexpr uint32_t RING = 1024;
 
 struct GenState {
     u128 s, inc, A32, C32;
+    u128 W0;                        // ChaCha: origin of the warp's keystream window
     uint32_t B0, D, seg, frontier;  // frontier: lowest position whose target is committed
 };
 
+template <bool CHA>
 __device__ __forceinline__ void gen_init(GenState &g, u128 s0, u128 inc, uint32_t n, int lane) {
     const bool lh = is_lehmer(inc);
     g.inc = inc;
-    g.s = gen_jump_small(s0, inc, lane + 1, lh);
-    g.A32 = gen_SA(lh, 32);
-    g.C32 = mul128(g_SG[32], inc);
+    if constexpr (CHA) {
+        g.s = cha_add(s0, (uint64_t)lane + 1);
+        g.W0 = cha_win_unset(s0);
+    } else {
+        g.s = gen_jump_small(s0, inc, lane + 1, lh);
+        g.A32 = gen_SA(lh, 32);
+        g.C32 = mul128(g_SG[32], inc);
+    }
     g.B0 = 0;
     g.D = 0;
     g.seg = 0;
@@ -244,21 +269,23 @@ __device__ __forceinline__ void gen_init(GenState &g, u128 s0, u128 inc, uint32_
 }
 
 // One generation step: 32 batches evaluated, the accepted prefix committed.
-template <typename Sink>
+template <bool CHA, typename Sink>
 __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const DevSeg *segs, Sink sink, int lane,
-                                         uint64_t *rk_first) {
+                                         uint64_t *rk_first, uint64_t *chawin, const ChaKey &ck) {
     const bool lh = is_lehmer(g.inc);
     const uint32_t nb = plan.nbatches;
     const uint32_t b = g.B0 + lane;
     bool fail = false;
     uint32_t low = 0xFFFFFFFFu;  // lowest position this lane's batch covers
+    uint64_t rc = 0;
+    if constexpr (CHA) rc = cha_warp_word(chawin, ck, g.W0, cha_prev(g.s), lane);  // warp-collective
     if (b < nb) {
         uint32_t sg = g.seg;
         while (sg + 1 < plan.nseg && segs[sg + 1].first_batch <= b) ++sg;
         const DevSeg S = segs[sg];
         const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
         const uint64_t t = __ldg(plan.thresh + b);
-        uint64_t r = gen_out(g.s, lh);
+        uint64_t r = CHA ? rc : gen_out(g.s, lh);
         const uint32_t pos = nbb - 1;
         for (uint32_t m = 0; m < S.k; ++m) sink(pos - m, die(nbb - m, r));
         low = nbb - S.k;
@@ -276,12 +303,14 @@ __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const
     __syncwarp();
     if (fm == 0) {
         g.B0 += 32;
-        g.s = mad128(g.s, g.A32, g.C32);
+        if constexpr (CHA) g.s = cha_add(g.s, 32);
+        else g.s = mad128(g.s, g.A32, g.C32);
     } else {
         const int l = __ffs(fm) - 1;
         g.B0 += l;
         g.D += 1;
-        g.s = gen_jump_small(g.s, g.inc, l + 1, lh);
+        if constexpr (CHA) g.s = cha_add(g.s, (uint64_t)l + 1);
+        else g.s = gen_jump_small(g.s, g.inc, l + 1, lh);
     }
     while (g.seg + 1 < plan.nseg && segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
 }
@@ -372,16 +401,15 @@ __device__ __forceinline__ void apply_group(T *z, const uint16_t *ring, uint8_t 
     __syncwarp();
 }
 
-template <typename T, bool SEGMENTED>
-__global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
-                                                         uint32_t zbytes, uint64_t run_seed, int64_t base,
-                                                         uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                         uint64_t *words64, uint64_t *rk_first, int use_tma, int gen) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ DevSeg segs[MAX_SEGS];
-    __shared__ __align__(16) uint16_t ring[RING];
-    __shared__ int8_t predslot[32];
-    __shared__ __align__(8) uint64_t bar;
+// CM (ChaCha mode): 0 = PCG64/Lehmer only, 1 = ChaCha only, 2 = decided per array from the
+// stream state's tag (stream calls, where only the device knows the generator).
+template <typename T, bool SEGMENTED, bool CHA>
+__device__ __forceinline__ void shuffle_mid_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
+                                                 uint32_t zbytes, uint64_t run_seed, int64_t base,
+                                                 uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                 uint64_t *words64, uint64_t *rk_first, int use_tma, int gen,
+                                                 unsigned char *smem_raw, DevSeg *segs, uint16_t *ring,
+                                                 int8_t *predslot, uint64_t &bar, uint64_t *chawin) {
     const int lane = threadIdx.x & 31;
     T *z = reinterpret_cast<T *>(smem_raw);
     uint8_t *H = smem_raw + zbytes;
@@ -407,21 +435,30 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         }
         u128 s0, inc;
         bool lh;
+        ChaKey ck;
         if constexpr (SEGMENTED) {
-            lh = gen != 0;
-            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
+            lh = gen == 1;
+            const uint64_t seed = array_seed(run_seed, (uint64_t)(base + a));
+            if constexpr (CHA) {
+                chacha_seed(seed, ck);
+                s0 = mk128(0, 0);
+                inc = mk128(ck.nonce, CHACHA_TAG);
+            } else {
+                gen_seed(seed, s0, inc, lh);
+            }
         } else {
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
             lh = is_lehmer(inc);
+            if constexpr (CHA) ck = cha_key_of_state(state_io);
         }
         GenState gs;
-        gen_init(gs, s0, inc, n, lane);
+        gen_init<CHA>(gs, s0, inc, n, lane);
         uint64_t *rkf = SEGMENTED ? nullptr : rk_first;
         // the first targets are generated while the payload streams in
         uint16_t *ringp = ring;
         auto sink = [ringp](uint32_t pos, uint32_t v) { ringp[pos & (RING - 1)] = (uint16_t)v; };
-        if (plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
+        if (plan.nbatches) gen_step<CHA>(gs, plan, segs, sink, lane, rkf, chawin, ck);
         if (use_tma) {
             mbar_wait(&bar, parity);
             parity ^= 1u;
@@ -429,11 +466,12 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         __syncwarp();
         for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= 32) {
             const uint32_t need = top >= (int64_t)lim + 31 ? (uint32_t)top - 31 : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
+            while (gs.frontier > need && gs.B0 < plan.nbatches)
+                gen_step<CHA>(gs, plan, segs, sink, lane, rkf, chawin, ck);
             apply_group<T>(z, ring, H, predslot, (uint32_t)top, lim, jbits, lane);
         }
         // finish the word accounting (a trailing rejection can follow the last position)
-        while (gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
+        while (gs.B0 < plan.nbatches) gen_step<CHA>(gs, plan, segs, sink, lane, rkf, chawin, ck);
         if (use_tma) {
             if (lane == 0) {
                 fence_proxy_async();
@@ -447,7 +485,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
             if constexpr (SEGMENTED) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = gen_jump(s0, inc, words, lh);
+                const u128 sf = CHA ? cha_add(s0, words) : gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -456,6 +494,29 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
         __syncwarp();
     }
     if (use_tma && lane == 0) bulk_wait_all();
+}
+
+template <typename T, bool SEGMENTED, int CM>
+__global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
+                                                         uint32_t zbytes, uint64_t run_seed, int64_t base,
+                                                         uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                         uint64_t *words64, uint64_t *rk_first, int use_tma, int gen) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ DevSeg segs[MAX_SEGS];
+    __shared__ __align__(16) uint16_t ring[RING];
+    __shared__ int8_t predslot[32];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(16) uint64_t chawin[CM ? 256 : 2];
+    bool cha = CM == 1;
+    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if (CM != 0 && cha)
+        shuffle_mid_body<T, SEGMENTED, CM != 0>(data, num_arrays, plan, zbytes, run_seed, base, words32, state_io,
+                                                words64, rk_first, use_tma, gen, smem_raw, segs, ring, predslot,
+                                                bar, chawin);
+    else if (CM != 1)
+        shuffle_mid_body<T, SEGMENTED, false>(data, num_arrays, plan, zbytes, run_seed, base, words32, state_io,
+                                              words64, rk_first, use_tma, gen, smem_raw, segs, ring, predslot, bar,
+                                              chawin);
 }
 
 
@@ -468,236 +529,12 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
 // (where such groups are common), fall back to warp groups run by warp 0.
 static constexpr uint32_t CRING = 2048;
 
-template <typename T, int W, typename RT = uint16_t>
-struct CtaShared {
-    DevSeg segs[MAX_SEGS];
-    RT ring[CRING];
-    int16_t P[32 * W];
-    T VI[32 * W];
-    T AV[32 * W];
-    uint32_t fmin;
-    uint32_t frontier[2];
-    uint64_t bar;
-};
-
 template <int W>
 struct CtaGen {
     u128 s, inc, AJ, CJ;
+    u128 W0;  // ChaCha: origin of the CTA's keystream window
     uint32_t B0, D, seg, frontier, parity;
 };
-
-template <typename T, int W, typename RT>
-__device__ __forceinline__ void cta_gen_step(CtaGen<W> &g, const DevPlan &plan, CtaShared<T, W, RT> &sh, int L,
-                                             uint64_t *rk_first) {
-    const bool lh = is_lehmer(g.inc);
-    constexpr int G = 32 * W;
-    const uint32_t nb = plan.nbatches;
-    const uint32_t b = g.B0 + L;
-    bool fail = false;
-    uint32_t low = 0xFFFFFFFFu;
-    if (b < nb) {
-        uint32_t sg = g.seg;
-        while (sg + 1 < plan.nseg && sh.segs[sg + 1].first_batch <= b) ++sg;
-        const DevSeg S = sh.segs[sg];
-        const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
-        const uint64_t t = __ldg(plan.thresh + b);
-        uint64_t r = gen_out(g.s, lh);
-        const uint32_t pos = nbb - 1;
-        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (CRING - 1)] = (RT)die(nbb - m, r);
-        low = nbb - S.k;
-        fail = r < t;
-        if (rk_first && b == 0 && g.D == 0) *rk_first = r;
-    }
-    const uint32_t nact = nb - g.B0 < (uint32_t)G ? nb - g.B0 : (uint32_t)G;
-    const uint32_t par = g.parity;
-    g.parity ^= 1u;
-    if (L == (int)nact - 1) sh.frontier[par] = low;  // frontier if nothing is rejected
-    if (!__syncthreads_or(fail)) {
-        g.frontier = sh.frontier[par];
-        g.B0 += G;
-        g.s = mad128(g.s, g.AJ, g.CJ);
-    } else {  // rare: find the first rejected lane, commit the lanes before it
-        if (L == 0) sh.fmin = G;
-        __syncthreads();
-        if (fail) atomicMin(&sh.fmin, (uint32_t)L);
-        __syncthreads();
-        const uint32_t f = sh.fmin;
-        if (f > 0 && L == (int)f - 1) sh.frontier[par] = low;
-        __syncthreads();
-        if (f > 0) g.frontier = sh.frontier[par];
-        g.B0 += f;
-        g.D += 1;
-        g.s = gen_jump_small(g.s, g.inc, (int)f + 1, lh);
-        __syncthreads();  // fmin / frontier reuse
-    }
-    while (g.seg + 1 < plan.nseg && sh.segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
-}
-
-// returns false if the group must be redone with warp groups (three+ lanes on a target)
-template <typename T, int W>
-__device__ __forceinline__ bool apply_group_cta(T *z, uint8_t *H, CtaShared<T, W> &sh, uint32_t top, uint32_t lim,
-                                                int L) {
-    constexpr int G = 32 * W;
-    const int64_t i64 = (int64_t)top - L;
-    const bool act = i64 >= (int64_t)lim;
-    const uint32_t i = act ? (uint32_t)i64 : 0;
-    const uint32_t j = act ? (uint32_t)sh.ring[i & (CRING - 1)] : 0;
-    const T vi = act ? z[i] : T(0);
-    const T vj = act ? z[j] : T(0);
-    const uint32_t lo_pos = top >= lim + (G - 1) ? top - (G - 1) : lim;
-    sh.VI[L] = vi;
-    sh.P[L] = -1;
-    if (act) H[j] = (uint8_t)L;
-    const bool inrange = act && j >= lo_pos && j < i;
-    __syncthreads();
-    const uint32_t w = act ? H[j] : (uint32_t)L;
-    const bool dupl = w != (uint32_t)L;
-    if (!__syncthreads_or(dupl || inrange)) {  // direct path
-        if (act) {
-            z[i] = vj;
-            z[j] = vi;
-        }
-        __syncthreads();
-        return true;
-    }
-    int partner = L;
-    if (__syncthreads_or(dupl)) {
-        if (dupl) H[j] = (uint8_t)L;
-        __syncthreads();
-        const uint32_t h2 = act ? H[j] : (uint32_t)L;
-        partner = dupl ? (int)w : (int)h2;
-        const bool triple = dupl && h2 != (uint32_t)L;
-        if (__syncthreads_or(triple)) return false;
-    }
-    const int tl = partner < L ? partner : -1;
-    const bool later = partner > L;
-    if (inrange && !later) sh.P[top - j] = (int16_t)L;
-    __syncthreads();
-    int p = sh.P[L];
-    p = p >= 0 ? p : L;
-    // pointer jumping to the root of the Pred chain (P holds the chain links)
-    for (;;) {
-        const int pp = sh.P[p];
-        const int np = pp >= 0 ? pp : p;
-        if (!__syncthreads_or(np != p)) break;
-        p = np;
-    }
-    const T A = sh.VI[p];
-    sh.AV[L] = A;
-    __syncthreads();
-    const T B = tl >= 0 ? sh.AV[tl] : vj;
-    if (act) {
-        z[i] = B;
-        if (!later && j < lo_pos) z[j] = A;
-    }
-    __syncthreads();
-    return true;
-}
-
-template <typename T, int W>
-__global__ void __launch_bounds__(32 * W) shuffle_cta_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
-                                                             uint32_t zbytes, uint64_t run_seed, int64_t base,
-                                                             uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                             uint64_t *words64, uint64_t *rk_first, int use_tma,
-                                                             int segmented, int gen) {
-    constexpr int G = 32 * W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ CtaShared<T, W> sh;
-    const int L = threadIdx.x;
-    const int lane = L & 31, warp = L >> 5;
-    T *z = reinterpret_cast<T *>(smem_raw);
-    uint8_t *H = smem_raw + zbytes;
-    for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
-    if (use_tma && L == 0) mbar_init(&sh.bar, 1);
-    __syncthreads();
-    const uint32_t n = plan.n;
-    const uint32_t bytes = n * (uint32_t)sizeof(T);
-    const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
-    const int jbits = n > 1 ? 32 - __clz(n - 1) : 1;
-    const uint32_t warp_below = 4 * G;  // below this position warp groups do the apply
-    uint32_t parity = 0;
-    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
-        T *g = data + a * (int64_t)n;
-        if (use_tma) {
-            if (L == 0) {
-                bulk_wait_read();
-                fence_proxy_async();
-                mbar_arrive_expect_tx(&sh.bar, bytes);
-                bulk_load(z, g, bytes, &sh.bar);
-            }
-        } else {
-            for (uint32_t e = L; e < n; e += G) z[e] = g[e];
-        }
-        u128 s0, inc;
-        bool lh;
-        if (segmented) {
-            lh = gen != 0;
-            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
-        } else {
-            s0 = mk128(state_io[0], state_io[1]);
-            inc = mk128(state_io[2], state_io[3]);
-            lh = is_lehmer(inc);
-        }
-        CtaGen<W> gs;
-        gs.inc = inc;
-        gs.s = gen_jump_small(s0, inc, L + 1, lh);
-        gs.AJ = gen_SA(lh, G);
-        gs.CJ = mul128(g_SG[G], inc);
-        gs.B0 = 0;
-        gs.D = 0;
-        gs.seg = 0;
-        gs.frontier = n;
-        gs.parity = 0;
-        uint64_t *rkf = segmented ? nullptr : rk_first;
-        if (plan.nbatches) cta_gen_step<T, W, uint16_t>(gs, plan, sh, L, rkf);
-        if (use_tma) {
-            mbar_wait(&sh.bar, parity);
-            parity ^= 1u;
-        }
-        __syncthreads();
-        int64_t top = (int64_t)n - 1;
-        for (; top >= (int64_t)lim && top >= (int64_t)warp_below; top -= G) {
-            const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) cta_gen_step<T, W, uint16_t>(gs, plan, sh, L, rkf);
-            if (!apply_group_cta<T, W>(z, H, sh, (uint32_t)top, lim, L)) {
-                // three or more lanes share a target: redo this group as W warp groups, in order
-                for (int w = 0; w < W; ++w) {
-                    const int64_t t2 = top - 32 * w;
-                    if (warp == 0 && t2 >= (int64_t)lim)
-                        apply_group<T, CRING>(z, sh.ring, H, reinterpret_cast<int8_t *>(sh.P), (uint32_t)t2, lim, jbits, lane);
-                    __syncthreads();
-                }
-            }
-        }
-        // bottom of the array: all remaining targets, then warp groups by warp 0
-        while (gs.B0 < plan.nbatches) cta_gen_step<T, W, uint16_t>(gs, plan, sh, L, rkf);
-        if (warp == 0)
-            for (; top >= (int64_t)lim; top -= 32)
-                apply_group<T, CRING>(z, sh.ring, H, reinterpret_cast<int8_t *>(sh.P), (uint32_t)top, lim, jbits, lane);
-        __syncthreads();
-        if (use_tma) {
-            if (L == 0) {
-                fence_proxy_async();
-                bulk_store(g, z, bytes);
-            }
-        } else {
-            for (uint32_t e = L; e < n; e += G) g[e] = z[e];
-        }
-        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
-        if (L == 0) {
-            if (segmented) {
-                if (words32) words32[a] = (uint32_t)words;
-            } else {
-                const u128 sf = gen_jump(s0, inc, words, lh);
-                state_io[0] = sf.hi;
-                state_io[1] = sf.lo;
-                if (words64) words64[0] = words;
-            }
-        }
-        __syncthreads();
-    }
-    if (use_tma && L == 0) bulk_wait_all();
-}
 
 // -------------------------------------------------------------------------------------
 // arrays in global memory: one CTA (W warps) per array, groups of G = 32*W steps
@@ -778,22 +615,24 @@ __device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W, R
     __syncthreads();
 }
 
-template <typename T, int W, typename RT, uint32_t RS, int HB>
+template <bool CHA, typename T, int W, typename RT, uint32_t RS, int HB>
 __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan, LargeShared<T, W, RT, RS, HB> &sh,
-                                               int L, uint64_t *rk_first) {
+                                               int L, uint64_t *rk_first, uint64_t *chawin, const ChaKey &ck) {
     const bool lh = is_lehmer(g.inc);
     constexpr int G = 32 * W;
     const uint32_t nb = plan.nbatches;
     const uint32_t b = g.B0 + L;
     bool fail = false;
     uint32_t low = 0xFFFFFFFFu;
+    uint64_t rc = 0;
+    if constexpr (CHA) rc = cha_cta_word<G>(chawin, ck, g.W0, cha_prev(g.s), L);  // CTA-collective
     if (b < nb) {
         uint32_t sg = g.seg;
         while (sg + 1 < plan.nseg && sh.segs[sg + 1].first_batch <= b) ++sg;
         const DevSeg S = sh.segs[sg];
         const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
         const uint64_t t = __ldg(plan.thresh + b);
-        uint64_t r = gen_out(g.s, lh);
+        uint64_t r = CHA ? rc : gen_out(g.s, lh);
         const uint32_t pos = nbb - 1;
         for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (RS - 1)] = (RT)die(nbb - m, r);
         low = nbb - S.k;
@@ -807,7 +646,8 @@ __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan
     if (!__syncthreads_or(fail)) {
         g.frontier = sh.frontier[par];
         g.B0 += G;
-        g.s = mad128(g.s, g.AJ, g.CJ);
+        if constexpr (CHA) g.s = cha_add(g.s, G);
+        else g.s = mad128(g.s, g.AJ, g.CJ);
     } else {
         if (L == 0) sh.fmin = G;
         __syncthreads();
@@ -819,20 +659,58 @@ __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan
         if (f > 0) g.frontier = sh.frontier[par];
         g.B0 += f;
         g.D += 1;
-        g.s = gen_jump_small(g.s, g.inc, (int)f + 1, lh);
+        if constexpr (CHA) g.s = cha_add(g.s, (uint64_t)f + 1);
+        else g.s = gen_jump_small(g.s, g.inc, (int)f + 1, lh);
         __syncthreads();
     }
     while (g.seg + 1 < plan.nseg && sh.segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
 }
 
-template <typename T, int W>
-__global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict__ data, int64_t num_arrays,
-                                                                   DevPlan plan, uint64_t run_seed, int64_t base,
-                                                                   uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                                   uint64_t *words64, uint64_t *rk_first,
-                                                                   int segmented, int gen) {
+// per-array generator setup shared by the CTA kernels
+template <bool CHA, int W>
+__device__ __forceinline__ void cta_gen_setup(CtaGen<W> &gs, u128 &s0, u128 &inc, bool &lh, ChaKey &ck, int segmented,
+                                              int gen, uint64_t run_seed, int64_t a, uint64_t *state_io, uint32_t n,
+                                              int L) {
     constexpr int G = 32 * W;
-    __shared__ LargeShared<T, W> sh;
+    if (segmented) {
+        lh = gen == 1;
+        const uint64_t seed = array_seed(run_seed, (uint64_t)a);
+        if constexpr (CHA) {
+            chacha_seed(seed, ck);
+            s0 = mk128(0, 0);
+            inc = mk128(ck.nonce, CHACHA_TAG);
+        } else {
+            gen_seed(seed, s0, inc, lh);
+        }
+    } else {
+        s0 = mk128(state_io[0], state_io[1]);
+        inc = mk128(state_io[2], state_io[3]);
+        lh = is_lehmer(inc);
+        if constexpr (CHA) ck = cha_key_of_state(state_io);
+    }
+    gs.inc = inc;
+    if constexpr (CHA) {
+        gs.s = cha_add(s0, (uint64_t)L + 1);
+        gs.W0 = cha_win_unset(s0);
+    } else {
+        gs.s = gen_jump_small(s0, inc, L + 1, lh);
+        gs.AJ = gen_SA(lh, G);
+        gs.CJ = mul128(g_SG[G], inc);
+    }
+    gs.B0 = 0;
+    gs.D = 0;
+    gs.seg = 0;
+    gs.frontier = n;
+    gs.parity = 0;
+}
+
+template <typename T, int W, bool CHA>
+__device__ __forceinline__ void shuffle_cta_large_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
+                                                       uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
+                                                       uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
+                                                       int segmented, int gen, LargeShared<T, W> &sh,
+                                                       uint64_t *chawin) {
+    constexpr int G = 32 * W;
     const int L = threadIdx.x;
     for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
     for (uint32_t q = L; q < (1u << HBITS); q += G) sh.ht[q] = 0;
@@ -844,28 +722,13 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
         T *z = data + a * (int64_t)n;
         u128 s0, inc;
         bool lh;
-        if (segmented) {
-            lh = gen != 0;
-            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
-        } else {
-            s0 = mk128(state_io[0], state_io[1]);
-            inc = mk128(state_io[2], state_io[3]);
-            lh = is_lehmer(inc);
-        }
+        ChaKey ck;
         CtaGen<W> gs;
-        gs.inc = inc;
-        gs.s = gen_jump_small(s0, inc, L + 1, lh);
-        gs.AJ = gen_SA(lh, G);
-        gs.CJ = mul128(g_SG[G], inc);
-        gs.B0 = 0;
-        gs.D = 0;
-        gs.seg = 0;
-        gs.frontier = n;
-        gs.parity = 0;
+        cta_gen_setup<CHA, W>(gs, s0, inc, lh, ck, segmented, gen, run_seed, base + a, state_io, n, L);
         uint64_t *rkf = segmented ? nullptr : rk_first;
         for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= G) {
             const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
+            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step<CHA>(gs, plan, sh, L, rkf, chawin, ck);
             tag = (tag + 1) & 0xFFFFu;
             if (tag == 0) {  // tag wrap: clear the slots (every 65535 groups)
                 for (uint32_t q = L; q < (1u << HBITS); q += G) sh.ht[q] = 0;
@@ -874,13 +737,13 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
             }
             apply_group_cta_global(z, sh, tag, (uint32_t)top, lim, L);
         }
-        while (gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
+        while (gs.B0 < plan.nbatches) large_gen_step<CHA>(gs, plan, sh, L, rkf, chawin, ck);
         const uint64_t words = (uint64_t)plan.nbatches + gs.D;
         if (L == 0) {
             if (segmented) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = gen_jump(s0, inc, words, lh);
+                const u128 sf = CHA ? cha_add(s0, words) : gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -890,19 +753,37 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
     }
 }
 
+template <typename T, int W, int CM>
+__global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                   DevPlan plan, uint64_t run_seed, int64_t base,
+                                                                   uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                                   uint64_t *words64, uint64_t *rk_first,
+                                                                   int segmented, int gen) {
+    __shared__ LargeShared<T, W> sh;
+    __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
+    bool cha = CM == 1;
+    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if (CM != 0 && cha)
+        shuffle_cta_large_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+                                              rk_first, segmented, gen, sh, chawin);
+    else if (CM != 1)
+        shuffle_cta_large_body<T, W, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+                                            rk_first, segmented, gen, sh, chawin);
+}
+
 // Shared-memory-resident arrays with the same hashed CTA groups: payload moved by TMA bulk
 // copies, targets in a u16 ring, 1024-slot lane-chain hash.
-template <typename T, int W>
-__global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict__ data, int64_t num_arrays,
-                                                                  DevPlan plan, uint64_t run_seed, int64_t base,
-                                                                  uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                                  uint64_t *words64, uint64_t *rk_first, int use_tma,
-                                                                  int segmented, int gen) {
+static constexpr int HASH_HB = 10;
+
+template <typename T, int W, bool CHA>
+__device__ __forceinline__ void shuffle_cta_hash_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
+                                                      uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
+                                                      uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
+                                                      int use_tma, int segmented, int gen, unsigned char *smem_raw,
+                                                      LargeShared<T, W, uint16_t, CRING, HASH_HB> &sh, uint64_t &bar,
+                                                      uint64_t *chawin) {
     constexpr int G = 32 * W;
-    constexpr int HB = 10;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ LargeShared<T, W, uint16_t, CRING, HB> sh;
-    __shared__ __align__(8) uint64_t bar;
+    constexpr int HB = HASH_HB;
     const int L = threadIdx.x;
     T *z = reinterpret_cast<T *>(smem_raw);
     for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
@@ -927,26 +808,11 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
         }
         u128 s0, inc;
         bool lh;
-        if (segmented) {
-            lh = gen != 0;
-            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
-        } else {
-            s0 = mk128(state_io[0], state_io[1]);
-            inc = mk128(state_io[2], state_io[3]);
-            lh = is_lehmer(inc);
-        }
+        ChaKey ck;
         CtaGen<W> gs;
-        gs.inc = inc;
-        gs.s = gen_jump_small(s0, inc, L + 1, lh);
-        gs.AJ = gen_SA(lh, G);
-        gs.CJ = mul128(g_SG[G], inc);
-        gs.B0 = 0;
-        gs.D = 0;
-        gs.seg = 0;
-        gs.frontier = n;
-        gs.parity = 0;
+        cta_gen_setup<CHA, W>(gs, s0, inc, lh, ck, segmented, gen, run_seed, base + a, state_io, n, L);
         uint64_t *rkf = segmented ? nullptr : rk_first;
-        if (plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);  // overlaps the payload load
+        if (plan.nbatches) large_gen_step<CHA>(gs, plan, sh, L, rkf, chawin, ck);  // overlaps the payload load
         if (use_tma) {
             mbar_wait(&bar, parity);
             parity ^= 1u;
@@ -954,7 +820,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
         __syncthreads();
         for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= G) {
             const uint32_t need = top >= (int64_t)lim + (G - 1) ? (uint32_t)top - (G - 1) : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
+            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step<CHA>(gs, plan, sh, L, rkf, chawin, ck);
             tag = (tag + 1) & 0xFFFFu;
             if (tag == 0) {
                 for (uint32_t q = L; q < (1u << HB); q += G) sh.ht[q] = 0;
@@ -963,7 +829,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
             }
             apply_group_cta_global(z, sh, tag, (uint32_t)top, lim, L);
         }
-        while (gs.B0 < plan.nbatches) large_gen_step(gs, plan, sh, L, rkf);
+        while (gs.B0 < plan.nbatches) large_gen_step<CHA>(gs, plan, sh, L, rkf, chawin, ck);
         if (use_tma) {
             if (L == 0) {
                 fence_proxy_async();
@@ -977,7 +843,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
             if (segmented) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = gen_jump(s0, inc, words, lh);
+                const u128 sf = CHA ? cha_add(s0, words) : gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -988,43 +854,70 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
     if (use_tma && L == 0) bulk_wait_all();
 }
 
+template <typename T, int W, int CM>
+__global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                  DevPlan plan, uint64_t run_seed, int64_t base,
+                                                                  uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                                  uint64_t *words64, uint64_t *rk_first, int use_tma,
+                                                                  int segmented, int gen) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ LargeShared<T, W, uint16_t, CRING, HASH_HB> sh;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
+    bool cha = CM == 1;
+    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if (CM != 0 && cha)
+        shuffle_cta_hash_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+                                             rk_first, use_tma, segmented, gen, smem_raw, sh, bar, chawin);
+    else if (CM != 1)
+        shuffle_cta_hash_body<T, W, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+                                           rk_first, use_tma, segmented, gen, smem_raw, sh, bar, chawin);
+}
+
 // -------------------------------------------------------------------------------------
 // arrays larger than shared memory: targets into a global buffer, then warp-group apply
 // on the array in global memory
 // -------------------------------------------------------------------------------------
-template <bool SEGMENTED>
-__global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_arrays, DevPlan plan, uint64_t run_seed,
-                                                               int64_t base, uint32_t *__restrict__ J,
-                                                               uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                               uint64_t *words64, uint64_t *rk_first, int gen) {
-    __shared__ DevSeg segs[MAX_SEGS];
+template <bool SEGMENTED, bool CHA>
+__device__ __forceinline__ void shuffle_large_gen_body(int64_t num_arrays, const DevPlan &plan, uint64_t run_seed,
+                                                       int64_t base, uint32_t *__restrict__ J,
+                                                       uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                       uint64_t *words64, uint64_t *rk_first, int gen, DevSeg *segs,
+                                                       uint64_t *chawin) {
     const int lane = threadIdx.x & 31;
-    for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
-    __syncwarp();
     const uint32_t n = plan.n;
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         uint32_t *Ja = J + a * (int64_t)n;
         u128 s0, inc;
         bool lh;
+        ChaKey ck;
         if constexpr (SEGMENTED) {
-            lh = gen != 0;
-            gen_seed(array_seed(run_seed, (uint64_t)(base + a)), s0, inc, lh);
+            lh = gen == 1;
+            const uint64_t seed = array_seed(run_seed, (uint64_t)(base + a));
+            if constexpr (CHA) {
+                chacha_seed(seed, ck);
+                s0 = mk128(0, 0);
+                inc = mk128(ck.nonce, CHACHA_TAG);
+            } else {
+                gen_seed(seed, s0, inc, lh);
+            }
         } else {
             s0 = mk128(state_io[0], state_io[1]);
             inc = mk128(state_io[2], state_io[3]);
             lh = is_lehmer(inc);
+            if constexpr (CHA) ck = cha_key_of_state(state_io);
         }
         GenState gs;
-        gen_init(gs, s0, inc, n, lane);
+        gen_init<CHA>(gs, s0, inc, n, lane);
         auto sink = [Ja](uint32_t pos, uint32_t v) { Ja[pos] = v; };
         uint64_t *rkf = SEGMENTED ? nullptr : rk_first;
-        while (gs.B0 < plan.nbatches) gen_step(gs, plan, segs, sink, lane, rkf);
+        while (gs.B0 < plan.nbatches) gen_step<CHA>(gs, plan, segs, sink, lane, rkf, chawin, ck);
         const uint64_t words = (uint64_t)plan.nbatches + gs.D;
         if (lane == 0) {
             if constexpr (SEGMENTED) {
                 if (words32) words32[a] = (uint32_t)words;
             } else {
-                const u128 sf = gen_jump(s0, inc, words, lh);
+                const u128 sf = CHA ? cha_add(s0, words) : gen_jump(s0, inc, words, lh);
                 state_io[0] = sf.hi;
                 state_io[1] = sf.lo;
                 if (words64) words64[0] = words;
@@ -1032,6 +925,26 @@ __global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_array
         }
         __syncwarp();
     }
+}
+
+template <bool SEGMENTED, int CM>
+__global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_arrays, DevPlan plan, uint64_t run_seed,
+                                                               int64_t base, uint32_t *__restrict__ J,
+                                                               uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                               uint64_t *words64, uint64_t *rk_first, int gen) {
+    __shared__ DevSeg segs[MAX_SEGS];
+    __shared__ __align__(16) uint64_t chawin[CM ? 256 : 2];
+    const int lane = threadIdx.x & 31;
+    for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
+    __syncwarp();
+    bool cha = CM == 1;
+    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if (CM != 0 && cha)
+        shuffle_large_gen_body<SEGMENTED, CM != 0>(num_arrays, plan, run_seed, base, J, words32, state_io, words64,
+                                                   rk_first, gen, segs, chawin);
+    else if (CM != 1)
+        shuffle_large_gen_body<SEGMENTED, false>(num_arrays, plan, run_seed, base, J, words32, state_io, words64,
+                                                 rk_first, gen, segs, chawin);
 }
 
 // Same group resolution as apply_group, on global memory (no lane-id table: repeated

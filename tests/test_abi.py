@@ -42,7 +42,7 @@ def test_struct_layouts(N):
     assert C.sizeof(N.Pcg64State) == 32
     assert C.sizeof(N.Regime) == 16
     assert C.sizeof(N.Segment) == 24
-    assert N.lib().br_abi_version() == 2
+    assert N.lib().br_abi_version() == 3
 
 
 def test_host_generator_helpers_match_oracle(N, O, golden):
@@ -183,3 +183,43 @@ def test_cli_parser_and_csv_schema():
     assert buf.getvalue().splitlines() == [cli.CSV_HEADER, "shuffle_6_b200,pcg64,64,12.500,11.250"]
     with pytest.raises(SystemExit):
         cli.build_parser().parse_args(["bench", "--sizes", "1"])
+
+
+def test_host_chacha_matches_golden(N, O, golden):
+    import paper_2408_06213_b200 as B
+
+    L = N.lib()
+    assert C.sizeof(N.ChachaState) == 64
+    for rec in golden["chacha"]:
+        st = N.ChachaState()
+        L.br_chacha_seed(rec["seed"], C.byref(st))
+        assert list(st.key) == rec["key"] and st.inc_hi == rec["nonce"] and st.inc_lo == N.BR_CHACHA_TAG
+        assert [L.br_pcg64_next(C.byref(st)) for _ in range(20)] == rec["words"]
+        s = B.make_source("chacha", rec["seed"])
+        assert s.key_words == tuple(rec["key"]) and s.nonce == rec["nonce"]
+        assert [s.next_word() for _ in range(20)] == rec["words"]
+    st = N.ChachaState()
+    L.br_chacha_seed(11, C.byref(st))
+    L.br_pcg64_advance(C.byref(st), 1000)
+    assert L.br_pcg64_next(C.byref(st)) == O.words(O.chacha(11), 1001)[-1]
+    rec = golden["chacha_block_rfc8439"]
+    from paper_2408_06213_b200 import batchrand as BR
+
+    assert BR._chacha_block_words(rec["key"], rec["nonce"], rec["counter"]) == rec["block"]
+
+
+def test_chacha_position_mapping():
+    from paper_2408_06213_b200 import batchrand as B
+
+    s = B.ChaChaSource(3)
+    for drawn in range(0, 20):
+        assert B._chacha_position(s) == drawn
+        s.next_word()
+    t = B.ChaChaSource(3)
+    B._chacha_set_position(t, 13)
+    assert (t.counter, t._pos) == (2, 10)
+    u = B.ChaChaSource(3)
+    w = [u.next_word() for _ in range(20)]
+    v = B.ChaChaSource(3)
+    B._chacha_set_position(v, 13)
+    assert [v.next_word() for _ in range(7)] == w[13:20]

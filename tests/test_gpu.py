@@ -470,6 +470,104 @@ def test_lehmer_rolls(B, O, golden):
     assert (st.state_hi << 64 | st.state_lo) == src.state
 
 
+# ------------------------------------------------------------------ ChaCha20
+def test_chacha_fill(B, O):
+    for seed, offset, count in ((0, 0, 1), (3, 5, 20), (77, 123, 50001), (9, (1 << 40) + 3, 4096)):
+        got = u64(B.pcg64_fill(seed, count, offset, generator="chacha"))
+        assert np.array_equal(got, O.pcg64_fill(O.chacha(seed), offset, count)), (seed, offset)
+    assert "cha_fill_kernel" in B.last_kernel()
+    s = B.ChaChaSource(77)
+    [s.next_word() for _ in range(5)]  # mid-block source: fill starts at its position
+    o = O.chacha(77)
+    O.words(o, 5)
+    assert u64(B.pcg64_fill(s, 30)).tolist() == O.words(o, 30)
+
+
+def test_chacha_dropin_shuffles_golden(B, O, golden):
+    scheds = {k: B.ShuffleSchedule(tuple(tuple(e) for e in v["entries"]), v["max_batch"])
+              for k, v in golden["schedules"].items()}
+    for rec in golden["shuffle_batched_chacha"]:
+        s = B.make_source("chacha", rec["seed"])
+        for _ in range(rec["pre"]):
+            s.next_word()
+        z = np.arange(rec["n"], dtype=np.uint32)
+        B.shuffle_batched(s, z, scheds[rec["schedule"]])
+        assert sha_u32(z) == rec["sha"], (rec["n"], rec["schedule"], B.last_kernel())
+        assert (s.counter, s._pos) == (rec["counter_after"], rec["pos_after"])
+        if s._pos < 16:  # the refilled buffer is the block the reference would hold
+            o = O.chacha(rec["seed"])
+            O.words(o, rec["pre"] + rec["words"])
+            assert s._buffer == list(o.buf)
+    for rec in golden["shuffle_unbatched_chacha"]:
+        s = B.ChaChaSource(rec["seed"])
+        z = B.shuffle_unbatched(s, list(range(rec["n"])))
+        assert sha_u32(z) == rec["sha"]
+
+
+@pytest.mark.parametrize("n,eb", [(64, 4), (100, 8), (4096, 4), (20000, 8), (70000, 4), (1 << 20, 8)])
+def test_chacha_segmented(B, O, n, eb):
+    na = max(2, min(400, (1 << 20) // n))
+    dt = np.uint32 if eb == 4 else np.uint64
+    payload = np.arange(n * na, dtype=dt)
+    dev = torch.from_numpy(payload.view(np.int32 if eb == 4 else np.int64).copy()).cuda()
+    _, w = B.shuffle_many(dev, n, 777, array_index_base=3, return_words=True, generator="chacha")
+    ref = payload.copy()
+    rw = O.shuffle_segmented(ref, n, 777, array_index_base=3, generator="chacha")
+    assert np.array_equal(dev.cpu().numpy().view(dt), ref), B.last_kernel()
+    assert np.array_equal(u32(w), rw)
+
+
+@pytest.mark.parametrize("n", [1000, 70000])
+def test_chacha_wide_schedule_paths(B, O, n):
+    """k = 16 in the tail regime moves n=1000 to the warp kernel and n=70000 to the
+    global-target fallback, in both the segmented and the stream form."""
+    entries = ((1 << 30, 2), (17, 16))
+    sched = B.ShuffleSchedule(entries, 16)
+    na = 6
+    payload = np.arange(n * na, dtype=np.uint32)
+    dev = torch.from_numpy(payload.view(np.int32).copy()).cuda()
+    B.shuffle_many(dev, n, 31, schedule=sched, generator="chacha")
+    kern = B.last_kernel()
+    ref = payload.copy()
+    O.shuffle_segmented(ref, n, 31, entries=list(entries), generator="chacha")
+    assert np.array_equal(u32(dev), ref), kern
+    assert ("mid" in kern) if n == 1000 else ("large_gen" in kern)
+    s = B.ChaChaSource(55)
+    z = torch.arange(n, dtype=torch.int32, device="cuda")
+    B.shuffle_batched(s, z, sched)
+    o = O.chacha(55)
+    zr = O.shuffle_batched(o, np.arange(n, dtype=np.uint32), list(entries))
+    assert np.array_equal(u32(z), zr) and (s.counter, s._pos) == (o.counter, o.pos)
+
+
+def test_chacha_rolls(B, O, golden):
+    for rec in golden["roll_batch_chacha"]:
+        s = B.ChaChaSource(rec["seed"])
+        k = len(rec["bases"])
+        res = B.roll_batches(s, dev_u32(np.tile(np.asarray(rec["bases"], dtype=np.uint32), len(rec["results"]))), k,
+                             flags=True, final_remainder=True)
+        assert u32(res.rolls).reshape(-1, k).tolist() == [x[0] for x in rec["results"]]
+        assert res.words.cpu().tolist() == [x[1] for x in rec["results"]]
+        assert res.flags.cpu().tolist() == [x[2] for x in rec["results"]]
+        assert u64(res.final_remainder).tolist() == [x[3] for x in rec["results"]]
+        assert (s.counter, s._pos) == (rec["counter_after"], rec["pos_after"])
+    for k, nb in ((2, 300000), (1, 100003), (3, 50001)):
+        bounds = O.gen_bounds(8, k * nb)
+        if k == 2:  # products near 2^64: rejections at the head of the run
+            bounds[:1000:2] = 0xFFFFFFFF
+            bounds[1:1000:2] = 3006477107
+        src = O.chacha(5)
+        rolls, words, flags, rk = O.roll_batches(src, bounds, k)
+        ds = B.DeviceStream(5, generator="chacha")
+        r = B.roll_batches(ds, dev_u32(bounds), k, flags=True, final_remainder=True)
+        st = ds.host_state()
+        assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words), k
+        assert np.array_equal(r.flags.cpu().numpy(), flags) and np.array_equal(u64(r.final_remainder), rk)
+        assert (st.state_hi << 64 | st.state_lo) == O.chacha_position(src)
+        if k == 2:
+            assert int(words.sum()) > nb  # the forced rejections happened
+
+
 def test_cli_bench_and_shuffle(B, O, tmp_path):
     import io
     import contextlib
