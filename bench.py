@@ -150,7 +150,7 @@ def cpu_cores():
 
 
 # ------------------------------------------------------------------------------ C2 (rolls)
-def setup_c2(torch, B, rank, nb):
+def setup_c2(torch, B, rank, nb, generator="pcg64"):
     import numpy as np
 
     from paper_2408_06213_b200 import _native as N
@@ -164,9 +164,14 @@ def setup_c2(torch, B, rank, nb):
     r = B.roll_batches(gen, spans, 1)
     bounds = (r.rolls + 2).contiguous()
     del spans, r
-    # roll stream: pcg64(array_seed(7, 1)) advanced to this rank's first batch
-    st = N.Pcg64State()
-    N.lib().br_pcg64_seed(N.lib().br_array_seed(7, 1), C.byref(st))
+    # roll stream: make_source(generator, array_seed(7, 1)) advanced to this rank's first batch
+    seed = N.lib().br_array_seed(7, 1)
+    if generator == "chacha":
+        st = N.ChachaState()
+        N.lib().br_chacha_seed(seed, C.byref(st))
+    else:
+        st = N.Pcg64State()
+        (N.lib().br_lehmer_seed if generator == "lehmer" else N.lib().br_pcg64_seed)(seed, C.byref(st))
     N.lib().br_pcg64_advance(C.byref(st), rank * nb)
     stream = B.DeviceStream.from_struct(st)
     rolls = torch.empty(2 * nb, dtype=torch.int32, device="cuda")
@@ -180,7 +185,7 @@ def bench_c2(args, torch, B, ws, rank):
 
     L = N.lib()
     nb = NB_C2
-    bounds, stream, rolls, words = setup_c2(torch, B, rank, nb)
+    bounds, stream, rolls, words = setup_c2(torch, B, rank, nb, args.generator)
     sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     ptrs = [C.c_void_p(x.data_ptr()) for x in (bounds, stream.state, rolls, words)]
     wsp = C.c_void_p(stream.workspace.data_ptr())
@@ -229,6 +234,8 @@ def bench_c2(args, torch, B, ws, rank):
     rolls_total = 2 * nb * K * ws
     value = rolls_total / (total_ms / 1e3)
     t_main = statistics.mean(main_ms) / 1e3
+    if args.generator == "chacha":  # ChaCha streams are rolled inside the fixup kernel: time the step
+        t_main = total_ms / K / 1e3
     peak, peak_kind = load_peaks()
     achieved = BYTES_PER_BATCH_C2 * nb / t_main / 1e9
     traffic = load_traffic().get("roll_fast_kernel")
@@ -237,7 +244,8 @@ def bench_c2(args, torch, B, ws, rank):
         "ms_per_step": total_ms / K,
         "main_ms": statistics.mean(main_ms),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "roll_fast_kernel<2>",
+                     "traffic": traffic,
+                     "kernel": "roll_fast_kernel<2>" if args.generator != "chacha" else "roll_fixup_kernel<2>",
                      "algorithmic_bytes_per_launch": BYTES_PER_BATCH_C2 * nb, "peak_source": peak_kind},
         "clocks": clk.summary(),
         "gpu_launches": 2 * K,
@@ -296,15 +304,15 @@ def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
         data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
     K = steps or args.steps
     for _ in range(args.warmup):
-        B.shuffle_many(data, n, cfg["seed"], array_index_base=base)
+        B.shuffle_many(data, n, cfg["seed"], array_index_base=base, generator=args.generator)
     kernel = B.last_kernel()
-    soak(torch, lambda: B.shuffle_many(data, n, cfg["seed"], array_index_base=base))
+    soak(torch, lambda: B.shuffle_many(data, n, cfg["seed"], array_index_base=base, generator=args.generator))
     barrier(torch, ws)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     with ClockSampler(torch.cuda.current_device()) as clk:
         for a, b in evs:
             a.record()
-            B.shuffle_many(data, n, cfg["seed"], array_index_base=base)
+            B.shuffle_many(data, n, cfg["seed"], array_index_base=base, generator=args.generator)
             b.record()
         torch.cuda.synchronize()
     per = [a.elapsed_time(b) for a, b in evs]
@@ -432,6 +440,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--generator", default="pcg64", choices=["pcg64", "lehmer", "chacha"],
+                    help="word generator of the timed path (the headline is pcg64)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     ws, rank, local = dist_info()
@@ -463,13 +473,14 @@ def main():
                               "U[2,2^16) from seed 7, words from pcg64(hash(7,1)); output 2^26 u32 rolls + 2^25 u8 "
                               "words per GPU", "batches_per_gpu": NB_C2, "k": 2,
                   "l2": "inputs+outputs 544 MiB per step > 126 MB L2 (no flush needed)",
-                  "parallelism": f"dp{ws} (stream sections by jump-ahead)"}
+                  "parallelism": f"dp{ws} (stream sections by jump-ahead)", "generator": args.generator}
         dtype = "u64"
     else:
         cfg = SHUFFLE_CFG[args.config]
         r = bench_shuffle(cfg, args, torch, B, ws, rank)
         metric, unit = "shuffled elements/sec", "elements/s"
-        config = {"workload": cfg["workload"], "l2": "payload larger than L2", "parallelism": f"dp{ws} (arrays)"}
+        config = {"workload": cfg["workload"], "l2": "payload larger than L2", "parallelism": f"dp{ws} (arrays)",
+                  "generator": args.generator}
         dtype = "u32"
         r["e2e"] = None
     line = {"metric": metric, "value": r["value"], "unit": unit, "n_gpus": ws, "steps": args.steps,
