@@ -146,6 +146,13 @@ int br_roll_batches_phase(const uint32_t *bounds_dev, int k, int64_t num_batches
                           br_pcg64 *state_dev, uint32_t *rolls_dev, uint8_t *words_dev,
                           uint8_t *flags_dev, uint64_t *final_rk_dev, void *workspace_dev,
                           int phase, void *stream);
+/* roll_batch_naive (batched.py:126-128) in the same bulk form: one Lemire draw on the
+ * product of the k bounds, digits by division (mixed_radix.py:53-67).  Same words, digits
+ * and acceptance as br_roll_batches (Theorem 1); the division-based baseline of the paper.
+ * Status through br_roll_check as for br_roll_batches. */
+int br_roll_batches_naive(const uint32_t *bounds_dev, int k, int64_t num_batches, br_pcg64 *state_dev,
+                          uint32_t *rolls_dev, uint8_t *words_dev, uint8_t *flags_dev,
+                          uint64_t *final_rk_dev, void *workspace_dev, void *stream);
 /* Synchronises `stream`, returns the deferred status of the last br_roll_batches on this
  * workspace (BR_OK / BR_E_INVALID / BR_E_BOUND_OVERFLOW) and clears it.  *extra_words (may
  * be NULL) receives the words consumed beyond one per batch (rejections). */
@@ -180,6 +187,15 @@ int br_shuffle_stream_segments(void *z_dev, int elem_bytes, uint64_t n, br_pcg64
 int br_shuffle_segmented(void *data_dev, int elem_bytes, int64_t num_arrays, uint64_t n,
                          uint64_t run_seed, int64_t array_index_base, const br_regime *entries,
                          int n_entries, int generator, uint32_t *words_dev, void *stream);
+
+/* shuffle.py:228-266 shuffle_naive_batched(src, z): Fisher-Yates two indices at a time,
+ * one draw on (i+1)*i split by division, a single roll on 2 for a leftover index 1.
+ * Stream form (as br_shuffle_stream) and the segmented form (as br_shuffle_segmented). */
+int br_shuffle_naive_stream(void *z_dev, int elem_bytes, uint64_t n, br_pcg64 *state_dev,
+                            uint64_t *words_dev, void *stream);
+int br_shuffle_naive_segmented(void *data_dev, int elem_bytes, int64_t num_arrays, uint64_t n,
+                               uint64_t run_seed, int64_t array_index_base, int generator,
+                               uint32_t *words_dev, void *stream);
 
 /* Kernel-selection report for the last device call on this thread (diagnostics). */
 const char *br_last_kernel(void);

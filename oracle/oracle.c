@@ -396,6 +396,50 @@ int or_shuffle_unbatched(or_source *s, void *zv, int32_t eb, uint64_t n) {
     return OR_OK;
 }
 
+/* shuffle.py:228-266 shuffle_naive_batched (literal): pairs by division, then index 1 */
+int or_shuffle_naive_batched(or_source *s, void *zv, int32_t eb, uint64_t n) {
+    unsigned char *z = (unsigned char *)zv;
+    int bits = s->word_bits;
+    u128 mask = mask_of(bits), top = mask + 1;
+    uint64_t w;
+    if (n < 2) return OR_OK;
+    uint64_t i = n - 1;
+    if (i >= 2 && (u128)(i + 1) * i > top) return OR_E_BOUND_OVERFLOW;
+    while (i >= 2) {
+        u128 b = (u128)(i + 1) * i;
+        if (or_next_word(s, &w)) return OR_E_EXHAUSTED;
+        u128 p = b * w, lo = p & mask;
+        if (lo < b) {
+            u128 t = (top - b) % b;
+            while (lo < t) {
+                if (or_next_word(s, &w)) return OR_E_EXHAUSTED;
+                p = b * w;
+                lo = p & mask;
+            }
+        }
+        u128 v = p >> bits;
+        uint64_t j1 = (uint64_t)(v / i), j2 = (uint64_t)(v % i);
+        swap_elem(z, eb, i, j1);
+        i -= 1;
+        swap_elem(z, eb, i, j2);
+        i -= 1;
+    }
+    if (i == 1) {
+        if (or_next_word(s, &w)) return OR_E_EXHAUSTED;
+        u128 p = (u128)2 * w, lo = p & mask;
+        if (lo < 2) {
+            u128 t = (top - 2) % 2;
+            while (lo < t) {
+                if (or_next_word(s, &w)) return OR_E_EXHAUSTED;
+                p = (u128)2 * w;
+                lo = p & mask;
+            }
+        }
+        swap_elem(z, eb, 1, (uint64_t)(p >> bits));
+    }
+    return OR_OK;
+}
+
 /* shuffle.py:100-134 _run_batches (literal, with the carried bound u) */
 static int run_batches(or_source *s, unsigned char *z, int eb, uint64_t n, uint32_t k,
                        u128 *u_io, uint64_t count, int bits) {
@@ -612,6 +656,46 @@ int or_gen_bounds(or_source *s, uint32_t *out, int64_t count, uint64_t lo, uint6
         out[i] = (uint32_t)(lo + v);
     }
     return OR_OK;
+}
+
+/* batched.py:126-128 roll_batch_naive: roll_single on the product, then decode
+ * (mixed_radix.py:53-67: divmod by the bases in reverse) */
+int or_roll_batch_naive(or_source *s, const uint64_t *bases, int32_t k, uint64_t *digits) {
+    u128 prod;
+    int st = radix_product(bases, k, s->word_bits, &prod);
+    if (st) return st;
+    uint64_t v, words;
+    int32_t ro;
+    st = or_roll_single(s, (uint64_t)prod, (uint64_t)(prod >> 64), &v, &words, &ro);
+    if (st) return st;
+    u128 val = v;
+    for (int m = k - 1; m >= 0; --m) {
+        digits[m] = (uint64_t)(val % bases[m]);
+        val /= bases[m];
+    }
+    return OR_OK;
+}
+
+/* segmented shuffle_naive_batched: array a shuffled with make_source(G, hash(run_seed, base + a)) */
+int or_shuffle_naive_segmented(void *data, int32_t eb, int64_t num_arrays, uint64_t n, uint64_t run_seed,
+                               int64_t base, uint32_t *words_out, int32_t nthreads, int32_t generator) {
+    int err = OR_OK;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+#endif
+    for (int64_t a = 0; a < num_arrays; ++a) {
+        or_source src;
+        const uint64_t seed = or_array_seed(run_seed, (uint64_t)(base + a));
+        if (generator == 2) or_source_chacha(&src, seed);
+        else if (generator == 1) or_source_lehmer(&src, seed);
+        else or_source_pcg64(&src, seed);
+        int st = or_shuffle_naive_batched(&src, (unsigned char *)data + (size_t)a * n * eb, eb, n);
+        if (st) err = st;
+        if (words_out) words_out[a] = (uint32_t)src.drawn;
+    }
+    (void)nthreads;
+    return err;
 }
 
 int or_shuffle_segmented(void *data, int32_t eb, int64_t num_arrays, uint64_t n,

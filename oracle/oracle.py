@@ -110,6 +110,9 @@ def lib():
             "or_shuffle_segmented_gen": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, vp, i32, vp, i32, i32, i32]),
             "or_pcg64_fill": (None, [P(Source), u64, vp, i64]),
             "or_chacha_block": (None, [vp, u64, u64, vp]),
+            "or_shuffle_naive_batched": (C.c_int, [P(Source), vp, i32, u64]),
+            "or_roll_batch_naive": (C.c_int, [P(Source), vp, i32, vp]),
+            "or_shuffle_naive_segmented": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, i32, i32]),
             "or_source_chacha": (None, [P(Source), u64]),
             "or_chacha_advance": (None, [P(Source), u64]),
         }
@@ -172,7 +175,7 @@ def chacha_position(s: Source) -> int:
     return s.counter * 8 if s.pos == 16 else (s.counter - 1) * 8 + s.pos // 2
 
 
-GENERATOR_MAKERS = {"pcg64": pcg64, "lehmer": lehmer, "chacha": chacha}
+
 
 
 def fixed(words, bits: int = 64) -> Source:
@@ -329,3 +332,34 @@ def shuffle_segmented(data: np.ndarray, n: int, run_seed: int, array_index_base:
                                           nthreads, int(unbatched), {"pcg64": 0, "lehmer": 1, "chacha": 2}[generator]),
            "shuffle_segmented")
     return wds
+
+
+# ---------------------------------------------------------------- division-based baselines
+def shuffle_naive_batched(s: Source, z) -> np.ndarray:
+    """shuffle.py:228-266 (in place on a copy; returns it)."""
+    a = _as_array(z)
+    _check(lib().or_shuffle_naive_batched(C.byref(s), _ptr(a), a.dtype.itemsize, a.size), "shuffle_naive_batched")
+    return a
+
+
+def roll_batch_naive(s: Source, bases) -> tuple:
+    """batched.py:126-128."""
+    b = np.asarray(bases, dtype=np.uint64)
+    d = np.zeros(len(b), dtype=np.uint64)
+    _check(lib().or_roll_batch_naive(C.byref(s), _ptr(b), len(b), _ptr(d)), "roll_batch_naive")
+    return tuple(int(x) for x in d)
+
+
+def shuffle_naive_segmented(data: np.ndarray, n: int, run_seed: int, array_index_base: int = 0,
+                            nthreads: int = 0, generator: str = "pcg64"):
+    assert data.flags.c_contiguous
+    num_arrays = data.size // n
+    wds = np.empty(num_arrays, dtype=np.uint32)
+    _check(lib().or_shuffle_naive_segmented(_ptr(data), data.dtype.itemsize, num_arrays, n, run_seed & MASK64,
+                                            array_index_base, _ptr(wds), nthreads,
+                                            {"pcg64": 0, "lehmer": 1, "chacha": 2}[generator]),
+           "shuffle_naive_segmented")
+    return wds
+
+
+GENERATOR_MAKERS = {"pcg64": pcg64, "lehmer": lehmer, "chacha": chacha}

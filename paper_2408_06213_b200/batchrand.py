@@ -396,6 +396,18 @@ def digit_pass(r0: int, bases: RadixBases):
     return tuple(int(x) & 0xFFFFFFFF for x in d.cpu().tolist()), int(rk[0]) & MASK64
 
 
+def roll_batch_naive(source, bases: RadixBases) -> tuple:
+    """batched.py:126-128: one uniform draw on the product, decoded by division (device)."""
+    torch = _torch()
+    if bases.bits != 64:
+        raise TypeError("the device path needs 64-bit words")
+    st = _state_struct(source)
+    dstream = DeviceStream.from_struct(st)
+    r = roll_batches(dstream, _device_bases(bases.bases, torch), len(bases.bases), naive=True)
+    dstream.write_back(source)
+    return tuple(int(x) & 0xFFFFFFFF for x in r.rolls.cpu().tolist())
+
+
 def roll_batch_known_threshold(source, spec: BatchSpec) -> BatchResult:
     """batched.py:85-99."""
     if spec.precomputed_threshold is None:
@@ -510,7 +522,7 @@ def _call_scratch(torch):
     return t
 
 
-def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=False):
+def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=False, naive=False):
     torch = _torch()
     st = _state_struct(source)
     dev, fin = _device_payload(z, torch)
@@ -521,7 +533,10 @@ def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=
     words = scratch[8:9]
     rk = scratch[9:10] if want_rk else None
     L = N.lib()
-    if segments is None:
+    if naive:
+        N.check(L.br_shuffle_naive_stream(_ptr(dev), dev.element_size(), n, _ptr(ds.state), _ptr(words),
+                                          _stream_ptr(torch)), "shuffle")
+    elif segments is None:
         regs = regimes if regimes is not None else (N.Regime * 1)()
         nreg = len(regimes) if regimes is not None else 0
         N.check(L.br_shuffle_stream(_ptr(dev), dev.element_size(), n, _ptr(ds.state), regs, nreg, int(unbatched),
@@ -559,6 +574,18 @@ def shuffle_unbatched(source, z):
     if len(z) < 2:
         return z
     return _shuffle_stream(source, z, None, True)
+
+
+def shuffle_naive_batched(source, z):
+    """shuffle.py:228-266 on the device: pairs (i, i-1) from one draw on (i+1)*i split by
+    division, a single roll on 2 for a leftover index 1.  The division-based baseline."""
+    bits = getattr(source, "word_bits", 64)
+    i = len(z) - 1
+    if i >= 2 and (i + 1) * i > 1 << bits:
+        raise BoundOverflow(f"pair product {(i + 1) * i} exceeds 2**{bits}")
+    if len(z) < 2:
+        return z
+    return _shuffle_stream(source, z, None, False, naive=True)
 
 
 def partial_shuffle_batch(source, z, n: int, k: int, u: int) -> int:
@@ -638,7 +665,7 @@ class RollBatchesResult(NamedTuple):
 
 
 def roll_batches(stream, bounds, k: Optional[int] = None, *, flags: bool = False, final_remainder: bool = False,
-                 out=None, check: bool = True, chunks: int = 8) -> RollBatchesResult:
+                 out=None, check: bool = True, chunks: int = 8, naive: bool = False) -> RollBatchesResult:
     """Bulk roll_batch: batch i rolls the k dice bounds[i*k:(i+1)*k] (4-byte items, >= 1)
     from the PCG64 ``stream`` (a DeviceStream or a host PCG64 source, advanced in place).
 
@@ -647,7 +674,9 @@ def roll_batches(stream, bounds, k: Optional[int] = None, *, flags: bool = False
     view of u64).  Host ``bounds`` (CPU tensor / ndarray, ideally pinned) give host results;
     the copies are pipelined in ``chunks`` pieces over two copy streams so host-to-device,
     rolling and device-to-host overlap.  ``check`` synchronises and raises ValueError /
-    BoundOverflow like RadixBases.of."""
+    BoundOverflow like RadixBases.of.  ``naive`` takes the digits by division of one draw
+    on the product (roll_batch_naive, batched.py:126-128) -- identical results, the
+    division-based baseline."""
     torch = _torch()
     host_source = None
     if not isinstance(stream, DeviceStream):
@@ -660,9 +689,9 @@ def roll_batches(stream, bounds, k: Optional[int] = None, *, flags: bool = False
     if k is None:
         raise ValueError("k is required for flat bounds")
     if not (hasattr(bounds, "is_cuda") and bounds.is_cuda):
-        res = _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, torch)
+        res = _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, torch, naive)
     else:
-        res = _roll_batches_dev(stream, bounds.reshape(-1), k, flags, final_remainder, out, torch)
+        res = _roll_batches_dev(stream, bounds.reshape(-1), k, flags, final_remainder, out, torch, naive)
     if check:
         extra = C.c_uint64()
         N.check(N.lib().br_roll_check(_ptr(stream.workspace), _stream_ptr(torch), C.byref(extra)), "roll_batches")
@@ -671,7 +700,11 @@ def roll_batches(stream, bounds, k: Optional[int] = None, *, flags: bool = False
     return res
 
 
-def _roll_batches_dev(stream, b, k, flags, final_remainder, out, torch):
+def _roll_fn(naive: bool):
+    return N.lib().br_roll_batches_naive if naive else N.lib().br_roll_batches
+
+
+def _roll_batches_dev(stream, b, k, flags, final_remainder, out, torch, naive=False):
     if b.element_size() != 4 or not b.is_contiguous():
         raise TypeError("bounds must be a contiguous tensor of 4-byte items")
     nb = b.numel() // k
@@ -682,12 +715,12 @@ def _roll_batches_dev(stream, b, k, flags, final_remainder, out, torch):
         rolls, words = out[0], out[1]
     fl = torch.empty(nb, dtype=torch.uint8, device="cuda") if flags else None
     rk = torch.empty(nb, dtype=torch.int64, device="cuda") if final_remainder else None
-    N.check(N.lib().br_roll_batches(_ptr(b), k, nb, _ptr(stream.state), _ptr(rolls), _ptr(words), _ptr(fl), _ptr(rk),
-                                    _ptr(stream.workspace), _stream_ptr(torch)), "roll_batches")
+    N.check(_roll_fn(naive)(_ptr(b), k, nb, _ptr(stream.state), _ptr(rolls), _ptr(words), _ptr(fl), _ptr(rk),
+                            _ptr(stream.workspace), _stream_ptr(torch)), "roll_batches")
     return RollBatchesResult(rolls, words, fl, rk)
 
 
-def _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, torch):
+def _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, torch, naive=False):
     import numpy as np
 
     if isinstance(bounds, np.ndarray):
@@ -727,9 +760,9 @@ def _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, t
             ready = torch.cuda.Event()
             ready.record(h2d)
         comp.wait_event(ready)
-        N.check(L.br_roll_batches(_ptr(dbufs[slot]), k, cnt, _ptr(stream.state), _ptr(dro[slot]), _ptr(dwo[slot]),
-                                  _ptr(dfl[slot]), _ptr(drk[slot]), _ptr(stream.workspace),
-                                  C.c_void_p(comp.cuda_stream)), "roll_batches")
+        N.check(_roll_fn(naive)(_ptr(dbufs[slot]), k, cnt, _ptr(stream.state), _ptr(dro[slot]), _ptr(dwo[slot]),
+                                _ptr(dfl[slot]), _ptr(drk[slot]), _ptr(stream.workspace),
+                                C.c_void_p(comp.cuda_stream)), "roll_batches")
         done = torch.cuda.Event()
         done.record(comp)
         with torch.cuda.stream(d2h):
@@ -793,11 +826,12 @@ def pcg64_fill(source_or_seed, count: int, offset: int = 0, generator: str = "pc
 
 def shuffle_many(data, n: int, run_seed: int, array_index_base: int = 0,
                  schedule: ShuffleSchedule = DEFAULT_SCHEDULE, return_words: bool = False,
-                 generator: str = "pcg64"):
+                 generator: str = "pcg64", naive: bool = False):
     """Independent shuffles of the num_arrays = data.numel() // n contiguous arrays of a CUDA
     tensor (4- or 8-byte items), in place: array a is
     shuffle_batched(make_source(generator, array_seed(run_seed, array_index_base + a)), ...)
-    with generator "pcg64", "lehmer" or "chacha"."""
+    with generator "pcg64", "lehmer" or "chacha" -- or, with ``naive``,
+    shuffle_naive_batched(make_source(...), ...) (schedule ignored)."""
     if generator not in _GENERATOR_IDS:
         raise UnknownGenerator(f"no device generator {generator!r}")
     torch = _torch()
@@ -808,6 +842,11 @@ def shuffle_many(data, n: int, run_seed: int, array_index_base: int = 0,
         raise ValueError("data length must be a multiple of n")
     num_arrays = flat.numel() // n
     words = torch.empty(num_arrays, dtype=torch.int32, device="cuda") if return_words else None
+    if naive:
+        N.check(N.lib().br_shuffle_naive_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64,
+                                                   array_index_base, _GENERATOR_IDS[generator], _ptr(words),
+                                                   _stream_ptr(torch)), "shuffle_many")
+        return (data, words) if return_words else data
     regs = schedule._regimes()
     N.check(N.lib().br_shuffle_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64,
                                          array_index_base, regs, len(regs), _GENERATOR_IDS[generator], _ptr(words),
@@ -828,6 +867,7 @@ __all__ = [
     "RollBatchesResult", "ShuffleSchedule", "SourceExhausted", "UnknownGenerator", "ValueOutOfRange",
     "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",
     "make_source", "mul_full", "LehmerSource", "ChaChaSource", "GENERATORS", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
+    "roll_batch_naive", "shuffle_naive_batched",
     "roll_batches", "shuffle_batched", "shuffle_many", "shuffle_unbatched", "splitmix64_stream", "threshold",
     "last_kernel",
 ]

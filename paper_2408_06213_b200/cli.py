@@ -10,11 +10,13 @@ concatenated with the reference's own CSV and fed to its benchplots ratio curves
 (plots.py:90-156).  The device algorithms are registered like the reference's ALGORITHMS
 (cli.py:44-49):
 
-  * ``shuffle_b200`` / ``shuffle_2_b200`` / ``shuffle_6_b200``: one array per call through the
-    drop-in API on a device-resident tensor (includes the generator-state round trip that a
-    single call implies);
-  * ``many_6_b200``: the bulk segmented shuffle of 4096 independent arrays of length n per call
-    (ns per element amortised over all arrays) -- the workload a GPU is built for.
+  * ``shuffle_b200`` / ``naive_shuffle_2_b200`` / ``shuffle_2_b200`` / ``shuffle_6_b200``: one
+    array per call through the drop-in API on a device-resident tensor (includes the
+    generator-state round trip that a single call implies) -- the reference's four
+    algorithms (cli.py:44-49) on the device;
+  * ``many_naive_2_b200`` / ``many_6_b200``: the bulk segmented shuffle of 4096 independent
+    arrays of length n per call (ns per element amortised over all arrays) -- the workload a
+    GPU is built for -- with division-split pairs and with the default 6-dice schedule.
 
 Each cell repeats the call until the time budget is spent (cli.py:75-121), timed with CUDA
 events; the "min" column is the fastest single call.
@@ -46,11 +48,17 @@ def _unbatched(source, data):
     return B.shuffle_unbatched(source, data)
 
 
+def _naive(source, data):
+    return B.shuffle_naive_batched(source, data)
+
+
 ALGORITHMS = {
     "shuffle_b200": _unbatched,
+    "naive_shuffle_2_b200": _naive,
     "shuffle_2_b200": _one_array(B.default_schedule(2)),
     "shuffle_6_b200": _one_array(B.default_schedule(6)),
-    "many_6_b200": None,  # bulk segmented shuffle, see bench()
+    "many_naive_2_b200": None,  # bulk segmented shuffles, see bench()
+    "many_6_b200": None,
 }
 
 
@@ -65,12 +73,12 @@ def bench(generator="pcg64", sizes=DEFAULT_SIZES, algorithms=tuple(ALGORITHMS), 
     records = []
     for name in algorithms:
         for n in sizes:
-            if name == "many_6_b200":
+            if name.startswith("many_"):
                 data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(MANY_ARRAYS)
                 elems = n * MANY_ARRAYS
 
-                def call(data=data, n=n):
-                    B.shuffle_many(data, n, seed, generator=generator)
+                def call(data=data, n=n, naive=name == "many_naive_2_b200"):
+                    B.shuffle_many(data, n, seed, generator=generator, naive=naive)
             else:
                 source = B.make_source(generator, seed)
                 data = torch.arange(n, dtype=torch.int32, device="cuda")
@@ -151,7 +159,7 @@ def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="batchrand-b200", description="Device batched dice rolls and shuffles.")
     sub = parser.add_subparsers(dest="command", required=True)
     p = sub.add_parser("bench", help="time the device shuffles, emit the reference CSV schema")
-    p.add_argument("--generator", choices=("pcg64", "lehmer"), default="pcg64")
+    p.add_argument("--generator", choices=("pcg64", "lehmer", "chacha"), default="pcg64")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--sizes", type=_sizes_arg, default=DEFAULT_SIZES)
     p.add_argument("--algorithms", type=lambda t: tuple(x for x in t.split(",") if x), default=tuple(ALGORITHMS))
@@ -159,7 +167,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.set_defaults(func=_cmd_bench)
     p = sub.add_parser("shuffle", help="shuffle input lines on the device")
     p.add_argument("input", nargs="?")
-    p.add_argument("--generator", choices=("pcg64", "lehmer"), default="pcg64")
+    p.add_argument("--generator", choices=("pcg64", "lehmer", "chacha"), default="pcg64")
     p.add_argument("--seed", type=int, default=None)
     p.add_argument("--output")
     p.add_argument("--max-batch", type=int, default=6)

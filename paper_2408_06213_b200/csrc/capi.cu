@@ -149,13 +149,14 @@ struct CachedPlan {
 std::map<std::pair<int, std::string>, CachedPlan> g_plans;
 
 // Compile segments into a device plan (cached per device and segment list).
-int get_plan(uint64_t n, const std::vector<br_segment> &segs, CachedPlan *out) {
+int get_plan(uint64_t n, const std::vector<br_segment> &segs, bool naive, CachedPlan *out) {
     int dev;
     DeviceInfo di;
     int st = ensure_device(&dev, &di);
     if (st) return st;
     std::string key((const char *)segs.data(), segs.size() * sizeof(br_segment));
     key.append((const char *)&n, sizeof(n));
+    key.push_back(naive ? 'N' : 'B');
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_plans.find({dev, key});
     if (it != g_plans.end()) {
@@ -206,7 +207,7 @@ int get_plan(uint64_t n, const std::vector<br_segment> &segs, CachedPlan *out) {
         uint64_t steps = 0;
         for (const br_segment &sg : segs) steps += (uint64_t)sg.k * sg.count;
         cp.plan.lo = (uint32_t)(n > steps ? n - steps : 0);
-        cp.plan.pad = 0;
+        cp.plan.naive = naive ? 1u : 0u;
     }
     cp.plan.segs = (const DevSeg *)p;
     cp.plan.thresh = (const uint64_t *)((char *)p + off);
@@ -281,6 +282,11 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
                                              : (const void *)roll_fast_kernel<K, true, false>)
                                      : (a.rk ? (const void *)roll_fast_kernel<K, false, true>
                                              : (const void *)roll_fast_kernel<K, false, false>);
+            if (K == 2 && a.naive)  // division digits (k = 1 has nothing to divide)
+                kp = a.flags ? (a.rk ? (const void *)roll_fast_kernel<K, true, true, true>
+                                     : (const void *)roll_fast_kernel<K, true, false, true>)
+                             : (a.rk ? (const void *)roll_fast_kernel<K, false, true, true>
+                                     : (const void *)roll_fast_kernel<K, false, false, true>);
             int grid = grid_for(di, kp, threads, 0, work_blocks);
             RollArgs b = a;
             void *args[] = {&b};
@@ -424,7 +430,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
 
 int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std::vector<br_segment> &segs,
                    bool segmented, uint64_t run_seed, int64_t base, uint32_t *words32, br_pcg64 *state_dev,
-                   uint64_t *words64, uint64_t *rk_first, int gen, void *stream) {
+                   uint64_t *words64, uint64_t *rk_first, int gen, void *stream, bool naive = false) {
     if (gen < 0 || gen > 2) return fail(BR_E_UNSUPPORTED, "generator must be 0 (pcg64), 1 (lehmer) or 2 (chacha)");
     if (eb != 4 && eb != 8) return fail(BR_E_UNSUPPORTED, "elem_bytes must be 4 or 8");
     if (num_arrays < 0) return fail(BR_E_INVALID, "num_arrays < 0");
@@ -443,7 +449,7 @@ int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std
     if (!data) return fail(BR_E_INVALID, "null data pointer");
     if (!segmented && !state_dev) return fail(BR_E_INVALID, "null state pointer");
     CachedPlan cp;
-    stt = get_plan(n, segs, &cp);
+    stt = get_plan(n, segs, naive, &cp);
     if (stt) return stt;
     if (eb == 4)
         return launch_shuffle<uint32_t>(data, num_arrays, n, cp, segmented, run_seed, base, words32,
@@ -617,8 +623,9 @@ int br_roll_batches(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *state_d
     return br_roll_batches_phase(bounds, k, nb, state_dev, rolls, words, flags, final_rk, ws, 3, stream);
 }
 
-int br_roll_batches_phase(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *state_dev, uint32_t *rolls,
-                          uint8_t *words, uint8_t *flags, uint64_t *final_rk, void *ws, int phase, void *stream) {
+static int roll_batches_impl(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *state_dev, uint32_t *rolls,
+                      uint8_t *words, uint8_t *flags, uint64_t *final_rk, void *ws, int phase, int naive,
+                      void *stream) {
     if (phase < 1 || phase > 3) return fail(BR_E_INVALID, "phase must be 1, 2 or 3");
     if (nb < 0) return fail(BR_E_INVALID, "num_batches < 0");
     if (k < 1) return fail(BR_E_INVALID, "at least one base is required");
@@ -644,6 +651,7 @@ int br_roll_batches_phase(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *s
     a.flags = flags;
     a.rk = final_rk;
     a.ws = (RollWs *)ws;
+    a.naive = naive;
     cudaStream_t st = (cudaStream_t)stream;
     switch (k) {
         case 1: return launch_roll<1>(a, di, st, phase);
@@ -655,6 +663,16 @@ int br_roll_batches_phase(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *s
         case 7: return launch_roll<7>(a, di, st, phase);
         default: return launch_roll<8>(a, di, st, phase);
     }
+}
+
+int br_roll_batches_phase(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *state_dev, uint32_t *rolls,
+                          uint8_t *words, uint8_t *flags, uint64_t *final_rk, void *ws, int phase, void *stream) {
+    return roll_batches_impl(bounds, k, nb, state_dev, rolls, words, flags, final_rk, ws, phase, 0, stream);
+}
+
+int br_roll_batches_naive(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *state_dev, uint32_t *rolls,
+                          uint8_t *words, uint8_t *flags, uint64_t *final_rk, void *ws, void *stream) {
+    return roll_batches_impl(bounds, k, nb, state_dev, rolls, words, flags, final_rk, ws, 3, 1, stream);
 }
 
 int br_roll_check(void *ws, void *stream, uint64_t *extra_words) {
@@ -728,6 +746,38 @@ int br_shuffle_segmented(void *data, int eb, int64_t num_arrays, uint64_t n, uin
     if (st) return st;
     return shuffle_common(data, eb, num_arrays, n, segs, true, run_seed, base, words_dev, nullptr, nullptr, nullptr,
                           generator, stream);
+}
+
+// shuffle.py:228-266 shuffle_naive_batched as a plan: pairs (i, i-1) from the top while
+// i >= 2, then a single roll on 2 if index 1 is left.
+static void naive_segments(uint64_t n, std::vector<br_segment> &segs) {
+    if (n < 2) return;
+    br_segment s{};
+    s.start_n = n;
+    s.k = 2;
+    s.count = (n - 1) / 2;
+    if (s.count) segs.push_back(s);
+    if ((n - 1) & 1) {
+        br_segment t{};
+        t.start_n = 2;
+        t.k = 1;
+        t.count = 1;
+        segs.push_back(t);
+    }
+}
+
+int br_shuffle_naive_stream(void *z, int eb, uint64_t n, br_pcg64 *state_dev, uint64_t *words_dev, void *stream) {
+    std::vector<br_segment> segs;
+    naive_segments(n, segs);
+    return shuffle_common(z, eb, 1, n, segs, false, 0, 0, nullptr, state_dev, words_dev, nullptr, 0, stream, true);
+}
+
+int br_shuffle_naive_segmented(void *data, int eb, int64_t num_arrays, uint64_t n, uint64_t run_seed, int64_t base,
+                               int generator, uint32_t *words_dev, void *stream) {
+    std::vector<br_segment> segs;
+    naive_segments(n, segs);
+    return shuffle_common(data, eb, num_arrays, n, segs, true, run_seed, base, words_dev, nullptr, nullptr, nullptr,
+                          generator, stream, true);
 }
 
 void br_release(void) {

@@ -48,16 +48,34 @@ struct RollArgs {
     uint8_t *__restrict__ flags;
     uint64_t *__restrict__ rk;
     RollWs *ws;
+    int naive;  // digits by division of one draw on the product (batched.py:126-128)
 };
+
+// roll_batch_naive (batched.py:126-128): value v = hi(P*w) of one Lemire draw on the
+// product P, decoded by divisions (mixed_radix.py:53-67), least significant digit first.
+// Accepts exactly when the batched form does (Theorem 1: r_k == P*w mod 2^64), so only the
+// digit extraction differs -- the k-1 divisions are what the baseline measures.
+template <int K>
+__device__ __forceinline__ void naive_digits(const uint32_t (&b)[K], uint64_t v, uint32_t (&d)[K]) {
+#pragma unroll
+    for (int m = K - 1; m > 0; --m) {
+        const uint64_t q = v / b[m];
+        d[m] = (uint32_t)(v - q * b[m]);
+        v = q;
+    }
+    d[0] = (uint32_t)v;
+}
 
 // Evaluate one batch on word w (batched.py:102-123).  Returns 0 accept, 1 reject,
 // 2 invalid bases (err set).  d[] receives the digits, r the final remainder.
 template <int K>
 __device__ __forceinline__ int eval_batch(const uint32_t (&b)[K], uint64_t w, uint32_t (&d)[K],
-                                          uint64_t &r, uint8_t &tc, int &err) {
+                                          uint64_t &r, uint8_t &tc, int &err, bool naive = false) {
     r = w;
+    if (!naive || K == 1) {
 #pragma unroll
-    for (int m = 0; m < K; ++m) d[m] = die(b[m], r);
+        for (int m = 0; m < K; ++m) d[m] = die(b[m], r);
+    }
     uint64_t prod;
     bool full = false;
     if constexpr (K == 1) {
@@ -83,6 +101,10 @@ __device__ __forceinline__ int eval_batch(const uint32_t (&b)[K], uint64_t w, ui
         }
         full = (hi == 1);
         prod = lo;
+    }
+    if (naive && K > 1) {  // one draw on the product, digits by division (bases are non-zero here)
+        naive_digits<K>(b, full ? w : mulhi64(prod, w), d);
+        r = full ? 0 : prod * w;
     }
     if (full) { tc = 1; return 0; }  // product 2^64: threshold 0, always accepted
     if (r >= prod) { tc = 0; return 0; }
@@ -172,7 +194,7 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
                 uint32_t d[K];
                 uint64_t r;
                 uint8_t tc = 0;
-                int st = eval_batch<K>(cur[u], w, d, r, tc, err);
+                int st = eval_batch<K>(cur[u], w, d, r, tc, err, a.naive != 0);
                 store_rolls<K>(a.rolls + b * K, d);
                 a.words[b] = 1;
                 if (a.flags) a.flags[b] = tc;
@@ -232,7 +254,7 @@ __device__ __forceinline__ void roll_range_cha(const RollArgs &a, u128 s0, int64
             load_bounds<K>(a.bounds + b * K, bb);
             uint64_t r;
             uint8_t tc = 0;
-            const int st = eval_batch<K>(bb, w, d, r, tc, err);
+            const int st = eval_batch<K>(bb, w, d, r, tc, err, a.naive != 0);
             store_rolls<K>(a.rolls + b * K, d);
             a.words[b] = 1;
             if (a.flags) a.flags[b] = tc;
@@ -337,7 +359,7 @@ __device__ __forceinline__ void st_vec(uint32_t *p, const Vec<LB> &r) {
 // (VB = LB/(4K) batches), U loads in flight, and rolls LB bytes / words VB bytes per store.
 // Lane l of sub-step u owns batches base + 32*VB*u + VB*l + v (v < VB); its words come
 // from VB consecutive PCG steps, the lane state then jumps 32*VB words.
-template <int K, bool FLAGS, bool RK>
+template <int K, bool FLAGS, bool RK, bool NAIVE = false>
 __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     static_assert(K == 1 || K == 2, "fast path is for k <= 2");
     constexpr int LB = ROLL_LB;
@@ -385,7 +407,15 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
                 for (int v = 0; v < VB; ++v) {
                     uint64_t r = gen_out(st, lh);
                     uint64_t prod;
-                    if constexpr (K == 2) {
+                    if constexpr (K == 2 && NAIVE) {  // roll_batch_naive: one division by b1
+                        const uint32_t b1 = cur[u].v[2 * v + 1];
+                        prod = (uint64_t)cur[u].v[2 * v] * b1;
+                        const uint64_t val = mulhi64(prod, r);
+                        r = prod * r;
+                        const uint64_t q = b1 ? val / b1 : 0;
+                        dd.v[2 * v] = (uint32_t)q;
+                        dd.v[2 * v + 1] = (uint32_t)(val - q * b1);
+                    } else if constexpr (K == 2) {
                         dd.v[2 * v] = die(cur[u].v[2 * v], r);
                         dd.v[2 * v + 1] = die(cur[u].v[2 * v + 1], r);
                         prod = (uint64_t)cur[u].v[2 * v] * cur[u].v[2 * v + 1];
@@ -476,7 +506,7 @@ __device__ __forceinline__ void roll_fixup_body(const RollArgs &a, uint64_t *win
                     uint8_t tc;
                     int err = 0;
                     const uint64_t w = CHA ? cha_out_cached(ck, cc, st) : gen_out(st, lh);
-                    int res = eval_batch<K>(bb, w, d, r, tc, err);
+                    int res = eval_batch<K>(bb, w, d, r, tc, err, a.naive != 0);
                     if (res != 1) {
                         store_rolls<K>(a.rolls + cur * K, d);
                         a.words[cur] = (uint8_t)(1 + extra > 255 ? 255 : 1 + extra);

@@ -34,10 +34,25 @@ static constexpr int MAX_SEGS = 40;
 struct DevPlan {
     uint32_t n, nbatches, nseg, max_k;
     uint32_t lo;              // lowest position that has a step (0 or 1 for full plans)
-    uint32_t pad;
+    uint32_t naive;           // pairs split by division (shuffle_naive_batched), see naive_pair
     const DevSeg *segs;       // [nseg]     (device)
     const uint64_t *thresh;   // [nbatches] (device)
 };
+
+// shuffle.py:242-253 (shuffle_naive_batched): the pair (i, i-1), i = nb - 1, takes ONE
+// Lemire draw v = hi(b*w) on b = (i+1)*i and splits it by division, (j1, j2) = divmod(v, i).
+// The acceptance (lo = b*w mod 2^64 >= 2^64 mod b) is the batched one (Theorem 1:
+// r_2 == b*w mod 2^64), so the naive shuffle is the PAIR plan with division digits; the
+// 64-by-32-bit division per pair is the cost this baseline exists to measure.
+__device__ __forceinline__ void naive_pair(uint32_t nb, uint64_t &r, uint32_t &j1, uint32_t &j2) {
+    const uint64_t i = nb - 1;
+    const uint64_t b = (uint64_t)nb * i;
+    const uint64_t v = __umul64hi(b, r);
+    r = b * r;
+    const uint64_t q = v / i;
+    j1 = (uint32_t)q;
+    j2 = (uint32_t)(v - q * i);
+}
 
 template <typename T>
 __device__ __forceinline__ void swap_sm(T *p, uint32_t i, uint32_t j) {
@@ -54,7 +69,7 @@ __device__ __forceinline__ void swap_sm(T *p, uint32_t i, uint32_t j) {
 template <int K, typename T, bool CHA>
 __device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count, const uint64_t *thresh, u128 &s,
                                               u128 inc, uint32_t &words, bool lh, const ChaKey &ck,
-                                              ChaCursor &cur) {
+                                              ChaCursor &cur, bool naive) {
     for (uint32_t c = 0; c < count; ++c, nb -= K) {
         const uint64_t t = __ldg(thresh + c);
         uint32_t d[K];
@@ -67,8 +82,12 @@ __device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count,
                 r = gen_next(s, inc, lh);
             }
             ++words;
+            if (K == 2 && naive) {
+                naive_pair(nb, r, d[0], d[K - 1]);
+            } else {
 #pragma unroll
-            for (int m = 0; m < K; ++m) d[m] = die(nb - m, r);
+                for (int m = 0; m < K; ++m) d[m] = die(nb - m, r);
+            }
         } while (r < t);  // reject: re-draw the whole batch (shuffle.py:121-128)
 #pragma unroll
         for (int m = 0; m < K; ++m) swap_sm(z, nb - 1 - m, d[m]);
@@ -78,16 +97,16 @@ __device__ __forceinline__ void small_segment(T *z, uint32_t nb, uint32_t count,
 template <typename T, bool CHA>
 __device__ __forceinline__ void small_segment_any(T *z, uint32_t k, uint32_t nb, uint32_t count,
                                                   const uint64_t *thresh, u128 &s, u128 inc, uint32_t &words,
-                                                  bool lh, const ChaKey &ck, ChaCursor &cur) {
+                                                  bool lh, const ChaKey &ck, ChaCursor &cur, bool naive) {
     switch (k) {
-        case 1: small_segment<1, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
-        case 2: small_segment<2, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
-        case 3: small_segment<3, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
-        case 4: small_segment<4, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
-        case 5: small_segment<5, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
-        case 6: small_segment<6, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
-        case 7: small_segment<7, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
-        default: small_segment<8, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur); break;
+        case 1: small_segment<1, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 2: small_segment<2, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 3: small_segment<3, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 4: small_segment<4, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 5: small_segment<5, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 6: small_segment<6, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 7: small_segment<7, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        default: small_segment<8, T, CHA>(z, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
     }
 }
 
@@ -194,7 +213,7 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
         for (uint32_t sg = 0; sg < plan.nseg; ++sg) {
             const DevSeg S = segs[sg];
             small_segment_any<T, CHA>(z, S.k, S.start_n, S.count, plan.thresh + S.first_batch, s, inc, words, lh,
-                                      ck, cur);
+                                      ck, cur, plan.naive != 0);
         }
         if (words_out) words_out[a0 + tid] = words;
     }
@@ -287,7 +306,14 @@ __device__ __forceinline__ void gen_step(GenState &g, const DevPlan &plan, const
         const uint64_t t = __ldg(plan.thresh + b);
         uint64_t r = CHA ? rc : gen_out(g.s, lh);
         const uint32_t pos = nbb - 1;
-        for (uint32_t m = 0; m < S.k; ++m) sink(pos - m, die(nbb - m, r));
+        if (plan.naive && S.k == 2) {
+            uint32_t j1, j2;
+            naive_pair(nbb, r, j1, j2);
+            sink(pos, j1);
+            sink(pos - 1, j2);
+        } else {
+            for (uint32_t m = 0; m < S.k; ++m) sink(pos - m, die(nbb - m, r));
+        }
         low = nbb - S.k;
         fail = r < t;
         if (rk_first && b == 0 && g.D == 0) *rk_first = r;
@@ -634,7 +660,14 @@ __device__ __forceinline__ void large_gen_step(CtaGen<W> &g, const DevPlan &plan
         const uint64_t t = __ldg(plan.thresh + b);
         uint64_t r = CHA ? rc : gen_out(g.s, lh);
         const uint32_t pos = nbb - 1;
-        for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (RS - 1)] = (RT)die(nbb - m, r);
+        if (plan.naive && S.k == 2) {
+            uint32_t j1, j2;
+            naive_pair(nbb, r, j1, j2);
+            sh.ring[pos & (RS - 1)] = (RT)j1;
+            sh.ring[(pos - 1) & (RS - 1)] = (RT)j2;
+        } else {
+            for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (RS - 1)] = (RT)die(nbb - m, r);
+        }
         low = nbb - S.k;
         fail = r < t;
         if (rk_first && b == 0 && g.D == 0) *rk_first = r;

@@ -291,6 +291,27 @@ def main():
                     "pos_after": src._pos})
     out["roll_batch_chacha"] = crb
 
+    # division-based baselines (shuffle.py:228-266, batched.py:126-128)
+    nsh = []
+    for gen in ("pcg64", "lehmer", "chacha"):
+        for n in (0, 1, 2, 3, 4, 5, 64, 100, 101, 1000, 4096, 10000, 70001):
+            seed = rng.getrandbits(64)
+            src = CountingSource(R.make_source(gen, seed))
+            z = R.shuffle_naive_batched(src, list(range(n)))
+            rec = {"gen": gen, "n": n, "seed": seed, "words": src.count, "sha": sha_u32(z)}
+            if n <= 100:
+                rec["perm"] = z
+            nsh.append(rec)
+    out["shuffle_naive_batched"] = nsh
+    nrb = []
+    for seed, bases in ((51, (6, 5)), (52, (2**32 - 1, 2**31 + 11)), (53, (1 << 16, 3, 5)), (54, (10,)),
+                        (55, (65535, 65521, 4099, 17))):
+        src = CountingSource(R.make_source("pcg64", seed))
+        rb = R.RadixBases.of(bases, 64)
+        res = [list(R.roll_batch_naive(src, rb)) for _ in range(40)]
+        nrb.append({"seed": seed, "bases": list(bases), "digits": res, "words": src.count})
+    out["roll_batch_naive"] = nrb
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)

@@ -568,6 +568,61 @@ def test_chacha_rolls(B, O, golden):
             assert int(words.sum()) > nb  # the forced rejections happened
 
 
+# ------------------------------------------------------------------ division-based baselines (8(f) row 3)
+def test_naive_shuffle_dropin_golden(B, O, golden):
+    for rec in golden["shuffle_naive_batched"]:
+        s = B.make_source(rec["gen"], rec["seed"])
+        z = B.shuffle_naive_batched(s, list(range(rec["n"])))
+        assert sha_u32(z) == rec["sha"], (rec["gen"], rec["n"], B.last_kernel())
+        o = O.GENERATOR_MAKERS[rec["gen"]](rec["seed"])
+        O.words(o, rec["words"])
+        if rec["gen"] == "chacha":
+            assert B.batchrand._chacha_position(s) == O.chacha_position(o)
+        else:
+            assert s.state == o.state
+    with pytest.raises(B.BoundOverflow):
+        class Narrow:
+            word_bits = 8
+        B.shuffle_naive_batched(Narrow(), list(range(17)))
+
+
+@pytest.mark.parametrize("gen", ["pcg64", "chacha"])
+@pytest.mark.parametrize("n,eb", [(64, 4), (101, 8), (4096, 4), (20001, 8), (70000, 4)])
+def test_naive_shuffle_segmented(B, O, gen, n, eb):
+    na = max(2, min(300, (1 << 20) // n))
+    dt = np.uint32 if eb == 4 else np.uint64
+    payload = np.arange(n * na, dtype=dt)
+    dev = torch.from_numpy(payload.view(np.int32 if eb == 4 else np.int64).copy()).cuda()
+    _, w = B.shuffle_many(dev, n, 2024, array_index_base=5, return_words=True, generator=gen, naive=True)
+    ref = payload.copy()
+    rw = O.shuffle_naive_segmented(ref, n, 2024, array_index_base=5, generator=gen)
+    assert np.array_equal(dev.cpu().numpy().view(dt), ref), B.last_kernel()
+    assert np.array_equal(u32(w), rw)
+
+
+def test_naive_rolls(B, O, golden):
+    for rec in golden["roll_batch_naive"]:
+        s = B.Pcg64Source(rec["seed"])
+        rb = B.RadixBases.of(tuple(rec["bases"]))
+        assert [list(B.roll_batch_naive(s, rb)) for _ in range(len(rec["digits"]))] == rec["digits"]
+        o = O.pcg64(rec["seed"])
+        O.words(o, rec["words"])
+        assert s.state == o.state
+    for k, nb in ((2, 300000), (3, 50001), (5, 20000)):
+        bounds = O.gen_bounds(9, k * nb) if k < 5 else O.gen_bounds(9, k * nb, 2, 4000)
+        if k == 2:
+            bounds[:1000:2] = 0xFFFFFFFF
+            bounds[1:1000:2] = 3006477107
+        src = O.pcg64(6)
+        rolls, words, flags, rk = O.roll_batches(src, bounds, k)
+        ds = B.DeviceStream(6)
+        r = B.roll_batches(ds, dev_u32(bounds), k, flags=True, final_remainder=True, naive=True)
+        st = ds.host_state()
+        assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words), k
+        assert np.array_equal(r.flags.cpu().numpy(), flags) and np.array_equal(u64(r.final_remainder), rk)
+        assert (st.state_hi << 64 | st.state_lo) == src.state
+
+
 def test_cli_bench_and_shuffle(B, O, tmp_path):
     import io
     import contextlib
