@@ -272,10 +272,32 @@ int grid_for(const DeviceInfo &di, const void *kernel, int threads, size_t smem,
     return (int)(g < 1 ? 1 : g);
 }
 
+// Generator of each state buffer as last uploaded by br_state_upload: picks the main roll
+// kernel.  Only a hint -- the kernels check the tag and fall back (see roll.cuh mark_main).
+std::mutex g_kind_mu;
+std::map<const void *, bool> g_is_chacha;
+
+void note_state_kind(const void *dev, bool chacha) {
+    std::lock_guard<std::mutex> lk(g_kind_mu);
+    g_is_chacha[dev] = chacha;
+}
+
+bool state_is_chacha(const void *dev) {
+    std::lock_guard<std::mutex> lk(g_kind_mu);
+    auto it = g_is_chacha.find(dev);
+    return it != g_is_chacha.end() && it->second;
+}
+
 template <int K>
 int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int phase) {
     const int threads = 256;
-    if (phase & 1) {
+    const bool cha = (phase & 1) && state_is_chacha(a.state);
+    if (cha) {
+        const int64_t warps = (a.nb + 255) / 256;  // a 256-word keystream window per warp
+        int grid = grid_for(di, (const void *)roll_cha_kernel<K>, threads, 0, (warps + 7) / 8);
+        roll_cha_kernel<K><<<grid, threads, 0, st>>>(a);
+        CK(cudaGetLastError());
+    } else if (phase & 1) {
         int64_t work_blocks = (a.nb + 8 * 512 - 1) / (8 * 512);
         if constexpr (K <= 2) {
             const void *kp = a.flags ? (a.rk ? (const void *)roll_fast_kernel<K, true, true>
@@ -322,7 +344,8 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
         }
         if (e != cudaSuccess) return fail(BR_E_CUDA, std::string("fixup launch: ") + cudaGetErrorString(e));
     }
-    g_kernel = std::string(K <= 2 ? "roll_fast_kernel<" : "roll_main_kernel<") + std::to_string(K) + ">+roll_fixup_kernel";
+    g_kernel = std::string(cha ? "roll_cha_kernel<" : K <= 2 ? "roll_fast_kernel<" : "roll_main_kernel<") +
+               std::to_string(K) + ">+roll_fixup_kernel";
     return BR_OK;
 }
 
@@ -605,6 +628,7 @@ int br_state_upload(br_pcg64 *state_dev, const br_pcg64 *st, void *stream) {
     if (!state_dev || !st) return fail(BR_E_INVALID, "null state");
     const size_t bytes = host_is_chacha(st) ? sizeof(br_chacha) : sizeof(br_pcg64);
     CK(cudaMemcpyAsync(state_dev, st, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    note_state_kind(state_dev, host_is_chacha(st));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     return BR_OK;
 }

@@ -29,7 +29,8 @@ struct RollWs {
     unsigned int error;            // deferred status (BR_E_INVALID / BR_E_BOUND_OVERFLOW)
     unsigned int bar_count;
     unsigned int bar_gen;
-    unsigned int pad[3];
+    unsigned int main_done;  // 1: this call's main kernel rolled the stream (else the fixup does)
+    unsigned int pad[2];
     unsigned long long final_hi, final_lo;  // state after nb words (no-rejection case), by the main kernel
 };
 
@@ -280,10 +281,35 @@ __device__ __forceinline__ void roll_cha_main(const RollArgs &a, uint64_t *win) 
 
 __device__ __forceinline__ bool roll_is_chacha(const RollArgs &a) { return a.state[3] == CHACHA_TAG; }
 
+// Which main kernel runs is the host's guess (the generator of a state buffer is known where
+// it was uploaded); the device has the final word: a main kernel that does not match the
+// stream's tag exits and records main_done = 0, and the fixup kernel then rolls the stream
+// itself.  One writer (block 0, thread 0), read by the fixup after griddepcontrol.wait.
+__device__ __forceinline__ void mark_main(const RollArgs &a, unsigned done) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ws->main_done = done;
+}
+
+// ChaCha main pass at full occupancy (launched when the host knows the stream is ChaCha)
+template <int K>
+__global__ void __launch_bounds__(256) roll_cha_kernel(RollArgs a) {
+    __shared__ __align__(16) uint64_t win[8][256];
+    pdl_launch_dependents();
+    if (!roll_is_chacha(a)) {
+        mark_main(a, 0);
+        return;
+    }
+    mark_main(a, 1);
+    roll_cha_main<K>(a, win[(threadIdx.x >> 5) & 7]);
+}
+
 template <int K>
 __global__ void __launch_bounds__(256) roll_main_kernel(RollArgs a) {
     pdl_launch_dependents();
-    if (roll_is_chacha(a)) return;  // the fixup kernel rolls ChaCha streams
+    if (roll_is_chacha(a)) {  // the fixup kernel rolls ChaCha streams met here
+        mark_main(a, 0);
+        return;
+    }
+    mark_main(a, 1);
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
     publish_final(a, s0, inc);
@@ -368,7 +394,11 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     constexpr int U = ROLL_U;
     constexpr int64_t CH = 32 * VB * U;
     pdl_launch_dependents();
-    if (roll_is_chacha(a)) return;  // the fixup kernel rolls ChaCha streams
+    if (roll_is_chacha(a)) {  // the fixup kernel rolls ChaCha streams met here
+        mark_main(a, 0);
+        return;
+    }
+    mark_main(a, 1);
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
     const bool lh = is_lehmer(inc);
@@ -546,12 +576,21 @@ template <int K>
 __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
     pdl_wait();
     __shared__ __align__(16) uint64_t win[8][256];
+    const bool done = ((volatile RollWs *)a.ws)->main_done != 0;
     if (roll_is_chacha(a)) {
         uint64_t *w = win[(threadIdx.x >> 5) & 7];
-        roll_cha_main<K>(a, w);
-        grid_barrier(a.ws);
+        if (!done) {
+            roll_cha_main<K>(a, w);
+            grid_barrier(a.ws);
+        }
         roll_fixup_body<K, true>(a, w);
     } else {
+        if (!done) {  // the main kernel was the ChaCha one: roll the PCG64/Lehmer stream here
+            const u128 s0 = mk128(a.state[0], a.state[1]), inc = mk128(a.state[2], a.state[3]);
+            publish_final(a, s0, inc);
+            roll_range<K, 1>(a, s0, inc, 0, a.nb, 0, false);
+            grid_barrier(a.ws);
+        }
         roll_fixup_body<K, false>(a, nullptr);
     }
 }

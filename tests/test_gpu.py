@@ -568,6 +568,35 @@ def test_chacha_rolls(B, O, golden):
             assert int(words.sum()) > nb  # the forced rejections happened
 
 
+def test_roll_kernel_choice_is_only_a_hint(B, O):
+    """The host picks the main roll kernel from the kind recorded at br_state_upload; a state
+    written behind its back (stale or unknown kind) is still rolled exactly by the fixup."""
+    nb, k = 70001, 2
+    bounds = O.gen_bounds(12, k * nb)
+    db = dev_u32(bounds)
+    for first, second in (("chacha", "pcg64"), ("pcg64", "chacha"), ("lehmer", "chacha")):
+        ds = B.DeviceStream(3, generator=first)  # kind recorded for ds.state: `first`
+        other = B.DeviceStream(4, generator=second)
+        ds.state.copy_(other.state)  # now holds a `second` stream; the record still says `first`
+        src = O.GENERATOR_MAKERS[second](4)
+        rolls, words, _, _ = O.roll_batches(src, bounds, k)
+        r = B.roll_batches(ds, db, k)
+        st = ds.host_state()
+        assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words), (first, second)
+        pos = (st.state_hi << 64) | st.state_lo
+        assert pos == (O.chacha_position(src) if second == "chacha" else src.state)
+    # an unrecorded buffer (a clone) takes the default guess and the same fallback
+    ds = B.DeviceStream(8, generator="chacha")
+    ds.state = ds.state.clone()
+    src = O.chacha(8)
+    rolls, words, _, _ = O.roll_batches(src, bounds, k)
+    r = B.roll_batches(ds, db, k)
+    assert np.array_equal(u32(r.rolls), rolls)
+    ds = B.DeviceStream(8, generator="chacha")
+    B.roll_batches(ds, db, k)
+    assert "roll_cha_kernel" in B.last_kernel()
+
+
 # ------------------------------------------------------------------ division-based baselines (8(f) row 3)
 def test_naive_shuffle_dropin_golden(B, O, golden):
     for rec in golden["shuffle_naive_batched"]:
