@@ -312,6 +312,28 @@ def main():
         nrb.append({"seed": seed, "bases": list(bases), "digits": res, "words": src.count})
     out["roll_batch_naive"] = nrb
 
+    # cost model (cost_model.py): crossovers and schedules for a spread of
+    # cost parameters, including GPU-like ones (expensive generator words / divisions)
+    cm = []
+    for rng_cost, div_cost, bits in ((2.0, 16.0, 64), (2.0, 16.0, 32), (1.0, 16.0, 64), (6.0, 20.0, 64),
+                                     (3.0, 25.0, 64), (30.0, 20.0, 64), (60.0, 40.0, 64), (0.5, 4.0, 64),
+                                     (10.0, 10.0, 32), (2.5, 70.0, 64)):
+        params = R.CostParams(rng_cost=rng_cost, div_cost=div_cost, word_bits=bits)
+        rec = {"rng_cost": rng_cost, "div_cost": div_cost, "bits": bits, "nk": {}}
+        for k in range(2, 9 if bits == 64 else 5):
+            try:
+                rec["nk"][str(k)] = R.find_nk(k, params)
+            except R.NoCrossover:
+                rec["nk"][str(k)] = None
+        try:
+            rec["schedule6"] = [list(e) for e in R.build_schedule(params, 6 if bits == 64 else 4).entries]
+        except (R.NoCrossover, ValueError) as e:
+            rec["schedule6"] = type(e).__name__
+        pts = ((1000, 2), (26573, 4), (815, 6), (146, 8), (70000, 3)) if bits == 64 else ((1000, 2), (500, 3), (100, 4))
+        rec["costs"] = [[n, k, R.cost_per_roll(n, k, params)] for n, k in pts]
+        cm.append(rec)
+    out["cost_model"] = cm
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)

@@ -23,6 +23,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2408_06213_b200 as B  # noqa: E402
 from paper_2408_06213_b200 import _native as N  # noqa: E402
+from paper_2408_06213_b200 import cost_model  # noqa: E402
 
 
 def timed(fn, steps, warmup=3):
@@ -69,7 +70,8 @@ def main():
         steps = max(2, args.steps // (4 if key == "c5" else 1))
         for gen in ("pcg64", "lehmer", "chacha"):
             for alg, kw in (("shuffle_6", {}), ("shuffle_2", {"schedule": B.PAIR_SCHEDULE}),
-                            ("naive_shuffle_2", {"naive": True})):
+                            ("naive_shuffle_2", {"naive": True}),
+                            ("shuffle_6_gpu_cost_model", {"schedule": cost_model.gpu_schedule(gen)})):
                 ms = timed(lambda: B.shuffle_many(data, n, cfg["seed"], generator=gen, **kw), steps, warmup=2)
                 print(json.dumps({"workload": cfg["workload"], "generator": gen, "algorithm": alg, "ms": ms,
                                   "elements_per_s": n * na / (ms / 1e3), "kernel": B.last_kernel()}), flush=True)
