@@ -6,6 +6,7 @@
 
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -357,6 +358,27 @@ constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 #ifndef CTA_W
 #define CTA_W 4
 #endif
+#ifndef RES_W
+#define RES_W 8
+#endif
+
+// BR_SHUFFLE_KERNEL=small|resolve|hash|mid|large|global restricts the dispatch below to one
+// shuffle kernel where it is eligible (tests cover every kernel; A/B timing).  Unset: the
+// first eligible kernel in the order below.
+enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_LARGE, K_GLOBAL };
+int forced_kernel() {
+    const char *e = getenv("BR_SHUFFLE_KERNEL");
+    if (!e || !*e) return K_ANY;
+    static const char *names[] = {"", "small", "resolve", "hash", "mid", "large", "global"};
+    for (int i = 1; i <= K_GLOBAL; ++i)
+        if (!strcmp(e, names[i])) return i;
+    return K_ANY;
+}
+
+inline bool allow(int k) {
+    const int f = forced_kernel();
+    return f == K_ANY || f == k;
+}
 
 template <typename T>
 int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan &cp, bool segmented,
@@ -365,7 +387,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     const uint32_t stride = (uint32_t)(n | 1u);
     const int tpb = 64;  // 2 warps: many small blocks per SM overlap their load/compute/store phases
     const size_t small_smem = (size_t)tpb * stride * sizeof(T);
-    if (segmented && cp.plan.max_k <= 8 && small_smem <= SMALL_SMEM_MAX / 2) {
+    if (allow(K_SMALL) && segmented && cp.plan.max_k <= 8 && small_smem <= SMALL_SMEM_MAX / 2) {
         auto kern = gen == 2 ? shuffle_small_kernel<T, true> : shuffle_small_kernel<T, false>;
         CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
         int64_t blocks = (num_arrays + tpb - 1) / tpb;
@@ -378,11 +400,28 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         g_kernel = std::string("shuffle_small_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
     }
+    if (forced_kernel() == K_RESOLVE && n <= 65535 && resolve_smem_bytes<T>((uint32_t)n) <= MID_SMEM_MAX) {
+        constexpr int W = RES_W;
+        const size_t rsmem = resolve_smem_bytes<T>((uint32_t)n);
+        auto kern = !segmented ? shuffle_resolve_kernel<T, W, 2>
+                               : (gen == 2 ? shuffle_resolve_kernel<T, W, 1> : shuffle_resolve_kernel<T, W, 0>);
+        const void *kp = (const void *)kern;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+        int grid = segmented ? grid_for(di, kp, 32 * W, rsmem, num_arrays) : 1;
+        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+        kern<<<grid, 32 * W, rsmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
+                                          rk_first, use_tma, segmented ? 1 : 0, gen);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_resolve_kernel<u") + std::to_string(8 * sizeof(T)) + "," + std::to_string(W) +
+                   ">";
+        return BR_OK;
+    }
     const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);
     const uint32_t hbytes = (uint32_t)((n + 15) & ~(uint64_t)15);  // lane-id table indexed by target
     const size_t smem = (size_t)zbytes + hbytes;
     const size_t csmem = (size_t)zbytes;  // payload only; the rest is static
-    if (n < 65536 && csmem <= MID_SMEM_MAX && (uint64_t)cp.plan.max_k * 32 * CTA_W + 32 * CTA_W <= CRING) {
+    if (allow(K_HASH) && n < 65536 && csmem <= MID_SMEM_MAX &&
+        (uint64_t)cp.plan.max_k * 32 * CTA_W + 32 * CTA_W <= CRING) {
         constexpr int W = CTA_W;
         auto kern = !segmented ? shuffle_cta_hash_kernel<T, W, 2>
                                : (gen == 2 ? shuffle_cta_hash_kernel<T, W, 1> : shuffle_cta_hash_kernel<T, W, 0>);
@@ -397,7 +436,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
                    std::to_string(W) + ">";
         return BR_OK;
     }
-    if (n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 30) {
+    if (allow(K_MID) && n <= 65536 && smem <= MID_SMEM_MAX && cp.plan.max_k <= 30) {
         auto kern = !segmented ? shuffle_mid_kernel<T, false, 2>
                                : (gen == 2 ? shuffle_mid_kernel<T, true, 1> : shuffle_mid_kernel<T, true, 0>);
         const void *kp = (const void *)kern;
@@ -411,7 +450,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         return BR_OK;
     }
     // large arrays: one CTA per array, targets generated in-CTA, array in global memory
-    if ((uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= LRING) {
+    if (allow(K_LARGE) && (uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= LRING) {
         constexpr int W = LARGE_W;
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
         auto kern = !segmented ? shuffle_cta_large_kernel<T, W, 2>

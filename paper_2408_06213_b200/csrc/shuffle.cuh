@@ -908,6 +908,216 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
 }
 
 // -------------------------------------------------------------------------------------
+// one CTA per shared-memory-resident array, whole-array resolution (no group chain)
+// -------------------------------------------------------------------------------------
+// The sequential Fisher-Yates z[i] <-> z[J[i]] (i = n-1 .. lim) has a closed form.  Let
+//   ns(i) = min{m > i : J[m] = J[i]}   (the next step, in index order, with i's target)
+//   ft(x) = min{m > x : J[m] = x}      (the last step before x's own that targeted x)
+//   F(x)  = x if ft(x) is undefined, else F(ft(x))
+// Then the final value at position i >= lim is z0[F(ns(i))] if ns(i) exists, else z0[J[i]];
+// below lim it is z0[F(i)].  (Position J[i] < i is only ever written by steps m with
+// J[m] = J[i]; the most recent one before step i is ns(i), and the value it deposited is the
+// one position ns(i) held just before its own step -- which is z0[F(ns(i))] by the same
+// argument on ft.)  Checked against the sequential loop exhaustively in tests (oracle) and
+// bit-exactly on the device.
+//
+// So one array costs: all targets (lane-parallel generation, G batches per step), one
+// atomicExch per step to thread per-target lists, a list walk per position for ns and ft,
+// pointer jumping on F, and one gather z0[r] per position written straight to global
+// memory -- about ten barriers per array instead of five per 32*W steps.  Measured on B200
+// it is slower than the hashed group kernel for C4 (3.25 vs 2.52 ms: the divergent list
+// walks and the jumping rounds cost more instructions than the barriers they save), so the
+// dispatcher only uses it when asked (BR_SHUFFLE_KERNEL=resolve); it stays as an
+// independently derived, fully tested second algorithm.
+static constexpr uint16_t RES_NONE = 0xFFFF;
+
+template <bool CHA, int W>
+__device__ __forceinline__ void gen_all_targets(CtaGen<W> &g, const DevPlan &plan, const DevSeg *segs,
+                                                uint16_t *J, uint32_t *fmin, int L, uint64_t *rk_first,
+                                                uint64_t *chawin, const ChaKey &ck) {
+    constexpr int G = 32 * W;
+    const bool lh = is_lehmer(g.inc);
+    const uint32_t nb = plan.nbatches;
+    while (g.B0 < nb) {
+        const uint32_t b = g.B0 + L;
+        bool fail = false;
+        uint64_t rc = 0;
+        if constexpr (CHA) rc = cha_cta_word<G>(chawin, ck, g.W0, cha_prev(g.s), L);  // CTA-collective
+        if (b < nb) {
+            uint32_t sg = g.seg;
+            while (sg + 1 < plan.nseg && segs[sg + 1].first_batch <= b) ++sg;
+            const DevSeg S = segs[sg];
+            const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
+            const uint64_t t = __ldg(plan.thresh + b);
+            uint64_t r = CHA ? rc : gen_out(g.s, lh);
+            const uint32_t pos = nbb - 1;
+            if (plan.naive && S.k == 2) {
+                uint32_t j1, j2;
+                naive_pair(nbb, r, j1, j2);
+                J[pos] = (uint16_t)j1;
+                J[pos - 1] = (uint16_t)j2;
+            } else {
+                for (uint32_t m = 0; m < S.k; ++m) J[pos - m] = (uint16_t)die(nbb - m, r);
+            }
+            fail = r < t;
+            if (rk_first && b == 0 && g.D == 0) *rk_first = r;
+        }
+        // a rejected batch is re-drawn from the next word by the lane that lands on it in the
+        // next step; it rewrites the same positions (barrier-separated)
+        if (!__syncthreads_or(fail)) {
+            g.B0 += G;
+            if constexpr (CHA) g.s = cha_add(g.s, G);
+            else g.s = mad128(g.s, g.AJ, g.CJ);
+        } else {
+            if (L == 0) *fmin = G;
+            __syncthreads();
+            if (fail) atomicMin(fmin, (uint32_t)L);
+            __syncthreads();
+            const uint32_t f = *fmin;
+            g.B0 += f;
+            g.D += 1;
+            if constexpr (CHA) g.s = cha_add(g.s, (uint64_t)f + 1);
+            else g.s = gen_jump_small(g.s, g.inc, (int)f + 1, lh);
+            __syncthreads();
+        }
+        while (g.seg + 1 < plan.nseg && segs[g.seg + 1].first_batch <= g.B0) ++g.seg;
+    }
+}
+
+// dynamic shared memory of the resolve kernel for n elements of T
+template <typename T>
+__host__ __device__ __forceinline__ uint32_t resolve_smem_bytes(uint32_t n) {
+    const uint32_t zb = (n * (uint32_t)sizeof(T) + 15) & ~15u;
+    const uint32_t h16 = (n * 2 + 15) & ~15u;
+    const uint32_t h32 = (n * 4 + 15) & ~15u;
+    return zb + 4 * h16 + h32;  // z0 | J | link | ns | p | head
+}
+
+template <typename T, int W, bool CHA>
+__device__ __forceinline__ void shuffle_resolve_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
+                                                     uint64_t run_seed, int64_t base,
+                                                     uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                     uint64_t *words64, uint64_t *rk_first, int use_tma,
+                                                     int segmented, int gen, unsigned char *smem_raw, DevSeg *segs,
+                                                     uint32_t *fmin, uint64_t &bar, uint64_t *chawin) {
+    constexpr int G = 32 * W;
+    const int L = threadIdx.x;
+    const uint32_t n = plan.n;
+    const uint32_t zb = (n * (uint32_t)sizeof(T) + 15) & ~15u, h16 = (n * 2 + 15) & ~15u;
+    T *z0 = reinterpret_cast<T *>(smem_raw);
+    uint16_t *J = reinterpret_cast<uint16_t *>(smem_raw + zb);
+    uint16_t *link = reinterpret_cast<uint16_t *>(smem_raw + zb + h16);
+    uint16_t *ns = reinterpret_cast<uint16_t *>(smem_raw + zb + 2 * h16);
+    uint16_t *pp = reinterpret_cast<uint16_t *>(smem_raw + zb + 3 * h16);
+    uint32_t *head = reinterpret_cast<uint32_t *>(smem_raw + zb + 4 * h16);
+    for (uint32_t q = L; q < plan.nseg; q += G) segs[q] = plan.segs[q];
+    if (use_tma && L == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    const uint32_t bytes = n * (uint32_t)sizeof(T);
+    const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
+    uint32_t parity = 0;
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        T *g = data + a * (int64_t)n;
+        if (use_tma) {
+            if (L == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bar, bytes);
+                bulk_load(z0, g, bytes, &bar);
+            }
+        } else {
+            for (uint32_t e = L; e < n; e += G) z0[e] = g[e];
+        }
+        for (uint32_t x = L; x < n; x += G) head[x] = 0;
+        u128 s0, inc;
+        bool lh;
+        ChaKey ck;
+        CtaGen<W> gs;
+        cta_gen_setup<CHA, W>(gs, s0, inc, lh, ck, segmented, gen, run_seed, base + a, state_io, n, L);
+        uint64_t *rkf = segmented ? nullptr : rk_first;
+        gen_all_targets<CHA, W>(gs, plan, segs, J, fmin, L, rkf, chawin, ck);
+        __syncthreads();
+        // per-target lists of steps: head[c] = 1 + a step with target c, link[i] = 1 + the
+        // step inserted before i into the same list (0 ends a list; n <= 65535)
+        for (uint32_t i = lim + L; i < n; i += G) link[i] = (uint16_t)atomicExch(&head[J[i]], i + 1);
+        __syncthreads();
+        for (uint32_t x = L; x < n; x += G) {
+            // ns(x) for a position with a step; ft(x) for every position (as F's parent)
+            uint32_t best = RES_NONE;
+            if (x >= lim) {
+                for (uint32_t m = head[J[x]]; m != 0; m = link[m - 1])
+                    if (m - 1 > x && m - 1 < best) best = m - 1;
+                ns[x] = (uint16_t)best;
+            }
+            best = RES_NONE;
+            for (uint32_t m = head[x]; m != 0; m = link[m - 1])
+                if (m - 1 > x && m - 1 < best) best = m - 1;
+            pp[x] = best == RES_NONE ? (uint16_t)x : (uint16_t)best;
+        }
+        // F by pointer jumping (in place: every value read is an ancestor, so races only
+        // shorten the chains); the rounds end when no pointer moves
+        for (;;) {
+            __syncthreads();
+            bool moved = false;
+            for (uint32_t x = L; x < n; x += G) {
+                const uint16_t q = pp[x], r = pp[q];
+                if (r != q) {
+                    pp[x] = r;
+                    moved = true;
+                }
+            }
+            if (!__syncthreads_or(moved)) break;
+        }
+        if (use_tma) {
+            mbar_wait(&bar, parity);
+            parity ^= 1u;
+        }
+        for (uint32_t i = L; i < n; i += G) {
+            uint32_t r;
+            if (i >= lim) {
+                const uint16_t m = ns[i];
+                r = m != RES_NONE ? pp[m] : J[i];
+            } else {
+                r = pp[i];
+            }
+            g[i] = z0[r];
+        }
+        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
+        if (L == 0) {
+            if (segmented) {
+                if (words32) words32[a] = (uint32_t)words;
+            } else {
+                const u128 sf = CHA ? cha_add(s0, words) : gen_jump(s0, inc, words, lh);
+                state_io[0] = sf.hi;
+                state_io[1] = sf.lo;
+                if (words64) words64[0] = words;
+            }
+        }
+        __syncthreads();  // z0 / lists are reused by the next array
+    }
+}
+
+template <typename T, int W, int CM>
+__global__ void __launch_bounds__(32 * W) shuffle_resolve_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                 DevPlan plan, uint64_t run_seed, int64_t base,
+                                                                 uint32_t *__restrict__ words32, uint64_t *state_io,
+                                                                 uint64_t *words64, uint64_t *rk_first, int use_tma,
+                                                                 int segmented, int gen) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ DevSeg segs[MAX_SEGS];
+    __shared__ uint32_t fmin;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
+    bool cha = CM == 1;
+    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if (CM != 0 && cha)
+        shuffle_resolve_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+                                            rk_first, use_tma, segmented, gen, smem_raw, segs, &fmin, bar, chawin);
+    else if (CM != 1)
+        shuffle_resolve_body<T, W, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+                                          rk_first, use_tma, segmented, gen, smem_raw, segs, &fmin, bar, chawin);
+}
+
+// -------------------------------------------------------------------------------------
 // arrays larger than shared memory: targets into a global buffer, then warp-group apply
 // on the array in global memory
 // -------------------------------------------------------------------------------------

@@ -222,6 +222,53 @@ def test_c4_sample(B, O, golden):
     assert np.array_equal(np.sort(got[::97], axis=1), np.tile(np.arange(n, dtype=np.uint32), (len(got[::97]), 1)))
 
 
+KERNEL_CASES = {  # forced kernel -> (name in last_kernel, lengths it can take)
+    "small": ("shuffle_small_kernel", (2, 5, 64, 100)),
+    "resolve": ("shuffle_resolve_kernel", (2, 3, 64, 100, 1000, 4096, 4097, 10000)),
+    "hash": ("shuffle_cta_hash_kernel", (2, 64, 1000, 4096, 10000, 20000)),
+    "mid": ("shuffle_mid_kernel", (2, 64, 1000, 4096, 10000)),
+    "large": ("shuffle_cta_large_kernel", (2, 64, 1000, 4096, 70000)),
+    "global": ("shuffle_large_gen_kernel", (2, 64, 1000, 4096, 70000)),
+}
+
+
+@pytest.mark.parametrize("kernel", sorted(KERNEL_CASES))
+@pytest.mark.parametrize("gen", ["pcg64", "chacha"])
+def test_every_shuffle_kernel(B, O, monkeypatch, kernel, gen):
+    """Each shuffle kernel (forced through BR_SHUFFLE_KERNEL) against the oracle, segmented and
+    stream form, u32 and u64, default and naive plans."""
+    monkeypatch.setenv("BR_SHUFFLE_KERNEL", kernel)
+    name, lengths = KERNEL_CASES[kernel]
+    for n in lengths:
+        for eb in (4, 8):
+            if kernel == "mid" and n * eb + n > 200 * 1024:
+                continue
+            na = max(2, min(64, (1 << 19) // n))
+            dt = np.uint32 if eb == 4 else np.uint64
+            payload = np.arange(n * na, dtype=dt)
+            for naive in (False, True):
+                dev = torch.from_numpy(payload.view(np.int32 if eb == 4 else np.int64).copy()).cuda()
+                _, w = B.shuffle_many(dev, n, 4321, array_index_base=17, return_words=True, generator=gen,
+                                      naive=naive)
+                kern = B.last_kernel()
+                ref = payload.copy()
+                if naive:
+                    rw = O.shuffle_naive_segmented(ref, n, 4321, array_index_base=17, generator=gen)
+                else:
+                    rw = O.shuffle_segmented(ref, n, 4321, array_index_base=17, generator=gen)
+                assert np.array_equal(dev.cpu().numpy().view(dt), ref), (kernel, n, eb, naive, kern)
+                assert np.array_equal(u32(w), rw)
+                if n > 2 and not (kernel == "small" and eb == 8 and n >= 64):
+                    assert name in kern, (kernel, n, eb, kern)
+        if kernel != "small":  # stream form (one array from a caller's source)
+            s = B.make_source(gen, 900 + n)
+            z = torch.arange(n, dtype=torch.int32, device="cuda")
+            B.shuffle_batched(s, z)
+            o = O.GENERATOR_MAKERS[gen](900 + n)
+            zr = O.shuffle_batched(o, np.arange(n, dtype=np.uint32))
+            assert np.array_equal(u32(z), zr), (kernel, n, B.last_kernel())
+
+
 @pytest.mark.parametrize("eb", [4, 8])
 @pytest.mark.parametrize("n", [2, 3, 5, 7, 8, 9, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 255, 256, 257, 511,
                                512, 513, 1000, 2047, 2048, 2049, 4095, 4097, 10000, 16384])
@@ -519,8 +566,8 @@ def test_chacha_segmented(B, O, n, eb):
 
 @pytest.mark.parametrize("n", [1000, 70000])
 def test_chacha_wide_schedule_paths(B, O, n):
-    """k = 16 in the tail regime moves n=1000 to the warp kernel and n=70000 to the
-    global-target fallback, in both the segmented and the stream form."""
+    """k = 16 in the tail regime: n=1000 runs in the warp kernel and n=70000 in
+    the global-target fallback, in both the segmented and the stream form."""
     entries = ((1 << 30, 2), (17, 16))
     sched = B.ShuffleSchedule(entries, 16)
     na = 6
