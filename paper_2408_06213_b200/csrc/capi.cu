@@ -361,15 +361,18 @@ constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 #ifndef RES_W
 #define RES_W 8
 #endif
+#ifndef PIPE_W
+#define PIPE_W 8
+#endif
 
-// BR_SHUFFLE_KERNEL=small|resolve|hash|mid|large|global restricts the dispatch below to one
+// BR_SHUFFLE_KERNEL=small|resolve|hash|mid|pipe|large|global restricts the dispatch below to one
 // shuffle kernel where it is eligible (tests cover every kernel; A/B timing).  Unset: the
 // first eligible kernel in the order below.
-enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_LARGE, K_GLOBAL };
+enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL };
 int forced_kernel() {
     const char *e = getenv("BR_SHUFFLE_KERNEL");
     if (!e || !*e) return K_ANY;
-    static const char *names[] = {"", "small", "resolve", "hash", "mid", "large", "global"};
+    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global"};
     for (int i = 1; i <= K_GLOBAL; ++i)
         if (!strcmp(e, names[i])) return i;
     return K_ANY;
@@ -449,7 +452,23 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
     }
-    // large arrays: one CTA per array, targets generated in-CTA, array in global memory
+    // large arrays: one CTA per array, targets generated in-CTA, array in global memory,
+    // next group's values prefetched (pipe) or loaded per group (large)
+    if (forced_kernel() == K_PIPE && (uint64_t)cp.plan.max_k * 32 * PIPE_W + 2 * 32 * PIPE_W <= PRING) {
+        constexpr int W = PIPE_W;
+        const size_t psmem = sizeof(PipeShared<T, W>);
+        auto kern = !segmented ? shuffle_cta_pipe_kernel<T, W, 2>
+                               : (gen == 2 ? shuffle_cta_pipe_kernel<T, W, 1> : shuffle_cta_pipe_kernel<T, W, 0>);
+        const void *kp = (const void *)kern;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+        const int grid = segmented ? grid_for(di, kp, 32 * W, psmem, num_arrays) : 1;
+        kern<<<grid, 32 * W, psmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
+                                          rk_first, segmented ? 1 : 0, gen);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_cta_pipe_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
+                   std::to_string(W) + ">";
+        return BR_OK;
+    }
     if (allow(K_LARGE) && (uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= LRING) {
         constexpr int W = LARGE_W;
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
