@@ -242,25 +242,37 @@ __device__ __forceinline__ void roll_range_cha(const RollArgs &a, u128 s0, int64
     u128 W0 = cha_win_unset(cha_add(s0, (uint64_t)wb + D));
     int err = 0;
     volatile RollWs *vws = a.ws;
-    for (int64_t b0 = wb; b0 < we; b0 += 32) {
+    // windows of U sub-steps: the bounds of all U are requested before the keystream block
+    // computation, which then hides their latency
+    constexpr int U = K <= 2 ? 8 : 4;
+    for (int64_t c0 = wb; c0 < we; c0 += 32 * U) {
         if (early_exit) {  // warp-uniform decision: the window refill is warp-collective
             unsigned long long nf = lane == 0 ? vws->neg_first : 0ull;
             nf = __shfl_sync(0xFFFFFFFFu, nf, 0);
-            if (nf != 0 && (int64_t)(~nf) < b0) break;
+            if (nf != 0 && (int64_t)(~nf) < c0) break;
         }
-        const int64_t b = b0 + lane;
-        const uint64_t w = cha_warp_word(win, ck, W0, cha_add(s0, (uint64_t)b + D), lane);
-        if (b < we) {
-            uint32_t bb[K], d[K];
-            load_bounds<K>(a.bounds + b * K, bb);
-            uint64_t r;
-            uint8_t tc = 0;
-            const int st = eval_batch<K>(bb, w, d, r, tc, err, a.naive != 0);
-            store_rolls<K>(a.rolls + b * K, d);
-            a.words[b] = 1;
-            if (a.flags) a.flags[b] = tc;
-            if (a.rk) a.rk[b] = r;
-            if (st == 1) atomicMax(&a.ws->neg_first, ~(unsigned long long)b);
+        uint32_t bb[U][K];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = c0 + 32 * u + lane;
+            if (b < we) load_bounds<K>(a.bounds + b * K, bb[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = c0 + 32 * u + lane;
+            if (c0 + 32 * u >= we) break;  // warp-uniform
+            const uint64_t w = cha_warp_word(win, ck, W0, cha_add(s0, (uint64_t)b + D), lane);
+            if (b < we) {
+                uint32_t d[K];
+                uint64_t r;
+                uint8_t tc = 0;
+                const int st = eval_batch<K>(bb[u], w, d, r, tc, err, a.naive != 0);
+                store_rolls<K>(a.rolls + b * K, d);
+                a.words[b] = 1;
+                if (a.flags) a.flags[b] = tc;
+                if (a.rk) a.rk[b] = r;
+                if (st == 1) atomicMax(&a.ws->neg_first, ~(unsigned long long)b);
+            }
         }
     }
     if (err) set_error(a.ws, err);
