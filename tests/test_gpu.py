@@ -552,6 +552,33 @@ def test_chacha_dropin_shuffles_golden(B, O, golden):
         assert sha_u32(z) == rec["sha"]
 
 
+def test_chacha_counter_wrap(B, O):
+    """A ChaCha source two blocks before its 64-bit block counter wraps (wordsource.py:160
+    masks the counter): words, shuffles and rolls cross the wrap like the reference."""
+    for pre, n in ((0, 1000), (5, 1000), (3, 70000)):
+        s = B.ChaChaSource(77)
+        s.counter, s._pos = (1 << 64) - 2, 16
+        o = O.chacha(77)
+        o.counter, o.pos = (1 << 64) - 2, 16
+        for _ in range(pre):
+            assert s.next_word() == O.next_word(o)
+        z = torch.arange(n, dtype=torch.int32, device="cuda")
+        B.shuffle_batched(s, z)
+        zr = O.shuffle_batched(o, np.arange(n, dtype=np.uint32))
+        assert np.array_equal(u32(z), zr) and (s.counter, s._pos) == (o.counter, o.pos), (pre, n, B.last_kernel())
+        assert s.counter < 1 << 20  # wrapped
+        assert [s.next_word() for _ in range(9)] == O.words(o, 9)
+    s = B.ChaChaSource(9)
+    s.counter, s._pos = (1 << 64) - 1, 16
+    o = O.chacha(9)
+    o.counter, o.pos = (1 << 64) - 1, 16
+    bounds = O.gen_bounds(3, 2 * 5000)
+    r = B.roll_batches(s, dev_u32(bounds), 2)
+    rolls, words, _, _ = O.roll_batches(o, bounds, 2)
+    assert np.array_equal(u32(r.rolls), rolls) and (s.counter, s._pos) == (o.counter, o.pos)
+    assert u64(B.pcg64_fill(s, 20)).tolist() == O.words(o, 20)
+
+
 @pytest.mark.parametrize("n,eb", [(64, 4), (100, 8), (4096, 4), (20000, 8), (70000, 4), (1 << 20, 8)])
 def test_chacha_segmented(B, O, n, eb):
     na = max(2, min(400, (1 << 20) // n))
