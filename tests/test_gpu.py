@@ -745,3 +745,67 @@ def test_cli_bench_and_shuffle(B, O, tmp_path):
     got = out.getvalue().splitlines()
     perm = O.shuffle_batched(O.pcg64(7), np.arange(500, dtype=np.uint32)).tolist()
     assert got == [f"line{p}" for p in perm]
+
+
+# ------------------------------------------------------------------ C-ABI argument errors
+def test_abi_error_paths(B):
+    """Status codes of the device entry points on bad arguments (no launch happens) and the
+    edge cases that need no work (n < 2, zero arrays, zero batches)."""
+    import ctypes as C
+
+    from paper_2408_06213_b200 import _native as N
+
+    L = N.lib()
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    z = torch.zeros(64, dtype=torch.int32, device="cuda")
+    st = torch.zeros(8, dtype=torch.int64, device="cuda")
+    w64 = torch.full((1,), 7, dtype=torch.int64, device="cuda")
+    zp, stp, wp = (C.c_void_p(t.data_ptr()) for t in (z, st, w64))
+    regs = B.DEFAULT_SCHEDULE._regimes()
+    assert L.br_shuffle_stream(zp, 2, 64, stp, regs, len(regs), 0, None, sp) == N.BR_E_UNSUPPORTED  # elem size
+    assert L.br_shuffle_stream(zp, 4, 1 << 32, stp, regs, len(regs), 0, None, sp) != N.BR_OK  # n >= 2^32
+    assert L.br_shuffle_stream(None, 4, 64, stp, regs, len(regs), 0, None, sp) == N.BR_E_INVALID
+    assert L.br_shuffle_stream(zp, 4, 64, None, regs, len(regs), 0, None, sp) == N.BR_E_INVALID
+    assert L.br_shuffle_segmented(zp, 4, 1, 64, 1, 0, regs, len(regs), 3, None, sp) == N.BR_E_UNSUPPORTED  # generator
+    assert L.br_shuffle_segmented(zp, 4, -1, 64, 1, 0, regs, len(regs), 0, None, sp) == N.BR_E_INVALID
+    bad = (N.Segment * 1)()
+    bad[0].start_n, bad[0].k, bad[0].count = 64, 5, 13  # 65 steps on 64 positions
+    assert L.br_shuffle_stream_segments(zp, 4, 64, stp, bad, 1, None, None, sp) == N.BR_E_INVALID
+    # n < 2: nothing to do, zero words reported, data untouched
+    assert L.br_shuffle_stream(zp, 4, 1, stp, regs, len(regs), 0, wp, sp) == N.BR_OK
+    assert int(w64.item()) == 0
+    assert L.br_shuffle_segmented(zp, 4, 0, 64, 1, 0, regs, len(regs), 0, None, sp) == N.BR_OK
+    ws = torch.zeros(L.br_roll_workspace_bytes(), dtype=torch.uint8, device="cuda")
+    b = torch.ones(16, dtype=torch.int32, device="cuda")
+    r = torch.zeros(16, dtype=torch.int32, device="cuda")
+    wd = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    bp, rp, wdp, wsp = (C.c_void_p(t.data_ptr()) for t in (b, r, wd, ws))
+    assert L.br_roll_batches(bp, 0, 8, stp, rp, wdp, None, None, wsp, sp) == N.BR_E_INVALID  # k < 1
+    assert L.br_roll_batches(bp, 9, 1, stp, rp, wdp, None, None, wsp, sp) == N.BR_E_UNSUPPORTED  # k > 8
+    assert L.br_roll_batches(bp, 2, -1, stp, rp, wdp, None, None, wsp, sp) == N.BR_E_INVALID
+    assert L.br_roll_batches(C.c_void_p(b.data_ptr() + 4), 2, 4, stp, rp, wdp, None, None, wsp, sp) == N.BR_E_INVALID
+    assert L.br_roll_batches(bp, 2, 0, stp, rp, wdp, None, None, wsp, sp) == N.BR_OK  # zero batches
+    assert L.br_roll_batches_phase(bp, 2, 4, stp, rp, wdp, None, None, wsp, 4, sp) == N.BR_E_INVALID
+    assert L.br_pcg64_fill(None, 5, C.byref(N.Pcg64State()), 0, sp) == N.BR_E_INVALID
+    assert L.br_state_upload(None, C.byref(N.Pcg64State()), sp) == N.BR_E_INVALID
+    assert "null" in N.last_error() or N.last_error()
+
+
+def test_dropin_edge_cases(B, O):
+    """Empty and single-element inputs consume nothing (test_shuffle.py:61-67); k = n batch;
+    bounds of 1 (a die with one face) and a product of exactly 2^64."""
+    for gen in ("pcg64", "lehmer", "chacha"):
+        s = B.make_source(gen, 3)
+        before = B.batchrand._state_struct(s)
+        assert B.shuffle_batched(s, []) == [] and B.shuffle_unbatched(s, [5]) == [5]
+        assert B.shuffle_naive_batched(s, [9]) == [9]
+        after = B.batchrand._state_struct(s)
+        assert (before.state_hi, before.state_lo) == (after.state_hi, after.state_lo)
+    s = B.Pcg64Source(4)
+    r = B.roll_batch(s, B.BatchSpec(B.RadixBases.of((1, 1, 1))))
+    assert r.digits == (0, 0, 0) and r.words_consumed == 1
+    o = O.pcg64(4)
+    ro = O.roll_batch(o, (1 << 16, 1 << 16, 1 << 16, 1 << 16))  # product exactly 2^64: never rejected
+    s = B.Pcg64Source(4)
+    r = B.roll_batch(s, B.BatchSpec(B.RadixBases.of((1 << 16,) * 4)))
+    assert r == B.BatchResult(ro[0], ro[1], ro[2], ro[3]) and s.state == o.state
