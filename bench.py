@@ -407,7 +407,6 @@ def run_reference(args, ws, rank):
         dt = time.perf_counter() - t
         value, unit, cores = 2 * sample * args.steps / dt, "rolls/s", 1
         desc = f"{sample} batches of C2 per step (one sequential stream; the reference roll_batch loop)"
-        metric = "bounded rolls/sec (C2: 2^25 batches of k=2, bounds U[2,2^16))"
     else:
         c = SHUFFLE_CFG[cfg]
         n = c["n"]
@@ -425,18 +424,35 @@ def run_reference(args, ws, rank):
         dt = time.perf_counter() - t
         value, unit, cores = n * arrays * args.steps / dt, "elements/s", cpu_cores()
         desc = f"{arrays} arrays of {n} per step, OpenMP over arrays"
-        metric = "shuffled elements/sec"
+    metric, unit_b, config, dtype = headline(args, ws)
+    assert unit == unit_b
+    config = dict(config, reference_note="oracle/oracle.c port of the reference (pure Python upstream, so there is "
+                                         "no compiled reference to run); each step a bounded sample: " + desc)
     line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": cfg, "note": "oracle/oracle.c port of the reference (pure Python upstream, "
-                                               "so there is no compiled reference to run)"},
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": config,
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": desc},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line
 
 
 # ------------------------------------------------------------------------------ main
+def headline(args, ws):
+    """metric, unit, config and dtype of the line (shared by both arms)."""
+    if args.config == "c2":
+        config = {"workload": "C2: BASELINE configs[1], 2^25 batches x k=2 bounded rolls per GPU, bounds iid "
+                              "U[2,2^16) from seed 7, words from pcg64(hash(7,1)); output 2^26 u32 rolls + 2^25 u8 "
+                              "words per GPU", "batches_per_gpu": NB_C2, "k": 2,
+                  "l2": "inputs+outputs 544 MiB per step > 126 MB L2 (no flush needed)",
+                  "parallelism": f"dp{ws} (stream sections by jump-ahead)", "generator": args.generator}
+        return "bounded rolls/sec (C2: 2^25 batches of k=2 per GPU, bounds U[2,2^16))", "rolls/s", config, "u64"
+    cfg = SHUFFLE_CFG[args.config]
+    config = {"workload": cfg["workload"], "l2": "payload larger than L2", "parallelism": f"dp{ws} (arrays)",
+              "generator": args.generator}
+    return "shuffled elements/sec", "elements/s", config, "u32" if cfg["eb"] == 4 else "u64"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -471,23 +487,11 @@ def main():
         torch.distributed.barrier()
     import paper_2408_06213_b200 as B
 
+    metric, unit, config, dtype = headline(args, ws)
     if args.config == "c2":
         r = bench_c2(args, torch, B, ws, rank)
-        metric = "bounded rolls/sec (C2: 2^25 batches of k=2 per GPU, bounds U[2,2^16))"
-        unit = "rolls/s"
-        config = {"workload": "C2: BASELINE configs[1], 2^25 batches x k=2 bounded rolls per GPU, bounds iid "
-                              "U[2,2^16) from seed 7, words from pcg64(hash(7,1)); output 2^26 u32 rolls + 2^25 u8 "
-                              "words per GPU", "batches_per_gpu": NB_C2, "k": 2,
-                  "l2": "inputs+outputs 544 MiB per step > 126 MB L2 (no flush needed)",
-                  "parallelism": f"dp{ws} (stream sections by jump-ahead)", "generator": args.generator}
-        dtype = "u64"
     else:
-        cfg = SHUFFLE_CFG[args.config]
-        r = bench_shuffle(cfg, args, torch, B, ws, rank)
-        metric, unit = "shuffled elements/sec", "elements/s"
-        config = {"workload": cfg["workload"], "l2": "payload larger than L2", "parallelism": f"dp{ws} (arrays)",
-                  "generator": args.generator}
-        dtype = "u32"
+        r = bench_shuffle(SHUFFLE_CFG[args.config], args, torch, B, ws, rank)
         r["e2e"] = None
     line = {"metric": metric, "value": r["value"], "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
