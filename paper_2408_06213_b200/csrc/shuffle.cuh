@@ -8,15 +8,19 @@
 // finding 3; re-checked by tests/test_oracle.py, whose oracle keeps the literal u logic).
 // Swaps of batch b: z[n_b-1-m] <-> z[d_m], m = 0..k_b-1, in that order.
 //
-// Work units sized to the array (north star item 3):
-//   shuffle_small_kernel  one THREAD per array (n <= SMALL_MAX), the block's arrays staged
-//                         in shared memory with an odd row stride so the coalesced loads
-//                         and stores and the per-position swaps are bank-conflict free;
-//   shuffle_mid_kernel    one WARP per array (n <= MID_MAX), array + swap targets in
-//                         shared memory; words generated 32 batches at a time (lane =
-//                         batch, jump-ahead per lane, ballot on the rare rejection), swaps
-//                         applied 32 steps at a time with an exact intra-group conflict
-//                         resolution (see apply_group).
+// Work units sized to the array (north star item 3; dispatch in capi.cu launch_shuffle):
+//   shuffle_small_kernel     one THREAD per array (small n), the block's arrays staged in
+//                            shared memory with an odd row stride (conflict-free coalesced
+//                            staging and uniform-position accesses);
+//   shuffle_cta_hash_kernel  one CTA per shared-memory-resident array: TMA bulk copies in
+//                            and out, targets generated just in time 32*W batches at a
+//                            time, swaps applied 32*W steps at a time with an exact
+//                            intra-group resolution (lane-chain hash + pointer jumping);
+//   shuffle_cta_large_kernel the same groups on arrays in global memory (HBM-resident);
+//   shuffle_mid_kernel / shuffle_large_gen+apply  warp-group forms for schedules with
+//                            large k; shuffle_resolve_kernel / shuffle_cta_pipe_kernel are
+//                            measured alternatives, run only when BR_SHUFFLE_KERNEL asks.
+// Words: lane = batch, jump-ahead per lane, a CTA-wide vote on the rare rejection.
 #pragma once
 #include "chacha.cuh"
 #include "jump.cuh"
