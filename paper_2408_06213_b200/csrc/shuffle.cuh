@@ -1,6 +1,6 @@
 // shuffle.cuh -- segmented Fisher-Yates shuffles with batched dice (shuffle.py:100-225).
 //
-// A compiled plan (plan.h) lists the batches of shuffle_batched for one length n; batch b
+// A compiled plan (capi.cu get_plan) lists the batches of shuffle_batched for one length n; batch b
 // has remaining length n_b, size k_b and exact threshold t_b = 2^64 mod ff(n_b, k_b).
 // A batch is accepted iff its final remainder r_k >= t_b.  This is exactly the
 // reference's acceptance: the carried bound u of _run_batches (shuffle.py:118-128) only
