@@ -86,6 +86,34 @@ def test_roll_batches_c2_large_vs_oracle(B, O):
     assert st == src.state
 
 
+def test_roll_batches_c2_full_size(B, O):
+    """The whole C2 workload (BASELINE configs[1]: 2^25 batches, the bench's bounds and stream)
+    bit-exact against the oracle, through the production call (no flags requested)."""
+    nb = 1 << 25
+    bounds = O.gen_bounds(7, 2 * nb)
+    src = O.pcg64(O.array_seed(7, 1))
+    rolls, words, _, _ = O.roll_batches(src, bounds, 2)
+    ds = B.DeviceStream(O.array_seed(7, 1))
+    r = B.roll_batches(ds, dev_u32(bounds), 2)
+    assert "roll_fast_kernel<2>" in B.last_kernel()
+    st = ds.host_state()
+    assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words)
+    assert (st.state_hi << 64 | st.state_lo) == src.state
+
+
+def test_one_huge_array(B, O):
+    """A single array of 2^25 elements (128 MiB) through the stream call, bit-exact against the
+    oracle (hundreds of rejected batches at these lengths exercise the realignment)."""
+    n = 1 << 25
+    s = B.Pcg64Source(2026)
+    z = torch.arange(n, dtype=torch.int32, device="cuda")
+    B.shuffle_batched(s, z)
+    o = O.pcg64(2026)
+    ref = O.shuffle_batched(o, np.arange(n, dtype=np.uint32))
+    assert np.array_equal(u32(z), ref) and s.state == o.state, B.last_kernel()
+    assert o.drawn > len(O.shuffle_trace(n)[0]) + 100  # the rejection path was exercised
+
+
 @pytest.mark.parametrize("heavy_fraction", [0.001, 0.05, 1.0])
 def test_roll_batches_forced_rejections(B, O, heavy_fraction):
     """Products near 0.7*2^64 reject ~30% of words: exercises the exact fixup path."""
