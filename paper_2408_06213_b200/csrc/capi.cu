@@ -148,6 +148,7 @@ struct CachedPlan {
     uint64_t nbatches = 0;
 };
 std::map<std::pair<int, std::string>, CachedPlan> g_plans;
+constexpr size_t PLAN_CACHE_MAX = 4096;
 
 // Compile segments into a device plan (cached per device and segment list).
 int get_plan(uint64_t n, const std::vector<br_segment> &segs, bool naive, CachedPlan *out) {
@@ -213,6 +214,13 @@ int get_plan(uint64_t n, const std::vector<br_segment> &segs, bool naive, Cached
     cp.plan.segs = (const DevSeg *)p;
     cp.plan.thresh = (const uint64_t *)((char *)p + off);
     cp.nbatches = fb;
+    if (g_plans.size() >= PLAN_CACHE_MAX) {
+        // bounded cache: drop every plan once the device is idle (no kernel still reads
+        // one); callers with thousands of distinct lengths pay a rebuild, not memory
+        cudaDeviceSynchronize();
+        for (auto &kv : g_plans) cudaFree(kv.second.dev);
+        g_plans.clear();
+    }
     g_plans[{dev, key}] = cp;
     *out = cp;
     return BR_OK;
