@@ -595,9 +595,8 @@ template <typename T, int W, typename RT, uint32_t RS, int HB>
 __device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W, RT, RS, HB> &sh, uint32_t tag,
                                                        uint32_t top, uint32_t lim, int L) {
     constexpr int G = 32 * W;
-    const int64_t i64 = (int64_t)top - L;
-    const bool act = i64 >= (int64_t)lim;
-    const uint32_t i = act ? (uint32_t)i64 : 0;
+    const bool act = top >= lim + (uint32_t)L;  // 32-bit: lim + L < 2^32 for n < 2^32
+    const uint32_t i = top - (uint32_t)L;
     const uint32_t j = act ? (uint32_t)sh.ring[i & (RS - 1)] : 0;
     const T vi = act ? z[i] : T(0);
     const T vj = act ? z[j] : T(0);
