@@ -59,7 +59,7 @@ __host__ __device__ __forceinline__ void chacha_block(const ChaKey &K, uint64_t 
     uint32_t x12 = (uint32_t)ctr, x13 = (uint32_t)(ctr >> 32);
     uint32_t x14 = (uint32_t)K.nonce, x15 = (uint32_t)(K.nonce >> 32);
 #ifdef __CUDA_ARCH__
-#pragma unroll 2
+#pragma unroll
 #endif
     for (int r = 0; r < 10; ++r) {
         BR_CHA_QR(x0, x4, x8, x12)

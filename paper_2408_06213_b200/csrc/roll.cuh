@@ -301,17 +301,53 @@ __device__ __forceinline__ void mark_main(const RollArgs &a, unsigned done) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.ws->main_done = done;
 }
 
-// ChaCha main pass at full occupancy (launched when the host knows the stream is ChaCha)
+// ChaCha main pass at full occupancy (launched when the host knows the stream is ChaCha).
+// Each thread owns whole keystream blocks: block m (positions 8m..8m+7) is computed once in
+// registers and rolls the batches whose words it holds (batch b uses position s0 + b), so
+// no word goes through shared memory.  Bounds and rolls move 8 bytes per batch with lanes
+// 64 bytes apart; consecutive batches of a lane reuse the same sectors (L1 for loads, L2
+// write combining for stores).
 template <int K>
 __global__ void __launch_bounds__(256) roll_cha_kernel(RollArgs a) {
-    __shared__ __align__(16) uint64_t win[8][256];
     pdl_launch_dependents();
     if (!roll_is_chacha(a)) {
         mark_main(a, 0);
         return;
     }
     mark_main(a, 1);
-    roll_cha_main<K>(a, win[(threadIdx.x >> 5) & 7]);
+    const u128 s0 = mk128(a.state[0], a.state[1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const u128 sf = cha_add(s0, (uint64_t)a.nb);
+        a.ws->final_hi = sf.hi;
+        a.ws->final_lo = sf.lo;
+    }
+    const ChaKey ck = cha_key_of_state(a.state);
+    const uint32_t q0 = (uint32_t)(s0.lo & 7);          // word of the first block that is batch 0
+    const uint64_t blk0 = cha_block_of(s0);
+    const int64_t nblk = ((int64_t)q0 + a.nb + 7) >> 3;
+    int err = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nblk; t += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t kb[16];
+        chacha_block(ck, blk0 + (uint64_t)t, kb);
+        const int64_t b0 = t * 8 - q0;  // batch of word 0 of this block
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t b = b0 + q;
+            if (b < 0 || b >= a.nb) continue;
+            const uint64_t w = ((uint64_t)kb[2 * q + 1] << 32) | kb[2 * q];
+            uint32_t bb[K], d[K];
+            load_bounds<K>(a.bounds + b * K, bb);
+            uint64_t r;
+            uint8_t tc = 0;
+            const int st = eval_batch<K>(bb, w, d, r, tc, err, a.naive != 0);
+            store_rolls<K>(a.rolls + b * K, d);
+            a.words[b] = 1;
+            if (a.flags) a.flags[b] = tc;
+            if (a.rk) a.rk[b] = r;
+            if (st == 1) atomicMax(&a.ws->neg_first, ~(unsigned long long)b);
+        }
+    }
+    if (err) set_error(a.ws, err);
 }
 
 template <int K>
