@@ -92,6 +92,23 @@ __global__ void k_div(uint64_t *out, uint32_t seed) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// peak of the partial-product instruction itself: 8 independent IMAD.WIDE.U32 chains per thread
+__global__ void k_imad_wide(uint64_t *out, uint32_t seed) {
+    uint64_t acc[8];
+    uint32_t m = 0x9E3779B9u + threadIdx.x + seed;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = (uint64_t)(threadIdx.x + c * 7919u + blockIdx.x);
+#pragma unroll 4
+    for (int i = 0; i < ITERS / 8; ++i) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = (uint64_t)(uint32_t)acc[c] * m + (acc[c] >> 32);
+    }
+    uint64_t x = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x ^= acc[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x;
+}
+
 template <typename F>
 double run(F kern, uint64_t *out, int grid, int threads, double ops_per_thread) {
     cudaEvent_t a, b;
@@ -119,6 +136,7 @@ int main() {
     const double cha = run(k_chacha, out, grid, threads, ITERS);  // ITERS/8 blocks = ITERS words
     const double mod = run(k_mod64, out, grid, threads, ITERS);
     const double dv = run(k_div, out, grid, threads, ITERS);
+    const double iw = run(k_imad_wide, out, grid, threads, ITERS);  // ITERS/8 x 8 chains
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         fprintf(stderr, "cuda error: %s\n", cudaGetErrorString(e));
@@ -127,9 +145,10 @@ int main() {
     printf("{\"device_sms\": %d, \"grid\": %d, \"threads\": %d, \"ns_per_op\": {\"die\": %.6g, \"pcg64_word\": %.6g, "
            "\"lehmer_word\": %.6g, \"chacha_word\": %.6g, \"mod64\": %.6g, \"div64_32\": %.6g}, "
            "\"in_dice\": {\"pcg64_word\": %.4g, \"lehmer_word\": %.4g, \"chacha_word\": %.4g, \"mod64\": %.4g, "
-           "\"div64_32\": %.4g}, \"method\": \"dependent chains on every thread of %d x %d threads, CUDA events, "
-           "5 launches after warm-up; ns per op of the whole GPU\"}\n",
-           sms, grid, threads, die, pcg, leh, cha, mod, dv, pcg / die, leh / die, cha / die, mod / die, dv / die, grid,
-           threads);
+           "\"div64_32\": %.4g}, \"imad_wide_per_s\": %.6g, \"method\": \"dependent chains on every thread of %d x %d "
+           "threads, CUDA events, 5 launches after warm-up; ns per op of the whole GPU; imad_wide_per_s = IMAD.WIDE.U32 "
+           "(32x32+64 -> 64) throughput with 8 independent chains per thread\"}\n",
+           sms, grid, threads, die, pcg, leh, cha, mod, dv, pcg / die, leh / die, cha / die, mod / die, dv / die,
+           1e9 / iw, grid, threads);
     return 0;
 }
