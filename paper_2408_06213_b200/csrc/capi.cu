@@ -369,6 +369,9 @@ constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 #ifndef RES_W
 #define RES_W 8
 #endif
+#ifndef RES_WS
+#define RES_WS 16  // single-array stream calls: one CTA, as wide as its window allows
+#endif
 #ifndef PIPE_W
 #define PIPE_W 8
 #endif
@@ -411,20 +414,32 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         g_kernel = std::string("shuffle_small_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
     }
-    if (forced_kernel() == K_RESOLVE && n <= 65535 && resolve_smem_bytes<T>((uint32_t)n) <= MID_SMEM_MAX) {
-        constexpr int W = RES_W;
+    // closed-form resolution (shuffle_resolve_kernel): the single-array stream calls, where one
+    // CTA's latency is the whole call and it needs ~10 barriers instead of 5 per 128 steps;
+    // for many arrays the hashed groups win, so there only on request
+    const bool res_fit = n <= 65535 && resolve_smem_bytes<T>((uint32_t)n) <= MID_SMEM_MAX;
+    if (res_fit && (forced_kernel() == K_RESOLVE || (!segmented && forced_kernel() == K_ANY))) {
         const size_t rsmem = resolve_smem_bytes<T>((uint32_t)n);
-        auto kern = !segmented ? shuffle_resolve_kernel<T, W, 2>
-                               : (gen == 2 ? shuffle_resolve_kernel<T, W, 1> : shuffle_resolve_kernel<T, W, 0>);
-        const void *kp = (const void *)kern;
+        const void *kp;
+        int threads;
+        if (segmented) {
+            kp = gen == 2 ? (const void *)shuffle_resolve_kernel<T, RES_W, 1> : (const void *)shuffle_resolve_kernel<T, RES_W, 0>;
+            threads = 32 * RES_W;
+        } else {
+            kp = (const void *)shuffle_resolve_kernel<T, RES_WS, 2>;
+            threads = 32 * RES_WS;
+        }
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
-        int grid = segmented ? grid_for(di, kp, 32 * W, rsmem, num_arrays) : 1;
-        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
-        kern<<<grid, 32 * W, rsmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
-                                          rk_first, use_tma, segmented ? 1 : 0, gen);
-        CK(cudaGetLastError());
-        g_kernel = std::string("shuffle_resolve_kernel<u") + std::to_string(8 * sizeof(T)) + "," + std::to_string(W) +
-                   ">";
+        int grid = segmented ? grid_for(di, kp, threads, rsmem, num_arrays) : 1;
+        int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+        int seg = segmented ? 1 : 0;
+        T *dp = (T *)data;
+        DevPlan plan = cp.plan;
+        void *args[] = {&dp, &num_arrays, &plan, &run_seed, &base, &words32, &state_dev, &words64, &rk_first, &use_tma,
+                        &seg, &gen};
+        CK(cudaLaunchKernel(kp, dim3(grid), dim3(threads), args, rsmem, st));
+        g_kernel = std::string("shuffle_resolve_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
+                   std::to_string(threads / 32) + ">";
         return BR_OK;
     }
     const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);

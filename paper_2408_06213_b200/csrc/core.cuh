@@ -161,10 +161,12 @@ __host__ __device__ __forceinline__ uint32_t die(uint32_t b, uint64_t &r) {
 __host__ __device__ __forceinline__ uint64_t threshold64(uint64_t b) { return b ? (0 - b) % b : 0; }
 
 // Jump tables: A_d = M^d, G_d = sum_{i<d} M^i so that state_{t+d} = A_d*state_t + G_d*inc.
+// The direct tables cover every lane offset of a CTA (up to 1024 threads).
+static constexpr int JUMP_SMALL = 1024;
 struct JumpTables {
     u128 A[64], G[64];       // d = 2^k
-    u128 SA[257], SG[257];   // d = 0..256 (lane offsets / small realignments)
-    u128 LA[64], LSA[257];   // Lehmer: multiplier powers M_L^(2^k), M_L^d
+    u128 SA[JUMP_SMALL + 1], SG[JUMP_SMALL + 1];  // d = 0..JUMP_SMALL (lane offsets, realignments)
+    u128 LA[64], LSA[JUMP_SMALL + 1];             // Lehmer: multiplier powers M_L^(2^k), M_L^d
 };
 
 // Host construction (also used by the C-ABI host helpers)
@@ -184,13 +186,13 @@ inline void build_jump_tables(JumpTables &t) {
         lm = mul128(lm, lm);
     }
     u128 la = mk128(0, 1);
-    for (int d = 0; d <= 256; ++d) {
+    for (int d = 0; d <= JUMP_SMALL; ++d) {
         t.LSA[d] = la;
         la = mul128(mk128(0, LEHMER_MULT), la);
     }
     u128 a = mk128(0, 1), gg = mk128(0, 0);
     u128 M = mk128(PCG_MULT_HI, PCG_MULT_LO);
-    for (int d = 0; d <= 256; ++d) {
+    for (int d = 0; d <= JUMP_SMALL; ++d) {
         t.SA[d] = a;
         t.SG[d] = gg;
         gg = add128(mul128(M, gg), mk128(0, 1));  // G_{d+1} = M*G_d + 1

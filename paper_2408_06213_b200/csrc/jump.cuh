@@ -4,7 +4,7 @@
 // d more words is A_d*s + G_d*inc (LCG jump-ahead; checked against numpy's PCG64.advance
 // and against stepping in tests/test_oracle.py and tests/test_gpu_*.py).
 //   c_A/c_G : d = 2^k, read with warp-uniform k      -> __constant__ (broadcast)
-//   g_SA/g_SG: d = 0..256, read with per-lane d        -> global (L1-cached)
+//   g_SA/g_SG: d = 0..JUMP_SMALL (1024), per-lane d    -> global (L1-cached)
 #pragma once
 #include "core.cuh"
 
@@ -13,9 +13,9 @@ namespace br {
 __constant__ u128 c_A[64];
 __constant__ u128 c_G[64];
 __constant__ u128 c_LA[64];
-__device__ u128 g_SA[257];
-__device__ u128 g_SG[257];
-__device__ u128 g_LSA[257];
+__device__ u128 g_SA[JUMP_SMALL + 1];
+__device__ u128 g_SG[JUMP_SMALL + 1];
+__device__ u128 g_LSA[JUMP_SMALL + 1];
 
 // state after d more updates (any d; cost popcount(d) affine steps)
 __device__ __forceinline__ u128 jump(u128 s, u128 inc, uint64_t d) {
@@ -28,7 +28,7 @@ __device__ __forceinline__ u128 jump(u128 s, u128 inc, uint64_t d) {
     return s;
 }
 
-// state after d (0..256) more updates; d may differ per lane
+// state after d (0..JUMP_SMALL) more updates; d may differ per lane
 __device__ __forceinline__ u128 jump_small(u128 s, u128 inc, int d) {
     u128 A = g_SA[d], G = g_SG[d];
     return mad128(s, A, mul128(G, inc));

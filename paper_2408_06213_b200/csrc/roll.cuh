@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     static_assert(K == 1 || K == 2, "fast path is for k <= 2");
     constexpr int LB = ROLL_LB;
     constexpr int VB = LB / (4 * K);
-    static_assert(32 * VB <= 256, "jump table covers 256 words");
+    static_assert(32 * VB <= JUMP_SMALL, "jump table covers the lane offsets");
     constexpr int U = ROLL_U;
     constexpr int64_t CH = 32 * VB * U;
     pdl_launch_dependents();

@@ -18,8 +18,9 @@
 //                            intra-group resolution (lane-chain hash + pointer jumping);
 //   shuffle_cta_large_kernel the same groups on arrays in global memory (HBM-resident);
 //   shuffle_mid_kernel / shuffle_large_gen+apply  warp-group forms for schedules with
-//                            large k; shuffle_resolve_kernel / shuffle_cta_pipe_kernel are
-//                            measured alternatives, run only when BR_SHUFFLE_KERNEL asks.
+//                            large k; shuffle_resolve_kernel (closed-form, whole array)
+//                            serves single-array stream calls; shuffle_cta_pipe_kernel is a
+//                            measured alternative, run only when BR_SHUFFLE_KERNEL asks.
 // Words: lane = batch, jump-ahead per lane, a CTA-wide vote on the rare rejection.
 #pragma once
 #include "chacha.cuh"
