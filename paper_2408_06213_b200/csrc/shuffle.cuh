@@ -1147,10 +1147,10 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
 // atomicExch per step to thread per-target lists, a list walk per position for ns and ft,
 // pointer jumping on F, and one gather z0[r] per position written straight to global
 // memory -- about ten barriers per array instead of five per 32*W steps.  Measured on B200
-// it is slower than the hashed group kernel for C4 (3.25 vs 2.52 ms: the divergent list
-// walks and the jumping rounds cost more instructions than the barriers they save), so the
-// dispatcher only uses it when asked (BR_SHUFFLE_KERNEL=resolve); it stays as an
-// independently derived, fully tested second algorithm.
+// it is slower than the hashed group kernel for many arrays (C4: 3.25 vs 2.49 ms: the
+// divergent list walks and the jumping rounds cost more instructions than the barriers they
+// save), but faster for ONE array, where the CTA's latency is the whole call (C1: 0.033 vs
+// 0.070 ms with 512 threads); the dispatcher uses it for single-array stream calls.
 static constexpr uint16_t RES_NONE = 0xFFFF;
 
 template <bool CHA, int W>
