@@ -313,6 +313,35 @@ class RadixBases:
         return len(self.bases)
 
 
+def encode(digits, bases: RadixBases) -> int:
+    """mixed_radix.py:40-51: the value of a digit tuple, most significant digit first
+    (host arithmetic; the device produces digits, this is the inverse view)."""
+    if len(digits) != len(bases.bases):
+        raise DigitOutOfRange(f"expected {len(bases.bases)} digits, got {len(digits)}")
+    acc = 0
+    for base, digit in zip(bases.bases, digits):
+        if digit < 0 or digit >= base:
+            raise DigitOutOfRange(f"digit {digit} not in [0, {base})")
+        acc = acc * base + digit
+    return acc
+
+
+def decode(value: int, bases: RadixBases) -> tuple:
+    """mixed_radix.py:54-67: the digit tuple of value < prod(bases) (host arithmetic)."""
+    if value < 0 or value >= bases.product.value:
+        raise ValueOutOfRange(f"value {value} not in [0, {bases.product.value})")
+    out = [0] * len(bases.bases)
+    for pos in range(len(bases.bases) - 1, -1, -1):
+        value, out[pos] = divmod(value, bases.bases[pos])
+    return tuple(out)
+
+
+def chacha_block(key_words, counter: int, nonce: int) -> list:
+    """wordsource.py:102-133: one 16-word ChaCha20 block (64-bit counter and nonce), computed
+    by the native library's block function."""
+    return _chacha_block_words(tuple(key_words), nonce, counter & MASK64)
+
+
 # ---------------------------------------------------------------------------- batched.py
 @dataclass(frozen=True)
 class BatchSpec:
@@ -867,7 +896,7 @@ __all__ = [
     "RollBatchesResult", "ShuffleSchedule", "SourceExhausted", "UnknownGenerator", "ValueOutOfRange",
     "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",
     "make_source", "mul_full", "LehmerSource", "ChaChaSource", "GENERATORS", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
-    "roll_batch_naive", "shuffle_naive_batched",
+    "roll_batch_naive", "shuffle_naive_batched", "encode", "decode", "chacha_block",
     "roll_batches", "shuffle_batched", "shuffle_many", "shuffle_unbatched", "splitmix64_stream", "threshold",
     "last_kernel",
 ]

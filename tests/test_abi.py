@@ -223,3 +223,25 @@ def test_chacha_position_mapping():
     v = B.ChaChaSource(3)
     B._chacha_set_position(v, 13)
     assert [v.next_word() for _ in range(7)] == w[13:20]
+
+
+def test_public_api_covers_the_reference():
+    """Every public name of the reference package (batchrand/__init__.py) exists here, except
+    the two host-only word sources the device path does not draw from (8(b))."""
+    import paper_2408_06213_b200 as B
+
+    names = ["BatchRandError", "BatchResult", "BatchSpec", "BoundEncoding", "BoundOverflow", "ChaChaSource",
+             "CostParams", "DEFAULT_SCHEDULE", "DigitOutOfRange", "FullProduct", "InsufficientTrials", "LehmerSource",
+             "NoCrossover", "PAIR_SCHEDULE", "Pcg64Source", "RadixBases", "RollOutcome", "ShuffleSchedule",
+             "SourceExhausted", "UnknownAlgorithm", "UnknownGenerator", "ValueOutOfRange", "WordSource",
+             "build_schedule", "chacha_block", "cost_per_roll", "decode", "default_schedule", "digit_pass", "encode",
+             "falling_factorial", "find_nk", "make_source", "mul_full", "partial_shuffle_batch", "roll_batch",
+             "roll_batch_known_threshold", "roll_batch_naive", "roll_single", "roll_single_traced",
+             "shuffle_batched", "shuffle_naive_batched", "shuffle_unbatched", "threshold"]
+    assert [n for n in names if not hasattr(B, n)] == []
+    rb = B.RadixBases.of((4, 3, 5))
+    assert B.decode(37, rb) == (2, 1, 2) and B.encode((2, 1, 2), rb) == 37  # mixed_radix.py:40-67
+    with pytest.raises(B.DigitOutOfRange):
+        B.encode((4, 0, 0), rb)
+    with pytest.raises(B.ValueOutOfRange):
+        B.decode(60, rb)
