@@ -93,8 +93,17 @@ void br_pcg64_seed(uint64_t seed, br_pcg64 *out);
 void br_lehmer_seed(uint64_t seed, br_pcg64 *out);
 /* wordsource.py:147-153 ChaChaSource.__init__ (position 0) */
 void br_chacha_seed(uint64_t seed, br_chacha *out);
+/* wordsource.py:191-207 FixedSequenceSource with 64-bit words: a stream that replays the
+ * `nwords` words at words_dev (device memory, kept alive by the caller for every call that
+ * uses the state).  head.state = position of the next word, head.inc_hi = nwords,
+ * head.inc_lo = BR_WORDS_TAG, key[0..1] = the address.  Words past the end read as
+ * 2^64 - 1 (accepted by every batch, so the call terminates): the caller raises
+ * SourceExhausted when a call ends at a position beyond nwords. */
+#define BR_WORDS_TAG 4
+int br_words_state(const uint64_t *words_dev, uint64_t nwords, br_chacha *out);
 /* wordsource.py:85-89 Pcg64Source.next_word / :65-67 LehmerSource.next_word /
- * :155-164 ChaChaSource.next_word (any of the three, told apart by the increment) */
+ * :155-164 ChaChaSource.next_word / a replayed word (synchronous device read), told apart
+ * by the increment */
 uint64_t br_pcg64_next(br_pcg64 *st);
 /* O(log d) jump-ahead by `delta` words (numpy PCG64.advance semantics; ChaCha: position + d) */
 void br_pcg64_advance(br_pcg64 *st, uint64_t delta);

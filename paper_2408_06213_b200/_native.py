@@ -32,6 +32,7 @@ class ChachaState(Pcg64State):
 
 
 BR_CHACHA_TAG = 2
+BR_WORDS_TAG = 4
 
 
 class Regime(C.Structure):
@@ -52,6 +53,7 @@ PROTOTYPES = {
     "br_pcg64_seed": (None, [u64, P(Pcg64State)]),
     "br_lehmer_seed": (None, [u64, P(Pcg64State)]),
     "br_chacha_seed": (None, [u64, P(ChachaState)]),
+    "br_words_state": (C.c_int, [vp, u64, P(ChachaState)]),
     "br_pcg64_next": (u64, [P(Pcg64State)]),
     "br_pcg64_advance": (None, [P(Pcg64State), u64]),
     "br_array_seed": (u64, [u64, u64]),

@@ -164,6 +164,54 @@ def _chacha_set_position(source, p: int) -> None:
         source.counter, source._pos = (blk + 1) & MASK64, 2 * q
 
 
+class FixedSequenceSource(WordSource):
+    """Replays a given word sequence (wordsource.py:191-207); raises SourceExhausted on an
+    over-read.  With 64-bit words the device draws from it too: the remaining words are
+    copied to the device for the call and `cursor` advances by the words consumed.  A call
+    that would read past the end raises SourceExhausted and leaves the payload unchanged
+    (the reference would have left it partly shuffled)."""
+
+    def __init__(self, words, bit_width: int = 64):
+        self.word_bits = bit_width
+        self.words = list(words)
+        for w in self.words:
+            if not 0 <= w < 1 << bit_width:
+                raise ValueError(f"word {w} does not fit in {bit_width} bits")
+        self.cursor = 0
+
+    def next_word(self) -> int:
+        if self.cursor >= len(self.words):
+            raise SourceExhausted(f"sequence of {len(self.words)} words over-read")
+        w = self.words[self.cursor]
+        self.cursor += 1
+        return w
+
+
+class ExhaustiveSource(WordSource):
+    """Every word of a small width once, in order (wordsource.py:167-188).  Host only: the
+    device path needs 64-bit words, so device calls with it raise TypeError."""
+
+    def __init__(self, bit_width: int):
+        if not 1 <= bit_width <= 16:
+            raise ValueError(f"bit_width must be in [1, 16], got {bit_width}")
+        self.word_bits = bit_width
+        self.cursor = 0
+
+    @property
+    def exhausted(self) -> bool:
+        return self.cursor == 1 << self.word_bits
+
+    def next_word(self) -> int:
+        if self.exhausted:
+            raise SourceExhausted(f"all {1 << self.word_bits} words emitted")
+        self.cursor += 1
+        return self.cursor - 1
+
+
+def _is_fixed(source) -> bool:
+    return hasattr(source, "words") and hasattr(source, "cursor") and not hasattr(source, "state")
+
+
 GENERATORS = {"pcg64": Pcg64Source, "lehmer": LehmerSource, "chacha": ChaChaSource}
 _GENERATOR_IDS = {"pcg64": 0, "lehmer": 1, "chacha": 2}
 
@@ -189,6 +237,14 @@ def _is_lehmer(source) -> bool:
 def _state_struct(source) -> N.Pcg64State:
     if getattr(source, "word_bits", 64) != 64:
         raise TypeError("the device path needs 64-bit words")
+    if _is_fixed(source):  # the remaining words go to the device for this call
+        torch = _torch()
+        rest = [w - (1 << 64) if w >= 1 << 63 else w for w in source.words[source.cursor:]]
+        dev = torch.tensor(rest if rest else [0], dtype=torch.int64, device="cuda")
+        st = N.ChachaState()
+        N.check(N.lib().br_words_state(_ptr(dev), len(rest), C.byref(st)), "words state")
+        st._keep = dev  # the device words live as long as the state that points at them
+        return st
     if _is_chacha(source):
         st = N.ChachaState()
         p = _chacha_position(source)
@@ -659,6 +715,7 @@ class DeviceStream:
 
     def _init(self, st, state=None):
         torch = _torch()
+        self._keep = getattr(st, "_keep", None)  # device words of a replayed sequence
         # 8 words: a br_pcg64 head, then the ChaCha key (unused by PCG64 / Lehmer)
         self.state = torch.empty(8, dtype=torch.int64, device="cuda") if state is None else state
         self._workspace = None
@@ -680,7 +737,14 @@ class DeviceStream:
 
     def write_back(self, source) -> None:
         st = self.host_state()
-        if _is_chacha(source):
+        if _is_fixed(source):
+            used = (st.state_hi << 64) | st.state_lo
+            avail = len(source.words) - source.cursor
+            if used > avail:
+                source.cursor = len(source.words)
+                raise SourceExhausted(f"sequence of {len(source.words)} words over-read")
+            source.cursor += used
+        elif _is_chacha(source):
             _chacha_set_position(source, (st.state_hi << 64) | st.state_lo)
         else:
             source.state = (st.state_hi << 64) | st.state_lo
@@ -897,6 +961,7 @@ __all__ = [
     "WordSource", "array_seed", "default_schedule", "digit_pass", "digit_pass_many", "falling_factorial",
     "make_source", "mul_full", "LehmerSource", "ChaChaSource", "GENERATORS", "partial_shuffle_batch", "pcg64_fill", "roll_batch", "roll_batch_known_threshold",
     "roll_batch_naive", "shuffle_naive_batched", "encode", "decode", "chacha_block",
+    "FixedSequenceSource", "ExhaustiveSource",
     "roll_batches", "shuffle_batched", "shuffle_many", "shuffle_unbatched", "splitmix64_stream", "threshold",
     "last_kernel",
 ]

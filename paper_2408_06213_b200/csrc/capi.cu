@@ -252,7 +252,7 @@ __global__ void cha_fill_kernel(uint64_t *__restrict__ out, int64_t count, ChaKe
     const uint64_t blk0 = cha_block_of(p0);
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nblk; t += (int64_t)gridDim.x * blockDim.x) {
         uint32_t b[16];
-        chacha_block(K, blk0 + (uint64_t)t, b);
+        cha_block_any(K, blk0 + (uint64_t)t, b);
         const int64_t i0 = t * 8 - q0;  // out index of word 0 of this block
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -262,13 +262,22 @@ __global__ void cha_fill_kernel(uint64_t *__restrict__ out, int64_t count, ChaKe
     }
 }
 
-inline bool host_is_chacha(const br_pcg64 *st) { return st->inc_lo == CHACHA_TAG; }
+// position-addressed streams (ChaCha keystream or replayed words): 64-byte states
+inline bool host_is_chacha(const br_pcg64 *st) { return st->inc_lo == CHACHA_TAG || st->inc_lo == WORDS_TAG; }
 
 inline ChaKey host_cha_key(const br_pcg64 *st) {
     const br_chacha *c = reinterpret_cast<const br_chacha *>(st);
     ChaKey K;
     for (int i = 0; i < 8; ++i) K.k[i] = c->key[i];
     K.nonce = st->inc_hi;
+    K.words = nullptr;
+    K.nwords = 0;
+    if (st->inc_lo == WORDS_TAG) {
+        uint64_t addr;
+        memcpy(&addr, c->key, sizeof addr);
+        K.words = reinterpret_cast<const uint64_t *>(addr);
+        K.nwords = st->inc_hi;
+    }
     return K;
 }
 
@@ -609,7 +618,25 @@ void br_chacha_seed(uint64_t seed, br_chacha *out) {
     for (int i = 0; i < 8; ++i) out->key[i] = K.k[i];
 }
 
+int br_words_state(const uint64_t *words_dev, uint64_t nwords, br_chacha *out) {
+    if (!out || (nwords && !words_dev)) return fail(BR_E_INVALID, "null words");
+    memset(out, 0, sizeof *out);
+    out->head.inc_hi = nwords;
+    out->head.inc_lo = WORDS_TAG;
+    const uint64_t addr = reinterpret_cast<uint64_t>(words_dev);
+    memcpy(out->key, &addr, sizeof addr);
+    return BR_OK;
+}
+
 uint64_t br_pcg64_next(br_pcg64 *st) {
+    if (st->inc_lo == WORDS_TAG) {  // one replayed word, read back from the device
+        const uint64_t p = st->state_lo;
+        st->state_lo = p + 1;
+        if (p >= st->inc_hi || st->state_hi) return ~0ull;  // past the end: as on the device
+        uint64_t w = 0;
+        cudaMemcpy(&w, host_cha_key(st).words + p, sizeof w, cudaMemcpyDeviceToHost);
+        return w;
+    }
     if (host_is_chacha(st)) {
         const u128 s = add128(mk128(st->state_hi, st->state_lo), mk128(0, 1));
         st->state_hi = s.hi;

@@ -25,13 +25,26 @@ namespace br {
 // inc.lo == 2 marks a ChaCha stream (PCG64 increments are odd, Lehmer's is 0); inc.hi is
 // the nonce.  The 8 key words follow the 32-byte head of a device/host state (br_chacha).
 static constexpr uint64_t CHACHA_TAG = 2;
+// A replayed word sequence (wordsource.py:191-207 FixedSequenceSource, 64-bit words) is the
+// same kind of position-addressed stream: word p is words[p] of a device array (inc.hi =
+// its length, the first key slot = its address).  Words past the end read as 2^64 - 1, which
+// every batch accepts (its final remainder is 2^64 - prod >= 2^64 mod prod), so a call that
+// over-reads still terminates; the host then raises SourceExhausted from the position the
+// call ended at.
+static constexpr uint64_t WORDS_TAG = 4;
 
 struct ChaKey {
     uint32_t k[8];
     uint64_t nonce;
+    const uint64_t *words;  // non-null: replayed words instead of the ChaCha block function
+    uint64_t nwords;
 };
 
 __host__ __device__ __forceinline__ bool is_chacha(u128 inc) { return inc.lo == CHACHA_TAG; }
+// position-addressed streams: ChaCha keystreams and replayed word sequences
+__host__ __device__ __forceinline__ bool is_posgen(u128 inc) {
+    return inc.lo == CHACHA_TAG || inc.lo == WORDS_TAG;
+}
 
 __host__ __device__ __forceinline__ uint32_t rotl32(uint32_t v, int r) {
 #ifdef __CUDA_ARCH__
@@ -100,6 +113,27 @@ __host__ __device__ __forceinline__ void chacha_seed(uint64_t seed, ChaKey &K) {
         K.k[2 * i + 1] = (uint32_t)(c >> 32);
     }
     K.nonce = splitmix64_next(x);
+    K.words = nullptr;
+    K.nwords = 0;
+}
+
+// the 8 words of block `blk` of either kind of position-addressed stream
+__host__ __device__ __forceinline__ void cha_block_any(const ChaKey &K, uint64_t blk, uint32_t out[16]) {
+    if (K.words) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint64_t idx = blk * 8 + q;
+#ifdef __CUDA_ARCH__
+            const uint64_t w = idx < K.nwords ? __ldg(K.words + idx) : ~0ull;
+#else
+            const uint64_t w = 0;  // host code never reads device words directly
+#endif
+            out[2 * q] = (uint32_t)w;
+            out[2 * q + 1] = (uint32_t)(w >> 32);
+        }
+    } else {
+        chacha_block(K, blk, out);
+    }
 }
 
 // block counter of word position p: (p >> 3) mod 2^64 (the counter wraps like the
@@ -137,7 +171,7 @@ __host__ __device__ __forceinline__ u128 cha_add(u128 s, uint64_t d) {
 __host__ __device__ __forceinline__ uint64_t cha_out(const ChaKey &K, u128 s) {
     const u128 p = cha_prev(s);
     uint32_t b[16];
-    chacha_block(K, cha_block_of(p), b);
+    cha_block_any(K, cha_block_of(p), b);
     return cha_pick(b, (uint32_t)(p.lo & 7));
 }
 
@@ -152,7 +186,7 @@ __host__ __device__ __forceinline__ uint64_t cha_out_cached(const ChaKey &K, Cha
     const u128 p = cha_prev(s);
     const uint64_t blk = cha_block_of(p);
     if (!c.valid || blk != c.blk) {
-        chacha_block(K, blk, c.b);
+        cha_block_any(K, blk, c.b);
         c.blk = blk;
         c.valid = true;
     }
@@ -171,7 +205,7 @@ __device__ __forceinline__ uint32_t cha_win_index(uint32_t i) {  // logical word
 
 __device__ __forceinline__ void cha_fill(uint64_t *win, const ChaKey &K, u128 W0, uint32_t t) {
     uint32_t b[16];
-    chacha_block(K, cha_block_of(W0) + t, b);
+    cha_block_any(K, cha_block_of(W0) + t, b);
     uint4 *dst = reinterpret_cast<uint4 *>(win + 8 * t);
     const uint32_t sw = (t >> 1) & 3;
     dst[0 ^ sw] = make_uint4(b[0], b[1], b[2], b[3]);
@@ -224,6 +258,8 @@ __device__ __forceinline__ uint64_t cha_cta_word(uint64_t *win, const ChaKey &K,
 // key of a device stream state (state[0..3] = br_pcg64 head, state[4..7] = key words)
 __device__ __forceinline__ ChaKey cha_key_of_state(const uint64_t *state) {
     ChaKey K;
+    K.words = state[3] == WORDS_TAG ? reinterpret_cast<const uint64_t *>(state[4]) : nullptr;
+    K.nwords = state[2];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint64_t w = state[4 + i];

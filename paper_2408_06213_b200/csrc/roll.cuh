@@ -291,7 +291,10 @@ __device__ __forceinline__ void roll_cha_main(const RollArgs &a, uint64_t *win) 
     roll_range_cha<K>(a, s0, 0, a.nb, 0, false, win);
 }
 
-__device__ __forceinline__ bool roll_is_chacha(const RollArgs &a) { return a.state[3] == CHACHA_TAG; }
+// ChaCha keystreams and replayed word sequences take the position-addressed roll path
+__device__ __forceinline__ bool roll_is_chacha(const RollArgs &a) {
+    return a.state[3] == CHACHA_TAG || a.state[3] == WORDS_TAG;
+}
 
 // Which main kernel runs is the host's guess (the generator of a state buffer is known where
 // it was uploaded); the device has the final word: a main kernel that does not match the
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(256) roll_cha_kernel(RollArgs a) {
     int err = 0;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nblk; t += (int64_t)gridDim.x * blockDim.x) {
         uint32_t kb[16];
-        chacha_block(ck, blk0 + (uint64_t)t, kb);
+        cha_block_any(ck, blk0 + (uint64_t)t, kb);
         const int64_t b0 = t * 8 - q0;  // batch of word 0 of this block
 #pragma unroll
         for (int q = 0; q < 8; ++q) {

@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(16) uint64_t chawin[CM ? 256 : 2];
     bool cha = CM == 1;
-    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_mid_body<T, SEGMENTED, CM != 0>(data, num_arrays, plan, zbytes, run_seed, base, words32, state_io,
                                                 words64, rk_first, use_tma, gen, smem_raw, segs, ring, predslot,
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
     __shared__ LargeShared<T, W> sh;
     __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
     bool cha = CM == 1;
-    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_cta_large_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                               rk_first, segmented, gen, sh, chawin);
@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_pipe_kernel(T *__restrict_
     PipeShared<T, W> &sh = *reinterpret_cast<PipeShared<T, W> *>(smem_raw);
     __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
     bool cha = CM == 1;
-    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_cta_pipe_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                              rk_first, segmented, gen, sh, chawin);
@@ -1120,7 +1120,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_hash_kernel(T *__restrict_
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
     bool cha = CM == 1;
-    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_cta_hash_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                              rk_first, use_tma, segmented, gen, smem_raw, sh, bar, chawin);
@@ -1330,7 +1330,7 @@ __global__ void __launch_bounds__(32 * W) shuffle_resolve_kernel(T *__restrict__
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
     bool cha = CM == 1;
-    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_resolve_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                             rk_first, use_tma, segmented, gen, smem_raw, segs, &fmin, bar, chawin);
@@ -1403,7 +1403,7 @@ __global__ void __launch_bounds__(32) shuffle_large_gen_kernel(int64_t num_array
     for (uint32_t q = lane; q < plan.nseg; q += 32) segs[q] = plan.segs[q];
     __syncwarp();
     bool cha = CM == 1;
-    if constexpr (CM == 2) cha = is_chacha(mk128(state_io[2], state_io[3]));
+    if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_large_gen_body<SEGMENTED, CM != 0>(num_arrays, plan, run_seed, base, J, words32, state_io, words64,
                                                    rk_first, gen, segs, chawin);

@@ -837,3 +837,52 @@ def test_dropin_edge_cases(B, O):
     s = B.Pcg64Source(4)
     r = B.roll_batch(s, B.BatchSpec(B.RadixBases.of((1 << 16,) * 4)))
     assert r == B.BatchResult(ro[0], ro[1], ro[2], ro[3]) and s.state == o.state
+
+
+# ------------------------------------------------------------------ replayed word sequences
+def test_fixed_sequence_source(B, O):
+    """FixedSequenceSource with 64-bit words on the device (wordsource.py:191-207): the
+    reference's own cases (test_shuffle.py:70-100), long sequences against the oracle's fixed
+    source, cursor accounting, and SourceExhausted on an over-read."""
+    z = B.shuffle_unbatched(B.FixedSequenceSource([5], 64), [0, 1])  # test_shuffle.py:68-74
+    assert z == [1, 0]
+    assert B.shuffle_unbatched(B.FixedSequenceSource([1 << 63], 64), [0, 1]) == [0, 1]
+    s = B.FixedSequenceSource([1], 64)  # test_shuffle.py:83-92: k = n = 3 ends with a self-swap
+    z = [0, 1, 2]
+    assert B.partial_shuffle_batch(s, z, 3, 3, 6) == 6 and z == [1, 2, 0] and s.cursor == 1
+    s = B.FixedSequenceSource([(1 << 64) - 1], 64)
+    assert B.shuffle_batched(s, [0, 1]) == O.shuffle_batched(O.fixed([(1 << 64) - 1]),
+                                                              np.arange(2, dtype=np.uint32)).tolist()
+    assert s.cursor == 1
+    words = O.pcg64_fill(O.pcg64(99), 0, 5000).tolist()
+    for n, sched in ((1000, None), (4000, None), (3000, "pair")):
+        s = B.FixedSequenceSource(words, 64)
+        s.next_word()  # start one word in
+        o = O.fixed(words)
+        O.next_word(o)
+        entries = [(1 << 30, 2)] if sched == "pair" else None
+        z = np.arange(n, dtype=np.uint32)
+        if entries:
+            B.shuffle_batched(s, z, B.PAIR_SCHEDULE)
+            ref = O.shuffle_batched(o, np.arange(n, dtype=np.uint32), entries)
+        else:
+            B.shuffle_batched(s, z)
+            ref = O.shuffle_batched(o, np.arange(n, dtype=np.uint32))
+        assert np.array_equal(z, ref) and s.cursor == o.cursor, (n, B.last_kernel())
+    # bulk rolls and fill from a replayed sequence
+    s = B.FixedSequenceSource(words, 64)
+    o = O.fixed(words)
+    bounds = O.gen_bounds(4, 2 * 1500)
+    r = B.roll_batches(s, dev_u32(bounds), 2)
+    rolls, wds, _, _ = O.roll_batches(o, bounds, 2)
+    assert np.array_equal(u32(r.rolls), rolls) and s.cursor == o.cursor
+    # over-read: SourceExhausted, host payload untouched, cursor at the end (wordsource.py:203-204)
+    s = B.FixedSequenceSource(words[:100], 64)
+    z = list(range(1000))
+    with pytest.raises(B.SourceExhausted):
+        B.shuffle_batched(s, z)
+    assert z == list(range(1000)) and s.cursor == 100
+    with pytest.raises(TypeError):
+        B.shuffle_batched(B.FixedSequenceSource([1, 2, 3], 16), [1, 2, 3], B.ShuffleSchedule(((1 << 4, 2),), 2, 16))
+    with pytest.raises(TypeError):
+        B.shuffle_batched(B.ExhaustiveSource(8), [1, 2, 3], B.ShuffleSchedule(((8, 2),), 2, 8))
