@@ -226,8 +226,7 @@ def test_chacha_position_mapping():
 
 
 def test_public_api_covers_the_reference():
-    """Every public name of the reference package (batchrand/__init__.py) exists here, except
-    the two host-only word sources the device path does not draw from (8(b))."""
+    """Every public name of the reference package (batchrand/__init__.py) exists here."""
     import paper_2408_06213_b200 as B
 
     names = ["BatchRandError", "BatchResult", "BatchSpec", "BoundEncoding", "BoundOverflow", "ChaChaSource",
@@ -237,7 +236,8 @@ def test_public_api_covers_the_reference():
              "build_schedule", "chacha_block", "cost_per_roll", "decode", "default_schedule", "digit_pass", "encode",
              "falling_factorial", "find_nk", "make_source", "mul_full", "partial_shuffle_batch", "roll_batch",
              "roll_batch_known_threshold", "roll_batch_naive", "roll_single", "roll_single_traced",
-             "shuffle_batched", "shuffle_naive_batched", "shuffle_unbatched", "threshold"]
+             "shuffle_batched", "shuffle_naive_batched", "shuffle_unbatched", "threshold", "FixedSequenceSource",
+             "ExhaustiveSource"]
     assert [n for n in names if not hasattr(B, n)] == []
     rb = B.RadixBases.of((4, 3, 5))
     assert B.decode(37, rb) == (2, 1, 2) and B.encode((2, 1, 2), rb) == 37  # mixed_radix.py:40-67
