@@ -167,6 +167,15 @@ int br_roll_batches_naive(const uint32_t *bounds_dev, int k, int64_t num_batches
  * be NULL) receives the words consumed beyond one per batch (rejections). */
 int br_roll_check(void *workspace_dev, void *stream, uint64_t *extra_words);
 
+/* One roll_batch (batched.py:102-123) with 64-bit bases -- any base below 2^64, product at
+ * most 2^64 -- on the stream in *state_dev (any generator kind; advanced in place), or, with
+ * state_dev NULL, one digit_pass (batched.py:69-82) of the word *r0_dev.  out_dev receives
+ * k + 3 u64: the digits, the words consumed, threshold_computed (0/1), the final remainder.
+ * A base of 0 encodes 2^64 (the full range, bounded.py:35-56).  The bulk entry points take
+ * u32 bounds; this is the drop-in path for wider ones. */
+int br_roll_batch64(const uint64_t *bases_dev, int k, br_pcg64 *state_dev, const uint64_t *r0_dev,
+                    uint64_t *out_dev, void *stream);
+
 /* batched.py:69-82 digit_pass over many words (no generator): for word i with bases
  * bounds[i*k:(i+1)*k] (u32), digits[i*k+m] and the final remainder rk[i] (rk may be NULL). */
 int br_digit_pass(const uint64_t *words_dev, const uint32_t *bounds_dev, int k, int64_t count,

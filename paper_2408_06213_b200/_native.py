@@ -69,6 +69,7 @@ PROTOTYPES = {
     "br_roll_batches_naive": (C.c_int, [vp, C.c_int, i64, vp, vp, vp, vp, vp, vp, vp]),
     "br_roll_check": (C.c_int, [vp, vp, P(u64)]),
     "br_digit_pass": (C.c_int, [vp, vp, C.c_int, i64, vp, vp, vp]),
+    "br_roll_batch64": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
     "br_shuffle_stream": (C.c_int, [vp, C.c_int, u64, vp, P(Regime), C.c_int, C.c_int, vp, vp]),
     "br_shuffle_stream_segments": (C.c_int, [vp, C.c_int, u64, vp, P(Segment), C.c_int, vp, vp, vp]),
     "br_shuffle_segmented": (C.c_int, [vp, C.c_int, i64, u64, u64, i64, P(Regime), C.c_int, C.c_int, vp, vp]),

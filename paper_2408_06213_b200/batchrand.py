@@ -457,11 +457,35 @@ def _device_bases(bases, torch):
     return torch.from_numpy(host).cuda()
 
 
+def _wide64(torch, values):
+    """u64 values (2^64 encoded as 0) as an int64 CUDA tensor."""
+    vals = [v & MASK64 for v in values]
+    return torch.tensor([v - (1 << 64) if v >= 1 << 63 else v for v in vals], dtype=torch.int64, device="cuda")
+
+
+def _roll_one64(source, bases) -> BatchResult:
+    """One batch with a base of 2^32 or more: br_roll_batch64 (one device thread, 64-bit
+    bases; a base of 2^64 travels as 0, the full range)."""
+    torch = _torch()
+    st = _state_struct(source)
+    dstream = DeviceStream.from_struct(st)
+    b = _wide64(torch, bases)
+    out = torch.empty(len(bases) + 3, dtype=torch.int64, device="cuda")
+    N.check(N.lib().br_roll_batch64(_ptr(b), len(bases), _ptr(dstream.state), None, _ptr(out), _stream_ptr(torch)),
+            "roll_batch")
+    dstream.write_back(source)
+    v = [int(x) & MASK64 for x in out.cpu().tolist()]
+    k = len(bases)
+    return BatchResult(tuple(v[:k]), v[k], bool(v[k + 1]), v[k + 2])
+
+
 def _roll_one(source, spec: BatchSpec) -> BatchResult:
     torch = _torch()
     bases = spec.bases.bases
     if spec.bases.bits != 64:
         raise TypeError("the device path needs 64-bit words")
+    if any(b >= 1 << 32 for b in bases):
+        return _roll_one64(source, bases)
     st = _state_struct(source)
     dstream = DeviceStream.from_struct(st)
     b = _device_bases(bases, torch)
@@ -476,6 +500,13 @@ def digit_pass(r0: int, bases: RadixBases):
     torch = _torch()
     if bases.bits != 64:
         raise TypeError("the device path needs 64-bit words")
+    if any(b >= 1 << 32 for b in bases.bases):
+        k = len(bases.bases)
+        out = torch.empty(k + 3, dtype=torch.int64, device="cuda")
+        b, w = _wide64(torch, bases.bases), _wide64(torch, [r0])  # alive until the result is read
+        N.check(N.lib().br_roll_batch64(_ptr(b), k, None, _ptr(w), _ptr(out), _stream_ptr(torch)), "digit_pass")
+        v = [int(x) & MASK64 for x in out.cpu().tolist()]
+        return tuple(v[:k]), v[k + 2]
     w = torch.tensor([r0 - (1 << 64) if r0 >= 1 << 63 else r0], dtype=torch.int64).cuda()
     d, rk = digit_pass_many(w, _device_bases(bases.bases, torch), len(bases.bases))
     return tuple(int(x) & 0xFFFFFFFF for x in d.cpu().tolist()), int(rk[0]) & MASK64

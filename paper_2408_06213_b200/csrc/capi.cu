@@ -262,6 +262,68 @@ __global__ void cha_fill_kernel(uint64_t *__restrict__ out, int64_t count, ChaKe
     }
 }
 
+// One batch with 64-bit bases (batched.py:69-123 with bases up to 2^64, product <= 2^64,
+// checked by the caller): the sequential roll_batch on one thread, any generator kind.  The
+// bulk kernels take u32 bounds; this is the drop-in path for wider bases (roll_single with a
+// bound above 2^32, RadixBases with a base above 2^32).  With state == nullptr it is a plain
+// digit pass of the word *r0 (digit_pass).  out: digits[k], words, threshold_computed, rk.
+__global__ void roll_one64_kernel(const uint64_t *__restrict__ bases, int k, uint64_t prod, int full,
+                                  uint64_t *state, const uint64_t *r0, uint64_t *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const bool stream = state != nullptr;
+    u128 s = mk128(0, 0), inc = mk128(0, 0);
+    bool pos = false, lh = false;
+    ChaKey ck;
+    ChaCursor cur;
+    cur.valid = false;
+    if (stream) {
+        s = mk128(state[0], state[1]);
+        inc = mk128(state[2], state[3]);
+        pos = is_posgen(inc);
+        lh = is_lehmer(inc);
+        if (pos) ck = cha_key_of_state(state);
+    }
+    uint64_t words = 0, r = 0, t = 0;
+    bool tc = false;
+    for (;;) {
+        uint64_t w;
+        if (!stream) {
+            w = *r0;
+        } else if (pos) {
+            s = cha_add(s, 1);
+            w = cha_out_cached(ck, cur, s);
+        } else {
+            w = gen_next(s, inc, lh);
+        }
+        ++words;
+        r = w;
+        for (int m = 0; m < k; ++m) {
+            const uint64_t b = bases[m];
+            if (b == 0) {  // the base 2^64 (alone in a batch): digit = r, remainder 0
+                out[m] = r;
+                r = 0;
+            } else {
+                out[m] = __umul64hi(b, r);
+                r = b * r;
+            }
+        }
+        if (!stream) break;
+        if (words == 1) {  // batched.py:116-119: the threshold only if r_k < product
+            if (!full && r >= prod) break;
+            tc = true;
+            t = full ? 0 : (0 - prod) % prod;
+        }
+        if (r >= t) break;
+    }
+    out[k] = words;
+    out[k + 1] = tc ? 1 : 0;
+    out[k + 2] = r;
+    if (stream) {
+        state[0] = s.hi;
+        state[1] = s.lo;
+    }
+}
+
 // position-addressed streams (ChaCha keystream or replayed words): 64-byte states
 inline bool host_is_chacha(const br_pcg64 *st) { return st->inc_lo == CHACHA_TAG || st->inc_lo == WORDS_TAG; }
 
@@ -835,6 +897,30 @@ int br_digit_pass(const uint64_t *words, const uint32_t *bounds, int k, int64_t 
     digit_pass_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(words, bounds, k, count, digits, rk);
     CK(cudaGetLastError());
     g_kernel = "digit_pass_kernel";
+    return BR_OK;
+}
+
+int br_roll_batch64(const uint64_t *bases_dev, int k, br_pcg64 *state_dev, const uint64_t *r0_dev,
+                    uint64_t *out_dev, void *stream) {
+    if (k < 1 || k > 64) return fail(BR_E_INVALID, "1 <= k <= 64 bases");
+    if (!bases_dev || !out_dev || (!state_dev && !r0_dev)) return fail(BR_E_INVALID, "null pointer argument");
+    int dev;
+    DeviceInfo di;
+    int s = ensure_device(&dev, &di);
+    if (s) return s;
+    std::vector<uint64_t> b(k);
+    CK(cudaMemcpyAsync(b.data(), bases_dev, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    h128 prod = 1;
+    for (int m = 0; m < k; ++m) {  // mixed_radix.py:28-35: product <= 2^64 (a 0 here encodes 2^64)
+        prod *= b[m] ? (h128)b[m] : ((h128)1 << 64);
+        if (prod > ((h128)1 << 64)) return fail(BR_E_BOUND_OVERFLOW, "product of the bases exceeds 2^64");
+    }
+    const int full = prod == ((h128)1 << 64) ? 1 : 0;
+    roll_one64_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(bases_dev, k, (uint64_t)prod, full, (uint64_t *)state_dev,
+                                                          r0_dev, out_dev);
+    CK(cudaGetLastError());
+    g_kernel = "roll_one64_kernel";
     return BR_OK;
 }
 

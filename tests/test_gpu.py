@@ -886,3 +886,35 @@ def test_fixed_sequence_source(B, O):
         B.shuffle_batched(B.FixedSequenceSource([1, 2, 3], 16), [1, 2, 3], B.ShuffleSchedule(((1 << 4, 2),), 2, 16))
     with pytest.raises(TypeError):
         B.shuffle_batched(B.ExhaustiveSource(8), [1, 2, 3], B.ShuffleSchedule(((8, 2),), 2, 8))
+
+
+def test_wide_bases_single_batches(B, O):
+    """roll_single / roll_batch / digit_pass with bases at or above 2^32, up to the full range
+    2^64 (bounded.py:35-104, batched.py:69-123): the one-thread 64-bit path."""
+    cases = [(1 << 40,), ((1 << 64) - 1,), (1 << 63, 2), (3 << 33, 1 << 20, 7), ((1 << 32) + 15, (1 << 31) - 1)]
+    for seed, bases in enumerate(cases):
+        s, o = B.Pcg64Source(seed), O.pcg64(seed)
+        spec = B.BatchSpec(B.RadixBases.of(bases))
+        for _ in range(30):
+            r = B.roll_batch(s, spec)
+            ro = O.roll_batch(o, bases)
+            assert (r.digits, r.words_consumed, r.threshold_computed, r.final_remainder) == ro, (bases, r, ro)
+        assert s.state == o.state
+        for r0 in (0, 1, (1 << 64) - 1, 0x123456789ABCDEF0):
+            assert B.digit_pass(r0, B.RadixBases.of(bases)) == O.digit_pass(r0, bases)
+    for gen in ("pcg64", "lehmer", "chacha"):  # bound 2^64 is the full range (the word itself)
+        s, o = B.make_source(gen, 5), O.GENERATOR_MAKERS[gen](5)
+        for bound in (1 << 33, (1 << 64) - 12345, 1 << 64):
+            for _ in range(10):
+                v, w, ro = O.roll_single(o, bound)
+                r = B.roll_single_traced(s, bound)
+                assert (r.value, r.words_consumed, r.remainder_ops) == (v, w, ro)
+    # heavy rejection: 2^63 + 1 rejects about half of all words
+    s, o = B.Pcg64Source(77), O.pcg64(77)
+    rej = 0
+    for _ in range(50):
+        v, w, ro = O.roll_single(o, (1 << 63) + 1)
+        r = B.roll_single_traced(s, (1 << 63) + 1)
+        assert (r.value, r.words_consumed, r.remainder_ops) == (v, w, ro)
+        rej += w - 1
+    assert rej > 5 and s.state == o.state
