@@ -69,11 +69,20 @@ def sharded_rolls(seed_state: tuple[int, int], total_batches: int, world: int, r
     first, count = even_split(total_batches, world, rank)
     state = advanced_state(seed_state[0], seed_state[1], first)
     res, extra = roll(state, first, count)
-    extras = all_gather_ints(extra, group, device)
-    d = rejection_prefix(extras, rank)
-    recomputed = False
-    if d:
-        state = advanced_state(seed_state[0], seed_state[1], first + d)
-        res, _ = roll(state, first, count)
-        recomputed = True
+    d, recomputed = 0, False
+    # A shifted rank re-rolls, which can change its own extra count and so the shift of the
+    # ranks after it: iterate to the fixed point (at most `world` rounds; rank 0 never
+    # moves, and each round fixes at least the next rank's prefix).  One round when nothing
+    # was rejected.
+    for _ in range(world):
+        extras = all_gather_ints(extra, group, device)
+        nd = rejection_prefix(extras, rank)
+        moved = nd != d
+        if moved:
+            d = nd
+            state = advanced_state(seed_state[0], seed_state[1], first + d)
+            res, extra = roll(state, first, count)
+            recomputed = True
+        if not any(all_gather_ints(int(moved), group, device)):
+            break
     return res, first, count, d, recomputed

@@ -34,13 +34,9 @@ def _worker(rank, world, port, mode, out_dir):
 
     from paper_2408_06213_b200 import shard
 
-    if mode == "rolls":
+    if mode in ("rolls", "rolls3"):
         nb = 6000
-        rng = np.random.default_rng(0)
-        bounds = rng.integers(2, 1 << 16, 2 * nb, dtype=np.uint32)
-        # a few heavy batches on rank 0's section force cross-rank shifts
-        bounds[0:40:2] = 0xFFFFFFFF
-        bounds[1:40:2] = 3006477107
+        bounds = _roll_bounds(nb, mode == "rolls3")
         seed_state = shard.seeded_state(O.array_seed(7, 1))
 
         def roll(state, first, count):
@@ -60,10 +56,24 @@ def _worker(rank, world, port, mode, out_dir):
     dist.destroy_process_group()
 
 
-def _run(mode, tmp_path):
+def _roll_bounds(nb, cascade):
+    rng = np.random.default_rng(0)
+    bounds = rng.integers(2, 1 << 16, 2 * nb, dtype=np.uint32)
+    # heavy batches (~30% rejection) on rank 0's section force cross-rank shifts; with
+    # `cascade` the middle rank's section has them too, so its re-roll changes its own
+    # rejection count and the last rank's shift needs a second round
+    spans = [(0, 40)] + ([(2 * 2000, 2 * 2000 + 400)] if cascade else [])
+    for a, b in spans:
+        bounds[a:b:2] = 0xFFFFFFFF
+        bounds[a + 1:b:2] = 3006477107
+    return bounds
+
+
+def _run(mode, tmp_path, world=2):
     port = _free_port()
-    mp.start_processes(_worker, args=(2, port, mode, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
-    return [np.load(tmp_path / f"r{r}.npz") for r in range(2)]
+    mp.start_processes(_worker, args=(world, port, mode, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    return [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
 
 
 def test_even_split():
@@ -87,11 +97,20 @@ def test_sharded_segmented_equals_single_process(tmp_path, O):
 def test_sharded_roll_stream_equals_single_stream(tmp_path, O):
     parts = _run("rolls", tmp_path)
     nb = 6000
-    rng = np.random.default_rng(0)
-    bounds = rng.integers(2, 1 << 16, 2 * nb, dtype=np.uint32)
-    bounds[0:40:2] = 0xFFFFFFFF
-    bounds[1:40:2] = 3006477107
+    bounds = _roll_bounds(nb, False)
     rolls, words, _, _ = O.roll_batches(O.pcg64(O.array_seed(7, 1)), bounds, 2)
     assert int(parts[1]["d"]) > 0 and bool(parts[1]["rec"])  # rank 1 was shifted by rank 0's rejections
+    assert np.array_equal(np.concatenate([p["rolls"] for p in parts]), rolls)
+    assert np.array_equal(np.concatenate([p["words"] for p in parts]), words)
+
+
+def test_sharded_roll_stream_cascading_shifts(tmp_path, O):
+    """Three ranks, rejections in two sections: the shifted middle rank's re-roll changes its
+    own extra count, and the last rank must follow (fixed-point rounds in sharded_rolls)."""
+    parts = _run("rolls3", tmp_path, world=3)
+    nb = 6000
+    bounds = _roll_bounds(nb, True)
+    rolls, words, _, _ = O.roll_batches(O.pcg64(O.array_seed(7, 1)), bounds, 2)
+    assert all(bool(p["rec"]) for p in parts[1:])
     assert np.array_equal(np.concatenate([p["rolls"] for p in parts]), rolls)
     assert np.array_equal(np.concatenate([p["words"] for p in parts]), words)
