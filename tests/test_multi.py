@@ -62,7 +62,7 @@ def _roll_bounds(nb, cascade):
     # heavy batches (~30% rejection) on rank 0's section force cross-rank shifts; with
     # `cascade` the middle rank's section has them too, so its re-roll changes its own
     # rejection count and the last rank's shift needs a second round
-    spans = [(0, 40)] + ([(2 * 2000, 2 * 2000 + 400)] if cascade else [])
+    spans = [(0, 40)] + ([(2 * 3800, 2 * 3800 + 300)] if cascade else [])  # rank 1 re-rolls 58 -> 63 extra
     for a, b in spans:
         bounds[a:b:2] = 0xFFFFFFFF
         bounds[a + 1:b:2] = 3006477107
