@@ -27,7 +27,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -54,51 +53,79 @@ def load_traffic():
         return {}
 
 
+_SAMPLER_SRC = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+print("ready", nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM), flush=True)
+while True:
+    print(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), int(get_r(h)), flush=True)
+    time.sleep(0.0002)
+"""
+
+
 class ClockSampler:
-    """SM clock and throttle reasons sampled (NVML, ~0.1-0.2 ms period) while the timed region
-    runs; also records the reasons nvidia-smi would show (hw_slowdown, thermal, power cap)."""
+    """SM clock and throttle reasons sampled by NVML (~0.2 ms period) while the timed region
+    runs, in a separate process so the samples keep coming while this one holds the GIL or
+    waits in a device synchronisation; also records the reasons nvidia-smi would show
+    (hw_slowdown, thermal, power cap)."""
 
     BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, device_index: int):
         self.dev = device_index
         self.samples = []
-        self.stop = threading.Event()
-        self.ok = False
+        self.max_sm = None
+        self.proc = None
 
     def __enter__(self):
-        try:
-            import pynvml as nv
+        import subprocess
 
-            nv.nvmlInit()
-            self.nv = nv
-            self.h = nv.nvmlDeviceGetHandleByIndex(self.dev)
-            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
-            self.ok = True
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(self._nvml_index())],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            head = self.proc.stdout.readline().split()  # blocks until NVML answers
+            if head and head[0] == "ready":
+                self.max_sm = int(head[1])
+                self.t0 = time.perf_counter()
+            else:
+                self._kill()
         except Exception:
-            self.ok = False
+            self._kill()
         return self
 
-    def _run(self):
-        nv = self.nv
-        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        while not self.stop.is_set():
+    def _nvml_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
             try:
-                self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), int(get_r(self.h))))
-            except Exception:
+                return int(vis.split(",")[self.dev])
+            except (ValueError, IndexError):
                 pass
-            time.sleep(0.0001)
+        return self.dev
+
+    def _kill(self):
+        if self.proc is not None:
+            self.proc.kill()
+            self.proc.wait()
+            self.proc = None
 
     def __exit__(self, *a):
-        self.stop.set()
-        if self.ok:
-            self.t.join(timeout=2)
+        if self.proc is None:
+            return
+        self.proc.kill()
+        out, _ = self.proc.communicate()
+        self.proc = None
+        for line in out.splitlines():
+            try:
+                c, r = line.split()
+                self.samples.append((int(c), int(r)))
+            except ValueError:
+                pass
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_sm", None), "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": [], "samples": 0}
         reasons = sorted({k for _, r in self.samples for k, b in self.BITS.items() if r & b})
         return {"sm_mhz": statistics.median(c for c, _ in self.samples), "sm_max_mhz": self.max_sm,
                 "reasons": reasons, "samples": len(self.samples)}
@@ -505,7 +532,7 @@ def main():
         for key in ("c3", "c4", "c5"):
             if key != args.config:
                 sec[key] = bench_shuffle(SHUFFLE_CFG[key], args, torch, B, ws, rank,
-                                         steps=min(args.steps, 3 if key == "c5" else 10))
+                                         steps={"c3": args.steps, "c4": min(args.steps, 10)}.get(key, min(args.steps, 3)))
         if ws == 1:
             sec["c1"] = bench_c1(args, torch, B)
         line["secondary"] = sec
