@@ -58,6 +58,7 @@ import sys, time, pynvml as nv
 nv.nvmlInit()
 h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
 get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), get_r(h)  # warm the query path
 print("ready", nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM), flush=True)
 while True:
     print(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), int(get_r(h)), flush=True)
@@ -88,7 +89,10 @@ class ClockSampler:
             head = self.proc.stdout.readline().split()  # blocks until NVML answers
             if head and head[0] == "ready":
                 self.max_sm = int(head[1])
-                self.t0 = time.perf_counter()
+                # the loop is running once its first sample is out; later ones fall in the region
+                first = self.proc.stdout.readline().split()
+                if len(first) != 2:
+                    self._kill()
             else:
                 self._kill()
         except Exception:
