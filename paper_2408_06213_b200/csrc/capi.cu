@@ -359,6 +359,7 @@ std::map<const void *, bool> g_is_chacha;
 
 void note_state_kind(const void *dev, bool chacha) {
     std::lock_guard<std::mutex> lk(g_kind_mu);
+    if (g_is_chacha.size() >= 65536) g_is_chacha.clear();  // only a hint: forgetting is safe
     g_is_chacha[dev] = chacha;
 }
 
