@@ -558,7 +558,10 @@ __global__ void __launch_bounds__(32) shuffle_mid_kernel(T *__restrict__ data, i
 // the serial chain per array is n/G groups instead of n/32, and W warps share the target
 // generation.  Groups with three or more lanes on one target, and the bottom of the array
 // (where such groups are common), fall back to warp groups run by warp 0.
-static constexpr uint32_t CRING = 2048;
+#ifndef BR_CRING
+#define BR_CRING 2048
+#endif
+static constexpr uint32_t CRING = BR_CRING;
 
 template <int W>
 struct CtaGen {
@@ -1028,7 +1031,10 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_pipe_kernel(T *__restrict_
 
 // Shared-memory-resident arrays with the same hashed CTA groups: payload moved by TMA bulk
 // copies, targets in a u16 ring, 1024-slot lane-chain hash.
-static constexpr int HASH_HB = 10;
+#ifndef BR_HASH_HB
+#define BR_HASH_HB 10
+#endif
+static constexpr int HASH_HB = BR_HASH_HB;
 
 template <typename T, int W, bool CHA>
 __device__ __forceinline__ void shuffle_cta_hash_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
