@@ -407,6 +407,7 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
         // always fits once the main kernel it waits for has drained, so a plain launch is used
         // (1.8 us less per call than the cooperative attribute, which BR_ROLL_FIXUP=cooperative
         // restores).
+        if (di.sms * (threads / 32) > ROLL_MAX_WARPS) return fail(BR_E_UNSUPPORTED, "more SMs than the roll workspace covers");
         RollArgs b = a;
         void *args[] = {&b};
         cudaLaunchConfig_t cfg = {};
@@ -884,9 +885,9 @@ int br_roll_batches_naive(const uint32_t *bounds, int k, int64_t nb, br_pcg64 *s
 
 int br_roll_check(void *ws, void *stream, uint64_t *extra_words) {
     if (!ws) return fail(BR_E_INVALID, "null workspace");
-    RollWs h;
+    RollWs h;  // the header only (the fixup's per-warp records are scratch)
     CK(cudaStreamSynchronize((cudaStream_t)stream));
-    CK(cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&h, ws, offsetof(RollWs, rec), cudaMemcpyDeviceToHost));
     if (extra_words) *extra_words = h.extra;
     if (h.error) {
         unsigned zero = 0;

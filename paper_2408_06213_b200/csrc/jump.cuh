@@ -70,6 +70,23 @@ __device__ __forceinline__ u128 gen_jump(u128 s, u128 inc, uint64_t d, bool lh) 
     return s;
 }
 
+// the affine map of a d-word jump: state' = A * state + C
+__device__ __forceinline__ void gen_affine(uint64_t d, u128 inc, bool lh, u128 &A, u128 &C) {
+    u128 a = mk128(0, 1), g = mk128(0, 0);
+    int k = 0;
+    while (d) {
+        if (d & 1) {
+            const u128 Ak = lh ? c_LA[k] : c_A[k];
+            a = mul128(a, Ak);
+            g = mad128(g, Ak, c_G[k]);
+        }
+        d >>= 1;
+        ++k;
+    }
+    A = a;
+    C = mul128(g, inc);
+}
+
 __device__ __forceinline__ u128 gen_jump_small(u128 s, u128 inc, int d, bool lh) {
     return mad128(s, lh ? g_LSA[d] : g_SA[d], mul128(g_SG[d], inc));
 }

@@ -22,6 +22,9 @@
 
 namespace br {
 
+// the fixup kernel runs one 256-thread block per SM: at most this many warps (256 SMs)
+constexpr int ROLL_MAX_WARPS = 2048;
+
 struct RollWs {
     unsigned long long neg_first;  // ~(first rejected batch); 0 = none
     unsigned long long D;          // shift published by the fixup resolver
@@ -32,6 +35,15 @@ struct RollWs {
     unsigned int main_done;  // 1: this call's main kernel rolled the stream (else the fixup does)
     unsigned int pad[2];
     unsigned long long final_hi, final_lo;  // state after nb words (no-rejection case), by the main kernel
+    unsigned long long q[3];  // fixup iteration i records its first rejection in q[i % 3]; all 0 between calls
+    unsigned long long prof[4];  // BR_FIXUP_PROF builds: block 0's ns in re-run / barrier / record reads, iterations
+    // Per-warp resolutions of the fixup (iteration i writes rec[i % 2]): the first rejected
+    // batch a warp met in its round, already re-drawn by the lane that met it
+    struct Rec {
+        unsigned long long extra;  // words beyond the first
+        unsigned long long hi, lo;  // PCG64 / Lehmer: the state whose output is the next batch's word
+        unsigned long long pad;
+    } rec[2][ROLL_MAX_WARPS];
 };
 
 // Programmatic dependent launch: the main kernel lets the fixup kernel be scheduled early;
@@ -529,22 +541,181 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
     if (nchunks * CH < a.nb) roll_range<K, 1>(a, s0, inc, nchunks * CH, a.nb, 0, false);
 }
 
+// Fixup re-run of batches [begin, end) at shift D (batch b uses word b + D), front first:
+// round r gives each warp one chunk of CHK = 32*U consecutive batches out of the nwarps*CHK
+// batches that follow begin + r*nwarps*CHK, so once a rejection is recorded in `slot`, every
+// warp stops after the round it is in.  (With one contiguous range per warp, each warp would
+// roll ~1/rejection-rate batches of its own range before the first rejection is known: about
+// nwarps/rate batches per resolved rejection, measured 40 us each at a rate of 1e-3.)
+template <bool CHA, int K>
+struct FrontPlan {
+    static constexpr int U = CHA ? (K <= 2 ? 8 : 4) : 4;
+    static constexpr int64_t CHK = 32 * U;
+    u128 AL, CL;    // word offset warp*CHK + lane (the lane's first batch of a round)
+    u128 AS, CS;    // one round: nwarps*CHK words
+    u128 A32, C32;  // one sub-step: 32 words
+};
+
+// once per fixup kernel (PCG64 / Lehmer streams)
+template <bool CHA, int K>
+__device__ __forceinline__ FrontPlan<CHA, K> front_plan(u128 inc, bool lh) {
+    FrontPlan<CHA, K> p{};
+    if constexpr (!CHA) {
+        const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        gen_affine((uint64_t)(warp * p.CHK + (threadIdx.x & 31)), inc, lh, p.AL, p.CL);
+        gen_affine((uint64_t)(nwarps * p.CHK), inc, lh, p.AS, p.CS);
+        p.A32 = gen_SA(lh, 32);
+        p.C32 = mul128(g_SG[32], inc);
+    }
+    return p;
+}
+
+// sb: (PCG64 / Lehmer) the state whose output is word begin + D
+// A warp's first rejected batch is re-drawn on the spot by the lane that met it (outputs
+// written, result in the warp's record), and the warp stops: the grid-wide first rejection
+// is some warp's first, so after the barrier every block finds its resolution in one record.
+template <int K, bool CHA>
+__device__ __forceinline__ void redraw_lane(const RollArgs &a, u128 s0, u128 inc, bool lh, u128 st, int64_t b,
+                                            uint64_t D, RollWs::Rec *rec) {
+    const uint64_t widx = (uint64_t)b + D + 1;
+    uint32_t bb[K];
+    load_bounds<K>(a.bounds + b * K, bb);  // cached: the lane just read them
+    ChaKey ck;
+    ChaCursor cc;
+    cc.valid = false;
+    if constexpr (CHA) {
+        ck = cha_key_of_state(a.state);
+        st = cha_add(s0, widx + 1);
+    } else {
+        st = mad128(st, gen_mult(lh), inc);  // st output word b + D: now word widx
+    }
+    uint64_t extra = 1;
+    for (;;) {
+        uint32_t d[K];
+        uint64_t r;
+        uint8_t tc;
+        int err = 0;
+        const uint64_t w = CHA ? cha_out_cached(ck, cc, st) : gen_out(st, lh);
+        if (eval_batch<K>(bb, w, d, r, tc, err, a.naive != 0) != 1) {
+            store_rolls<K>(a.rolls + b * K, d);
+            a.words[b] = (uint8_t)(1 + extra > 255 ? 255 : 1 + extra);
+            if (a.flags) a.flags[b] = 1;
+            if (a.rk) a.rk[b] = r;
+            break;
+        }
+        ++extra;
+        st = CHA ? cha_add(st, 1) : mad128(st, gen_mult(lh), inc);
+    }
+    if constexpr (!CHA) st = mad128(st, gen_mult(lh), inc);
+    rec->extra = extra;
+    rec->hi = st.hi;
+    rec->lo = st.lo;
+}
+
+template <int K, bool CHA>
+__device__ __forceinline__ void roll_front(const RollArgs &a, u128 s0, u128 inc, u128 sb, const FrontPlan<CHA, K> &fp,
+                                           bool lh, int64_t begin, int64_t end, uint64_t D,
+                                           unsigned long long *slot, RollWs::Rec *recs, uint64_t *win) {
+    constexpr int U = FrontPlan<CHA, K>::U;
+    constexpr int64_t CHK = FrontPlan<CHA, K>::CHK;
+    const uint32_t lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t stride = nwarps * CHK;
+    int64_t c0 = begin + warp * CHK;
+    if (c0 >= end) return;  // warp-uniform
+    volatile unsigned long long *vslot = slot;
+    u128 s, W0;
+    ChaKey ck;
+    if constexpr (CHA) {
+        ck = cha_key_of_state(a.state);
+        W0 = cha_win_unset(cha_add(s0, (uint64_t)c0 + D));
+    } else {
+        s = mad128(sb, fp.AL, fp.CL);  // lane state: word c0 + D + lane
+    }
+    int err = 0;
+    uint32_t cur[U][K], nxt[U][K];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t b = c0 + 32 * u + lane;
+        if (b < end) load_bounds<K>(a.bounds + b * K, cur[u]);
+    }
+    for (; c0 < end; c0 += stride) {
+        unsigned long long nf = lane == 0 ? *vslot : 0ull;
+        nf = __shfl_sync(0xFFFFFFFFu, nf, 0);
+        if (nf != 0 && (int64_t)(~nf) < c0) break;  // an earlier rejection supersedes this round
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = c0 + stride + 32 * u + lane;
+            if (b < end) load_bounds<K>(a.bounds + b * K, nxt[u]);
+        }
+        u128 st = s;
+        bool hit = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = c0 + 32 * u + lane;
+            if (c0 + 32 * u >= end) break;  // warp-uniform
+            uint64_t w;
+            if constexpr (CHA) w = cha_warp_word(win, ck, W0, cha_add(s0, (uint64_t)b + D), lane);
+            else w = gen_out(st, lh);
+            int res = 0;
+            if (b < end) {
+                uint32_t d[K];
+                uint64_t r;
+                uint8_t tc = 0;
+                res = eval_batch<K>(cur[u], w, d, r, tc, err, a.naive != 0);
+                store_rolls<K>(a.rolls + b * K, d);
+                a.words[b] = 1;
+                if (a.flags) a.flags[b] = tc;
+                if (a.rk) a.rk[b] = r;
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, res == 1);
+            if (m) {
+                if (lane == (uint32_t)(__ffs(m) - 1)) {
+                    atomicMax(slot, ~(unsigned long long)b);
+                    redraw_lane<K, CHA>(a, s0, inc, lh, st, b, D, &recs[warp]);
+                }
+                hit = true;
+                break;
+            }
+            if constexpr (!CHA) st = mad128(st, fp.A32, fp.C32);
+        }
+        if (hit) break;
+        if constexpr (!CHA) s = mad128(s, fp.AS, fp.CS);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < K; ++m) cur[u][m] = nxt[u][m];
+    }
+    if (err) set_error(a.ws, err);
+}
+
 // grid-wide barrier for the cooperative fixup kernel (co-residency guaranteed by
 // cudaLaunchCooperativeKernel)
+// Arrival is a release add on the count, departure an acquire read of the generation: the
+// block's writes (ordered before thread 0 by bar.sync, carried by the release's cumulativity)
+// are visible to every block that leaves.  The last arriver resets the count and bumps the
+// generation with release semantics.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void grid_barrier(RollWs *ws) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned *gen = &ws->bar_gen;
-        unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(&ws->bar_count, 1u) == gridDim.x - 1) {
+        const unsigned g = ld_acquire_u32(&ws->bar_gen);
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&ws->bar_count) : "memory");
+        if (old == gridDim.x - 1) {
             ws->bar_count = 0;
-            __threadfence();
-            atomicAdd(&ws->bar_gen, 1u);
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ws->bar_gen) : "memory");
         } else {
-            while (*gen == g) __nanosleep(64);
+            while (ld_acquire_u32(&ws->bar_gen) == g) {
+            }
         }
-        __threadfence();
     }
     __syncthreads();
 }
@@ -562,53 +733,115 @@ __device__ __forceinline__ void roll_fixup_body(const RollArgs &a, uint64_t *win
         if (leader) { ws->neg_first = 0; ws->extra = 0; }
         return;
     }
+    // One grid barrier per resolved rejection.  Iteration i: every block re-draws the rejected
+    // batch itself (same words, same answer; block 0 writes it), re-rolls the tail front first
+    // recording the next rejection in q[i % 3], and meets the others at the barrier.  q[(i+1) % 3]
+    // is cleared during iteration i: every block read it (as q[(i-2) % 3]) before barrier i-1.
+    __shared__ unsigned long long sh_D;
+    __shared__ u128 sh_base;
     unsigned long long nf = vws->neg_first;
     uint64_t D = 0;
+    int it = 0;
+    FrontPlan<CHA, K> fp;
+    u128 base = s0;  // PCG64 / Lehmer: the state whose output is word cur + 1 + D
+    int64_t cur = 0;
     if (nf != 0) {
-        for (;;) {
-            grid_barrier(ws);  // every block has read nf
-            if (nf == 0) break;
-            const int64_t cur = (int64_t)(~nf);
-            if (leader) {
-                // batch `cur` rejected word cur + D: re-draw the whole batch from the next
-                // words until accepted (batched.py:120-122)
-                uint64_t widx = (uint64_t)cur + D + 1;
-                u128 st = CHA ? cha_add(s0, widx + 1) : gen_jump(s0, inc, widx + 1, lh);
-                uint32_t bb[K];
-                load_bounds<K>(a.bounds + cur * K, bb);
-                uint64_t extra = 1;
-                ChaKey ck;
-                ChaCursor cc;
-                cc.valid = false;
-                if constexpr (CHA) ck = cha_key_of_state(a.state);
-                for (;;) {
-                    uint32_t d[K];
-                    uint64_t r;
-                    uint8_t tc;
-                    int err = 0;
-                    const uint64_t w = CHA ? cha_out_cached(ck, cc, st) : gen_out(st, lh);
-                    int res = eval_batch<K>(bb, w, d, r, tc, err, a.naive != 0);
-                    if (res != 1) {
+        fp = front_plan<CHA, K>(inc, lh);
+        cur = (int64_t)(~nf);
+        if (threadIdx.x == 0) {
+            // the main pass's first rejection: batch `cur` rejected word cur + D; every block
+            // re-draws it itself from the next words until accepted (batched.py:120-122), block 0
+            // writes it
+            uint64_t widx = (uint64_t)cur + 1;
+            u128 st = CHA ? cha_add(s0, widx + 1) : gen_jump(s0, inc, widx + 1, lh);
+            uint32_t bb[K];
+            load_bounds<K>(a.bounds + cur * K, bb);
+            uint64_t extra = 1;
+            ChaKey ck;
+            ChaCursor cc;
+            cc.valid = false;
+            if constexpr (CHA) ck = cha_key_of_state(a.state);
+            for (;;) {
+                uint32_t d[K];
+                uint64_t r;
+                uint8_t tc;
+                int err = 0;
+                const uint64_t w = CHA ? cha_out_cached(ck, cc, st) : gen_out(st, lh);
+                if (eval_batch<K>(bb, w, d, r, tc, err, a.naive != 0) != 1) {
+                    if (blockIdx.x == 0) {
                         store_rolls<K>(a.rolls + cur * K, d);
                         a.words[cur] = (uint8_t)(1 + extra > 255 ? 255 : 1 + extra);
                         if (a.flags) a.flags[cur] = 1;
                         if (a.rk) a.rk[cur] = r;
-                        break;
                     }
-                    ++extra;
-                    st = CHA ? cha_add(st, 1) : mad128(st, gen_mult(lh), inc);
+                    break;
                 }
-                ws->D = D + extra;
-                ws->neg_first = 0;
-                __threadfence();
+                ++extra;
+                st = CHA ? cha_add(st, 1) : mad128(st, gen_mult(lh), inc);
             }
-            grid_barrier(ws);
-            D = vws->D;
-            if constexpr (CHA) roll_range_cha<K>(a, s0, cur + 1, a.nb, D, true, win);
-            else roll_range<K, 1>(a, s0, inc, cur + 1, a.nb, D, true);
-            grid_barrier(ws);
-            nf = vws->neg_first;
+            sh_D = extra;
+            if constexpr (!CHA) sh_base = mad128(st, gen_mult(lh), inc);
         }
+        __syncthreads();
+        D = sh_D;
+        base = sh_base;
+    }
+    // One grid barrier per resolved rejection.  Iteration i re-rolls the tail after `cur` front
+    // first; the lane that meets the next rejection re-draws it (roll_front) and records it in
+    // q[i % 3] and its warp's rec[i % 2].  q[(i+1) % 3] is cleared during iteration i: every
+    // block read it (as q[(i-2) % 3]) before barrier i-1; rec[i % 2] is rewritten in iteration
+    // i+2, after every block has read it and reached barrier i+1.
+    constexpr int64_t CHK = FrontPlan<CHA, K>::CHK;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+#ifdef BR_FIXUP_PROF
+    uint64_t t_front = 0, t_bar = 0, t_post = 0, t0 = 0, t1 = 0;
+#define BR_PROF_T(x) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(x))
+#else
+#define BR_PROF_T(x)
+#endif
+    while (nf != 0) {
+        if (leader) ws->q[(it + 1) % 3] = 0;
+        BR_PROF_T(t0);
+        roll_front<K, CHA>(a, s0, inc, base, fp, lh, cur + 1, a.nb, D, &ws->q[it % 3], ws->rec[it & 1], win);
+        __syncthreads();
+        BR_PROF_T(t1);
+#ifdef BR_FIXUP_PROF
+        t_front += t1 - t0;
+#endif
+        grid_barrier(ws);
+        BR_PROF_T(t0);
+#ifdef BR_FIXUP_PROF
+        t_bar += t0 - t1;
+#endif
+        nf = vws->q[it % 3];
+        if (nf != 0) {
+            const int64_t nxt = (int64_t)(~nf);
+            const int64_t w = ((nxt - (cur + 1)) / CHK) % nwarps;  // the warp whose round held it
+            const volatile RollWs::Rec *r = &vws->rec[it & 1][w];
+            D += r->extra;
+            base = mk128(r->hi, r->lo);
+            cur = nxt;
+        }
+        BR_PROF_T(t1);
+#ifdef BR_FIXUP_PROF
+        t_post += t1 - t0;
+#endif
+        ++it;
+    }
+#ifdef BR_FIXUP_PROF
+    if (leader) {
+        ws->prof[0] = t_front;
+        ws->prof[1] = t_bar;
+        ws->prof[2] = t_post;
+        ws->prof[3] = it;
+    }
+#endif
+#undef BR_PROF_T
+    // every block has passed barrier it-1, so it read the initial neg_first and q[(it-2) % 3];
+    // q[(it-1) % 3] is 0 (the loop ended on it) and q[it % 3] was cleared in iteration it-1
+    if (leader && it > 0) {
+        ws->neg_first = 0;
+        ws->q[(it + 1) % 3] = 0;
     }
     if (leader) {
         if (D == 0) {

@@ -132,6 +132,34 @@ def test_roll_batches_forced_rejections(B, O, heavy_fraction):
     assert st == src.state
 
 
+@pytest.mark.parametrize("gen", ["pcg64", "lehmer", "chacha"])
+def test_roll_batches_dense_rejections(B, O, gen):
+    """Thousands of rejected batches spread over a long run (k = 5, bounds up to 4000: about
+    one batch in 1100 rejects), three calls in a row on one workspace: each fixup iteration
+    resolves one rejection and re-rolls the tail front first.  Bit-exact, and fast."""
+    import time
+    k, nb = 5, 1 << 21
+    maker = {"pcg64": O.pcg64, "lehmer": O.lehmer, "chacha": O.chacha}[gen]
+    src = maker(77)
+    ds = B.DeviceStream(77, generator=gen)
+    for call in range(3):
+        bounds = np.random.default_rng(call).integers(2, 4002, k * nb, dtype=np.uint32)
+        rolls, words, flags, rk = O.roll_batches(src, bounds, k)
+        db = dev_u32(bounds)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = B.roll_batches(ds, db, k, flags=True, final_remainder=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        assert int(words.sum()) - nb > 1000  # the rejections happened
+        assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words), (gen, call)
+        assert np.array_equal(r.flags.cpu().numpy(), flags) and np.array_equal(u64(r.final_remainder), rk)
+        st = ds.host_state()
+        pos = (st.state_hi << 64) | st.state_lo
+        assert pos == (O.chacha_position(src) if gen == "chacha" else src.state), (gen, call)
+        assert dt < 0.5, f"{gen} call {call}: {dt * 1e3:.1f} ms for ~{int(words.sum()) - nb} rejections"
+
+
 @pytest.mark.parametrize("k,nb", [(1, 50000), (1, 1 << 20), (1, 513), (2, 50001), (2, 255), (2, 1), (3, 50000),
                                   (4, 50000), (5, 50000), (6, 50000), (7, 50000), (8, 50000)])
 def test_roll_batches_k_variants(B, O, k, nb):
