@@ -19,6 +19,7 @@
 #include "jump.cuh"
 #include "roll.cuh"
 #include "shuffle.cuh"
+#include "warp_shuffle.cuh"
 
 using namespace br;
 
@@ -192,13 +193,28 @@ int get_plan(uint64_t n, const std::vector<br_segment> &segs, bool naive, Cached
         fb += s.count;
     }
     if (fb >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "too many batches");
-    size_t bytes = ds.size() * sizeof(DevSeg) + th.size() * sizeof(uint64_t) + 16;
+    // per-batch records for the warp kernel (n < 2^16): {threshold, n_b, k_b}
+    std::vector<uint32_t> br;
+    if (n < 65536) {
+        for (const br_segment &s : segs)
+            for (uint64_t c = 0; c < s.count; ++c) {
+                const uint64_t t = th[br.size() / 4];
+                br.push_back((uint32_t)t);
+                br.push_back((uint32_t)(t >> 32));
+                br.push_back((uint32_t)(s.start_n - c * s.k));
+                br.push_back(s.k);
+            }
+    }
+    size_t off = (ds.size() * sizeof(DevSeg) + 15) & ~(size_t)15;
+    const size_t boff = off + ((th.size() * sizeof(uint64_t) + 15) & ~(size_t)15);
+    size_t bytes = boff + br.size() * sizeof(uint32_t) + 16;
     void *p = nullptr;
     CK(cudaMalloc(&p, bytes));
     CK(cudaMemcpy(p, ds.data(), ds.size() * sizeof(DevSeg), cudaMemcpyHostToDevice));
-    size_t off = (ds.size() * sizeof(DevSeg) + 15) & ~(size_t)15;
     if (!th.empty())
         CK(cudaMemcpy((char *)p + off, th.data(), th.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    if (!br.empty())
+        CK(cudaMemcpy((char *)p + boff, br.data(), br.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CachedPlan cp;
     cp.dev = p;
     cp.plan.n = (uint32_t)n;
@@ -213,6 +229,7 @@ int get_plan(uint64_t n, const std::vector<br_segment> &segs, bool naive, Cached
     }
     cp.plan.segs = (const DevSeg *)p;
     cp.plan.thresh = (const uint64_t *)((char *)p + off);
+    cp.plan.brec = br.empty() ? nullptr : (const uint4 *)((char *)p + boff);
     cp.nbatches = fb;
     if (g_plans.size() >= PLAN_CACHE_MAX) {
         // bounded cache: drop every plan once the device is idle (no kernel still reads
@@ -445,6 +462,7 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
 
 constexpr uint32_t SMALL_SMEM_MAX = 64 * 1024;   // per 128-thread block
 constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
+constexpr uint32_t WARP_SMEM_MAX = 48 * 1024;    // warp kernel: several arrays per SM or none
 #ifndef LARGE_W
 #define LARGE_W 8
 #endif
@@ -461,15 +479,15 @@ constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 #define PIPE_W 8
 #endif
 
-// BR_SHUFFLE_KERNEL=small|resolve|hash|mid|pipe|large|global restricts the dispatch below to one
+// BR_SHUFFLE_KERNEL=small|resolve|warp|hash|mid|pipe|large|global restricts the dispatch below to one
 // shuffle kernel where it is eligible (tests cover every kernel; A/B timing).  Unset: the
 // first eligible kernel in the order below.
-enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL };
+enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL, K_WARP };
 int forced_kernel() {
     const char *e = getenv("BR_SHUFFLE_KERNEL");
     if (!e || !*e) return K_ANY;
-    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global"};
-    for (int i = 1; i <= K_GLOBAL; ++i)
+    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global", "warp"};
+    for (int i = 1; i <= K_WARP; ++i)
         if (!strcmp(e, names[i])) return i;
     return K_ANY;
 }
@@ -528,6 +546,21 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         return BR_OK;
     }
     const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);
+    // one warp per array (warp_shuffle.cuh): measured slower than the hash kernel on C4
+    // (2.67 vs 2.49 ms), so only on request
+    if (forced_kernel() == K_WARP && cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
+        (uint64_t)cp.plan.max_k * 32 + 32 <= WRING) {
+        auto kern = gen == 2 ? shuffle_warp_kernel<T, true, 1> : shuffle_warp_kernel<T, true, 0>;
+        const void *kp = (const void *)kern;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes));
+        const int grid = grid_for(di, kp, 32, zbytes, num_arrays);
+        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+        kern<<<grid, 32, zbytes, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
+                                       rk_first, use_tma, gen);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_warp_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
+        return BR_OK;
+    }
     const uint32_t hbytes = (uint32_t)((n + 15) & ~(uint64_t)15);  // lane-id table indexed by target
     const size_t smem = (size_t)zbytes + hbytes;
     const size_t csmem = (size_t)zbytes;  // payload only; the rest is static

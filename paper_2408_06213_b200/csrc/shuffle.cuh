@@ -42,6 +42,7 @@ struct DevPlan {
     uint32_t naive;           // pairs split by division (shuffle_naive_batched), see naive_pair
     const DevSeg *segs;       // [nseg]     (device)
     const uint64_t *thresh;   // [nbatches] (device)
+    const uint4 *brec;        // [nbatches] {threshold lo, hi, n_b, k_b} (device; plans with n < 2^16 only)
 };
 
 // shuffle.py:242-253 (shuffle_naive_batched): the pair (i, i-1), i = nb - 1, takes ONE
