@@ -45,6 +45,43 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def load_profile(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+# 7 partial products (IMAD.WIDE.U32) per C2 roll: 2 per die + a PCG64 step
+# (10) per k = 2 batch.  Peak: tools/micro/opcost.cu on B200 (profiles/opcost_r1.json).
+INT_PP_PER_ROLL = 7
+# smem bytes per element of a shared-memory-staged shuffle (algorithmic): stage in (4 B),
+# each step reads and writes z[i] and z[j] (16 B), stage out (4 B); u32 payload.
+SMEM_BYTES_PER_ELEM_U32 = 24
+
+
+def int_roofline(rolls_per_s):
+    p = load_profile("opcost_r1.json")
+    if not p:
+        return None
+    peak = p["imad_wide_per_s"] / 1e12
+    achieved = rolls_per_s * INT_PP_PER_ROLL / 1e12
+    return {"bound": "int", "achieved": achieved, "peak": peak, "unit": "T IMAD.WIDE.U32/s", "frac": achieved / peak,
+            "per_roll": INT_PP_PER_ROLL, "peak_source": "measured: profiles/opcost_r1.json (tools/micro/opcost.cu)"}
+
+
+def smem_roofline(elems_per_s):
+    p = load_profile("smem_r1.json")
+    if not p:
+        return None
+    peak = min(p["lds32_gbs"], p["sts32_gbs"])
+    achieved = elems_per_s * SMEM_BYTES_PER_ELEM_U32 / 1e9
+    return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "bytes_per_element": SMEM_BYTES_PER_ELEM_U32,
+            "peak_source": "measured: profiles/smem_r1.json (tools/micro/smem_bw.cu)"}
+
+
 def load_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -278,6 +315,8 @@ def bench_c2(args, torch, B, ws, rank):
                      "traffic": traffic,
                      "kernel": "roll_fast_kernel<2>" if args.generator != "chacha" else "roll_fixup_kernel<2>",
                      "algorithmic_bytes_per_launch": BYTES_PER_BATCH_C2 * nb, "peak_source": peak_kind},
+        # the north star's denominator for rolls: the integer multiply pipe (HBM binds first)
+        "roofline_int": int_roofline(2 * nb / t_main),
         "clocks": clk.summary(),
         "gpu_launches": 2 * K,
         "cross_rank_rejections": [int(x) for x in extras.cpu().tolist()] if ws > 1 else [int(extra.value)],
@@ -358,12 +397,15 @@ def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
     t = statistics.mean(per) / 1e3
     peak, kind = load_peaks()
     achieved = 2 * eb * n * na / t / 1e9
-    return {"workload": cfg["workload"], "value": elems / (total_ms / 1e3), "unit": "elements/s",
-            "ms_per_step": total_ms / K, "kernel": kernel,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": load_traffic().get(kernel.split("<")[0]),
-                         "algorithmic_bytes_per_launch": 2 * eb * n * na, "peak_source": kind},
-            "clocks": clk.summary(), "gpu_launches": K}
+    res = {"workload": cfg["workload"], "value": elems / (total_ms / 1e3), "unit": "elements/s",
+           "ms_per_step": total_ms / K, "kernel": kernel,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "traffic": load_traffic().get(kernel.split("<")[0]),
+                        "algorithmic_bytes_per_launch": 2 * eb * n * na, "peak_source": kind},
+           "clocks": clk.summary(), "gpu_launches": K}
+    if eb == 4 and "large" not in kernel:  # payload staged in shared memory
+        res["roofline_smem"] = smem_roofline(n * na / t)
+    return res
 
 
 def bench_c1(args, torch, B):
@@ -529,6 +571,9 @@ def main():
             "vs_baseline": None, "dtype": dtype, "data": "synthetic (BASELINE configs; generated on device)",
             "config": config, "roofline": r["roofline"], "clocks": r["clocks"], "gpu_launches": r["gpu_launches"],
             "e2e": r.get("e2e")}
+    for extra_roof in ("roofline_int", "roofline_smem"):
+        if r.get(extra_roof):
+            line[extra_roof] = r[extra_roof]
     if "cross_rank_rejections" in r:
         line["cross_rank_rejections"] = r["cross_rank_rejections"]
     if not args.no_secondary:
