@@ -343,24 +343,29 @@ def bench_c2(args, torch, B, ws, rank):
 
 
 def cpu_baseline_c2(sample_batches=1 << 24, target_s=10.0):
-    """The oracle port of roll_batch on one core (the stream is sequential), about target_s
-    seconds: the first 2^24 C2 bounds, rolled repeatedly by one continuing stream."""
+    """The oracle port of roll_batch on every host thread, about target_s seconds: the first
+    2^24 C2 bounds, rolled repeatedly by one continuing stream.  The stream is sequential in
+    the reference; the port splits it into per-thread chunks by jump-ahead and repairs chunks
+    after a rejected batch in order (or_roll_batches_mt: the same results)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
     O.build()
+    cores = cpu_cores()
     bounds = O.gen_bounds(7, 2 * sample_batches)
     src = O.pcg64(O.array_seed(7, 1))
+    O.roll_batches_mt(src, bounds, 2, nthreads=cores)  # warm-up (threads, pages)
     reps, t = 0, time.perf_counter()
     while True:
-        O.roll_batches(src, bounds, 2)
+        O.roll_batches_mt(src, bounds, 2, nthreads=cores)
         reps += 1
         dt = time.perf_counter() - t
         if dt >= target_s:
             break
-    return {"value": 2 * sample_batches * reps / dt, "unit": "rolls/s", "cores": 1, "kind": "port",
+    return {"value": 2 * sample_batches * reps / dt, "unit": "rolls/s", "cores": cores, "kind": "port",
             "sample": f"{reps} x {sample_batches} batches of C2 bounds on one continuing stream (the reference's "
-                      f"roll_batch loop; oracle/oracle.c or_roll_batches), {dt:.1f}s"}
+                      f"roll_batch loop in oracle/oracle.c, chunked over {cores} threads by jump-ahead: "
+                      f"or_roll_batches_mt), {dt:.1f}s"}
 
 
 # ------------------------------------------------------------------------------ shuffles
@@ -472,14 +477,16 @@ def run_reference(args, ws, rank):
         sample = 1 << 21
         bounds = O.gen_bounds(7, 2 * sample)
         src = O.pcg64(O.array_seed(7, 1))
+        cores = cpu_cores()
         for _ in range(args.warmup):
-            O.roll_batches(src, bounds, 2)
+            O.roll_batches_mt(src, bounds, 2, nthreads=cores)
         t = time.perf_counter()
         for _ in range(args.steps):
-            O.roll_batches(src, bounds, 2)
+            O.roll_batches_mt(src, bounds, 2, nthreads=cores)
         dt = time.perf_counter() - t
-        value, unit, cores = 2 * sample * args.steps / dt, "rolls/s", 1
-        desc = f"{sample} batches of C2 per step (one sequential stream; the reference roll_batch loop)"
+        value, unit = 2 * sample * args.steps / dt, "rolls/s"
+        desc = (f"{sample} batches of C2 per step (one continuing stream; the reference roll_batch loop chunked over "
+                f"{cores} threads by jump-ahead, or_roll_batches_mt)")
     else:
         c = SHUFFLE_CFG[cfg]
         n = c["n"]

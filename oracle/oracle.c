@@ -647,6 +647,60 @@ int or_roll_batches(or_source *s, const uint32_t *bounds, int32_t k, int64_t nb,
     return OR_OK;
 }
 
+/* Bulk rolls on all host threads: the CPU baseline of the bench (not in the reference; the
+ * results are or_roll_batches' exactly).  The batch range is split into contiguous chunks and
+ * chunk c is rolled from the stream advanced to its first batch, as if no earlier batch had
+ * been rejected.  Then, in chunk order, a chunk whose true first word differs (earlier chunks
+ * consumed extra words) is rolled again from the right word.  PCG64 and ChaCha sources (O(log)
+ * jump-ahead); any other source, or one thread, runs or_roll_batches. */
+static void or_source_skip(or_source *s, uint64_t delta) {
+    if (s->kind == 3) or_chacha_advance(s, delta);
+    else or_pcg64_advance(s, delta);
+    s->drawn += (int64_t)delta;
+}
+
+int or_roll_batches_mt(or_source *s, const uint32_t *bounds, int32_t k, int64_t nb, uint32_t *rolls,
+                       uint8_t *words, uint8_t *flags, uint64_t *rk, int32_t nthreads) {
+    int T = 1;
+#ifdef _OPENMP
+    T = nthreads > 0 ? nthreads : omp_get_max_threads();
+#endif
+    if ((s->kind != 0 && s->kind != 3) || T <= 1 || nb < (int64_t)T * 4096)
+        return or_roll_batches(s, bounds, k, nb, rolls, words, flags, rk);
+    if (T > 1024) T = 1024;
+    int64_t extra[1024];
+    int errs[1024];
+    const or_source base = *s;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+#endif
+    for (int c = 0; c < T; ++c) {
+        const int64_t lo = nb * c / T, hi = nb * (c + 1) / T;
+        or_source src = base;
+        or_source_skip(&src, (uint64_t)lo);
+        errs[c] = or_roll_batches(&src, bounds + lo * k, k, hi - lo, rolls + lo * k, words ? words + lo : NULL,
+                                  flags ? flags + lo : NULL, rk ? rk + lo : NULL);
+        extra[c] = (src.drawn - base.drawn) - hi;
+    }
+    uint64_t D = 0;
+    for (int c = 0; c < T; ++c) {
+        if (errs[c]) return errs[c];
+        const int64_t lo = nb * c / T, hi = nb * (c + 1) / T;
+        if (D != 0) {
+            or_source src = base;
+            or_source_skip(&src, (uint64_t)lo + D);
+            const int st = or_roll_batches(&src, bounds + lo * k, k, hi - lo, rolls + lo * k, words ? words + lo : NULL,
+                                           flags ? flags + lo : NULL, rk ? rk + lo : NULL);
+            if (st) return st;
+            extra[c] = (src.drawn - base.drawn) - hi - (int64_t)D;
+        }
+        D += (uint64_t)extra[c];
+    }
+    *s = base;
+    or_source_skip(s, (uint64_t)nb + D);
+    return OR_OK;
+}
+
 int or_gen_bounds(or_source *s, uint32_t *out, int64_t count, uint64_t lo, uint64_t span) {
     for (int64_t i = 0; i < count; ++i) {
         uint64_t v, nw;

@@ -105,6 +105,7 @@ def lib():
             "or_partial_shuffle_batch": (C.c_int, [P(Source), vp, i32, u64, u32, u64, u64, P(u64), P(u64)]),
             "or_shuffle_trace": (i64, [u64, vp, vp, i32, i32, vp, vp, i64]),
             "or_roll_batches": (C.c_int, [P(Source), vp, i32, i64, vp, vp, vp, vp]),
+            "or_roll_batches_mt": (C.c_int, [P(Source), vp, i32, i64, vp, vp, vp, vp, i32]),
             "or_gen_bounds": (C.c_int, [P(Source), vp, i64, u64, u64]),
             "or_shuffle_segmented": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, vp, i32, vp, i32, i32]),
             "or_shuffle_segmented_gen": (C.c_int, [vp, i32, i64, u64, u64, i64, vp, vp, i32, vp, i32, i32, i32]),
@@ -249,6 +250,19 @@ def roll_batch(s: Source, bases, bits: int = 64, upper_bound=None):
         "roll_batch",
     )
     return tuple(int(x) for x in d), w.value, bool(tc.value), rk.value
+
+
+def roll_batches_mt(s: Source, bounds: np.ndarray, k: int, nthreads: int = 0):
+    """roll_batches on all host threads (chunked jump-ahead with in-order repair; same results)."""
+    bounds = np.ascontiguousarray(bounds, dtype=np.uint32)
+    nb = len(bounds) // k
+    rolls = np.empty(nb * k, dtype=np.uint32)
+    wds = np.empty(nb, dtype=np.uint8)
+    flags = np.empty(nb, dtype=np.uint8)
+    rk = np.empty(nb, dtype=np.uint64)
+    _check(lib().or_roll_batches_mt(C.byref(s), _ptr(bounds), k, nb, _ptr(rolls), _ptr(wds), _ptr(flags), _ptr(rk),
+                                    nthreads), "roll_batches_mt")
+    return rolls, wds, flags, rk
 
 
 def roll_batches(s: Source, bounds: np.ndarray, k: int):
