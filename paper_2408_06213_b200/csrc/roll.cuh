@@ -160,10 +160,10 @@ __device__ __forceinline__ void set_error(RollWs *ws, int err) {
     atomicCAS(&ws->error, 0u, (unsigned)err);
 }
 
-// Process batches [begin, end) assuming shift D (batch i uses word i + D).
+// Speculative pass over batches [begin, end): batch i uses word i (no earlier rejection);
+// warp w owns one contiguous range.
 template <int K, int U>
-__device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc, int64_t begin,
-                                           int64_t end, uint64_t D, bool early_exit) {
+__device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc, int64_t begin, int64_t end) {
     const bool lh = is_lehmer(inc);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -174,13 +174,12 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
     const int64_t wb = begin + warp * per;
     const int64_t we = min(wb + per, end);
     if (wb >= we) return;
-    // lane state: word index wb + D + lane  ->  state index (word index + 1)
-    u128 s = gen_jump(s0, inc, (uint64_t)wb + D, lh);
+    // lane state: word index wb + lane  ->  state index (word index + 1)
+    u128 s = gen_jump(s0, inc, (uint64_t)wb, lh);
     s = gen_jump_small(s, inc, lane + 1, lh);
     const u128 A32 = gen_SA(lh, 32);
     const u128 C32 = mul128(g_SG[32], inc);
     int err = 0;
-    volatile RollWs *vws = a.ws;
     // software pipeline: the bounds of the next U*32 batches are in flight while the
     // current ones are rolled
     uint32_t cur[U][K], nxt[U][K];
@@ -190,10 +189,6 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
         if (b < we) load_bounds<K>(a.bounds + b * K, cur[u]);
     }
     for (int64_t b0 = wb; b0 < we; b0 += 32 * U) {
-        if (early_exit) {
-            unsigned long long nf = vws->neg_first;
-            if (nf != 0 && (int64_t)(~nf) < b0) return;  // an earlier rejection supersedes this work
-        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t b = b0 + 32 * (U + u) + lane;
@@ -237,10 +232,10 @@ __device__ __forceinline__ void publish_final(const RollArgs &a, u128 s0, u128 i
 // ---- ChaCha streams.  Only the device state says which generator a stream is (tag in
 // inc_lo, key after the head), so every roll kernel checks it and branches here.  Warp w
 // owns a contiguous batch range; lane l of a sub-step takes batch b0 + l, whose word
-// (position s0 + b + D) comes from the warp's 256-word keystream window.
+// (position s0 + b) comes from the warp's 256-word keystream window.
 template <int K>
-__device__ __forceinline__ void roll_range_cha(const RollArgs &a, u128 s0, int64_t begin, int64_t end, uint64_t D,
-                                               bool early_exit, uint64_t *win) {
+__device__ __forceinline__ void roll_range_cha(const RollArgs &a, u128 s0, int64_t begin, int64_t end,
+                                               uint64_t *win) {
     const ChaKey ck = cha_key_of_state(a.state);
     const uint32_t lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -251,18 +246,12 @@ __device__ __forceinline__ void roll_range_cha(const RollArgs &a, u128 s0, int64
     const int64_t wb = begin + warp * per;
     const int64_t we = min(wb + per, end);
     if (wb >= we) return;  // warp-uniform
-    u128 W0 = cha_win_unset(cha_add(s0, (uint64_t)wb + D));
+    u128 W0 = cha_win_unset(cha_add(s0, (uint64_t)wb));
     int err = 0;
-    volatile RollWs *vws = a.ws;
     // windows of U sub-steps: the bounds of all U are requested before the keystream block
     // computation, which then hides their latency
     constexpr int U = K <= 2 ? 8 : 4;
     for (int64_t c0 = wb; c0 < we; c0 += 32 * U) {
-        if (early_exit) {  // warp-uniform decision: the window refill is warp-collective
-            unsigned long long nf = lane == 0 ? vws->neg_first : 0ull;
-            nf = __shfl_sync(0xFFFFFFFFu, nf, 0);
-            if (nf != 0 && (int64_t)(~nf) < c0) break;
-        }
         uint32_t bb[U][K];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -273,7 +262,7 @@ __device__ __forceinline__ void roll_range_cha(const RollArgs &a, u128 s0, int64
         for (int u = 0; u < U; ++u) {
             const int64_t b = c0 + 32 * u + lane;
             if (c0 + 32 * u >= we) break;  // warp-uniform
-            const uint64_t w = cha_warp_word(win, ck, W0, cha_add(s0, (uint64_t)b + D), lane);
+            const uint64_t w = cha_warp_word(win, ck, W0, cha_add(s0, (uint64_t)b), lane);
             if (b < we) {
                 uint32_t d[K];
                 uint64_t r;
@@ -300,7 +289,7 @@ __device__ __forceinline__ void roll_cha_main(const RollArgs &a, uint64_t *win) 
         a.ws->final_hi = sf.hi;
         a.ws->final_lo = sf.lo;
     }
-    roll_range_cha<K>(a, s0, 0, a.nb, 0, false, win);
+    roll_range_cha<K>(a, s0, 0, a.nb, win);
 }
 
 // ChaCha keystreams and replayed word sequences take the position-addressed roll path
@@ -376,7 +365,7 @@ __global__ void __launch_bounds__(256) roll_main_kernel(RollArgs a) {
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
     publish_final(a, s0, inc);
-    roll_range<K, 4>(a, s0, inc, 0, a.nb, 0, false);
+    roll_range<K, 4>(a, s0, inc, 0, a.nb);
 }
 
 
@@ -538,7 +527,7 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
         }
     }
     // the last partial chunk (< CH batches) with the generic per-batch path
-    if (nchunks * CH < a.nb) roll_range<K, 1>(a, s0, inc, nchunks * CH, a.nb, 0, false);
+    if (nchunks * CH < a.nb) roll_range<K, 1>(a, s0, inc, nchunks * CH, a.nb);
 }
 
 // Fixup re-run of batches [begin, end) at shift D (batch b uses word b + D), front first:
@@ -691,8 +680,9 @@ __device__ __forceinline__ void roll_front(const RollArgs &a, u128 s0, u128 inc,
     if (err) set_error(a.ws, err);
 }
 
-// grid-wide barrier for the cooperative fixup kernel (co-residency guaranteed by
-// cudaLaunchCooperativeKernel)
+// Grid-wide barrier of the fixup kernel: one block per SM, co-resident once the main kernel
+// it waits for has drained (capi.cu launch_roll; BR_ROLL_FIXUP=cooperative makes the launch
+// guarantee it).
 // Arrival is a release add on the count, departure an acquire read of the generation: the
 // block's writes (ordered before thread 0 by bar.sync, carried by the release's cumulativity)
 // are visible to every block that leaves.  The last arriver resets the count and bumps the
@@ -872,7 +862,7 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(RollArgs a) {
         if (!done) {  // the main kernel was the ChaCha one: roll the PCG64/Lehmer stream here
             const u128 s0 = mk128(a.state[0], a.state[1]), inc = mk128(a.state[2], a.state[3]);
             publish_final(a, s0, inc);
-            roll_range<K, 1>(a, s0, inc, 0, a.nb, 0, false);
+            roll_range<K, 1>(a, s0, inc, 0, a.nb);
             grid_barrier(a.ws);
         }
         roll_fixup_body<K, false>(a, nullptr);

@@ -5,7 +5,8 @@ import torch
 import paper_2408_06213_b200 as B
 
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6542.7
-for k in (1, 2, 3, 4, 5, 6, 8):
+KS = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else (1, 2, 3, 4, 5, 6, 8)
+for k in KS:
     nb = (1 << 26) // k
     span = {1: 1 << 30, 2: 1 << 16, 3: 1 << 10, 4: 1 << 10, 5: 4000, 6: 1000, 8: 200}[k]
     bounds = (torch.randint(0, span - 2, (nb * k,), dtype=torch.int64, device="cuda") + 2).to(torch.int32)
