@@ -54,10 +54,47 @@ __host__ __device__ __forceinline__ u128 add128(u128 a, u128 b) {
     return r;
 }
 
-// s*a + c mod 2^128.  On the device through unsigned __int128: nvcc emits 6 IMAD.WIDE.U32
-// (+1 .X) for the partial products and ~10 adds, 17 SASS instructions per step against 25 for
-// a hand-written mad.lo/hi.cc chain over 32-bit limbs (measured on the cubin).
+// s*a + c mod 2^128.  On the device: a hand-written multiply-add carry chain over 32-bit
+// limbs (16 PTX mad.lo/hi.cc, 25 SASS instructions).
 __host__ __device__ __forceinline__ u128 mad128(u128 s, u128 a, u128 c) {
+#ifdef __CUDA_ARCH__
+    const uint32_t s0 = (uint32_t)s.lo, s1 = (uint32_t)(s.lo >> 32), s2 = (uint32_t)s.hi, s3 = (uint32_t)(s.hi >> 32);
+    const uint32_t a0 = (uint32_t)a.lo, a1 = (uint32_t)(a.lo >> 32), a2 = (uint32_t)a.hi, a3 = (uint32_t)(a.hi >> 32);
+    const uint32_t c0 = (uint32_t)c.lo, c1 = (uint32_t)(c.lo >> 32), c2 = (uint32_t)c.hi, c3 = (uint32_t)(c.hi >> 32);
+    uint32_t r0, r1, r2, r3;
+    asm("mad.lo.cc.u32 %0, %4, %8, %12;\n\t"
+        "madc.lo.cc.u32 %1, %4, %9, %13;\n\t"
+        "madc.lo.cc.u32 %2, %4, %10, %14;\n\t"
+        "madc.lo.u32 %3, %4, %11, %15;\n\t"
+        "mad.hi.cc.u32 %1, %4, %8, %1;\n\t"
+        "madc.hi.cc.u32 %2, %4, %9, %2;\n\t"
+        "madc.hi.u32 %3, %4, %10, %3;\n\t"
+        "mad.lo.cc.u32 %1, %5, %8, %1;\n\t"
+        "madc.lo.cc.u32 %2, %5, %9, %2;\n\t"
+        "madc.lo.u32 %3, %5, %10, %3;\n\t"
+        "mad.hi.cc.u32 %2, %5, %8, %2;\n\t"
+        "madc.hi.u32 %3, %5, %9, %3;\n\t"
+        "mad.lo.cc.u32 %2, %6, %8, %2;\n\t"
+        "madc.lo.u32 %3, %6, %9, %3;\n\t"
+        "mad.hi.u32 %3, %6, %8, %3;\n\t"
+        "mad.lo.u32 %3, %7, %8, %3;"
+        : "=&r"(r0), "=&r"(r1), "=&r"(r2), "=&r"(r3)
+        : "r"(s0), "r"(s1), "r"(s2), "r"(s3), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(c0), "r"(c1), "r"(c2),
+          "r"(c3));
+    u128 r;
+    r.lo = ((uint64_t)r1 << 32) | r0;
+    r.hi = ((uint64_t)r3 << 32) | r2;
+    return r;
+#else
+    return add128(mul128(s, a), c);
+#endif
+}
+
+// s*a + c mod 2^128 through unsigned __int128: nvcc emits 6 IMAD.WIDE.U32 (+1 .X) for the
+// partial products and ~10 adds, 17 SASS instructions per step against 25 for mad128's
+// chain.  Faster where the generator step is the bound (k = 1 and k >= 3 bulk rolls: 15% and
+// 5%); at C2's register budget it spills and costs 2-4%, so mad128 stays the default.
+__host__ __device__ __forceinline__ u128 mad128_wide(u128 s, u128 a, u128 c) {
     const unsigned __int128 x = ((unsigned __int128)s.hi << 64) | s.lo;
     const unsigned __int128 m = ((unsigned __int128)a.hi << 64) | a.lo;
     const unsigned __int128 d = ((unsigned __int128)c.hi << 64) | c.lo;

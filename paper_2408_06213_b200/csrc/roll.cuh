@@ -209,7 +209,7 @@ __device__ __forceinline__ void roll_range(const RollArgs &a, u128 s0, u128 inc,
                 if (a.rk) a.rk[b] = r;
                 if (st == 1) atomicMax(&a.ws->neg_first, ~(unsigned long long)b);
             }
-            s = mad128(s, A32, C32);
+            s = K >= 3 ? mad128_wide(s, A32, C32) : mad128(s, A32, C32);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -436,21 +436,129 @@ __device__ __forceinline__ void st_vec(uint32_t *p, const Vec<LB> &r) {
 // Main kernel for k <= 2 (the C2 shape): every lane moves LB bytes of bounds per load
 // (VB = LB/(4K) batches), U loads in flight, and rolls LB bytes / words VB bytes per store.
 // Lane l of sub-step u owns batches base + 32*VB*u + VB*l + v (v < VB); its words come
-// from VB consecutive PCG steps, the lane state then jumps 32*VB words.
-template <int K, bool FLAGS, bool RK, bool NAIVE = false>
-__global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
-    static_assert(K == 1 || K == 2, "fast path is for k <= 2");
+// from VB consecutive generator steps, the lane state then jumps 32*VB words.  The
+// generator kind (PCG64 or Lehmer: inc == 0) is a template of the loop, chosen once.  The
+// rare path (r_k below the product: threshold needed; or a zero bound) is flagged per batch
+// and handled after the sub-step by re-deriving its words (fast_recheck).
+template <int K, bool NAIVE, bool LH, int VB, int LB>
+__device__ __noinline__ void fast_recheck(RollWs *ws, uint8_t *flags, u128 st, u128 inc, Vec<LB> bv, int64_t b0,
+                                          unsigned bad) {
+    const uint32_t *bb = bv.v;
+    const u128 M = gen_mult(LH);
+    for (int v = 0; v < VB; ++v) {
+        if ((bad >> v) & 1u) {
+            uint64_t r = gen_out(st, LH);
+            uint64_t prod;
+            if constexpr (K == 2 && NAIVE) {
+                prod = (uint64_t)bb[2 * v] * bb[2 * v + 1];
+                r = prod * r;
+            } else if constexpr (K == 2) {
+                die(bb[2 * v], r);
+                die(bb[2 * v + 1], r);
+                prod = (uint64_t)bb[2 * v] * bb[2 * v + 1];
+            } else {
+                die(bb[v], r);
+                prod = bb[v];
+            }
+            roll_slow(ws, flags, b0 + v, r, prod);
+        }
+        st = mad128(st, M, inc);
+    }
+}
+
+template <int K, bool FLAGS, bool RK, bool NAIVE, bool LH>
+__device__ __forceinline__ void roll_fast_body(const RollArgs &a, u128 s0, u128 inc) {
     constexpr int LB = ROLL_LB;
     constexpr int VB = LB / (4 * K);
     static_assert(32 * VB <= JUMP_SMALL, "jump table covers the lane offsets");
     constexpr int U = ROLL_U;
     constexpr int64_t CH = 32 * VB * U;
-    pdl_launch_dependents();
-    if (roll_is_chacha(a)) {  // the fixup kernel rolls ChaCha streams met here
-        mark_main(a, 0);
-        return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nchunks = a.nb / CH;
+    const int64_t cpw = (nchunks + nwarps - 1) / nwarps;
+    const int64_t c0 = warp * cpw, c1 = min(c0 + cpw, nchunks);
+    const u128 M = gen_mult(LH);
+    if (c0 < c1) {
+        const int64_t wb = c0 * CH;
+        u128 s = gen_jump(s0, inc, (uint64_t)wb, LH);
+        s = gen_jump_small(s, inc, VB * lane + 1, LH);
+        const u128 AJ = gen_SA(LH, 32 * VB);
+        const u128 CJ = mul128(g_SG[32 * VB], inc);
+        const uint32_t *bp = a.bounds + (wb + VB * lane) * K;
+        uint32_t *rp = a.rolls + (wb + VB * lane) * K;
+        uint8_t *wp = a.words + wb + VB * lane;
+        constexpr int STEP = 32 * VB * K;  // u32 per sub-step
+        Vec<LB> cur[U], nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = ld_vec<LB>(bp + STEP * u);
+        for (int64_t c = c0; c < c1; ++c) {
+            if (c + 1 < c1) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) nxt[u] = ld_vec<LB>(bp + STEP * (U + u));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                Vec<LB> dd;
+                u128 st = s;
+                const int64_t b0 = wb + (c - c0) * CH + 32 * VB * u + VB * lane;
+                unsigned bad = 0;
+#pragma unroll
+                for (int v = 0; v < VB; ++v) {
+                    uint64_t r = gen_out(st, LH);
+                    uint64_t prod;
+                    if constexpr (K == 2 && NAIVE) {  // roll_batch_naive: one division by b1
+                        const uint32_t b1 = cur[u].v[2 * v + 1];
+                        prod = (uint64_t)cur[u].v[2 * v] * b1;
+                        const uint64_t val = mulhi64(prod, r);
+                        r = prod * r;
+                        const uint64_t q = b1 ? val / b1 : 0;
+                        dd.v[2 * v] = (uint32_t)q;
+                        dd.v[2 * v + 1] = (uint32_t)(val - q * b1);
+                    } else if constexpr (K == 2) {
+                        dd.v[2 * v] = die(cur[u].v[2 * v], r);
+                        dd.v[2 * v + 1] = die(cur[u].v[2 * v + 1], r);
+                        prod = (uint64_t)cur[u].v[2 * v] * cur[u].v[2 * v + 1];
+                    } else {
+                        dd.v[v] = die(cur[u].v[v], r);
+                        prod = cur[u].v[v];
+                    }
+                    if constexpr (FLAGS) a.flags[b0 + v] = r < prod;
+                    if constexpr (RK) a.rk[b0 + v] = r;
+                    bad |= (unsigned)(r < prod || prod == 0) << v;
+                    if (v + 1 < VB) st = mad128_wide(st, M, inc);
+                }
+                if (__builtin_expect(bad != 0, 0)) fast_recheck<K, NAIVE, LH, VB, LB>(a.ws, a.flags, s, inc, cur[u], b0, bad);
+                st_vec<LB>(rp + STEP * u, dd);
+                if constexpr (VB == 2)
+                    *reinterpret_cast<uint16_t *>(wp + 32 * VB * u) = 0x0101;
+                else if constexpr (VB == 4)
+                    *reinterpret_cast<uint32_t *>(wp + 32 * VB * u) = 0x01010101u;
+                else
+                    *reinterpret_cast<uint2 *>(wp + 32 * VB * u) = make_uint2(0x01010101u, 0x01010101u);
+                s = mad128_wide(s, AJ, CJ);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+            bp += STEP * U;
+            rp += STEP * U;
+            wp += CH;
+        }
     }
-    mark_main(a, 1);
+    // the last partial chunk (< CH batches) with the generic per-batch path
+    if (nchunks * CH < a.nb) roll_range<K, 1>(a, s0, inc, nchunks * CH, a.nb);
+}
+
+// k = 2 (C2): one loop with the generator kind as a runtime value and the rare-path test
+// inline; the templated form below spills at this shape (measured 12% slower on C2)
+template <int K, bool FLAGS, bool RK, bool NAIVE>
+__device__ __forceinline__ void roll_fast_body_rt(const RollArgs &a) {
+    constexpr int LB = ROLL_LB;
+    constexpr int VB = LB / (4 * K);
+    static_assert(32 * VB <= JUMP_SMALL, "jump table covers the lane offsets");
+    constexpr int U = ROLL_U;
+    constexpr int64_t CH = 32 * VB * U;
     const u128 s0 = mk128(a.state[0], a.state[1]);
     const u128 inc = mk128(a.state[2], a.state[3]);
     const bool lh = is_lehmer(inc);
@@ -526,8 +634,27 @@ __global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
             wp += CH;
         }
     }
-    // the last partial chunk (< CH batches) with the generic per-batch path
     if (nchunks * CH < a.nb) roll_range<K, 1>(a, s0, inc, nchunks * CH, a.nb);
+}
+
+template <int K, bool FLAGS, bool RK, bool NAIVE = false>
+__global__ void __launch_bounds__(256, ROLL_MINB) roll_fast_kernel(RollArgs a) {
+    static_assert(K == 1 || K == 2, "fast path is for k <= 2");
+    pdl_launch_dependents();
+    if (roll_is_chacha(a)) {  // the fixup kernel rolls ChaCha streams met here
+        mark_main(a, 0);
+        return;
+    }
+    mark_main(a, 1);
+    if constexpr (K == 2) {
+        roll_fast_body_rt<K, FLAGS, RK, NAIVE>(a);
+    } else {
+        const u128 s0 = mk128(a.state[0], a.state[1]);
+        const u128 inc = mk128(a.state[2], a.state[3]);
+        publish_final(a, s0, inc);
+        if (is_lehmer(inc)) roll_fast_body<K, FLAGS, RK, NAIVE, true>(a, s0, inc);
+        else roll_fast_body<K, FLAGS, RK, NAIVE, false>(a, s0, inc);
+    }
 }
 
 // Fixup re-run of batches [begin, end) at shift D (batch b uses word b + D), front first:
