@@ -2,7 +2,7 @@
 // Every thread runs a dependent chain of one operation; the whole GPU is filled, so the time
 // per operation is the machine throughput cost, as the cost model wants it.  Printed as JSON:
 //   die          one batched die, (digit, r') = b (x) r            (core.cuh die)
-//   pcg64_word   one PCG64 step + XSL-RR output                    (mad128 + xslrr)
+//   pcg64_word   one PCG64 step + XSL-RR output                    (mad128_wide + xslrr)
 //   lehmer_word  one Lehmer128 step + top word
 //   chacha_word  one ChaCha20 block / 8                            (chacha.cuh)
 //   mod64        2^64 mod b for a 64-bit b (the threshold remainder)
@@ -36,7 +36,7 @@ __global__ void k_pcg(uint64_t *out, uint32_t seed) {
     uint64_t acc = 0;
 #pragma unroll 8
     for (int i = 0; i < ITERS; ++i) {
-        s = mad128(s, M, inc);
+        s = mad128_wide(s, M, inc);
         acc += xslrr(s);
     }
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
@@ -48,7 +48,7 @@ __global__ void k_lehmer(uint64_t *out, uint32_t seed) {
     uint64_t acc = 0;
 #pragma unroll 8
     for (int i = 0; i < ITERS; ++i) {
-        s = mad128(s, M, Z);
+        s = mad128_wide(s, M, Z);
         acc += s.hi;
     }
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
