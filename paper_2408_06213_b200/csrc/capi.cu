@@ -463,6 +463,7 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
 constexpr uint32_t SMALL_SMEM_MAX = 64 * 1024;   // per 128-thread block
 constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 constexpr uint32_t WARP_SMEM_MAX = 48 * 1024;    // warp kernel: several arrays per SM or none
+constexpr uint32_t WARP_SMEM_DEFAULT = 16 * 1024; // warp kernel by default (measured crossover)
 #ifndef LARGE_W
 #define LARGE_W 8
 #endif
@@ -546,10 +547,12 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         return BR_OK;
     }
     const uint32_t zbytes = (uint32_t)((n * sizeof(T) + 15) & ~(uint64_t)15);
-    // one warp per array (warp_shuffle.cuh): measured slower than the hash kernel on C4
-    // (2.67 vs 2.49 ms), so only on request
-    if (forced_kernel() == K_WARP && cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
-        (uint64_t)cp.plan.max_k * 32 + 32 <= WRING) {
+    // one warp per array (warp_shuffle.cuh): the default for many arrays of up to 16 KB
+    // (12 arrays per SM; C4 1.93 vs 2.49 ms for the hash kernel).  Beyond that too few
+    // arrays fit per SM and the CTA groups of the hash kernel win.
+    const bool warp_fit = cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
+                          (uint64_t)cp.plan.max_k * 32 + 64 <= WRING;
+    if (warp_fit && (forced_kernel() == K_WARP || (forced_kernel() == K_ANY && zbytes <= WARP_SMEM_DEFAULT))) {
         auto kern = gen == 2 ? shuffle_warp_kernel<T, true, 1> : shuffle_warp_kernel<T, true, 0>;
         const void *kp = (const void *)kern;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes));

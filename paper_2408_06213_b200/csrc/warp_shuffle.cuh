@@ -1,23 +1,27 @@
 // warp_shuffle.cuh -- one warp per shared-memory-resident array, 32 Fisher-Yates steps per
-// warp step, for the many-arrays calls of moderate length (C4: 65,536 x u32[4096]).
+// warp step: the default for many arrays of up to 16 KB (C4: 65,536 x u32[4096]).
 //
 // Same algorithm as shuffle.cuh (shuffle.py:100-225: batches of k dice, rejection re-draws
-// the batch from the next word), built for few instructions per element:
+// the batch from the next word), built for few instructions and short dependency chains:
 //   * per-batch records {threshold, n_b, k_b} (plan.brec) replace the segment walk;
-//   * targets go into a 512-entry u16 ring just ahead of the groups that read them;
-//   * a group of 32 steps i_l = top - l (lane l) is applied as independent swaps, except
-//     for "dirty" lanes, which are then replayed one at a time in step order.  Lane l is
-//     dirty iff its target is shared with another lane (match.any), lies inside the group
-//     (another lane's position), or some other lane targets i_l.  A clean lane's two
-//     positions are touched by no other lane, so applying the clean lanes first and the
-//     dirty ones sequentially equals the sequential loop.  For n = 4096 about one lane in
-//     sixty is dirty.
+//   * targets go into a 256-entry u16 ring just ahead of the groups that read them;
+//   * a group of 32 steps i_l = top - l (lane l) is resolved exactly in registers
+//     (warp_apply_group_exact): equal targets through a byte table instead of MATCH.ANY,
+//     predecessor chains through 32 bytes of shared memory and shuffles, no serial replay;
+//   * the next group's targets and equality mask are prepared around the current group.
+// The earlier form (BR_WARP_EXACT=0: independent swaps plus serial replay of "dirty" lanes)
+// is kept for A/B timing.
 #pragma once
 #include "shuffle.cuh"
 
 namespace br {
 
-static constexpr uint32_t WRING = 512;
+#ifndef BR_WARP_EXACT
+#define BR_WARP_EXACT 1
+#endif
+// 256 entries hold the current and next group and one generation step for k <= 6 (the
+// default schedule); with the 1 KB target table that keeps 12 arrays of 16 KB per SM
+static constexpr uint32_t WRING = BR_WARP_EXACT ? 256 : 512;
 
 struct WarpGen {
     u128 s, inc, A32, C32;
@@ -72,6 +76,125 @@ __device__ __forceinline__ void warp_gen_step(WarpGen &g, const DevPlan &plan, u
     }
 }
 
+// Shared-memory accesses of the group loop through 32-bit shared addresses: with generic
+// pointers ptxas re-forms the shared window base (S2R SR_CgaCtaId + LEA) inside the loop,
+// and every swap waits on that S2R.  The base is laundered through a volatile move once.
+__device__ __forceinline__ uint32_t smem_base(const void *p) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), b;
+    asm volatile("mov.b32 %0, %1;" : "=r"(b) : "r"(a));
+    return b;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void lds_v(uint32_t a, uint32_t &v) {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void lds_v(uint32_t a, uint64_t &v) {
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void sts_v(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v(uint32_t a, uint64_t v) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ int lds_s8(uint32_t a) {
+    int16_t v;
+    asm volatile("ld.shared.s8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_s8(uint32_t a, int v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((int16_t)v) : "memory");
+}
+
+// The caller loads group g+1's targets and their equality mask ahead of group g's swaps.
+// same = the lanes whose target equals this lane's.  MATCH.ANY computes it in one
+// instruction but is slow on sm_100 (C4: 2.18 ms with it, 1.41 ms with the mask stubbed
+// out), so lanes write their id into a 1024-slot byte table at j mod 1024 and read the slot
+// back: a lane that reads another id shares a slot, and only then are the slot's lanes
+// split by exact target, one ballot per distinct target.  Stale slots are never read (a
+// lane reads only the slot it has just written).
+static constexpr uint32_t WTBL = 1024;
+
+// issue: targets and the slot read-back (consumed after the current group's swaps)
+__device__ __forceinline__ void warp_group_targets(uint32_t ring, uint32_t tbl, uint32_t top, uint32_t lim,
+                                                   int lane, uint32_t &j, bool &shared_slot) {
+    const bool act = (uint32_t)lane <= top - lim;
+    j = act ? lds_u16(ring + 2u * ((top - lane) & (WRING - 1))) : 0u;
+    const uint32_t slot = tbl + (j & (WTBL - 1));
+    if (act) sts_s8(slot, lane);
+    __syncwarp();
+    shared_slot = act && lds_s8(slot) != lane;
+}
+
+// finish: split the lanes of shared slots by exact target
+__device__ __forceinline__ unsigned warp_group_same(uint32_t top, uint32_t lim, int lane, uint32_t j, bool shared_slot) {
+    const bool act = (uint32_t)lane <= top - lim;
+    unsigned pending = __ballot_sync(FULL, shared_slot);
+    unsigned same = 1u << lane;
+    while (pending) {
+        const uint32_t jf = __shfl_sync(FULL, j, __ffs(pending) - 1);
+        const unsigned S = __ballot_sync(FULL, act && j == jf);
+        if ((S >> lane) & 1u) same = S;
+        pending &= ~S;
+    }
+    return same;
+}
+
+// steps top, top-1, ..., max(top-31, lim) of z[i] <-> z[J[i]] (i descending), resolved
+// exactly in registers (the warp form of apply_group_cta_global):
+//   lane l owns step i_l = top - l with target j_l <= i_l; all values are loaded first;
+//   T(l)    = latest earlier lane with target j_l           (equality mask below l)
+//   Pred(l) = latest earlier lane whose target is i_l       (one byte per lane in P)
+//   A_l = A_Pred(l), else z[i_l]    -- the value step l moves to j_l
+//   B_l = A_T(l),    else z[j_l]    -- the value step l leaves at i_l (final: no later step
+//                                      of the group can target i_l, all j are <= their i)
+// z[j_l] = A_l is written by the last lane of each target below the group; targets inside
+// the group are positions whose own lane writes B.  No lane is replayed serially.
+template <typename T>
+__device__ __forceinline__ void warp_apply_group_exact(uint32_t z, uint32_t P, uint32_t top, uint32_t lim, int lane,
+                                                       uint32_t j, unsigned same) {
+    constexpr uint32_t E = sizeof(T);
+    const bool act = (uint32_t)lane <= top - lim;
+    const uint32_t i = top - lane;
+    const uint32_t lo = top - lim >= 31 ? top - 31 : lim;
+    T vi = T(0), vj = T(0);
+    if (act) {
+        lds_v(z + E * i, vi);
+        lds_v(z + E * j, vj);
+    }
+    const unsigned below = same & ((1u << lane) - 1u);
+    const unsigned above = same & ~((2u << lane) - 1u);  // later lanes (lane 31: 2u << 31 == 0)
+    const bool inr = act && j >= lo && j != i;            // j = i_l' of a later lane l' = top - j
+    T A = vi;
+    if (__ballot_sync(FULL, inr)) {
+        sts_s8(P + lane, -1);
+        __syncwarp();
+        // the latest lane before l' = top - j targeting i_l' (l' itself may target it: a self-swap)
+        if (inr && (above & ~(1u << (top - j))) == 0) sts_s8(P + (top - j), lane);
+        __syncwarp();
+        const int p = lds_s8(P + lane);
+        int r = p >= 0 ? p : lane;
+        for (;;) {  // pointer jumping to the root of the Pred chain (Pred(l) < l)
+            const int rr = __shfl_sync(FULL, r, r);
+            if (!__ballot_sync(FULL, rr != r)) break;
+            r = rr;
+        }
+        A = shfl_t<T>(vi, r);
+        __syncwarp();
+    }
+    const int tl = below ? 31 - __clz(below) : lane;
+    const T Bt = shfl_t<T>(A, tl);
+    if (act) {
+        sts_v(z + E * i, below ? Bt : vj);
+        if (!above && j < lo) sts_v(z + E * j, A);
+    }
+    __syncwarp();
+}
+
 // steps top, top-1, ..., max(top-31, lim) of z[i] <-> z[J[i]] (i descending)
 template <typename T>
 __device__ __forceinline__ void warp_apply_group(T *z, const uint16_t *ring, uint32_t top, uint32_t lim, int lane) {
@@ -112,8 +235,8 @@ template <typename T, bool SEGMENTED, bool CHA>
 __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
                                                   uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
                                                   uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
-                                                  int use_tma, int gen, T *z, uint16_t *ring, uint64_t &bar,
-                                                  uint64_t *chawin) {
+                                                  int use_tma, int gen, T *z, uint16_t *ring, int8_t *P,
+                                                  int8_t *tbl, uint64_t &bar, uint64_t *chawin) {
     const int lane = threadIdx.x & 31;
     if (use_tma && lane == 0) mbar_init(&bar, 1);
     __syncwarp();
@@ -173,12 +296,54 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
             parity ^= 1u;
         }
         __syncwarp();
+#if BR_WARP_EXACT
+        if (n > lim) {
+            // software-pipelined: group g+1's targets and equality mask are prepared around
+            // group g's swaps
+            uint32_t top = n - 1, j;
+            unsigned same;
+            const uint32_t need0 = top - lim >= 31 ? top - 31 : lim;
+            while (gs.frontier > need0 && gs.B0 < plan.nbatches) warp_gen_step<CHA>(gs, plan, ring, lane, rkf, chawin, ck);
+            __syncwarp();
+            const uint32_t zs = smem_base(z), rs = smem_base(ring), ps = smem_base(P), ts = smem_base(tbl);
+            bool sh;
+            warp_group_targets(rs, ts, top, lim, lane, j, sh);
+            same = warp_group_same(top, lim, lane, j, sh);
+            // one group: issue the next group's targets into jn, swap this one, then finish
+            // the next group's equality mask sn (its table read-back hides behind the swaps)
+            auto group = [&](uint32_t t, uint32_t jc, unsigned sc, uint32_t &jn, unsigned &sn) -> bool {
+                const bool last = t < lim + 32;
+                const uint32_t nt = t - 32;
+                bool shn = false;
+                if (!last) {
+                    const uint32_t need = nt - lim >= 31 ? nt - 31 : lim;
+                    // the ring has room for the current group, the next and one generation step
+                    while (gs.frontier > need && gs.B0 < plan.nbatches)
+                        warp_gen_step<CHA>(gs, plan, ring, lane, rkf, chawin, ck);
+                    __syncwarp();
+                    warp_group_targets(rs, ts, nt, lim, lane, jn, shn);
+                }
+                warp_apply_group_exact<T>(zs, ps, t, lim, lane, jc, sc);
+                if (!last) sn = warp_group_same(nt, lim, lane, jn, shn);
+                return last;
+            };
+            uint32_t j2;
+            unsigned same2;
+            for (;;) {  // unrolled by two: the prefetched values are never copied
+                if (group(top, j, same, j2, same2)) break;
+                top -= 32;
+                if (group(top, j2, same2, j, same)) break;
+                top -= 32;
+            }
+        }
+#else
         for (uint32_t top = n - 1; n > lim; top -= 32) {
             const uint32_t need = top - lim >= 31 ? top - 31 : lim;
             while (gs.frontier > need && gs.B0 < plan.nbatches) warp_gen_step<CHA>(gs, plan, ring, lane, rkf, chawin, ck);
             warp_apply_group<T>(z, ring, top, lim, lane);
             if (top < lim + 32) break;
         }
+#endif
         // finish the word accounting (a trailing rejection can follow the last position)
         while (gs.B0 < plan.nbatches) warp_gen_step<CHA>(gs, plan, ring, lane, rkf, chawin, ck);
         if (use_tma) {
@@ -215,16 +380,18 @@ __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(16) uint16_t ring[WRING];
     __shared__ __align__(8) uint64_t bar;
+    __shared__ int8_t P[32];
+    __shared__ int8_t tbl[BR_WARP_EXACT ? WTBL : 1];
     __shared__ __align__(16) uint64_t chawin[CM ? 256 : 2];
     T *z = reinterpret_cast<T *>(smem_raw);
     bool cha = CM == 1;
     if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_warp_body<T, SEGMENTED, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
-                                                 rk_first, use_tma, gen, z, ring, bar, chawin);
+                                                 rk_first, use_tma, gen, z, ring, P, tbl, bar, chawin);
     else if (CM != 1)
         shuffle_warp_body<T, SEGMENTED, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
-                                               rk_first, use_tma, gen, z, ring, bar, chawin);
+                                               rk_first, use_tma, gen, z, ring, P, tbl, bar, chawin);
 }
 
 }  // namespace br

@@ -263,7 +263,7 @@ def test_c4_sample(B, O, golden):
     n, na = 4096, 1 << 16
     data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
     _, words = B.shuffle_many(data, n, 99, return_words=True)
-    assert "shuffle_cta_hash_kernel" in B.last_kernel()
+    assert "shuffle_warp_kernel" in B.last_kernel()
     got = u32(data).reshape(na, n)
     w = u32(words)
     for rec in golden["c4"]:

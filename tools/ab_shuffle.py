@@ -5,9 +5,16 @@ import torch
 import bench
 import paper_2408_06213_b200 as B
 
-cfg = bench.SHUFFLE_CFG[sys.argv[1]]
+# argv[1]: a bench config name (c3/c4/c5) or n:arrays:elem_bytes
+if ":" in sys.argv[1]:
+    _n, _na, _eb = (int(x) for x in sys.argv[1].split(":"))
+    cfg = {"n": _n, "arrays": _na, "eb": _eb, "seed": 7}
+else:
+    cfg = bench.SHUFFLE_CFG[sys.argv[1]]
 n, na, eb = cfg["n"], cfg["arrays"], cfg["eb"]
 data = B.pcg64_fill(cfg["seed"], n * na) if eb == 8 else torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
+if eb == 8 and data.dtype != torch.int64:
+    data = data.view(torch.int64)
 for _ in range(3):
     B.shuffle_many(data, n, cfg["seed"])
 torch.cuda.synchronize()
