@@ -483,12 +483,12 @@ constexpr uint32_t WARP_SMEM_DEFAULT = 16 * 1024; // warp kernel by default (mea
 // BR_SHUFFLE_KERNEL=small|resolve|warp|hash|mid|pipe|large|global restricts the dispatch below to one
 // shuffle kernel where it is eligible (tests cover every kernel; A/B timing).  Unset: the
 // first eligible kernel in the order below.
-enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL, K_WARP };
+enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL, K_WARP, K_WARP64 };
 int forced_kernel() {
     const char *e = getenv("BR_SHUFFLE_KERNEL");
     if (!e || !*e) return K_ANY;
-    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global", "warp"};
-    for (int i = 1; i <= K_WARP; ++i)
+    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global", "warp", "warp64"};
+    for (int i = 1; i <= K_WARP64; ++i)
         if (!strcmp(e, names[i])) return i;
     return K_ANY;
 }
@@ -550,6 +550,19 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     // one warp per array (warp_shuffle.cuh): the default for many arrays of up to 16 KB
     // (12 arrays per SM; C4 1.93 vs 2.49 ms for the hash kernel).  Beyond that too few
     // arrays fit per SM and the CTA groups of the hash kernel win.
+    if (forced_kernel() == K_WARP64 && cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
+        (uint64_t)cp.plan.max_k * 32 + 128 <= WRING64) {
+        auto kern = gen == 2 ? shuffle_warp_kernel<T, true, 1, 64> : shuffle_warp_kernel<T, true, 0, 64>;
+        const void *kp = (const void *)kern;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes));
+        const int grid = grid_for(di, kp, 32, zbytes, num_arrays);
+        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+        kern<<<grid, 32, zbytes, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
+                                       rk_first, use_tma, gen);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_warp_kernel<u") + std::to_string(8 * sizeof(T)) + ",64>";
+        return BR_OK;
+    }
     const bool warp_fit = cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
                           (uint64_t)cp.plan.max_k * 32 + 64 <= WRING;
     if (warp_fit && (forced_kernel() == K_WARP || (forced_kernel() == K_ANY && zbytes <= WARP_SMEM_DEFAULT))) {

@@ -287,6 +287,7 @@ KERNEL_CASES = {  # forced kernel -> (name in last_kernel, lengths it can take)
     "large": ("shuffle_cta_large_kernel", (2, 64, 1000, 4096, 70000)),
     "global": ("shuffle_large_gen_kernel", (2, 64, 1000, 4096, 70000)),
     "warp": ("shuffle_warp_kernel", (2, 33, 64, 1000, 4096, 6000, 12000)),
+    "warp64": ("shuffle_warp_kernel", (2, 33, 64, 65, 127, 1000, 4096, 6000, 12000)),
 }
 
 
@@ -316,7 +317,7 @@ def test_every_shuffle_kernel(B, O, monkeypatch, kernel, gen):
                     rw = O.shuffle_segmented(ref, n, 4321, array_index_base=17, generator=gen)
                 assert np.array_equal(dev.cpu().numpy().view(dt), ref), (kernel, n, eb, naive, kern)
                 assert np.array_equal(u32(w), rw)
-                if n > 2 and not (kernel == "small" and eb == 8 and n >= 64) and not (kernel == "warp" and n * eb > 48 * 1024):
+                if n > 2 and not (kernel == "small" and eb == 8 and n >= 64) and not (kernel.startswith("warp") and n * eb > 48 * 1024):
                     assert name in kern, (kernel, n, eb, kern)
         if kernel != "small":  # stream form (one array from a caller's source)
             s = B.make_source(gen, 900 + n)
