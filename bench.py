@@ -82,6 +82,29 @@ def smem_roofline(elems_per_s):
             "peak_source": "measured: profiles/smem_r1.json (tools/micro/smem_bw.cu)"}
 
 
+def random_roofline(steps_per_s, footprint_mb):
+    """HBM-resident arrays: every Fisher-Yates step reads z[j] at a random position and writes
+    it back.  Peak = the measured random 8-byte read-modify-write rate over a buffer of the same
+    footprint (tools/micro/randgather.cu rmw, profiles/randaccess_r1.jsonl).  The kernel can
+    exceed it: targets j are uniform on [0, i], so the low positions of each array are hit
+    often and stay in L2."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "randaccess_r1.jsonl")) as fh:
+            rows = [json.loads(x) for x in fh if x.strip()]
+    except Exception:
+        return None
+    big = [r for r in rows if r["buffer_mb"] >= footprint_mb]
+    if not big:
+        return None
+    r = min(big, key=lambda r: r["buffer_mb"])
+    peak = r["rmw_per_s"] / 1e9
+    achieved = steps_per_s / 1e9
+    return {"bound": "hbm_random", "achieved": achieved, "peak": peak, "unit": "G random RMW/s",
+            "frac": achieved / peak, "per_element": "one random 8-byte read + write of z[j]",
+            "peak_source": f"measured: random RMW over {r['buffer_mb']} MB (tools/micro/randgather.cu, "
+                           "profiles/randaccess_r1.jsonl)"}
+
+
 def load_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -410,6 +433,8 @@ def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
            "clocks": clk.summary(), "gpu_launches": K}
     if eb == 4 and "large" not in kernel:  # payload staged in shared memory
         res["roofline_smem"] = smem_roofline(n * na / t)
+    if "large" in kernel:  # payload in HBM: random accesses
+        res["roofline_random"] = random_roofline((n - 1) * na / t, n * na * eb / 2**20)
     return res
 
 
