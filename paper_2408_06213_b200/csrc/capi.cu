@@ -465,7 +465,7 @@ constexpr uint32_t MID_SMEM_MAX = 200 * 1024;    // per warp
 constexpr uint32_t WARP_SMEM_MAX = 48 * 1024;    // warp kernel: several arrays per SM or none
 constexpr uint32_t WARP_SMEM_DEFAULT = 16 * 1024; // warp kernel by default (measured crossover)
 #ifndef LARGE_W
-#define LARGE_W 8
+#define LARGE_W 16  // C5: 12.2 ms (8 warps: 12.9, 4 warps: 17.5)
 #endif
 #ifndef CTA_W
 #define CTA_W 4
@@ -631,8 +631,11 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
         auto kern = !segmented ? shuffle_cta_large_kernel<T, W, 2>
                                : (gen == 2 ? shuffle_cta_large_kernel<T, W, 1> : shuffle_cta_large_kernel<T, W, 0>);
-        kern<<<grid, 32 * W, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
-                                      rk_first, segmented ? 1 : 0, gen);
+        // dynamic shared memory: the ChaCha keystream window (8 words per thread), when there is one
+        const size_t wsmem = (!segmented || gen == 2) ? (size_t)8 * 32 * W * sizeof(uint64_t) : 0;
+        CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+        kern<<<grid, 32 * W, wsmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
+                                          rk_first, segmented ? 1 : 0, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_cta_large_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
                    std::to_string(W) + ">";

@@ -578,7 +578,10 @@ struct CtaGen {
 // targets are found exactly with one ballot per bit of j in every warp; lane L combines the
 // W*jbits masks through shared memory, which yields T(L) and "later" for any multiplicity.
 static constexpr uint32_t LRING = 4096;  // u32 target ring of the large kernel
-static constexpr int HBITS = 11;          // 2048-slot lane-chain hash per group
+#ifndef BR_LARGE_HB
+#define BR_LARGE_HB 11
+#endif
+static constexpr int HBITS = BR_LARGE_HB;  // 2048-slot lane-chain hash per group
 
 template <typename T, int W, typename RT = uint32_t, uint32_t RS = LRING, int HB = HBITS>
 struct LargeShared {
@@ -807,7 +810,8 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
                                                                    uint64_t *words64, uint64_t *rk_first,
                                                                    int segmented, int gen) {
     __shared__ LargeShared<T, W> sh;
-    __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
+    // the ChaCha keystream window is dynamic shared memory (8 words per thread; size set at launch)
+    extern __shared__ __align__(16) uint64_t chawin[];
     bool cha = CM == 1;
     if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
