@@ -789,7 +789,7 @@ class RollBatchesResult(NamedTuple):
 
 
 def roll_batches(stream, bounds, k: Optional[int] = None, *, flags: bool = False, final_remainder: bool = False,
-                 out=None, check: bool = True, chunks: int = 8, naive: bool = False) -> RollBatchesResult:
+                 out=None, check: bool = True, chunks: int = 16, naive: bool = False) -> RollBatchesResult:
     """Bulk roll_batch: batch i rolls the k dice bounds[i*k:(i+1)*k] (4-byte items, >= 1)
     from the PCG64 ``stream`` (a DeviceStream or a host PCG64 source, advanced in place).
 
@@ -866,6 +866,10 @@ def _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, t
     per = (per + 3) & ~3
     comp = torch.cuda.current_stream()
     h2d, d2h = _copy_streams(torch)
+    # the device buffers below may reuse memory the previous call's kernels (comp) were still
+    # reading or writing when it returned: the copy streams start after that work
+    h2d.wait_stream(comp)
+    d2h.wait_stream(comp)
     dbufs = [torch.empty(per * k, dtype=torch.int32, device="cuda") for _ in range(2)]
     dro = [torch.empty(per * k, dtype=torch.int32, device="cuda") for _ in range(2)]
     dwo = [torch.empty(per, dtype=torch.uint8, device="cuda") for _ in range(2)]
@@ -902,6 +906,11 @@ def _roll_batches_host(stream, bounds, k, flags, final_remainder, out, chunks, t
             freed[slot] = ev
     comp.wait_stream(d2h)
     comp.wait_stream(h2d)
+    # freed device buffers are reused only after the copy streams are done with them
+    for t in dbufs + dro + dwo + dfl + drk:
+        if t is not None:
+            t.record_stream(h2d)
+            t.record_stream(d2h)
     return RollBatchesResult(rolls, words, fl, rk)
 
 

@@ -10,7 +10,7 @@ bounds, stream, rolls, words = bench.setup_c2(torch, B, 0, nb)
 hb = bounds.cpu().pin_memory()
 hr = torch.empty(2 * nb, dtype=torch.int32).pin_memory()
 hw = torch.empty(nb, dtype=torch.uint8).pin_memory()
-for ch in (4, 8, 16, 32, 64):
+for ch in [int(x) for x in sys.argv[1:]] or (4, 8, 16, 32, 64):
     B.roll_batches(stream, hb, 2, out=(hr, hw), chunks=ch)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
