@@ -483,14 +483,21 @@ constexpr uint32_t WARP_SMEM_DEFAULT = 16 * 1024; // warp kernel by default (mea
 // BR_SHUFFLE_KERNEL=small|resolve|warp|hash|mid|pipe|large|global restricts the dispatch below to one
 // shuffle kernel where it is eligible (tests cover every kernel; A/B timing).  Unset: the
 // first eligible kernel in the order below.
-enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL, K_WARP, K_WARP64 };
+enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL, K_WARP, K_WARP64, K_IDX };
 int forced_kernel() {
     const char *e = getenv("BR_SHUFFLE_KERNEL");
     if (!e || !*e) return K_ANY;
-    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global", "warp", "warp64"};
-    for (int i = 1; i <= K_WARP64; ++i)
+    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global", "warp", "warp64", "idx"};
+    for (int i = 1; i <= K_IDX; ++i)
         if (!strcmp(e, names[i])) return i;
     return K_ANY;
+}
+
+// staging buffers per CTA of the index-permutation kernel (BR_IDX_STAGES, default 2)
+int idx_stages() {
+    const char *e = getenv("BR_IDX_STAGES");
+    const int v = e ? atoi(e) : 2;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
 }
 
 inline bool allow(int k) {
@@ -550,6 +557,47 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
     // one warp per array (warp_shuffle.cuh): the default for many arrays of up to 16 KB
     // (12 arrays per SM; C4 1.93 vs 2.49 ms for the hash kernel).  Beyond that too few
     // arrays fit per SM and the CTA groups of the hash kernel win.
+    // u16 index permutations, one CTA of NW warps per SM sharing staging buffers
+    // (warp_shuffle.cuh shuffle_idx_kernel).  By default when that gives at least 12 arrays
+    // per SM and 1.5x the warp kernel's (C4: 20 vs 12 arrays per SM, 1.84 vs 1.93 ms; u64[4096]:
+    // 17 per SM, 1.19 ms vs 1.59 for the hash kernel); DESIGN.md section 4.
+    if ((forced_kernel() == K_IDX || forced_kernel() == K_ANY) && cp.plan.brec && segmented && n <= 65536 &&
+        (uint64_t)cp.plan.max_k * 32 + 64 <= WRING) {
+        const int cm = gen == 2 ? 1 : 0;
+        const void *kp = gen == 2 ? (const void *)shuffle_idx_kernel<T, 1> : (const void *)shuffle_idx_kernel<T, 0>;
+        int dev = 0, optin = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        const int nstage = idx_stages();
+        const size_t selems = (n + 3) & ~(uint64_t)3;
+        const size_t sbytes = (selems * sizeof(T) + 15) & ~(size_t)15;
+        const size_t per_warp = ((2 * n + 15) & ~(uint64_t)15) + idx_warp_fixed(cm);
+        const size_t fixed = (size_t)nstage * sbytes + IDX_CTL_BYTES;
+        if ((size_t)optin > fixed + per_warp) {
+            int nw = (int)std::min<size_t>(24, ((size_t)optin - fixed) / per_warp);
+            // arrays per SM the one-warp-per-array kernel would hold (0: not eligible)
+            const size_t zb = (n * sizeof(T) + 15) & ~(uint64_t)15;
+            const int warp_chains = zb <= WARP_SMEM_DEFAULT ? (int)std::min<size_t>(32, (size_t)optin / (zb + 2624)) : 0;
+            const bool pick = forced_kernel() == K_IDX || (nw >= 12 && 2 * nw >= 3 * warp_chains);
+            const int64_t need = (num_arrays + di.sms - 1) / di.sms;  // warps per SM that have work
+            if (need < nw) nw = (int)std::max<int64_t>(1, need);
+            if (pick) {
+                const size_t smem = fixed + (size_t)nw * per_warp;
+                CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                const int64_t ctas = (num_arrays + nw - 1) / nw;
+                const int grid = (int)std::min<int64_t>(ctas, di.sms);
+                const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+                T *dp = (T *)data;
+                DevPlan plan = cp.plan;
+                int ns = nstage;
+                void *args[] = {&dp, &num_arrays, &plan, &run_seed, &base, &words32, (void *)&use_tma, &gen, &ns};
+                CK(cudaLaunchKernel(kp, dim3(grid), dim3(32 * nw), args, smem, st));
+                g_kernel = std::string("shuffle_idx_kernel<u") + std::to_string(8 * sizeof(T)) + "," + std::to_string(nw) +
+                           ">";
+                return BR_OK;
+            }
+        }
+    }
     if (forced_kernel() == K_WARP64 && cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
         (uint64_t)cp.plan.max_k * 32 + 128 <= WRING64) {
         auto kern = gen == 2 ? shuffle_warp_kernel<T, true, 1, 64> : shuffle_warp_kernel<T, true, 0, 64>;

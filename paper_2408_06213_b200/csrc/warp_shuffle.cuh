@@ -19,6 +19,9 @@ namespace br {
 #ifndef BR_WARP_EXACT
 #define BR_WARP_EXACT 1
 #endif
+#ifndef BR_IDX_SLEEP
+#define BR_IDX_SLEEP 256  // ns a warp sleeps after finding every staging buffer taken
+#endif
 // 256 entries hold the current and next group and one generation step for k <= 6 (the
 // default schedule); with the 1 KB target table that keeps 12 arrays of 16 KB per SM
 static constexpr uint32_t WRING = BR_WARP_EXACT ? 256 : 512;
@@ -88,6 +91,12 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
     uint16_t v;
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
     return v;
+}
+__device__ __forceinline__ void lds_v(uint32_t a, uint16_t &v) {
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void sts_v(uint32_t a, uint16_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
 }
 __device__ __forceinline__ void lds_v(uint32_t a, uint32_t &v) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -336,22 +345,36 @@ __device__ __forceinline__ void warp_apply_group(T *z, const uint16_t *ring, uin
     __syncwarp();
 }
 
-template <typename T, bool SEGMENTED, bool CHA, int GS>
+// IDX: the warp shuffles a u16 index permutation of the array (2 bytes per element in shared
+// memory instead of sizeof(T)), then applies it to the payload through one of the CTA's
+// shared staging buffers: more arrays per SM (shuffle_idx_kernel).
+template <typename T, bool SEGMENTED, bool CHA, int GS, bool IDX = false>
 __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
                                                   uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
                                                   uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
-                                                  int use_tma, int gen, T *z, uint16_t *ring, int8_t *P,
-                                                  int8_t *tbl, uint64_t &bar, uint64_t *chawin) {
+                                                  int use_tma, int gen, std::conditional_t<IDX, uint16_t, T> *z,
+                                                  uint16_t *ring, int8_t *P, int8_t *tbl, uint64_t &bar,
+                                                  uint64_t *chawin, T *stage = nullptr, uint32_t *locks = nullptr,
+                                                  int nstage = 0, uint32_t stage_elems = 0) {
+    using E = std::conditional_t<IDX, uint16_t, T>;  // element type of the array being permuted
     const int lane = threadIdx.x & 31;
-    if (use_tma && lane == 0) mbar_init(&bar, 1);
+    if (!IDX && use_tma && lane == 0) mbar_init(&bar, 1);
     __syncwarp();
     const uint32_t n = plan.n;
     const uint32_t bytes = n * (uint32_t)sizeof(T);
     const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
     uint32_t parity = 0;
-    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+    const int64_t a0 = IDX ? (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) : blockIdx.x;
+    const int64_t astep = IDX ? (int64_t)gridDim.x * (blockDim.x >> 5) : gridDim.x;
+    for (int64_t a = a0; a < num_arrays; a += astep) {
         T *g = data + a * (int64_t)n;
-        if (use_tma) {
+        if constexpr (IDX) {
+            // identity permutation; the payload is pulled into L2 for the staging copy
+            if (use_tma && lane == 0)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+            for (uint32_t p = lane; 2 * p < n; p += 32)
+                reinterpret_cast<uint32_t *>(z)[p] = (2 * p) | ((2 * p + 1) << 16);
+        } else if (use_tma) {
             if (lane == 0) {
                 bulk_wait_read();  // the previous array's bulk store has read z
                 fence_proxy_async();
@@ -396,7 +419,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
         uint64_t *rkf = SEGMENTED ? nullptr : rk_first;
         // the first targets are generated while the payload streams in
         if (plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
-        if (use_tma) {
+        if (!IDX && use_tma) {
             mbar_wait(&bar, parity);
             parity ^= 1u;
         }
@@ -425,7 +448,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                     __syncwarp();
                     w64_targets(rs, ts, nt, lim, lane, na, nb, sa, sb);
                 }
-                w64_apply<T>(zs, ps, t, lim, lane, ca, cb, csa, csb);
+                w64_apply<E>(zs, ps, t, lim, lane, ca, cb, csa, csb);
                 if (!last) w64_same(nt, lim, lane, na, nb, sa, sb, nsa, nsb);
                 return last;
             };
@@ -463,7 +486,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                     __syncwarp();
                     warp_group_targets(rs, ts, nt, lim, lane, jn, shn);
                 }
-                warp_apply_group_exact<T>(zs, ps, t, lim, lane, jc, sc);
+                warp_apply_group_exact<E>(zs, ps, t, lim, lane, jc, sc);
                 if (!last) sn = warp_group_same(nt, lim, lane, jn, shn);
                 return last;
             };
@@ -480,13 +503,62 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
         for (uint32_t top = n - 1; n > lim; top -= 32) {
             const uint32_t need = top - lim >= 31 ? top - 31 : lim;
             while (gs.frontier > need && gs.B0 < plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
-            warp_apply_group<T>(z, ring, top, lim, lane);
+            warp_apply_group<E>(z, ring, top, lim, lane);
             if (top < lim + 32) break;
         }
 #endif
         // finish the word accounting (a trailing rejection can follow the last position)
         while (gs.B0 < plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
-        if (use_tma) {
+        if constexpr (IDX) {
+            // take a free staging buffer, copy the payload in, write out[p] = payload[idx[p]]
+            int sb = 0;
+            if (lane == 0) {
+                for (;;) {
+                    if (atomicCAS(&locks[sb], 0u, 1u) == 0u) break;
+                    if (++sb == nstage) {
+                        sb = 0;
+                        __nanosleep(BR_IDX_SLEEP);  // a spinning warp takes issue slots from the shuffling ones
+                    }
+                }
+            }
+            sb = __shfl_sync(FULL, sb, 0);
+            __syncwarp();
+            T *buf = stage + (size_t)sb * stage_elems;
+            if (use_tma) {  // one bulk copy; the stage's mbarrier phase lives next to its lock
+                uint64_t *sbar = reinterpret_cast<uint64_t *>(locks + 16) + sb;
+                const uint32_t ph = locks[8 + sb];
+                if (lane == 0) {
+                    fence_proxy_async();  // the previous holder's generic reads of buf come first
+                    mbar_arrive_expect_tx(sbar, bytes);
+                    bulk_load(buf, g, bytes, sbar);
+                }
+                mbar_wait(sbar, ph);
+                if (lane == 0) locks[8 + sb] = ph ^ 1u;
+            } else {
+                warp_copy(buf, g, n, lane);
+            }
+            __syncwarp();
+            if (use_tma && (n & 3u) == 0) {  // 16-byte aligned payload: 4 elements per lane step
+#pragma unroll 4
+                for (uint32_t q = lane; 4 * q < n; q += 32) {
+                    const uint2 iv = reinterpret_cast<const uint2 *>(z)[q];
+                    const T v0 = buf[iv.x & 0xFFFFu], v1 = buf[iv.x >> 16], v2 = buf[iv.y & 0xFFFFu], v3 = buf[iv.y >> 16];
+                    if constexpr (sizeof(T) == 4) {
+                        reinterpret_cast<uint4 *>(g)[q] = make_uint4((uint32_t)v0, (uint32_t)v1, (uint32_t)v2, (uint32_t)v3);
+                    } else {
+                        reinterpret_cast<ulonglong2 *>(g)[2 * q] = make_ulonglong2((uint64_t)v0, (uint64_t)v1);
+                        reinterpret_cast<ulonglong2 *>(g)[2 * q + 1] = make_ulonglong2((uint64_t)v2, (uint64_t)v3);
+                    }
+                }
+            } else {
+                for (uint32_t p = lane; p < n; p += 32) g[p] = buf[z[p]];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                atomicExch(&locks[sb], 0u);
+            }
+        } else if (use_tma) {
             if (lane == 0) {
                 fence_proxy_async();
                 bulk_store(g, z, bytes);
@@ -507,7 +579,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
         }
         __syncwarp();
     }
-    if (use_tma && lane == 0) bulk_wait_all();
+    if (!IDX && use_tma && lane == 0) bulk_wait_all();
 }
 
 // CM as in shuffle_mid_kernel: 0 = PCG64/Lehmer, 1 = ChaCha, 2 = from the stream state's tag
@@ -532,6 +604,53 @@ __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, 
     else if (CM != 1)
         shuffle_warp_body<T, SEGMENTED, false, GS>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                                rk_first, use_tma, gen, z, ring, P, tbl, bar, chawin);
+}
+
+// Many arrays, u16 index permutations (IDX mode of shuffle_warp_body): one CTA per SM of NW
+// warps, each warp its own arrays; dynamic shared memory = nstage staging buffers (payload
+// of one array each, shared by the CTA's warps under a lock) + 16 B of locks + per warp
+// { u16 index array, target ring, equality table, Pred bytes, ChaCha window }.
+constexpr uint32_t idx_warp_fixed(int cm) { return 2 * WRING + WTBL + 32 + (cm ? 256 * 8 : 0); }
+constexpr uint32_t IDX_CTL_BYTES = 128;  // 8 locks, 8 phases, 8 mbarriers
+
+
+template <typename T, int CM>
+__global__ void __launch_bounds__(768, 1) shuffle_idx_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
+                                                           uint64_t run_seed, int64_t base,
+                                                           uint32_t *__restrict__ words32, int use_tma, int gen,
+                                                           int nstage) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t n = plan.n;
+    const uint32_t selems = (n + 3u) & ~3u;
+    const uint32_t sbytes = (uint32_t)(((uint64_t)selems * sizeof(T) + 15u) & ~15ull);
+    const uint32_t ibytes = (2u * n + 15u) & ~15u;
+    unsigned char *p = smem_raw;
+    T *stage = reinterpret_cast<T *>(p);
+    p += (size_t)nstage * sbytes;
+    // locks[0..7], mbarrier phases [8..15], mbarriers (u64) from word 16
+    uint32_t *locks = reinterpret_cast<uint32_t *>(p);
+    p += IDX_CTL_BYTES;
+    unsigned char *mine = p + (size_t)(threadIdx.x >> 5) * (ibytes + idx_warp_fixed(CM));
+    uint16_t *idx = reinterpret_cast<uint16_t *>(mine);
+    uint16_t *ring = reinterpret_cast<uint16_t *>(mine + ibytes);
+    int8_t *tbl = reinterpret_cast<int8_t *>(mine + ibytes + 2 * WRING);
+    int8_t *P = tbl + WTBL;
+    uint64_t *chawin = reinterpret_cast<uint64_t *>(P + 32);
+    if (threadIdx.x < (unsigned)nstage) {
+        locks[threadIdx.x] = 0u;
+        locks[8 + threadIdx.x] = 0u;
+        mbar_init(reinterpret_cast<uint64_t *>(locks + 16) + threadIdx.x, 1);
+    }
+    __syncthreads();
+    uint64_t bar = 0;
+    if constexpr (CM == 1)
+        shuffle_warp_body<T, true, true, 32, true>(data, num_arrays, plan, run_seed, base, words32, nullptr, nullptr,
+                                                   nullptr, use_tma, gen, idx, ring, P, tbl, bar, chawin, stage,
+                                                   locks, nstage, selems);
+    else
+        shuffle_warp_body<T, true, false, 32, true>(data, num_arrays, plan, run_seed, base, words32, nullptr,
+                                                    nullptr, nullptr, use_tma, gen, idx, ring, P, tbl, bar, chawin,
+                                                    stage, locks, nstage, selems);
 }
 
 }  // namespace br

@@ -263,7 +263,7 @@ def test_c4_sample(B, O, golden):
     n, na = 4096, 1 << 16
     data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
     _, words = B.shuffle_many(data, n, 99, return_words=True)
-    assert "shuffle_warp_kernel" in B.last_kernel()
+    assert "shuffle_idx_kernel" in B.last_kernel()
     got = u32(data).reshape(na, n)
     w = u32(words)
     for rec in golden["c4"]:
@@ -288,6 +288,7 @@ KERNEL_CASES = {  # forced kernel -> (name in last_kernel, lengths it can take)
     "global": ("shuffle_large_gen_kernel", (2, 64, 1000, 4096, 70000)),
     "warp": ("shuffle_warp_kernel", (2, 33, 64, 1000, 4096, 6000, 12000)),
     "warp64": ("shuffle_warp_kernel", (2, 33, 64, 65, 127, 1000, 4096, 6000, 12000)),
+    "idx": ("shuffle_idx_kernel", (2, 33, 64, 65, 127, 1000, 4096, 4097, 6000, 12000)),
 }
 
 
