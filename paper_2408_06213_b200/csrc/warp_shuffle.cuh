@@ -9,22 +9,17 @@
 //     (warp_apply_group_exact): equal targets through a byte table instead of MATCH.ANY,
 //     predecessor chains through 32 bytes of shared memory and shuffles, no serial replay;
 //   * the next group's targets and equality mask are prepared around the current group.
-// The earlier form (BR_WARP_EXACT=0: independent swaps plus serial replay of "dirty" lanes)
-// is kept for A/B timing.
 #pragma once
 #include "shuffle.cuh"
 
 namespace br {
 
-#ifndef BR_WARP_EXACT
-#define BR_WARP_EXACT 1
-#endif
 #ifndef BR_IDX_SLEEP
 #define BR_IDX_SLEEP 256  // ns a warp sleeps after finding every staging buffer taken
 #endif
 // 256 entries hold the current and next group and one generation step for k <= 6 (the
 // default schedule); with the 1 KB target table that keeps 12 arrays of 16 KB per SM
-static constexpr uint32_t WRING = BR_WARP_EXACT ? 256 : 512;
+static constexpr uint32_t WRING = 256;
 
 struct WarpGen {
     u128 s, inc, A32, C32;
@@ -309,42 +304,6 @@ __device__ __forceinline__ void w64_apply(uint32_t z, uint32_t P, uint32_t top, 
     __syncwarp();
 }
 
-// steps top, top-1, ..., max(top-31, lim) of z[i] <-> z[J[i]] (i descending)
-template <typename T>
-__device__ __forceinline__ void warp_apply_group(T *z, const uint16_t *ring, uint32_t top, uint32_t lim, int lane) {
-    const bool act = (uint32_t)lane <= top - lim;
-    const uint32_t i = top - lane;
-    const uint32_t lo = top - lim >= 31 ? top - 31 : lim;
-    uint32_t j = 0;
-    T vi = T(0), vj = T(0);
-    if (act) {
-        j = ring[i & (WRING - 1)];
-        vi = z[i];
-        vj = z[j];
-    }
-    const unsigned same = __match_any_sync(FULL, act ? j : 0x10000u + lane);
-    const bool inr = act && j >= lo && j != i;  // the target is another lane's position
-    const unsigned hit = __reduce_or_sync(FULL, inr ? 1u << (top - j) : 0u);
-    const bool dirty = act && (same != (1u << lane) || inr || ((hit >> lane) & 1u));
-    const unsigned dm = __ballot_sync(FULL, dirty);
-    if (act && !dirty) {
-        z[i] = vj;
-        z[j] = vi;
-    }
-    if (dm) {
-        __syncwarp();
-        for (unsigned m = dm; m; m &= m - 1) {
-            if (lane == __ffs(m) - 1) {
-                const T a = z[i], c = z[j];
-                z[i] = c;
-                z[j] = a;
-            }
-            __syncwarp();
-        }
-    }
-    __syncwarp();
-}
-
 // IDX: the warp shuffles a u16 index permutation of the array (2 bytes per element in shared
 // memory instead of sizeof(T)), then applies it to the payload through one of the CTA's
 // shared staging buffers: more arrays per SM (shuffle_idx_kernel).
@@ -424,7 +383,6 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
             parity ^= 1u;
         }
         __syncwarp();
-#if BR_WARP_EXACT
         if (GS == 64 && n > lim) {
             uint32_t top = n - 1, ja, jb;
             uint64_t sma, smb;
@@ -499,14 +457,6 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                 top -= 32;
             }
         }
-#else
-        for (uint32_t top = n - 1; n > lim; top -= 32) {
-            const uint32_t need = top - lim >= 31 ? top - 31 : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
-            warp_apply_group<E>(z, ring, top, lim, lane);
-            if (top < lim + 32) break;
-        }
-#endif
         // finish the word accounting (a trailing rejection can follow the last position)
         while (gs.B0 < plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
         if constexpr (IDX) {
@@ -593,7 +543,7 @@ __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, 
     __shared__ __align__(16) uint16_t ring[GS == 64 ? WRING64 : WRING];
     __shared__ __align__(8) uint64_t bar;
     __shared__ int8_t P[GS];
-    __shared__ int8_t tbl[BR_WARP_EXACT ? (GS == 64 ? WTBL64 : WTBL) : 1];
+    __shared__ int8_t tbl[GS == 64 ? WTBL64 : WTBL];
     __shared__ __align__(16) uint64_t chawin[CM ? 256 : 2];
     T *z = reinterpret_cast<T *>(smem_raw);
     bool cha = CM == 1;
