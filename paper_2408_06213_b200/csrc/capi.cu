@@ -577,7 +577,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
             int nw = (int)std::min<size_t>(24, ((size_t)optin - fixed) / per_warp);
             // arrays per SM the one-warp-per-array kernel would hold (0: not eligible)
             const size_t zb = (n * sizeof(T) + 15) & ~(uint64_t)15;
-            const int warp_chains = zb <= WARP_SMEM_DEFAULT ? (int)std::min<size_t>(32, (size_t)optin / (zb + 2624)) : 0;
+            const int warp_chains = zb <= WARP_SMEM_DEFAULT ? (int)std::min<size_t>(32, (size_t)optin / (zb + 2656)) : 0;
             const bool pick = forced_kernel() == K_IDX || (nw >= 12 && 2 * nw >= 3 * warp_chains);
             const int64_t need = (num_arrays + di.sms - 1) / di.sms;  // warps per SM that have work
             if (need < nw) nw = (int)std::max<int64_t>(1, need);

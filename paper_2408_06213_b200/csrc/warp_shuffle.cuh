@@ -126,12 +126,16 @@ static constexpr uint32_t WTBL = 1024;
 // issue: targets and the slot read-back (consumed after the current group's swaps)
 __device__ __forceinline__ void warp_group_targets(uint32_t ring, uint32_t tbl, uint32_t top, uint32_t lim,
                                                    int lane, uint32_t &j, bool &shared_slot) {
+    // branch-free (every lane loads and stores; a branch here costs reconvergence and a
+    // divergence check before each of the group's warp intrinsics): an inactive lane reads
+    // a wrapped ring entry it ignores and writes its own private byte after the table
     const bool act = (uint32_t)lane <= top - lim;
-    j = act ? lds_u16(ring + 2u * ((top - lane) & (WRING - 1))) : 0u;
-    const uint32_t slot = tbl + (j & (WTBL - 1));
-    if (act) sts_s8(slot, lane);
+    const uint32_t jr = lds_u16(ring + 2u * ((top - lane) & (WRING - 1)));
+    j = act ? jr : 0u;
+    const uint32_t slot = act ? tbl + (jr & (WTBL - 1)) : tbl + WTBL + (uint32_t)lane;
+    sts_s8(slot, lane);
     __syncwarp();
-    shared_slot = act && lds_s8(slot) != lane;
+    shared_slot = lds_s8(slot) != lane;
 }
 
 // finish: split the lanes of shared slots by exact target
@@ -165,11 +169,9 @@ __device__ __forceinline__ void warp_apply_group_exact(uint32_t z, uint32_t P, u
     const bool act = (uint32_t)lane <= top - lim;
     const uint32_t i = top - lane;
     const uint32_t lo = top - lim >= 31 ? top - 31 : lim;
-    T vi = T(0), vj = T(0);
-    if (act) {
-        lds_v(z + E * i, vi);
-        lds_v(z + E * j, vj);
-    }
+    T vi, vj;
+    lds_v(z + E * (act ? i : top), vi);  // inactive lanes (j = 0) load values nobody uses
+    lds_v(z + E * j, vj);
     const unsigned below = same & ((1u << lane) - 1u);
     const unsigned above = same & ~((2u << lane) - 1u);  // later lanes (lane 31: 2u << 31 == 0)
     const bool inr = act && j >= lo && j != i;            // j = i_l' of a later lane l' = top - j
@@ -192,10 +194,8 @@ __device__ __forceinline__ void warp_apply_group_exact(uint32_t z, uint32_t P, u
     }
     const int tl = below ? 31 - __clz(below) : lane;
     const T Bt = shfl_t<T>(A, tl);
-    if (act) {
-        sts_v(z + E * i, below ? Bt : vj);
-        if (!above && j < lo) sts_v(z + E * j, A);
-    }
+    if (act) sts_v(z + E * i, below ? Bt : vj);
+    if (act && !above && j < lo) sts_v(z + E * j, A);
     __syncwarp();
 }
 
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, 
     __shared__ __align__(16) uint16_t ring[GS == 64 ? WRING64 : WRING];
     __shared__ __align__(8) uint64_t bar;
     __shared__ int8_t P[GS];
-    __shared__ int8_t tbl[GS == 64 ? WTBL64 : WTBL];
+    __shared__ int8_t tbl[GS == 64 ? WTBL64 : WTBL + 32];
     __shared__ __align__(16) uint64_t chawin[CM ? 256 : 2];
     T *z = reinterpret_cast<T *>(smem_raw);
     bool cha = CM == 1;
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, 
 // warps, each warp its own arrays; dynamic shared memory = nstage staging buffers (payload
 // of one array each, shared by the CTA's warps under a lock) + 16 B of locks + per warp
 // { u16 index array, target ring, equality table, Pred bytes, ChaCha window }.
-constexpr uint32_t idx_warp_fixed(int cm) { return 2 * WRING + WTBL + 32 + (cm ? 256 * 8 : 0); }
+constexpr uint32_t idx_warp_fixed(int cm) { return 2 * WRING + WTBL + 32 + 32 + (cm ? 256 * 8 : 0); }
 constexpr uint32_t IDX_CTL_BYTES = 128;  // 8 locks, 8 phases, 8 mbarriers
 
 
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(768, 1) shuffle_idx_kernel(T *__restrict__ dat
     uint16_t *idx = reinterpret_cast<uint16_t *>(mine);
     uint16_t *ring = reinterpret_cast<uint16_t *>(mine + ibytes);
     int8_t *tbl = reinterpret_cast<int8_t *>(mine + ibytes + 2 * WRING);
-    int8_t *P = tbl + WTBL;
+    int8_t *P = tbl + WTBL + 32;  // the table's last 32 bytes: inactive lanes' private slots
     uint64_t *chawin = reinterpret_cast<uint64_t *>(P + 32);
     if (threadIdx.x < (unsigned)nstage) {
         locks[threadIdx.x] = 0u;
