@@ -11,6 +11,7 @@
 //   * the next group's targets and equality mask are prepared around the current group.
 #pragma once
 #include "shuffle.cuh"
+#include <type_traits>
 
 namespace br {
 
@@ -50,7 +51,21 @@ __device__ __forceinline__ void warp_gen_step(WarpGen &g, const DevPlan &plan, u
             ring[pos & (RS - 1)] = (uint16_t)j1;
             ring[(pos - 1) & (RS - 1)] = (uint16_t)j2;
         } else {
-            for (uint32_t m = 0; m < k; ++m) ring[(pos - m) & (RS - 1)] = (uint16_t)die(nbb - m, r);
+            // unrolled for the default schedule's k (k changes only at regime edges)
+            auto dice = [&](auto K) {
+#pragma unroll
+                for (uint32_t m = 0; m < decltype(K)::value; ++m)
+                    ring[(pos - m) & (RS - 1)] = (uint16_t)die(nbb - m, r);
+            };
+            switch (k) {
+            case 2: dice(std::integral_constant<uint32_t, 2>{}); break;
+            case 3: dice(std::integral_constant<uint32_t, 3>{}); break;
+            case 4: dice(std::integral_constant<uint32_t, 4>{}); break;
+            case 5: dice(std::integral_constant<uint32_t, 5>{}); break;
+            case 6: dice(std::integral_constant<uint32_t, 6>{}); break;
+            default:
+                for (uint32_t m = 0; m < k; ++m) ring[(pos - m) & (RS - 1)] = (uint16_t)die(nbb - m, r);
+            }
         }
         low = nbb - k;
         fail = r < t;
@@ -64,7 +79,7 @@ __device__ __forceinline__ void warp_gen_step(WarpGen &g, const DevPlan &plan, u
     if (fm == 0) {
         g.B0 += 32;
         if constexpr (CHA) g.s = cha_add(g.s, 32);
-        else g.s = mad128(g.s, g.A32, g.C32);
+        else g.s = mad128_wide(g.s, g.A32, g.C32);  // 17 SASS instructions against 25
     } else {
         const int l = __ffs(fm) - 1;
         g.B0 += l;
