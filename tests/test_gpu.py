@@ -329,6 +329,24 @@ def test_every_shuffle_kernel(B, O, monkeypatch, kernel, gen):
             assert np.array_equal(u32(z), zr), (kernel, n, B.last_kernel())
 
 
+@pytest.mark.parametrize("kernel", ["idx", "warp", "hash", "small"])
+def test_lehmer_segmented_kernels(B, O, monkeypatch, kernel):
+    """Lehmer128 streams (increment 0) through the shared-memory shuffle kernels, u32 and u64,
+    including partial last groups and arrays whose index permutation spans every group."""
+    monkeypatch.setenv("BR_SHUFFLE_KERNEL", kernel)
+    for n in ((33, 100, 127) if kernel == "small" else (33, 1000, 4096, 5003)):
+        for eb in (4, 8):
+            na = max(2, min(40, (1 << 18) // n))
+            dt = np.uint32 if eb == 4 else np.uint64
+            payload = np.arange(n * na, dtype=dt) * 3 + 1
+            dev = torch.from_numpy(payload.view(np.int32 if eb == 4 else np.int64).copy()).cuda()
+            _, w = B.shuffle_many(dev, n, 2718, array_index_base=5, return_words=True, generator="lehmer")
+            ref = payload.copy()
+            rw = O.shuffle_segmented(ref, n, 2718, array_index_base=5, generator="lehmer")
+            assert np.array_equal(dev.cpu().numpy().view(dt), ref), (kernel, n, eb, B.last_kernel())
+            assert np.array_equal(u32(w), rw), (kernel, n, eb)
+
+
 @pytest.mark.parametrize("eb", [4, 8])
 @pytest.mark.parametrize("n", [2, 3, 5, 7, 8, 9, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 255, 256, 257, 511,
                                512, 513, 1000, 2047, 2048, 2049, 4095, 4097, 10000, 16384])
