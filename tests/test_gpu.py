@@ -329,6 +329,25 @@ def test_every_shuffle_kernel(B, O, monkeypatch, kernel, gen):
             assert np.array_equal(u32(z), zr), (kernel, n, B.last_kernel())
 
 
+@pytest.mark.parametrize("kernel", ["idx", "warp", "hash", "small", "large"])
+def test_unaligned_payload(B, O, monkeypatch, kernel):
+    """Payload starting 4 bytes past a 16-byte boundary: the kernels fall back from bulk (TMA)
+    copies and 16-byte stores to element copies; results unchanged."""
+    monkeypatch.setenv("BR_SHUFFLE_KERNEL", kernel)
+    for n in ((64, 100) if kernel == "small" else (1000, 4096)):
+        na = 24
+        payload = np.arange(n * na, dtype=np.uint32) ^ 0x5A5A
+        big = torch.zeros(n * na + 4, dtype=torch.int32, device="cuda")
+        big[1:1 + n * na] = torch.from_numpy(payload.view(np.int32).copy()).cuda()
+        view = big[1:1 + n * na]
+        assert view.data_ptr() % 16 == 4
+        B.shuffle_many(view, n, 99, array_index_base=3)
+        ref = payload.copy()
+        O.shuffle_segmented(ref, n, 99, array_index_base=3)
+        assert np.array_equal(view.cpu().numpy().view(np.uint32), ref), (kernel, n, B.last_kernel())
+        assert int(big[0]) == 0 and int(big[-1]) == 0 and int(big[-2]) == 0 and int(big[-3]) == 0
+
+
 @pytest.mark.parametrize("kernel", ["idx", "warp", "hash", "small"])
 def test_lehmer_segmented_kernels(B, O, monkeypatch, kernel):
     """Lehmer128 streams (increment 0) through the shared-memory shuffle kernels, u32 and u64,
