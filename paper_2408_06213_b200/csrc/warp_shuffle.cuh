@@ -1,5 +1,10 @@
 // warp_shuffle.cuh -- one warp per shared-memory-resident array, 32 Fisher-Yates steps per
-// warp step: the default for many arrays of up to 16 KB (C4: 65,536 x u32[4096]).
+// warp step, in two kernels:
+//   * shuffle_warp_kernel: the array itself in shared memory, one warp per CTA (many arrays
+//     of up to 16 KB);
+//   * shuffle_idx_kernel: a u16 index permutation per warp, NW warps per CTA, the payload
+//     applied at the end through shared staging buffers (C4: 65,536 x u32[4096], 20 arrays
+//     per SM instead of 12).
 //
 // Same algorithm as shuffle.cuh (shuffle.py:100-225: batches of k dice, rejection re-draws
 // the batch from the next word), built for few instructions and short dependency chains:
