@@ -348,9 +348,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
     for (int64_t a = a0; a < num_arrays; a += astep) {
         T *g = data + a * (int64_t)n;
         if constexpr (IDX) {
-            // identity permutation; the payload is pulled into L2 for the staging copy
-            if (use_tma && lane == 0)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+            // identity permutation (an L2 prefetch of the payload here or later measured no gain)
             for (uint32_t p = lane; 2 * p < n; p += 32)
                 reinterpret_cast<uint32_t *>(z)[p] = (2 * p) | ((2 * p + 1) << 16);
         } else if (use_tma) {
