@@ -143,13 +143,15 @@ __device__ __forceinline__ void sts_s8(uint32_t a, int v) {
 // lane reads only the slot it has just written).
 static constexpr uint32_t WTBL = 1024;
 
-// issue: targets and the slot read-back (consumed after the current group's swaps)
+// issue: targets and the slot read-back (consumed after the current group's swaps).
+// FG: the group is full (top - lim >= 31), so every lane is active.
+template <bool FG = false>
 __device__ __forceinline__ void warp_group_targets(uint32_t ring, uint32_t tbl, uint32_t top, uint32_t lim,
                                                    int lane, uint32_t &j, bool &shared_slot) {
     // branch-free (every lane loads and stores; a branch here costs reconvergence and a
     // divergence check before each of the group's warp intrinsics): an inactive lane reads
     // a wrapped ring entry it ignores and writes its own private byte after the table
-    const bool act = (uint32_t)lane <= top - lim;
+    const bool act = FG || (uint32_t)lane <= top - lim;
     const uint32_t jr = lds_u16(ring + 2u * ((top - lane) & (WRING - 1)));
     j = act ? jr : 0u;
     const uint32_t slot = act ? tbl + (jr & (WTBL - 1)) : tbl + WTBL + (uint32_t)lane;
@@ -159,8 +161,9 @@ __device__ __forceinline__ void warp_group_targets(uint32_t ring, uint32_t tbl, 
 }
 
 // finish: split the lanes of shared slots by exact target
+template <bool FG = false>
 __device__ __forceinline__ unsigned warp_group_same(uint32_t top, uint32_t lim, int lane, uint32_t j, bool shared_slot) {
-    const bool act = (uint32_t)lane <= top - lim;
+    const bool act = FG || (uint32_t)lane <= top - lim;
     unsigned pending = __ballot_sync(FULL, shared_slot);
     unsigned same = 1u << lane;
     while (pending) {
@@ -182,13 +185,13 @@ __device__ __forceinline__ unsigned warp_group_same(uint32_t top, uint32_t lim, 
 //                                      of the group can target i_l, all j are <= their i)
 // z[j_l] = A_l is written by the last lane of each target below the group; targets inside
 // the group are positions whose own lane writes B.  No lane is replayed serially.
-template <typename T>
+template <typename T, bool FG = false>
 __device__ __forceinline__ void warp_apply_group_exact(uint32_t z, uint32_t P, uint32_t top, uint32_t lim, int lane,
                                                        uint32_t j, unsigned same) {
     constexpr uint32_t E = sizeof(T);
-    const bool act = (uint32_t)lane <= top - lim;
+    const bool act = FG || (uint32_t)lane <= top - lim;
     const uint32_t i = top - lane;
-    const uint32_t lo = top - lim >= 31 ? top - 31 : lim;
+    const uint32_t lo = (FG || top - lim >= 31) ? top - 31 : lim;
     T vi, vj;
     lds_v(z + E * (act ? i : top), vi);  // inactive lanes (j = 0) load values nobody uses
     lds_v(z + E * j, vj);
@@ -450,28 +453,39 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
             same = warp_group_same(top, lim, lane, j, sh);
             // one group: issue the next group's targets into jn, swap this one, then finish
             // the next group's equality mask sn (its table read-back hides behind the swaps)
-            auto group = [&](uint32_t t, uint32_t jc, unsigned sc, uint32_t &jn, unsigned &sn) -> bool {
-                const bool last = t < lim + 32;
+            // FG: this group and the next are full (t >= lim + 63): no partial-group predicates
+            auto group = [&](auto FG, uint32_t t, uint32_t jc, unsigned sc, uint32_t &jn, unsigned &sn) -> bool {
+                constexpr bool F = decltype(FG)::value;
+                const bool last = !F && t < lim + 32;
                 const uint32_t nt = t - 32;
                 bool shn = false;
                 if (!last) {
-                    const uint32_t need = nt - lim >= 31 ? nt - 31 : lim;
+                    const uint32_t need = (F || nt - lim >= 31) ? nt - 31 : lim;
                     // the ring has room for the current group, the next and one generation step
                     while (gs.frontier > need && gs.B0 < plan.nbatches)
                         warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
                     __syncwarp();
-                    warp_group_targets(rs, ts, nt, lim, lane, jn, shn);
+                    warp_group_targets<F>(rs, ts, nt, lim, lane, jn, shn);
                 }
-                warp_apply_group_exact<E>(zs, ps, t, lim, lane, jc, sc);
-                if (!last) sn = warp_group_same(nt, lim, lane, jn, shn);
+                warp_apply_group_exact<E, F>(zs, ps, t, lim, lane, jc, sc);
+                if (!last) sn = warp_group_same<F>(nt, lim, lane, jn, shn);
                 return last;
             };
             uint32_t j2;
             unsigned same2;
-            for (;;) {  // unrolled by two: the prefetched values are never copied
-                if (group(top, j, same, j2, same2)) break;
+            using Full = std::true_type;
+            using Part = std::false_type;
+            // unrolled by two: the prefetched values are never copied
+            while (top >= lim + 95) {  // both groups of the pair and their successors are full
+                group(Full{}, top, j, same, j2, same2);
                 top -= 32;
-                if (group(top, j2, same2, j, same)) break;
+                group(Full{}, top, j2, same2, j, same);
+                top -= 32;
+            }
+            for (;;) {
+                if (group(Part{}, top, j, same, j2, same2)) break;
+                top -= 32;
+                if (group(Part{}, top, j2, same2, j, same)) break;
                 top -= 32;
             }
         }
