@@ -638,8 +638,99 @@ def _call_scratch(torch):
     return t
 
 
+def _host_array(z, torch):
+    """A contiguous numpy view of a host array of 4/8-byte items (ndarray or CPU tensor), with
+    a finisher that writes results back; None for device tensors and other containers."""
+    import numpy as np
+
+    if isinstance(z, np.ndarray) and z.dtype.itemsize in (4, 8):
+        if z.flags.c_contiguous:
+            return z.reshape(-1), lambda a: z
+        a = np.ascontiguousarray(z).reshape(-1)
+
+        def fin(b):
+            z[...] = b.reshape(z.shape)
+            return z
+
+        return a, fin
+    if isinstance(z, torch.Tensor) and not z.is_cuda and z.element_size() in (4, 8):
+        t = z.contiguous()
+        a = t.view(-1).numpy()
+        if t.data_ptr() == z.data_ptr():
+            return a, lambda b: z
+
+        def fin(b):
+            z.copy_(torch.from_numpy(b).view(z.shape))
+            return z
+
+        return a, fin
+    return None
+
+
+# one pinned host buffer and one device buffer per thread and device for the single-array
+# calls on host arrays: [state (64 B) | words (8 B) | rk (8 B) | ... | payload from byte 128]
+_STAGE_HDR = 128
+
+
+def _stage_buffers(torch, nbytes):
+    dev = torch.cuda.current_device()
+    cache = getattr(_TLS, "stage", None)
+    if cache is None:
+        cache = _TLS.stage = {}
+    hb, db = cache.get(dev, (None, None))
+    if hb is None or hb.numel() < nbytes:
+        size = max(nbytes, 1 << 16)
+        hb = torch.empty(size, dtype=torch.uint8).pin_memory()
+        db = torch.empty(size, dtype=torch.uint8, device="cuda")
+        cache[dev] = (hb, db)
+    return hb, db
+
+
+def _shuffle_stream_host(source, arr, fin, regimes, unbatched, segments, want_rk, naive, torch):
+    """_shuffle_stream for a host array: state and payload go up in one copy and come back in
+    one copy through pinned staging, with one stream synchronisation per call."""
+    import numpy as np
+
+    st = _state_struct(source)
+    n = arr.size
+    nbytes = _STAGE_HDR + arr.nbytes
+    hb, db = _stage_buffers(torch, nbytes)
+    hnp = hb.numpy()
+    C.memmove(hnp.ctypes.data, C.addressof(st), C.sizeof(st))
+    hnp[_STAGE_HDR:nbytes] = arr.view(np.uint8)
+    db[:nbytes].copy_(hb[:nbytes], non_blocking=True)
+    base = db.data_ptr()
+    sp = _stream_ptr(torch)
+    dz, dstate, dwords, drk = (C.c_void_p(base + _STAGE_HDR), C.c_void_p(base), C.c_void_p(base + 64),
+                               C.c_void_p(base + 72))
+    L = N.lib()
+    if naive:
+        N.check(L.br_shuffle_naive_stream(dz, arr.itemsize, n, dstate, dwords, sp), "shuffle")
+    elif segments is None:
+        regs = regimes if regimes is not None else (N.Regime * 1)()
+        nreg = len(regimes) if regimes is not None else 0
+        N.check(L.br_shuffle_stream(dz, arr.itemsize, n, dstate, regs, nreg, int(unbatched), dwords, sp), "shuffle")
+    else:
+        segs = (N.Segment * len(segments))()
+        for i, (sn, k, cnt) in enumerate(segments):
+            segs[i].start_n, segs[i].k, segs[i].count = sn, k, cnt
+        N.check(L.br_shuffle_stream_segments(dz, arr.itemsize, n, dstate, segs, len(segments), dwords,
+                                             drk if want_rk else None, sp), "shuffle")
+    hb[:nbytes].copy_(db[:nbytes], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    _apply_state(source, N.Pcg64State.from_buffer_copy(bytes(hnp[:C.sizeof(N.Pcg64State)])))
+    arr[...] = hnp[_STAGE_HDR:nbytes].view(arr.dtype)
+    out = fin(arr)
+    if want_rk:
+        return out, int(hnp[72:80].view(np.uint64)[0])
+    return out
+
+
 def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=False, naive=False):
     torch = _torch()
+    host = _host_array(z, torch)
+    if host is not None:
+        return _shuffle_stream_host(source, host[0], host[1], regimes, unbatched, segments, want_rk, naive, torch)
     st = _state_struct(source)
     dev, fin = _device_payload(z, torch)
     n = dev.numel()
@@ -767,18 +858,22 @@ class DeviceStream:
         return st
 
     def write_back(self, source) -> None:
-        st = self.host_state()
-        if _is_fixed(source):
-            used = (st.state_hi << 64) | st.state_lo
-            avail = len(source.words) - source.cursor
-            if used > avail:
-                source.cursor = len(source.words)
-                raise SourceExhausted(f"sequence of {len(source.words)} words over-read")
-            source.cursor += used
-        elif _is_chacha(source):
-            _chacha_set_position(source, (st.state_hi << 64) | st.state_lo)
-        else:
-            source.state = (st.state_hi << 64) | st.state_lo
+        _apply_state(source, self.host_state())
+
+
+def _apply_state(source, st) -> None:
+    """Advance the host source to the device state st (a br_pcg64 head)."""
+    if _is_fixed(source):
+        used = (st.state_hi << 64) | st.state_lo
+        avail = len(source.words) - source.cursor
+        if used > avail:
+            source.cursor = len(source.words)
+            raise SourceExhausted(f"sequence of {len(source.words)} words over-read")
+        source.cursor += used
+    elif _is_chacha(source):
+        _chacha_set_position(source, (st.state_hi << 64) | st.state_lo)
+    else:
+        source.state = (st.state_hi << 64) | st.state_lo
 
 
 class RollBatchesResult(NamedTuple):
