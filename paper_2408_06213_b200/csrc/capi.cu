@@ -674,13 +674,13 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
                    std::to_string(W) + ">";
         return BR_OK;
     }
-    if (allow(K_LARGE) && (uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= LRING) {
+    if (allow(K_LARGE) && (uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= large_ring(LARGE_W)) {
         constexpr int W = LARGE_W;
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
         auto kern = !segmented ? shuffle_cta_large_kernel<T, W, 2>
                                : (gen == 2 ? shuffle_cta_large_kernel<T, W, 1> : shuffle_cta_large_kernel<T, W, 0>);
-        // dynamic shared memory: the ChaCha keystream window (8 words per thread), when there is one
-        const size_t wsmem = (!segmented || gen == 2) ? (size_t)8 * 32 * W * sizeof(uint64_t) : 0;
+        // dynamic shared memory: the CTA's tables and the ChaCha keystream window when there is one
+        const size_t wsmem = large_smem_bytes<T, W>(!segmented || gen == 2);
         CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
         kern<<<grid, 32 * W, wsmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
                                           rk_first, segmented ? 1 : 0, gen);

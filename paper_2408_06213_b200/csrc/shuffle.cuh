@@ -577,7 +577,10 @@ struct CtaGen {
 // Targets are generated in-CTA into a u32 ring (no global target buffer).  Repeated
 // targets are found exactly with one ballot per bit of j in every warp; lane L combines the
 // W*jbits masks through shared memory, which yields T(L) and "later" for any multiplicity.
-static constexpr uint32_t LRING = 4096;  // u32 target ring of the large kernel
+static constexpr uint32_t LRING = 4096;  // u32 target ring of the large kernel (up to 16 warps)
+// ring of the large kernel for W warps: one generation step (32W batches of up to k dice) and
+// one group ahead of the group being applied
+constexpr uint32_t large_ring(int W) { return W > 16 ? 8192u : LRING; }
 #ifndef BR_LARGE_HB
 #define BR_LARGE_HB 11
 #endif
@@ -758,7 +761,8 @@ template <typename T, int W, bool CHA>
 __device__ __forceinline__ void shuffle_cta_large_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
                                                        uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
                                                        uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
-                                                       int segmented, int gen, LargeShared<T, W> &sh,
+                                                       int segmented, int gen,
+                                                       LargeShared<T, W, uint32_t, large_ring(W)> &sh,
                                                        uint64_t *chawin) {
     constexpr int G = 32 * W;
     const int L = threadIdx.x;
@@ -803,15 +807,23 @@ __device__ __forceinline__ void shuffle_cta_large_body(T *__restrict__ data, int
     }
 }
 
+template <typename T, int W>
+constexpr size_t large_smem_bytes(bool chacha) {
+    return ((sizeof(LargeShared<T, W, uint32_t, large_ring(W)>) + 15) & ~(size_t)15) +
+           (chacha ? (size_t)8 * 32 * W * sizeof(uint64_t) : 0);
+}
+
 template <typename T, int W, int CM>
 __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict__ data, int64_t num_arrays,
                                                                    DevPlan plan, uint64_t run_seed, int64_t base,
                                                                    uint32_t *__restrict__ words32, uint64_t *state_io,
                                                                    uint64_t *words64, uint64_t *rk_first,
                                                                    int segmented, int gen) {
-    __shared__ LargeShared<T, W> sh;
-    // the ChaCha keystream window is dynamic shared memory (8 words per thread; size set at launch)
-    extern __shared__ __align__(16) uint64_t chawin[];
+    // dynamic shared memory: the CTA's tables, then the ChaCha keystream window (8 words per
+    // thread) when the launch asks for one; sizes set at launch (large_smem_bytes)
+    extern __shared__ __align__(16) unsigned char large_smem[];
+    auto &sh = *reinterpret_cast<LargeShared<T, W, uint32_t, large_ring(W)> *>(large_smem);
+    uint64_t *chawin = reinterpret_cast<uint64_t *>(large_smem + ((sizeof(sh) + 15) & ~(size_t)15));
     bool cha = CM == 1;
     if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
