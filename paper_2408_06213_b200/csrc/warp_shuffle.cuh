@@ -461,9 +461,13 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                 bool shn = false;
                 if (!last) {
                     const uint32_t need = (F || nt - lim >= 31) ? nt - 31 : lim;
-                    // the ring has room for the current group, the next and one generation step
-                    while (gs.frontier > need && gs.B0 < plan.nbatches)
-                        warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
+                    // the ring has room for the current group, the next and one generation step;
+                    // the common case (targets already there) costs one compare
+                    if (gs.frontier > need) {
+                        do {
+                            warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
+                        } while (gs.frontier > need && gs.B0 < plan.nbatches);
+                    }
                     __syncwarp();
                     warp_group_targets<F>(rs, ts, nt, lim, lane, jn, shn);
                 }
