@@ -59,6 +59,9 @@ INT_PP_PER_ROLL = 7
 # smem bytes per element of a shared-memory-staged shuffle (algorithmic): stage in (4 B),
 # each step reads and writes z[i] and z[j] (16 B), stage out (4 B); u32 payload.
 SMEM_BYTES_PER_ELEM_U32 = 24
+# the index-permutation kernel (u16 indices): identity written (2 B), each step reads and
+# writes two u16 (8 B), payload staged in (4 B), gather reads index and payload (6 B)
+SMEM_BYTES_PER_ELEM_IDX_U32 = 20
 
 
 def int_roofline(rolls_per_s):
@@ -71,14 +74,15 @@ def int_roofline(rolls_per_s):
             "per_roll": INT_PP_PER_ROLL, "peak_source": "measured: profiles/opcost_r1.json (tools/micro/opcost.cu)"}
 
 
-def smem_roofline(elems_per_s):
+def smem_roofline(elems_per_s, kernel=""):
     p = load_profile("smem_r1.json")
     if not p:
         return None
     peak = min(p["lds32_gbs"], p["sts32_gbs"])
-    achieved = elems_per_s * SMEM_BYTES_PER_ELEM_U32 / 1e9
+    per = SMEM_BYTES_PER_ELEM_IDX_U32 if "idx" in kernel else SMEM_BYTES_PER_ELEM_U32
+    achieved = elems_per_s * per / 1e9
     return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "bytes_per_element": SMEM_BYTES_PER_ELEM_U32,
+            "bytes_per_element": per,
             "peak_source": "measured: profiles/smem_r1.json (tools/micro/smem_bw.cu)"}
 
 
@@ -433,7 +437,7 @@ def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
                         "algorithmic_bytes_per_launch": 2 * eb * n * na, "peak_source": kind},
            "clocks": clk.summary(), "gpu_launches": K}
     if eb == 4 and "large" not in kernel:  # payload staged in shared memory
-        res["roofline_smem"] = smem_roofline(n * na / t)
+        res["roofline_smem"] = smem_roofline(n * na / t, kernel)
     if "large" in kernel:  # payload in HBM: random accesses
         res["roofline_random"] = random_roofline((n - 1) * na / t, n * na * eb / 2**20)
     return res
