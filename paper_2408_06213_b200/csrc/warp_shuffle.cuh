@@ -200,12 +200,12 @@ __device__ __forceinline__ void warp_apply_group_exact(uint32_t z, uint32_t P, u
     const bool inr = act && j >= lo && j != i;            // j = i_l' of a later lane l' = top - j
     T A = vi;
     if (__ballot_sync(FULL, inr)) {
-        sts_s8(P + lane, -1);
-        __syncwarp();
+        // P[l] is -1 on entry (set once per kernel, restored below after each use)
         // the latest lane before l' = top - j targeting i_l' (l' itself may target it: a self-swap)
         if (inr && (above & ~(1u << (top - j))) == 0) sts_s8(P + (top - j), lane);
         __syncwarp();
         const int p = lds_s8(P + lane);
+        sts_s8(P + lane, -1);  // ordered before the next group's writes by the syncwarps between
         int r = p >= 0 ? p : lane;
         for (;;) {  // pointer jumping to the root of the Pred chain (Pred(l) < l)
             const int rr = __shfl_sync(FULL, r, r);
@@ -341,6 +341,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
     using E = std::conditional_t<IDX, uint16_t, T>;  // element type of the array being permuted
     const int lane = threadIdx.x & 31;
     if (!IDX && use_tma && lane == 0) mbar_init(&bar, 1);
+    if (GS == 32) P[lane] = -1;  // warp_apply_group_exact's invariant
     __syncwarp();
     const uint32_t n = plan.n;
     const uint32_t bytes = n * (uint32_t)sizeof(T);
