@@ -670,6 +670,7 @@ def _host_array(z, torch):
 # one pinned host buffer and one device buffer per thread and device for the single-array
 # calls on host arrays: [state (64 B) | words (8 B) | rk (8 B) | ... | payload from byte 128]
 _STAGE_HDR = 128
+_STAGE_MAX = 64 << 20  # larger host arrays take the unstaged path (no pinned buffer kept for them)
 
 
 def _stage_buffers(torch, nbytes):
@@ -729,7 +730,7 @@ def _shuffle_stream_host(source, arr, fin, regimes, unbatched, segments, want_rk
 def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=False, naive=False):
     torch = _torch()
     host = _host_array(z, torch)
-    if host is not None:
+    if host is not None and host[0].nbytes <= _STAGE_MAX:
         return _shuffle_stream_host(source, host[0], host[1], regimes, unbatched, segments, want_rk, naive, torch)
     st = _state_struct(source)
     dev, fin = _device_payload(z, torch)
