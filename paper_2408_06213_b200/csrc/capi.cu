@@ -581,10 +581,12 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
             // arrays per SM of the hash kernel (one CTA per array, payload + tables + reserve)
             const size_t hash_cta = zb + sizeof(LargeShared<T, CTA_W, uint16_t, CRING, HASH_HB>) + 1024;
             const int hash_ctas = (int)((size_t)optin / hash_cta);
-            // measured: u32[4096] 20 vs 12 warp-kernel arrays per SM, 1.48 vs 1.52 ms; u32[8192] 9 vs 6
-            // hash CTAs, 1.31 vs 1.45; u64[8192] 5 vs 3, 1.19 vs 1.60; u32[12000] 5 vs 4, 1.59 vs 1.55
+            // measured (idx vs the alternative, arrays per SM and ms): u32[4096] 20 vs 12 (warp),
+            // 1.46 vs 1.52; u32[8192] 9 vs 6 (hash), 1.30 vs 1.45; u32[9000] 8 vs 4, 0.74 vs 0.95;
+            // u32[10000] 7 vs 4, 0.93 vs 1.05; u32[12000] 5 vs 3, 1.61 vs 1.55; u64[8192] 5 vs 3,
+            // 1.19 vs 1.60 (the hash kernel holds 8-byte payloads, the index kernel u16 indices)
             const bool pick = forced_kernel() == K_IDX || (nw >= 12 && 2 * nw >= 3 * warp_chains) ||
-                              (zb > WARP_SMEM_DEFAULT && n <= 8192 && 2 * nw >= 3 * hash_ctas);
+                              (zb > WARP_SMEM_DEFAULT && (nw >= 6 || sizeof(T) == 8) && 2 * nw >= 3 * hash_ctas);
             const int64_t need = (num_arrays + di.sms - 1) / di.sms;  // warps per SM that have work
             if (need < nw) nw = (int)std::max<int64_t>(1, need);
             if (pick) {
