@@ -602,16 +602,17 @@ struct LargeShared {
     uint32_t frontier[2];
 };
 
-template <typename T, int W, typename RT, uint32_t RS, int HB>
+// FG: the group is full (top >= lim + G - 1), every thread has a step
+template <bool FG = false, typename T, int W, typename RT, uint32_t RS, int HB>
 __device__ __forceinline__ void apply_group_cta_global(T *z, LargeShared<T, W, RT, RS, HB> &sh, uint32_t tag,
                                                        uint32_t top, uint32_t lim, int L) {
     constexpr int G = 32 * W;
-    const bool act = top >= lim + (uint32_t)L;  // 32-bit: lim + L < 2^32 for n < 2^32
+    const bool act = FG || top >= lim + (uint32_t)L;  // 32-bit: lim + L < 2^32 for n < 2^32
     const uint32_t i = top - (uint32_t)L;
     const uint32_t j = act ? (uint32_t)sh.ring[i & (RS - 1)] : 0;
     const T vi = act ? z[i] : T(0);
     const T vj = act ? z[j] : T(0);
-    const uint32_t lo_pos = top >= lim + (G - 1) ? top - (G - 1) : lim;
+    const uint32_t lo_pos = (FG || top >= lim + (G - 1)) ? top - (G - 1) : lim;
     const bool inrange = act && j >= lo_pos && j < i;
     // lanes with equal targets meet in a hash slot; each slot keeps a chain of its lanes
     const uint32_t h = (j * 2654435761u) >> (32 - HB);
@@ -1105,7 +1106,8 @@ __device__ __forceinline__ void shuffle_cta_hash_body(T *__restrict__ data, int6
                 tag = 1;
                 __syncthreads();
             }
-            apply_group_cta_global(z, sh, tag, (uint32_t)top, lim, L);
+            if (top >= (int64_t)lim + (G - 1)) apply_group_cta_global<true>(z, sh, tag, (uint32_t)top, lim, L);
+            else apply_group_cta_global<false>(z, sh, tag, (uint32_t)top, lim, L);
         }
         while (gs.B0 < plan.nbatches) large_gen_step<CHA, W>(gs, plan, sh, L, rkf, chawin, ck);
         if (use_tma) {
