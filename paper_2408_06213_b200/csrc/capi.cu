@@ -42,8 +42,6 @@ int fail(int code, const std::string &msg) {
 
 typedef unsigned __int128 h128;
 
-inline u128 to_u128(h128 v) { return mk128((uint64_t)(v >> 64), (uint64_t)v); }
-inline h128 from_u128(u128 v) { return ((h128)v.hi << 64) | v.lo; }
 
 const JumpTables &host_tables() {
     static JumpTables t;
