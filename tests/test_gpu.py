@@ -329,6 +329,34 @@ def test_every_shuffle_kernel(B, O, monkeypatch, kernel, gen):
             assert np.array_equal(u32(z), zr), (kernel, n, B.last_kernel())
 
 
+DISPATCH = [  # (n, item bytes, arrays, kernel the default dispatch picks)
+    (64, 4, 2048, "shuffle_small_kernel"),
+    (1000, 4, 2048, "shuffle_warp_kernel"),
+    (2048, 4, 2048, "shuffle_warp_kernel"),
+    (4096, 4, 4096, "shuffle_idx_kernel"),
+    (4096, 8, 2048, "shuffle_idx_kernel"),
+    (8192, 4, 1024, "shuffle_idx_kernel"),
+    (12000, 4, 512, "shuffle_cta_hash_kernel"),
+    (20000, 4, 256, "shuffle_cta_hash_kernel"),
+    (70000, 8, 8, "shuffle_cta_large_kernel"),
+]
+
+
+@pytest.mark.parametrize("n,eb,na,kernel", DISPATCH)
+def test_default_dispatch(B, O, n, eb, na, kernel):
+    """The size-based kernel choice (measured crossovers) and its result on sampled arrays."""
+    dt = np.uint32 if eb == 4 else np.uint64
+    payload = np.arange(n * na, dtype=dt)
+    dev = torch.from_numpy(payload.view(np.int32 if eb == 4 else np.int64).copy()).cuda()
+    _, w = B.shuffle_many(dev, n, 606, array_index_base=9, return_words=True)
+    assert kernel in B.last_kernel(), (n, eb, B.last_kernel())
+    got = dev.cpu().numpy().view(dt).reshape(na, n)
+    for a in (0, na // 2, na - 1):
+        ref = np.arange(a * n, (a + 1) * n, dtype=dt)
+        rw = O.shuffle_segmented(ref, n, 606, array_index_base=9 + a)
+        assert np.array_equal(got[a], ref) and int(u32(w)[a]) == int(rw[0]), (n, eb, a)
+
+
 @pytest.mark.parametrize("kernel", ["idx", "warp", "hash", "small", "large"])
 def test_unaligned_payload(B, O, monkeypatch, kernel):
     """Payload starting 4 bytes past a 16-byte boundary: the kernels fall back from bulk (TMA)
