@@ -29,6 +29,11 @@ def check_many(n, na, eb, seed):
 kerns = set()
 for n, na, eb in ((64, 300, 4), (100, 70, 8), (1000, 9, 4), (4096, 5, 4), (3000, 3, 8), (20000, 2, 8), (70000, 1, 4)):
     kerns.add(check_many(n, na, eb, 17))
+for forced in ("idx", "warp", "hash"):  # the shared-memory group kernels on partial and full groups
+    os.environ["BR_SHUFFLE_KERNEL"] = forced
+    for n, na, eb in ((33, 40, 8), (1000, 9, 4), (4096, 4, 4), (5003, 3, 8)):
+        kerns.add(check_many(n, na, eb, 23))
+os.environ.pop("BR_SHUFFLE_KERNEL")
 nb = 5000
 bounds = O.gen_bounds(3, 2 * nb)
 bounds[:200:2] = 0xFFFFFFFF
