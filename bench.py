@@ -2,20 +2,21 @@
 """Benchmark of the B200 batched-dice path (BASELINE.json metric: bounded rolls/sec and
 shuffled elements/sec per GPU and box-wide vs roofline).
 
-Headline workload = BASELINE.json configs[1] ("C2"): 2^25 batches of k=2 bounded rolls
-per GPU, bounds iid U[2, 2^16) drawn from seed 7 (2 + roll_single(pcg64(7), 65534),
-generated on the device by our own k=1 roll kernel), roll words from
-pcg64(array_seed(7, 1)).  One step = one bulk roll_batches over the resident bounds (2^26
-rolls).  Inputs (256 MiB bounds) and outputs (256 MiB rolls + 32 MiB words) exceed the
-126 MB L2, so no flush is needed between steps.
+Headline workload = BASELINE.json configs[1] ("C2"): 2^25 batches of k=2 bounded rolls,
+bounds iid U[2, 2^16) drawn from seed 7 (2 + roll_single(pcg64(7), 65534), generated on the
+device by our own k=1 roll kernel), roll words from pcg64(array_seed(7, 1)).  One step = one
+bulk roll_batches over the resident bounds (2^26 rolls).  Inputs (256 MiB bounds) and outputs
+(256 MiB rolls + 32 MiB words) exceed the 126 MB L2, so no flush is needed between steps.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c2|c3|c4|c1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c2|c3|c4|c5]
 
-Under torchrun (N > 1) every rank rolls its own 2^25-batch section of ONE global stream
-(jump-ahead by rank * 2^25 words; weak scaling); the only exchange is an all-gather of the
-per-rank rejection counts.  Secondary lines for the shuffle configs are
-reported under "secondary" (C3 2^20 x 64 u32, C4 65,536 x 4096 u32, C1 one 10,000-element
-stream).
+Under torchrun (N > 1) the job is split (strong scaling): C2's one stream is cut
+into N contiguous batch sections (rank r jumps ahead to its first word; the only exchange is
+the all-gather of per-rank rejection counts, after which a shifted section is re-rolled), and
+the shuffle configs' arrays into N contiguous array ranges (array_index_base; no exchange).
+The shuffle configs C3/C4/C5 (and C1 at N=1) are reported under "secondary", each with its
+roofline, the same-run CPU baseline and an end-to-end number through shuffle_many on pinned
+host buffers.
 """
 
 from __future__ import annotations
@@ -245,19 +246,24 @@ def cpu_cores():
 
 
 # ------------------------------------------------------------------------------ C2 (rolls)
-def setup_c2(torch, B, rank, nb, generator="pcg64"):
-    import numpy as np
+def c2_section(ws, rank):
+    """This rank's contiguous (first_batch, count) of the one C2 stream."""
+    from paper_2408_06213_b200 import shard
 
+    return shard.even_split(NB_C2, ws, rank)
+
+
+def setup_c2(torch, B, first, nb, generator="pcg64"):
     from paper_2408_06213_b200 import _native as N
 
-    # bounds: 2 + roll_single(pcg64(7), 65534), this rank's section of the global sequence
+    # bounds: 2 + roll_single(pcg64(7), 65534), drawn sequentially for the whole job (every
+    # rank draws all 2^26 and keeps its section, so the sequence is exact at any N)
     st = N.Pcg64State()
     N.lib().br_pcg64_seed(7, C.byref(st))
-    N.lib().br_pcg64_advance(C.byref(st), rank * 2 * nb)
     gen = B.DeviceStream.from_struct(st)
-    spans = torch.full((2 * nb,), 65534, dtype=torch.int32, device="cuda")
+    spans = torch.full((2 * NB_C2,), 65534, dtype=torch.int32, device="cuda")
     r = B.roll_batches(gen, spans, 1)
-    bounds = (r.rolls + 2).contiguous()
+    bounds = (r.rolls[2 * first: 2 * (first + nb)] + 2).contiguous()
     del spans, r
     # roll stream: make_source(generator, array_seed(7, 1)) advanced to this rank's first batch
     seed = N.lib().br_array_seed(7, 1)
@@ -267,7 +273,7 @@ def setup_c2(torch, B, rank, nb, generator="pcg64"):
     else:
         st = N.Pcg64State()
         (N.lib().br_lehmer_seed if generator == "lehmer" else N.lib().br_pcg64_seed)(seed, C.byref(st))
-    N.lib().br_pcg64_advance(C.byref(st), rank * nb)
+    N.lib().br_pcg64_advance(C.byref(st), first)
     stream = B.DeviceStream.from_struct(st)
     rolls = torch.empty(2 * nb, dtype=torch.int32, device="cuda")
     words = torch.empty(nb, dtype=torch.uint8, device="cuda")
@@ -279,12 +285,11 @@ def bench_c2(args, torch, B, ws, rank):
     from paper_2408_06213_b200 import _native as N
 
     L = N.lib()
-    nb = NB_C2
-    bounds, stream, rolls, words = setup_c2(torch, B, rank, nb, args.generator)
+    first, nb = c2_section(ws, rank)
+    bounds, stream, rolls, words = setup_c2(torch, B, first, nb, args.generator)
     sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     ptrs = [C.c_void_p(x.data_ptr()) for x in (bounds, stream.state, rolls, words)]
     wsp = C.c_void_p(stream.workspace.data_ptr())
-    extras = torch.zeros(ws, dtype=torch.int64, device="cuda")
 
     def step():  # production call: main kernel + PDL-launched fixup (br_roll_batches)
         N.check(L.br_roll_batches_phase(ptrs[0], 2, nb, ptrs[1], ptrs[2], ptrs[3], None, None, wsp, 3, sp), "roll")
@@ -316,17 +321,17 @@ def bench_c2(args, torch, B, ws, rank):
     main_ms = [a.elapsed_time(b) for a, b in zip(e0, e1)]
     barrier(torch, ws)
     total_ms = max_over_ranks(torch, total_ms, ws)
-    # cross-rank exchange: per-rank rejection counts (all zero unless a batch was rejected)
+    # the one exchange of a split stream: per-rank rejection counts (all zero unless a batch
+    # was rejected, P ~ 2^-10 per 2^25 batches); a rank after a rejecting rank is shifted and
+    # re-rolls its section (shard.sharded_rolls; gloo-tested in tests/test_multi.py)
     extra = C.c_uint64()
     N.check(L.br_roll_check(wsp, sp, C.byref(extra)), "check")
+    extras = [int(extra.value)]
     if ws > 1:
-        import torch.distributed as dist
+        from paper_2408_06213_b200 import shard
 
-        mine = torch.tensor([int(extra.value)], dtype=torch.int64, device="cuda")
-        gathered = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(ws)]
-        dist.all_gather(gathered, mine)
-        extras = torch.cat(gathered)
-    rolls_total = 2 * nb * K * ws
+        extras = shard.all_gather_ints(int(extra.value), device="cuda")
+    rolls_total = 2 * NB_C2 * K
     value = rolls_total / (total_ms / 1e3)
     t_main = statistics.mean(main_ms) / 1e3
     if args.generator == "chacha":  # ChaCha streams are rolled inside the fixup kernel: time the step
@@ -346,9 +351,10 @@ def bench_c2(args, torch, B, ws, rank):
         "roofline_int": int_roofline(2 * nb / t_main),
         "clocks": clk.summary(),
         "gpu_launches": 2 * K,
-        "cross_rank_rejections": [int(x) for x in extras.cpu().tolist()] if ws > 1 else [int(extra.value)],
+        "cross_rank_rejections": extras,
     }
-    # end to end through the public API with host (pinned) buffers
+    # end to end through the public API with host (pinned) buffers and the production status
+    # check (br_roll_check: one synchronisation and a 16-byte read per call)
     hb = bounds.cpu().pin_memory()
     hrolls = torch.empty(2 * nb, dtype=torch.int32).pin_memory()
     hwords = torch.empty(nb, dtype=torch.uint8).pin_memory()
@@ -360,40 +366,91 @@ def bench_c2(args, torch, B, ws, rank):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(E):
-        B.roll_batches(stream, hb, 2, out=(hrolls, hwords), check=False)
+        B.roll_batches(stream, hb, 2, out=(hrolls, hwords))
     t1.record()
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(torch, t0.elapsed_time(t1), ws)
-    res["e2e"] = {"value": 2 * nb * E * ws / (e2e_ms / 1e3), "unit": "rolls/s",
+    res["e2e"] = {"value": 2 * NB_C2 * E / (e2e_ms / 1e3), "unit": "rolls/s",
                   "h2d_bytes_per_step": 8 * nb, "d2h_bytes_per_step": 8 * nb + nb, "steps": E,
-                  "api": "paper_2408_06213_b200.roll_batches(host pinned tensors, 16-chunk pipelined copies)"}
+                  "api": "paper_2408_06213_b200.roll_batches(host pinned tensors, 16-chunk pipelined copies, "
+                         "check=True)"}
     return res
 
 
-def cpu_baseline_c2(sample_batches=1 << 24, target_s=10.0):
-    """The oracle port of roll_batch on every host thread, about target_s seconds: the first
-    2^24 C2 bounds, rolled repeatedly by one continuing stream.  The stream is sequential in
-    the reference; the port splits it into per-thread chunks by jump-ahead and repairs chunks
-    after a rejected batch in order (or_roll_batches_mt: the same results)."""
+def cpu_c2(cores, steps=None, warmup=1, target_s=None):
+    """The oracle port of roll_batch (the reference's batched.py:102-123 loop, oracle/oracle.c)
+    on `cores` host threads over the FULL C2 config per step: 2^25 batches of the C2 bounds on
+    one continuing stream, rolls and words into preallocated arrays (what the device call
+    returns).  The reference's single stream is cut into per-thread chunks by jump-ahead and
+    chunks after a rejected batch are repaired in order (or_roll_batches_mt: the same
+    results).  Used by both the reference arm and this arm's cpu_baseline, so the two agree."""
+    import numpy as np
+
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
     O.build()
-    cores = cpu_cores()
-    bounds = O.gen_bounds(7, 2 * sample_batches)
+    bounds = O.gen_bounds(7, 2 * NB_C2)
     src = O.pcg64(O.array_seed(7, 1))
-    O.roll_batches_mt(src, bounds, 2, nthreads=cores)  # warm-up (threads, pages)
+    rolls = np.empty(2 * NB_C2, dtype=np.uint32)
+    wds = np.empty(NB_C2, dtype=np.uint8)
+    rolls.fill(0)
+    wds.fill(0)  # pages touched before timing
+    for _ in range(warmup):
+        O.roll_batches_mt(src, bounds, 2, nthreads=cores, out=(rolls, wds))
     reps, t = 0, time.perf_counter()
     while True:
-        O.roll_batches_mt(src, bounds, 2, nthreads=cores)
+        O.roll_batches_mt(src, bounds, 2, nthreads=cores, out=(rolls, wds))
         reps += 1
         dt = time.perf_counter() - t
-        if dt >= target_s:
+        if (steps is not None and reps >= steps) or (steps is None and dt >= target_s):
             break
-    return {"value": 2 * sample_batches * reps / dt, "unit": "rolls/s", "cores": cores, "kind": "port",
-            "sample": f"{reps} x {sample_batches} batches of C2 bounds on one continuing stream (the reference's "
-                      f"roll_batch loop in oracle/oracle.c, chunked over {cores} threads by jump-ahead: "
-                      f"or_roll_batches_mt), {dt:.1f}s"}
+    return 2 * NB_C2 * reps / dt, reps, dt
+
+
+def python_reference_rate(cfg_key, budget_s=2.0):
+    """The vendored reference package itself (baseline/_ref, tools/vendor_reference.sh) on one
+    core: the pure-Python path a reference user runs today.  Context only (the port above is
+    the conservative, much faster CPU denominator).  None when the package is not vendored."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "batchrand")):
+        return None
+    sys.path.insert(0, ref_dir)
+    try:
+        import batchrand as R
+    except Exception:
+        return None
+    finally:
+        sys.path.remove(ref_dir)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    if cfg_key == "c2":
+        import numpy as np
+
+        bounds = O.gen_bounds(7, 2 * 50000)
+        src = R.make_source("pcg64", O.array_seed(7, 1))
+        t, done = time.perf_counter(), 0
+        while done < 50000 and time.perf_counter() - t < budget_s:
+            for i in range(done, min(done + 1000, 50000)):
+                R.roll_batch(src, R.BatchSpec(R.RadixBases.of((int(bounds[2 * i]), int(bounds[2 * i + 1])))))
+            done = min(done + 1000, 50000)
+        dt = time.perf_counter() - t
+        return {"value": 2 * done / dt, "unit": "rolls/s", "cores": 1, "kind": "reference",
+                "sample": f"{done} C2 batches through the reference's roll_batch(src, BatchSpec(RadixBases.of(b)))"}
+    cfg = SHUFFLE_CFG[cfg_key]
+    n = cfg["n"]
+    t, arrays = time.perf_counter(), 0
+    while True:
+        z = list(range(n))
+        R.shuffle_batched(R.make_source("pcg64", O.array_seed(cfg["seed"], arrays)), z)
+        arrays += 1
+        if time.perf_counter() - t >= budget_s:
+            break
+    dt = time.perf_counter() - t
+    return {"value": n * arrays / dt, "unit": "elements/s", "cores": 1, "kind": "reference",
+            "sample": f"{arrays} arrays of {n} through the reference's shuffle_batched(make_source('pcg64', "
+                      f"hash({cfg['seed']}, a)), list(range({n})))"}
 
 
 # ------------------------------------------------------------------------------ shuffles
@@ -404,29 +461,39 @@ SHUFFLE_CFG = {
 }
 
 
-def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
-    n, na, eb = cfg["n"], cfg["arrays"], cfg["eb"]
-    base = rank * na
-    if eb == 8:  # payload: consecutive words of pcg64(seed) (this rank's section)
-        data = B.pcg64_fill(cfg["seed"], n * na, offset=base * n)
-    else:
-        data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
+def shuffle_payload(torch, B, cfg, first, count):
+    n = cfg["n"]
+    if cfg["eb"] == 8:  # payload: consecutive words of pcg64(seed) (this rank's arrays)
+        return B.pcg64_fill(cfg["seed"], n * count, offset=first * n)
+    return torch.arange(n, dtype=torch.int32, device="cuda").repeat(count)
+
+
+def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None, e2e=True):
+    from paper_2408_06213_b200 import shard
+
+    n, eb = cfg["n"], cfg["eb"]
+    first, na = shard.even_split(cfg["arrays"], ws, rank)
+    data = shuffle_payload(torch, B, cfg, first, na)
     K = steps or args.steps
+
+    def call(d):
+        return B.shuffle_many(d, n, cfg["seed"], array_index_base=first, generator=args.generator)
+
     for _ in range(args.warmup):
-        B.shuffle_many(data, n, cfg["seed"], array_index_base=base, generator=args.generator)
+        call(data)
     kernel = B.last_kernel()
-    soak(torch, lambda: B.shuffle_many(data, n, cfg["seed"], array_index_base=base, generator=args.generator))
+    soak(torch, lambda: call(data))
     barrier(torch, ws)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     with ClockSampler(torch.cuda.current_device()) as clk:
         for a, b in evs:
             a.record()
-            B.shuffle_many(data, n, cfg["seed"], array_index_base=base, generator=args.generator)
+            call(data)
             b.record()
         torch.cuda.synchronize()
     per = [a.elapsed_time(b) for a, b in evs]
     total_ms = max_over_ranks(torch, evs[0][0].elapsed_time(evs[-1][1]), ws)
-    elems = n * na * K * ws
+    elems = n * cfg["arrays"] * K
     t = statistics.mean(per) / 1e3
     peak, kind = load_peaks()
     achieved = 2 * eb * n * na / t / 1e9
@@ -435,11 +502,29 @@ def bench_shuffle(cfg, args, torch, B, ws, rank, steps=None):
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                         "traffic": load_traffic().get(kernel.split("<")[0]),
                         "algorithmic_bytes_per_launch": 2 * eb * n * na, "peak_source": kind},
-           "clocks": clk.summary(), "gpu_launches": K}
-    if eb == 4 and "large" not in kernel:  # payload staged in shared memory
+           "clocks": clk.summary(), "gpu_launches": K, "l2": "payload larger than L2 (no flush needed)"}
+    if eb == 4 and "large" not in kernel and "stage" not in kernel:  # payload staged in shared memory
         res["roofline_smem"] = smem_roofline(n * na / t, kernel)
-    if "large" in kernel:  # payload in HBM: random accesses
-        res["roofline_random"] = random_roofline((n - 1) * na / t, n * na * eb / 2**20)
+    del data
+    if e2e:
+        # end to end through shuffle_many on a pinned host tensor: every step copies the arrays
+        # up, shuffles them and copies them back (chunked, copies overlapping the shuffles)
+        host = shuffle_payload(torch, B, cfg, first, na).cpu().pin_memory()
+        call(host)  # warm-up (copy streams, device chunk buffers)
+        E = 3
+        barrier(torch, ws)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(E):
+            call(host)
+        t1.record()
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(torch, t0.elapsed_time(t1), ws)
+        res["e2e"] = {"value": n * cfg["arrays"] * E / (e2e_ms / 1e3), "unit": "elements/s",
+                      "h2d_bytes_per_step": eb * n * na, "d2h_bytes_per_step": eb * n * na, "steps": E,
+                      "api": "paper_2408_06213_b200.shuffle_many(pinned host tensor, 8-chunk pipelined copies)"}
+        del host
     return res
 
 
@@ -476,7 +561,10 @@ def bench_c1(args, torch, B):
             "value": 10000 / statistics.median(ts), "unit": "elements/s"}
 
 
-def cpu_baseline_shuffle(cfg, sample_arrays):
+def cpu_shuffle(cfg, cores, target_s=3.0, steps=None):
+    """The oracle port of shuffle_batched (shuffle.py:149-225, oracle/oracle.c) over a bounded
+    sample of the config's arrays, OpenMP over arrays on `cores` threads.  The sample is sized
+    from a short calibration run so that it takes about target_s."""
     import numpy as np
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -484,66 +572,68 @@ def cpu_baseline_shuffle(cfg, sample_arrays):
 
     O.build()
     n = cfg["n"]
-    if cfg["eb"] == 8:
-        sample_arrays = max(sample_arrays, cpu_cores())
-    data = np.tile(np.arange(n, dtype=np.uint32 if cfg["eb"] == 4 else np.uint64), sample_arrays)
+
+    def payload(arrays):
+        if cfg["eb"] == 8:
+            return O.pcg64_fill(O.pcg64(cfg["seed"]), 0, n * arrays)
+        return np.tile(np.arange(n, dtype=np.uint32), arrays)
+
+    arrays = max(cores, (1 << 18) // n)
     t = time.perf_counter()
-    O.shuffle_segmented(data, n, cfg["seed"], nthreads=0)
+    O.shuffle_segmented(payload(arrays), n, cfg["seed"], nthreads=cores)
+    per_array = (time.perf_counter() - t) / arrays
+    arrays = int(min(cfg["arrays"], max(cores, target_s / max(per_array, 1e-9))))
+    arrays = max(cores, arrays - arrays % cores)
+    data = payload(arrays)
+    reps = steps or 1
+    t = time.perf_counter()
+    for _ in range(reps):
+        O.shuffle_segmented(data, n, cfg["seed"], nthreads=cores)
     dt = time.perf_counter() - t
-    return {"value": n * sample_arrays / dt, "unit": "elements/s", "cores": cpu_cores(), "kind": "port",
-            "sample": f"{sample_arrays} arrays of {n} (oracle shuffle_batched per array, OpenMP over arrays), {dt:.2f}s"}
+    return n * arrays * reps / dt, arrays, reps, dt
+
+
+def cpu_baseline_shuffle(cfg, key):
+    cores = cpu_cores()
+    v, arrays, reps, dt = cpu_shuffle(cfg, cores)
+    out = {"value": v, "unit": "elements/s", "cores": cores, "kind": "port",
+           "sample": f"{arrays} of the {cfg['arrays']} arrays of {cfg['n']} (the reference's shuffle_batched per "
+                     f"array in oracle/oracle.c, OpenMP over arrays), {dt:.2f}s"}
+    py = python_reference_rate(key)
+    if py is not None:
+        out["python_reference_1core"] = py
+    return out
 
 
 # ------------------------------------------------------------------------------ reference arm
 def run_reference(args, ws, rank):
     if rank != 0:
         return None
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-
-    O.build()
+    cores = cpu_cores()
     cfg = args.config
     if cfg == "c2":
-        sample = 1 << 21
-        bounds = O.gen_bounds(7, 2 * sample)
-        src = O.pcg64(O.array_seed(7, 1))
-        cores = cpu_cores()
-        for _ in range(args.warmup):
-            O.roll_batches_mt(src, bounds, 2, nthreads=cores)
-        t = time.perf_counter()
-        for _ in range(args.steps):
-            O.roll_batches_mt(src, bounds, 2, nthreads=cores)
-        dt = time.perf_counter() - t
-        value, unit = 2 * sample * args.steps / dt, "rolls/s"
-        desc = (f"{sample} batches of C2 per step (one continuing stream; the reference roll_batch loop chunked over "
-                f"{cores} threads by jump-ahead, or_roll_batches_mt)")
+        value, reps, dt = cpu_c2(cores, steps=args.steps, warmup=args.warmup)
+        unit = "rolls/s"
+        desc = (f"the full C2 config per step ({NB_C2} batches on one continuing stream; the reference's roll_batch "
+                f"loop in oracle/oracle.c chunked over {cores} threads by jump-ahead, or_roll_batches_mt)")
     else:
         c = SHUFFLE_CFG[cfg]
-        n = c["n"]
-        arrays = max(1, (1 << 22) // n)
-        if c["eb"] == 8:
-            arrays = max(arrays, cpu_cores())
-            data = O.pcg64_fill(O.pcg64(c["seed"]), 0, n * arrays)
-        else:
-            data = __import__("numpy").tile(__import__("numpy").arange(n, dtype="uint32"), arrays)
-        for _ in range(args.warmup):
-            O.shuffle_segmented(data, n, c["seed"], nthreads=0)
-        t = time.perf_counter()
-        for _ in range(args.steps):
-            O.shuffle_segmented(data, n, c["seed"], nthreads=0)
-        dt = time.perf_counter() - t
-        value, unit, cores = n * arrays * args.steps / dt, "elements/s", cpu_cores()
-        desc = f"{arrays} arrays of {n} per step, OpenMP over arrays"
-    metric, unit_b, config, dtype = headline(args, ws)
+        value, arrays, reps, dt = cpu_shuffle(c, cores, target_s=1.0, steps=args.steps)
+        unit = "elements/s"
+        desc = f"{arrays} of the {c['arrays']} arrays of {c['n']} per step, OpenMP over arrays"
+    metric, unit_b, config, dtype = headline(args, 1)
     assert unit == unit_b
     config = dict(config, reference_note="oracle/oracle.c port of the reference (pure Python upstream, so there is "
-                                         "no compiled reference to run); each step a bounded sample: " + desc)
+                                         "no compiled reference to run); " + desc)
     line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": dt / reps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": config,
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": desc},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    py = python_reference_rate(cfg)
+    if py is not None:
+        line["cpu_baseline"]["python_reference_1core"] = py
     return line
 
 
@@ -551,12 +641,13 @@ def run_reference(args, ws, rank):
 def headline(args, ws):
     """metric, unit, config and dtype of the line (shared by both arms)."""
     if args.config == "c2":
-        config = {"workload": "C2: BASELINE configs[1], 2^25 batches x k=2 bounded rolls per GPU, bounds iid "
+        config = {"workload": "C2: BASELINE configs[1], 2^25 batches x k=2 bounded rolls on one stream, bounds iid "
                               "U[2,2^16) from seed 7, words from pcg64(hash(7,1)); output 2^26 u32 rolls + 2^25 u8 "
-                              "words per GPU", "batches_per_gpu": NB_C2, "k": 2,
+                              "words", "batches": NB_C2, "k": 2,
                   "l2": "inputs+outputs 544 MiB per step > 126 MB L2 (no flush needed)",
-                  "parallelism": f"dp{ws} (stream sections by jump-ahead)", "generator": args.generator}
-        return "bounded rolls/sec (C2: 2^25 batches of k=2 per GPU, bounds U[2,2^16))", "rolls/s", config, "u64"
+                  "parallelism": f"dp{ws} (one stream cut into {ws} sections by jump-ahead)",
+                  "generator": args.generator}
+        return "bounded rolls/sec (C2: 2^25 batches of k=2, bounds U[2,2^16))", "rolls/s", config, "u64"
     cfg = SHUFFLE_CFG[args.config]
     config = {"workload": cfg["workload"], "l2": "payload larger than L2", "parallelism": f"dp{ws} (arrays)",
               "generator": args.generator}
@@ -566,7 +657,7 @@ def headline(args, ws):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
@@ -602,9 +693,8 @@ def main():
         r = bench_c2(args, torch, B, ws, rank)
     else:
         r = bench_shuffle(SHUFFLE_CFG[args.config], args, torch, B, ws, rank)
-        r["e2e"] = None
     line = {"metric": metric, "value": r["value"], "unit": unit, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic (BASELINE configs; generated on device)",
             "config": config, "roofline": r["roofline"], "clocks": r["clocks"], "gpu_launches": r["gpu_launches"],
             "e2e": r.get("e2e")}
@@ -618,15 +708,26 @@ def main():
         for key in ("c3", "c4", "c5"):
             if key != args.config:
                 sec[key] = bench_shuffle(SHUFFLE_CFG[key], args, torch, B, ws, rank,
-                                         steps={"c3": args.steps, "c4": min(args.steps, 10)}.get(key, min(args.steps, 3)))
+                                         steps={"c3": args.steps, "c4": min(args.steps, 10)}.get(key, min(args.steps, 5)))
+                if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+                    sec[key]["cpu_baseline"] = cpu_baseline_shuffle(SHUFFLE_CFG[key], key)
         if ws == 1:
             sec["c1"] = bench_c1(args, torch, B)
         line["secondary"] = sec
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cores = cpu_cores()
         if args.config == "c2":
-            line["cpu_baseline"] = cpu_baseline_c2()
+            v, reps, dt = cpu_c2(cores, target_s=8.0)
+            line["cpu_baseline"] = {
+                "value": v, "unit": "rolls/s", "cores": cores, "kind": "port",
+                "sample": f"{reps} x the full C2 config ({NB_C2} batches on one continuing stream; the reference's "
+                          f"roll_batch loop in oracle/oracle.c chunked over {cores} threads by jump-ahead: "
+                          f"or_roll_batches_mt, the same call the reference arm times), {dt:.1f}s"}
+            py = python_reference_rate("c2")
+            if py is not None:
+                line["cpu_baseline"]["python_reference_1core"] = py
         else:
-            line["cpu_baseline"] = cpu_baseline_shuffle(SHUFFLE_CFG[args.config], max(1, (1 << 23) // SHUFFLE_CFG[args.config]["n"]))
+            line["cpu_baseline"] = cpu_baseline_shuffle(SHUFFLE_CFG[args.config], args.config)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -252,10 +252,31 @@ def roll_batch(s: Source, bases, bits: int = 64, upper_bound=None):
     return tuple(int(x) for x in d), w.value, bool(tc.value), rk.value
 
 
-def roll_batches_mt(s: Source, bounds: np.ndarray, k: int, nthreads: int = 0):
-    """roll_batches on all host threads (chunked jump-ahead with in-order repair; same results)."""
+def roll_batch_known_threshold(s: Source, bases, bits: int = 64):
+    """batched.py:85-99: re-draw whole passes until r_k >= 2^bits mod product."""
+    b = np.asarray(bases, dtype=np.uint64)
+    prod = 1
+    for x in bases:
+        prod *= int(x)
+    t = threshold(prod, bits) if prod < 1 << bits else 0
+    d = np.zeros(len(b), dtype=np.uint64)
+    w, rk = C.c_uint64(), C.c_uint64()
+    _check(lib().or_roll_batch_known_threshold(C.byref(s), _ptr(b), len(b), bits, t, _ptr(d), C.byref(w),
+                                               C.byref(rk)), "roll_batch_known_threshold")
+    return tuple(int(x) for x in d), w.value, False, rk.value
+
+
+def roll_batches_mt(s: Source, bounds: np.ndarray, k: int, nthreads: int = 0, out=None):
+    """roll_batches on all host threads (chunked jump-ahead with in-order repair; same results).
+    ``out=(rolls, words)`` writes into preallocated arrays and skips flags/final remainders
+    (what the bulk device call returns by default)."""
     bounds = np.ascontiguousarray(bounds, dtype=np.uint32)
     nb = len(bounds) // k
+    if out is not None:
+        rolls, wds = out
+        _check(lib().or_roll_batches_mt(C.byref(s), _ptr(bounds), k, nb, _ptr(rolls), _ptr(wds), None, None,
+                                        nthreads), "roll_batches_mt")
+        return rolls, wds, None, None
     rolls = np.empty(nb * k, dtype=np.uint32)
     wds = np.empty(nb, dtype=np.uint8)
     flags = np.empty(nb, dtype=np.uint8)

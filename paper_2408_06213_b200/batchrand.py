@@ -484,15 +484,19 @@ def _roll_one(source, spec: BatchSpec) -> BatchResult:
     bases = spec.bases.bases
     if spec.bases.bits != 64:
         raise TypeError("the device path needs 64-bit words")
-    if any(b >= 1 << 32 for b in bases):
+    # bases of 2^32 or more, or more than the bulk kernels' 8 dice: the 64-bit single-batch kernel
+    if len(bases) > 8 or any(b >= 1 << 32 for b in bases):
         return _roll_one64(source, bases)
     st = _state_struct(source)
     dstream = DeviceStream.from_struct(st)
     b = _device_bases(bases, torch)
-    r = roll_batches(dstream, b, len(bases), flags=True, final_remainder=True)
+    r = roll_batches(dstream, b, len(bases), flags=True, final_remainder=True, check=False)
+    # exact words consumed: 1 + the rejections the fixup counted (the per-batch u8 saturates)
+    extra = C.c_uint64()
+    N.check(N.lib().br_roll_check(_ptr(dstream.workspace), _stream_ptr(torch), C.byref(extra)), "roll_batch")
     dstream.write_back(source)
     digits = tuple(int(x) & 0xFFFFFFFF for x in r.rolls.cpu().tolist())
-    return BatchResult(digits, int(r.words[0]), bool(int(r.flags[0])), int(r.final_remainder[0]) & MASK64)
+    return BatchResult(digits, 1 + int(extra.value), bool(int(r.flags[0])), int(r.final_remainder[0]) & MASK64)
 
 
 def digit_pass(r0: int, bases: RadixBases):
@@ -1053,34 +1057,92 @@ def pcg64_fill(source_or_seed, count: int, offset: int = 0, generator: str = "pc
     return out
 
 
+def _segmented_call(flat, n, num_arrays, run_seed, base, schedule, gen_id, naive, words, stream_ptr):
+    L = N.lib()
+    if naive:
+        return L.br_shuffle_naive_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64, base,
+                                            gen_id, _ptr(words), stream_ptr)
+    regs = schedule._regimes()
+    return L.br_shuffle_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64, base, regs,
+                                  len(regs), gen_id, _ptr(words), stream_ptr)
+
+
+def _shuffle_many_host(flat, n, num_arrays, run_seed, base, schedule, gen_id, naive, words, chunks, torch):
+    """shuffle_many on a host tensor (ideally pinned): the arrays go up, are shuffled and come
+    back in ``chunks`` pieces, the copies on two copy streams overlapping the shuffles."""
+    chunks = max(1, min(chunks, num_arrays))
+    per = -(-num_arrays // chunks)
+    comp = torch.cuda.current_stream()
+    h2d, d2h = _copy_streams(torch)
+    h2d.wait_stream(comp)
+    d2h.wait_stream(comp)
+    dbufs = [torch.empty(per * n, dtype=flat.dtype, device="cuda") for _ in range(min(2, chunks))]
+    dwords = [torch.empty(per, dtype=torch.int32, device="cuda") if words is not None else None
+              for _ in range(len(dbufs))]
+    freed = [None] * len(dbufs)
+    for c, a0 in enumerate(range(0, num_arrays, per)):
+        na = min(per, num_arrays - a0)
+        slot = c % len(dbufs)
+        with torch.cuda.stream(h2d):
+            if freed[slot] is not None:
+                h2d.wait_event(freed[slot])
+            dbufs[slot][: na * n].copy_(flat[a0 * n: (a0 + na) * n], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(h2d)
+        comp.wait_event(ready)
+        N.check(_segmented_call(dbufs[slot][: na * n], n, na, run_seed, base + a0, schedule, gen_id, naive,
+                                dwords[slot], C.c_void_p(comp.cuda_stream)), "shuffle_many")
+        done = torch.cuda.Event()
+        done.record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done)
+            flat[a0 * n: (a0 + na) * n].copy_(dbufs[slot][: na * n], non_blocking=True)
+            if words is not None:
+                words[a0: a0 + na].copy_(dwords[slot][:na], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(d2h)
+            freed[slot] = ev
+    comp.wait_stream(d2h)
+    comp.wait_stream(h2d)
+    for t in dbufs + dwords:
+        if t is not None:
+            t.record_stream(h2d)
+            t.record_stream(d2h)
+
+
 def shuffle_many(data, n: int, run_seed: int, array_index_base: int = 0,
                  schedule: ShuffleSchedule = DEFAULT_SCHEDULE, return_words: bool = False,
-                 generator: str = "pcg64", naive: bool = False):
-    """Independent shuffles of the num_arrays = data.numel() // n contiguous arrays of a CUDA
+                 generator: str = "pcg64", naive: bool = False, chunks: int = 8, sync: bool = True):
+    """Independent shuffles of the num_arrays = data.numel() // n contiguous arrays of a
     tensor (4- or 8-byte items), in place: array a is
     shuffle_batched(make_source(generator, array_seed(run_seed, array_index_base + a)), ...)
     with generator "pcg64", "lehmer" or "chacha" -- or, with ``naive``,
-    shuffle_naive_batched(make_source(...), ...) (schedule ignored)."""
+    shuffle_naive_batched(make_source(...), ...) (schedule ignored).
+
+    A CUDA tensor is shuffled where it is (asynchronously on the current stream).  A host
+    tensor (pinned for overlap) is copied up, shuffled and copied back in ``chunks`` pipelined
+    pieces; with ``sync`` the call returns once the host data holds the result."""
     if generator not in _GENERATOR_IDS:
         raise UnknownGenerator(f"no device generator {generator!r}")
     torch = _torch()
     flat = data.view(-1)
-    if not flat.is_cuda or flat.element_size() not in (4, 8):
-        raise TypeError("data must be a CUDA tensor of 4- or 8-byte items")
+    if flat.element_size() not in (4, 8):
+        raise TypeError("data must be a tensor of 4- or 8-byte items")
     if n <= 0 or flat.numel() % n:
         raise ValueError("data length must be a multiple of n")
     num_arrays = flat.numel() // n
-    words = torch.empty(num_arrays, dtype=torch.int32, device="cuda") if return_words else None
-    if naive:
-        N.check(N.lib().br_shuffle_naive_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64,
-                                                   array_index_base, _GENERATOR_IDS[generator], _ptr(words),
-                                                   _stream_ptr(torch)), "shuffle_many")
+    gid = _GENERATOR_IDS[generator]
+    if not flat.is_cuda:
+        words = torch.empty(num_arrays, dtype=torch.int32, pin_memory=flat.is_pinned()) if return_words else None
+        if num_arrays:
+            _shuffle_many_host(flat, n, num_arrays, run_seed, array_index_base, schedule, gid, naive, words, chunks,
+                               torch)
+        if sync:
+            torch.cuda.current_stream().synchronize()
         return (data, words) if return_words else data
-    regs = schedule._regimes()
-    N.check(N.lib().br_shuffle_segmented(_ptr(flat), flat.element_size(), num_arrays, n, run_seed & MASK64,
-                                         array_index_base, regs, len(regs), _GENERATOR_IDS[generator], _ptr(words),
-                                         _stream_ptr(torch)),
-            "shuffle_many")
+    words = torch.empty(num_arrays, dtype=torch.int32, device="cuda") if return_words else None
+    N.check(_segmented_call(flat, n, num_arrays, run_seed, array_index_base, schedule, gid, naive, words,
+                            _stream_ptr(torch)), "shuffle_many")
     return (data, words) if return_words else data
 
 

@@ -418,16 +418,15 @@ int launch_roll(const RollArgs &a, const DeviceInfo &di, cudaStream_t st, int ph
     if (phase & 2) {
         // fixup: one block per SM, launched as a programmatic dependent of the main kernel so
         // its launch latency overlaps the main kernel's tail.  Its grid barrier (only reached
-        // when a batch was rejected) needs the blocks co-resident; one 256-thread block per SM
-        // always fits once the main kernel it waits for has drained, so a plain launch is used
-        // (1.8 us less per call than the cooperative attribute, which BR_ROLL_FIXUP=cooperative
-        // restores).
+        // when a batch was rejected) needs every block co-resident, which only a cooperative
+        // launch guarantees (other streams, MPS SM limits or green contexts can hold SMs), so
+        // the cooperative attribute is the default; BR_ROLL_FIXUP=plain drops it (A/B only).
         if (di.sms * (threads / 32) > ROLL_MAX_WARPS) return fail(BR_E_UNSUPPORTED, "more SMs than the roll workspace covers");
         RollArgs b = a;
         void *args[] = {&b};
         cudaLaunchConfig_t cfg = {};
         const char *fx = getenv("BR_ROLL_FIXUP");
-        const bool coop = fx && !strcmp(fx, "cooperative");
+        const bool coop = !(fx && !strcmp(fx, "plain"));
         cfg.gridDim = dim3(di.sms);
         cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = 0;
@@ -954,6 +953,10 @@ static int roll_batches_impl(const uint32_t *bounds, int k, int64_t nb, br_pcg64
     }
     if (!bounds || !state_dev || !rolls || !words || !ws) return fail(BR_E_INVALID, "null pointer argument");
     if ((((uintptr_t)bounds | (uintptr_t)rolls) & 15) != 0) return fail(BR_E_INVALID, "bounds/rolls must be 16-byte aligned");
+    // the fast kernels store words in 8-byte vectors and final remainders as u64: a misaligned
+    // pointer would fault (a sticky error) instead of raising
+    if ((((uintptr_t)words | (uintptr_t)final_rk) & 7) != 0)
+        return fail(BR_E_INVALID, "words/final_remainder must be 8-byte aligned");
     if (!di.coop) return fail(BR_E_CUDA, "device lacks cooperative launch");
     RollArgs a;
     a.bounds = bounds;

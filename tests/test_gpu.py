@@ -136,8 +136,8 @@ def test_roll_batches_forced_rejections(B, O, heavy_fraction):
 def test_roll_batches_dense_rejections(B, O, gen):
     """Thousands of rejected batches spread over a long run (k = 5, bounds up to 4000: about
     one batch in 1100 rejects), three calls in a row on one workspace: each fixup iteration
-    resolves one rejection and re-rolls the tail front first.  Bit-exact, and fast."""
-    import time
+    resolves one rejection and re-rolls the tail front first.  Bit-exact (the time per
+    rejection is measured by tools/fixup_cost.py, not asserted here)."""
     k, nb = 5, 1 << 21
     maker = {"pcg64": O.pcg64, "lehmer": O.lehmer, "chacha": O.chacha}[gen]
     src = maker(77)
@@ -145,19 +145,13 @@ def test_roll_batches_dense_rejections(B, O, gen):
     for call in range(3):
         bounds = np.random.default_rng(call).integers(2, 4002, k * nb, dtype=np.uint32)
         rolls, words, flags, rk = O.roll_batches(src, bounds, k)
-        db = dev_u32(bounds)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = B.roll_batches(ds, db, k, flags=True, final_remainder=True)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        r = B.roll_batches(ds, dev_u32(bounds), k, flags=True, final_remainder=True)
         assert int(words.sum()) - nb > 1000  # the rejections happened
         assert np.array_equal(u32(r.rolls), rolls) and np.array_equal(r.words.cpu().numpy(), words), (gen, call)
         assert np.array_equal(r.flags.cpu().numpy(), flags) and np.array_equal(u64(r.final_remainder), rk)
         st = ds.host_state()
         pos = (st.state_hi << 64) | st.state_lo
         assert pos == (O.chacha_position(src) if gen == "chacha" else src.state), (gen, call)
-        assert dt < 0.5, f"{gen} call {call}: {dt * 1e3:.1f} ms for ~{int(words.sum()) - nb} rejections"
 
 
 @pytest.mark.parametrize("k,nb", [(1, 50000), (1, 1 << 20), (1, 513), (2, 50001), (2, 255), (2, 1), (3, 50000),
@@ -212,14 +206,34 @@ def test_roll_batch_dropin_golden(B, golden):
         assert s.state == rec["state_after"]
 
 
-def test_roll_batch_known_threshold(B):
-    spec = B.BatchSpec.with_threshold(B.RadixBases.of((52, 51)))
-    a, b = B.Pcg64Source(5), B.Pcg64Source(5)
-    r1 = B.roll_batch_known_threshold(a, spec)
-    r2 = B.roll_batch(b, B.BatchSpec(B.RadixBases.of((52, 51))))
-    assert r1.digits == r2.digits and r1.words_consumed == r2.words_consumed and not r1.threshold_computed
+def test_roll_batch_known_threshold(B, O):
+    """batched.py:85-99 against the oracle's restatement (or_roll_batch_known_threshold), on
+    streams that include rejected words (products near 2^64) and k > 8 bases."""
+    cases = [(52, 51), (6,) * 6, (0xFFFFFFFF, 3006477107), (3,) * 40, ((1 << 40) + 7,), (1 << 31, 1 << 31, 4)]
+    a, o = B.Pcg64Source(5), O.pcg64(5)
+    seen_reject = False
+    for rep in range(40):
+        for bases in cases:
+            spec = B.BatchSpec.with_threshold(B.RadixBases.of(bases))
+            r = B.roll_batch_known_threshold(a, spec)
+            ref = O.roll_batch_known_threshold(o, bases)
+            assert (tuple(r.digits), r.words_consumed, r.threshold_computed, r.final_remainder) == ref, (rep, bases)
+            seen_reject |= r.words_consumed > 1
+    assert a.state == o.state and seen_reject
     with pytest.raises(ValueError):
         B.roll_batch_known_threshold(a, B.BatchSpec(B.RadixBases.of((52, 51))))
+
+
+def test_roll_batch_words_beyond_255(B, O):
+    """A FixedSequenceSource whose first 300 words are all rejected: words_consumed is exact
+    (not the saturating u8 counter of the bulk kernel)."""
+    bases = (0xFFFFFFFF, 3006477107)
+    words = [0] * 300 + [2**64 - 1, 12345]
+    s = B.FixedSequenceSource(words)
+    r = B.roll_batch(s, B.BatchSpec(B.RadixBases.of(bases)))
+    ref = O.roll_batch(O.fixed(words), bases)
+    assert (tuple(r.digits), r.words_consumed, r.threshold_computed, r.final_remainder) == ref
+    assert r.words_consumed == 301 and s.cursor == 301
 
 
 def test_digit_pass_vs_oracle(B, O, golden):
