@@ -585,7 +585,9 @@ def cpu_shuffle(cfg, cores, target_s=3.0, steps=None):
     arrays = int(min(cfg["arrays"], max(cores, target_s / max(per_array, 1e-9))))
     arrays = max(cores, arrays - arrays % cores)
     data = payload(arrays)
-    reps = steps or 1
+    # the whole config fits the budget: repeat it (the arrays keep their seeds, so every
+    # repetition is the same work on the previous output)
+    reps = steps or max(1, int(target_s / max(per_array * arrays, 1e-9)))
     t = time.perf_counter()
     for _ in range(reps):
         O.shuffle_segmented(data, n, cfg["seed"], nthreads=cores)
@@ -597,8 +599,8 @@ def cpu_baseline_shuffle(cfg, key):
     cores = cpu_cores()
     v, arrays, reps, dt = cpu_shuffle(cfg, cores)
     out = {"value": v, "unit": "elements/s", "cores": cores, "kind": "port",
-           "sample": f"{arrays} of the {cfg['arrays']} arrays of {cfg['n']} (the reference's shuffle_batched per "
-                     f"array in oracle/oracle.c, OpenMP over arrays), {dt:.2f}s"}
+           "sample": f"{reps} x {arrays} of the {cfg['arrays']} arrays of {cfg['n']} (the reference's shuffle_batched "
+                     f"per array in oracle/oracle.c, OpenMP over arrays), {dt:.2f}s"}
     py = python_reference_rate(key)
     if py is not None:
         out["python_reference_1core"] = py

@@ -11,9 +11,13 @@
  * Conventions
  *   - Plain C types only.  Pointers named *_dev are CUDA device pointers owned by the
  *     caller; `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
- *   - All device entry points are asynchronous on `stream` unless stated otherwise and
- *     never synchronise the device.  They return a status code; no C++ exception crosses
- *     the ABI.  br_last_error() gives the thread-local message of the last failure.
+ *   - Device entry points are asynchronous on `stream` and never synchronise the device,
+ *     except the four marked SYNCHRONOUS below (br_state_download, br_roll_check and
+ *     br_roll_batch64 synchronise `stream`; br_pcg64_next on a replayed-word state reads one
+ *     word).  Shuffle plans are built on the device, stream-ordered, and cached; a cached
+ *     plan is freed with cudaFreeAsync after every stream that used it has passed its last
+ *     use.  Entry points return a status code; no C++ exception crosses the ABI.
+ *     br_last_error() gives the thread-local message of the last failure.
  *   - Generator state that evolves across calls lives in device memory (br_pcg64 in
  *     *_dev buffers) so that back-to-back calls need no host round trip.
  *   - Word width is 64 bits (PCG64 XSL-RR 128/64, wordsource.py:71-89); shuffled arrays
@@ -125,8 +129,9 @@ int64_t br_plan_build(uint64_t n, const br_regime *entries, int n_entries, br_se
 /* out_dev[i] = word (offset + i) of the stream `st` (host struct, not modified). */
 int br_pcg64_fill(uint64_t *out_dev, int64_t count, const br_pcg64 *st, uint64_t offset,
                   void *stream);
-/* Copy a host state to/from device memory on `stream` (both synchronise `stream`).  Upload
- * copies a whole br_chacha for a ChaCha state; download copies the 32-byte head (the key
+/* Copy a host state to/from device memory on `stream`.  Upload is asynchronous (the host
+ * struct is copied into pinned staging before the call returns) and copies a whole br_chacha for a ChaCha state;
+ * download is SYNCHRONOUS (it synchronises `stream`) and copies the 32-byte head (the key
  * never changes). */
 int br_state_upload(br_pcg64 *state_dev, const br_pcg64 *st, void *stream);
 int br_state_download(br_pcg64 *st, const br_pcg64 *state_dev, void *stream);
@@ -139,7 +144,8 @@ int br_state_download(br_pcg64 *st, const br_pcg64 *state_dev, void *stream);
  *       flags[i] = r.threshold_computed; final_rk[i] = r.final_remainder
  * with src the stream in *state_dev (PCG64, Lehmer or ChaCha; advanced in place by the
  * words consumed).
- * bounds are u32 (>= 1); flags_dev / final_rk_dev may be NULL.  `workspace_dev` is
+ * bounds are u32 (>= 1); flags_dev / final_rk_dev may be NULL.  bounds_dev and rolls_dev
+ * must be 16-byte aligned, words_dev and final_rk_dev 8-byte aligned (BR_E_INVALID otherwise).  `workspace_dev` is
  * br_roll_workspace_bytes() of zero-initialised device memory, reusable across calls on
  * one stream (calls sharing a workspace must be stream-ordered).  Invalid bounds (a zero
  * bound -> ValueError, product > 2^64 -> BoundOverflow) are reported through
@@ -162,7 +168,7 @@ int br_roll_batches_phase(const uint32_t *bounds_dev, int k, int64_t num_batches
 int br_roll_batches_naive(const uint32_t *bounds_dev, int k, int64_t num_batches, br_pcg64 *state_dev,
                           uint32_t *rolls_dev, uint8_t *words_dev, uint8_t *flags_dev,
                           uint64_t *final_rk_dev, void *workspace_dev, void *stream);
-/* Synchronises `stream`, returns the deferred status of the last br_roll_batches on this
+/* SYNCHRONOUS: synchronises `stream`, returns the deferred status of the last br_roll_batches on this
  * workspace (BR_OK / BR_E_INVALID / BR_E_BOUND_OVERFLOW) and clears it.  *extra_words (may
  * be NULL) receives the words consumed beyond one per batch (rejections). */
 int br_roll_check(void *workspace_dev, void *stream, uint64_t *extra_words);
@@ -172,7 +178,8 @@ int br_roll_check(void *workspace_dev, void *stream, uint64_t *extra_words);
  * state_dev NULL, one digit_pass (batched.py:69-82) of the word *r0_dev.  out_dev receives
  * k + 3 u64: the digits, the words consumed, threshold_computed (0/1), the final remainder.
  * A base of 0 encodes 2^64 (the full range, bounded.py:35-56).  The bulk entry points take
- * u32 bounds; this is the drop-in path for wider ones. */
+ * u32 bounds; this is the drop-in path for wider ones.  SYNCHRONOUS: reads the k bases back
+ * to check the product before the launch. */
 int br_roll_batch64(const uint64_t *bases_dev, int k, br_pcg64 *state_dev, const uint64_t *r0_dev,
                     uint64_t *out_dev, void *stream);
 

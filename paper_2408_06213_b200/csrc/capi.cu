@@ -8,7 +8,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <list>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -141,103 +143,215 @@ int ff_checked(uint64_t n, uint64_t k, h128 *out) {
     return BR_OK;
 }
 
-struct CachedPlan {
-    void *dev = nullptr;  // [DevSeg x nseg][u64 x nbatches]
-    DevPlan plan;
-    uint64_t nbatches = 0;
+// ---------------------------------------------------------------- device plans
+// A plan is built ON THE DEVICE, stream-ordered, from its segment list (at most MAX_SEGS
+// entries, passed by value): plan_build_kernel writes the segments, the exact threshold
+// 2^64 mod ff(n_b, k_b) of every batch and, for n < 2^16, the warp kernels' batch records.  No
+// host copy, no host memory per batch, no synchronisation.  Plans are cached per (device,
+// segments, n, naive) and shared by later calls on any stream (they wait for the build event);
+// each is reference-counted and, once evicted and unused, freed with cudaFreeAsync after an
+// event of every stream that used it -- never while a launched kernel can still read it.
+struct PlanSegs {
+    DevSeg s[MAX_SEGS];
+    uint32_t nseg, nbatches, brec;
 };
-std::map<std::pair<int, std::string>, CachedPlan> g_plans;
-constexpr size_t PLAN_CACHE_MAX = 4096;
 
-// Compile segments into a device plan (cached per device and segment list).
-int get_plan(uint64_t n, const std::vector<br_segment> &segs, bool naive, CachedPlan *out) {
+__global__ void plan_build_kernel(PlanSegs ps, DevSeg *__restrict__ segs_out, uint64_t *__restrict__ thresh,
+                                  uint4 *__restrict__ brec) {
+    const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t0 < ps.nseg) segs_out[t0] = ps.s[t0];
+    for (uint32_t b = t0; b < ps.nbatches; b += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = ps.nseg - 1;  // last segment with first_batch <= b
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (ps.s[mid].first_batch <= b) lo = mid;
+            else hi = mid - 1;
+        }
+        const DevSeg S = ps.s[lo];
+        const uint32_t nb = S.start_n - (b - S.first_batch) * S.k;
+        unsigned __int128 f = 1;  // ff(nb, k) <= 2^64, checked on the host for the segment start
+        for (uint32_t m = 0; m < S.k; ++m) f *= (uint64_t)(nb - m);
+        const uint64_t f64 = (uint64_t)f;
+        const uint64_t t = (f >> 64) ? 0 : (0 - f64) % f64;  // bounded.py:59-62 (2^64 mod ff)
+        thresh[b] = t;
+        if (ps.brec) brec[b] = make_uint4((uint32_t)t, (uint32_t)(t >> 32), nb, S.k);
+    }
+}
+
+cudaStream_t free_stream(int dev) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = streams.find(dev);
+    if (it != streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) s = nullptr;
+    streams[dev] = s;
+    return s;
+}
+
+struct PlanStore {
+    int dev = -1;
+    void *mem = nullptr;
+    size_t bytes = 0;
+    DevPlan plan{};
+    uint64_t nbatches = 0;
+    cudaEvent_t built = nullptr;
+    std::mutex mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;  // last use per stream
+
+    // make `st` wait for the build (a no-op once it has completed)
+    int ready_on(cudaStream_t st) {
+        if (built) CK(cudaStreamWaitEvent(st, built, 0));
+        return BR_OK;
+    }
+    // record that kernels reading this plan were queued on `st`
+    void used(cudaStream_t st) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto &u : uses)
+            if (u.first == st) {
+                cudaEventRecord(u.second, st);
+                return;
+            }
+        if (uses.size() >= 16) {  // many streams: retire the oldest record (a host wait on a past event)
+            cudaEventSynchronize(uses.front().second);
+            cudaEventDestroy(uses.front().second);
+            uses.erase(uses.begin());
+        }
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            cudaStreamSynchronize(st);  // cannot track it: make the use complete instead
+            return;
+        }
+        cudaEventRecord(ev, st);
+        uses.emplace_back(st, ev);
+    }
+    ~PlanStore() {
+        if (!mem) return;
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess) return;  // runtime gone (process exit)
+        cudaSetDevice(dev);
+        cudaStream_t fs = free_stream(dev);
+        for (auto &u : uses) {
+            cudaStreamWaitEvent(fs, u.second, 0);
+            cudaEventDestroy(u.second);
+        }
+        if (built) {
+            cudaStreamWaitEvent(fs, built, 0);
+            cudaEventDestroy(built);
+        }
+        cudaFreeAsync(mem, fs);
+        cudaGetLastError();
+        cudaSetDevice(cur);
+    }
+};
+using PlanRef = std::shared_ptr<PlanStore>;
+
+struct PlanCache {
+    std::map<std::pair<int, std::string>, PlanRef> map;
+    std::list<std::pair<int, std::string>> lru;  // front = most recent
+    size_t bytes = 0;
+};
+// never destroyed: plan destructors must not run after the CUDA runtime has shut down
+PlanCache &plan_cache() {
+    static PlanCache *c = new PlanCache;
+    return *c;
+}
+constexpr size_t PLAN_CACHE_MAX = 4096;          // plans
+constexpr size_t PLAN_CACHE_BYTES = 1ull << 30;  // device bytes over all cached plans
+constexpr size_t PLAN_ITEM_BYTES = 256ull << 20; // larger plans serve their call and are freed
+
+// Plan of segments `segs` for length n on the current device, ready on stream `st`.
+int get_plan(uint64_t n, const std::vector<br_segment> &segs, bool naive, cudaStream_t st, PlanRef *out) {
     int dev;
     DeviceInfo di;
-    int st = ensure_device(&dev, &di);
-    if (st) return st;
+    int e0 = ensure_device(&dev, &di);
+    if (e0) return e0;
     std::string key((const char *)segs.data(), segs.size() * sizeof(br_segment));
     key.append((const char *)&n, sizeof(n));
     key.push_back(naive ? 'N' : 'B');
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto it = g_plans.find({dev, key});
-    if (it != g_plans.end()) {
-        *out = it->second;
-        return BR_OK;
+    const auto ck = std::make_pair(dev, key);
+    PlanCache &pc = plan_cache();
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = pc.map.find(ck);
+        if (it != pc.map.end()) {
+            *out = it->second;
+            pc.lru.remove(ck);
+            pc.lru.push_front(ck);
+        }
     }
+    if (*out) return (*out)->ready_on(st);
     if (segs.size() > (size_t)MAX_SEGS) return fail(BR_E_UNSUPPORTED, "plan has too many segments");
-    std::vector<DevSeg> ds;
-    std::vector<uint64_t> th;
-    uint64_t fb = 0;
+    PlanSegs ps{};
+    uint64_t fb = 0, steps = 0;
     uint32_t maxk = 0;
     for (const br_segment &s : segs) {
         if (s.start_n >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements");
         if (s.k == 0 || (uint64_t)s.k * s.count > s.start_n)
             return fail(BR_E_INVALID, "segment runs past the start of the array");
-        DevSeg d;
+        h128 f;  // ff(n_b, k) grows with n_b: the segment's first batch is its largest
+        int e = ff_checked(s.start_n, s.k, &f);
+        if (e) return fail(e, "falling factorial of a batch exceeds 2^64");
+        DevSeg &d = ps.s[ps.nseg++];
         d.start_n = (uint32_t)s.start_n;
         d.k = s.k;
         d.count = (uint32_t)s.count;
         d.first_batch = (uint32_t)fb;
-        ds.push_back(d);
-        if (s.k > maxk) maxk = s.k;
-        for (uint64_t c = 0; c < s.count; ++c) {
-            uint64_t nb = s.start_n - c * s.k;
-            h128 f;
-            int e = ff_checked(nb, s.k, &f);
-            if (e) return fail(e, "falling factorial of a batch exceeds 2^64");
-            uint64_t f64 = (uint64_t)f;  // f < 2^64 because nb < 2^32 and ff <= 2^64
-            th.push_back(f == ((h128)1 << 64) ? 0 : (0 - f64) % f64);
-        }
+        maxk = std::max(maxk, s.k);
         fb += s.count;
+        steps += (uint64_t)s.k * s.count;
+        if (fb >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "too many batches");
     }
-    if (fb >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "too many batches");
-    // per-batch records for the warp kernel (n < 2^16): {threshold, n_b, k_b}
-    std::vector<uint32_t> br;
-    if (n < 65536) {
-        for (const br_segment &s : segs)
-            for (uint64_t c = 0; c < s.count; ++c) {
-                const uint64_t t = th[br.size() / 4];
-                br.push_back((uint32_t)t);
-                br.push_back((uint32_t)(t >> 32));
-                br.push_back((uint32_t)(s.start_n - c * s.k));
-                br.push_back(s.k);
+    ps.nbatches = (uint32_t)fb;
+    ps.brec = n < 65536 ? 1u : 0u;
+    const size_t off = (ps.nseg * sizeof(DevSeg) + 15) & ~(size_t)15;
+    const size_t boff = off + ((fb * sizeof(uint64_t) + 15) & ~(size_t)15);
+    const size_t bytes = boff + (ps.brec ? fb * sizeof(uint4) : 0) + 16;
+    auto p = std::make_shared<PlanStore>();
+    p->dev = dev;
+    p->bytes = bytes;
+    CK(cudaMallocAsync(&p->mem, bytes, st));
+    char *base = (char *)p->mem;
+    const int threads = 256;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((fb + threads - 1) / threads, (uint64_t)di.sms * 8));
+    plan_build_kernel<<<grid, threads, 0, st>>>(ps, (DevSeg *)base, (uint64_t *)(base + off),
+                                                ps.brec ? (uint4 *)(base + boff) : nullptr);
+    CK(cudaGetLastError());
+    CK(cudaEventCreateWithFlags(&p->built, cudaEventDisableTiming));
+    CK(cudaEventRecord(p->built, st));
+    p->plan.n = (uint32_t)n;
+    p->plan.nbatches = (uint32_t)fb;
+    p->plan.nseg = ps.nseg;
+    p->plan.max_k = maxk;
+    p->plan.lo = (uint32_t)(n > steps ? n - steps : 0);
+    p->plan.naive = naive ? 1u : 0u;
+    p->plan.segs = (const DevSeg *)base;
+    p->plan.thresh = (const uint64_t *)(base + off);
+    p->plan.brec = ps.brec ? (const uint4 *)(base + boff) : nullptr;
+    p->nbatches = fb;
+    if (bytes <= PLAN_ITEM_BYTES) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = pc.map.find(ck);
+        if (it != pc.map.end()) {  // another thread built it meanwhile: keep theirs, ours dies after use
+            pc.lru.remove(ck);
+        } else {
+            pc.bytes += bytes;
+        }
+        if (it == pc.map.end()) pc.map[ck] = p;
+        pc.lru.push_front(ck);
+        while ((pc.bytes > PLAN_CACHE_BYTES || pc.map.size() > PLAN_CACHE_MAX) && pc.lru.size() > 1) {
+            auto victim = pc.lru.back();
+            pc.lru.pop_back();
+            auto v = pc.map.find(victim);
+            if (v != pc.map.end()) {
+                pc.bytes -= v->second->bytes;
+                pc.map.erase(v);  // freed (stream-ordered) once no caller holds it
             }
+        }
     }
-    size_t off = (ds.size() * sizeof(DevSeg) + 15) & ~(size_t)15;
-    const size_t boff = off + ((th.size() * sizeof(uint64_t) + 15) & ~(size_t)15);
-    size_t bytes = boff + br.size() * sizeof(uint32_t) + 16;
-    void *p = nullptr;
-    CK(cudaMalloc(&p, bytes));
-    CK(cudaMemcpy(p, ds.data(), ds.size() * sizeof(DevSeg), cudaMemcpyHostToDevice));
-    if (!th.empty())
-        CK(cudaMemcpy((char *)p + off, th.data(), th.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
-    if (!br.empty())
-        CK(cudaMemcpy((char *)p + boff, br.data(), br.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CachedPlan cp;
-    cp.dev = p;
-    cp.plan.n = (uint32_t)n;
-    cp.plan.nbatches = (uint32_t)fb;
-    cp.plan.nseg = (uint32_t)ds.size();
-    cp.plan.max_k = maxk;
-    {
-        uint64_t steps = 0;
-        for (const br_segment &sg : segs) steps += (uint64_t)sg.k * sg.count;
-        cp.plan.lo = (uint32_t)(n > steps ? n - steps : 0);
-        cp.plan.naive = naive ? 1u : 0u;
-    }
-    cp.plan.segs = (const DevSeg *)p;
-    cp.plan.thresh = (const uint64_t *)((char *)p + off);
-    cp.plan.brec = br.empty() ? nullptr : (const uint4 *)((char *)p + boff);
-    cp.nbatches = fb;
-    if (g_plans.size() >= PLAN_CACHE_MAX) {
-        // bounded cache: drop every plan once the device is idle (no kernel still reads
-        // one); callers with thousands of distinct lengths pay a rebuild, not memory
-        cudaDeviceSynchronize();
-        for (auto &kv : g_plans) cudaFree(kv.second.dev);
-        g_plans.clear();
-    }
-    g_plans[{dev, key}] = cp;
-    *out = cp;
+    *out = p;
     return BR_OK;
 }
 
@@ -473,18 +587,15 @@ constexpr uint32_t WARP_SMEM_DEFAULT = 16 * 1024; // warp kernel by default (mea
 #ifndef RES_WS
 #define RES_WS 16  // single-array stream calls: one CTA, as wide as its window allows
 #endif
-#ifndef PIPE_W
-#define PIPE_W 8
-#endif
 
-// BR_SHUFFLE_KERNEL=small|resolve|warp|hash|mid|pipe|large|global restricts the dispatch below to one
+// BR_SHUFFLE_KERNEL=small|resolve|idx|warp|hash|mid|large|global restricts the dispatch below to one
 // shuffle kernel where it is eligible (tests cover every kernel; A/B timing).  Unset: the
 // first eligible kernel in the order below.
-enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_PIPE, K_LARGE, K_GLOBAL, K_WARP, K_WARP64, K_IDX };
+enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_LARGE, K_GLOBAL, K_WARP, K_IDX };
 int forced_kernel() {
     const char *e = getenv("BR_SHUFFLE_KERNEL");
     if (!e || !*e) return K_ANY;
-    static const char *names[] = {"", "small", "resolve", "hash", "mid", "pipe", "large", "global", "warp", "warp64", "idx"};
+    static const char *names[] = {"", "small", "resolve", "hash", "mid", "large", "global", "warp", "idx"};
     for (int i = 1; i <= K_IDX; ++i)
         if (!strcmp(e, names[i])) return i;
     return K_ANY;
@@ -503,7 +614,7 @@ inline bool allow(int k) {
 }
 
 template <typename T>
-int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan &cp, bool segmented,
+int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &cp, bool segmented,
                    uint64_t run_seed, int64_t base, uint32_t *words32, uint64_t *state_dev, uint64_t *words64,
                    uint64_t *rk_first, int gen, const DeviceInfo &di, cudaStream_t st) {
     const uint32_t stride = (uint32_t)(n | 1u);
@@ -603,19 +714,6 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
             }
         }
     }
-    if (forced_kernel() == K_WARP64 && cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
-        (uint64_t)cp.plan.max_k * 32 + 128 <= WRING64) {
-        auto kern = gen == 2 ? shuffle_warp_kernel<T, true, 1, 64> : shuffle_warp_kernel<T, true, 0, 64>;
-        const void *kp = (const void *)kern;
-        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes));
-        const int grid = grid_for(di, kp, 32, zbytes, num_arrays);
-        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
-        kern<<<grid, 32, zbytes, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
-                                       rk_first, use_tma, gen);
-        CK(cudaGetLastError());
-        g_kernel = std::string("shuffle_warp_kernel<u") + std::to_string(8 * sizeof(T)) + ",64>";
-        return BR_OK;
-    }
     const bool warp_fit = cp.plan.brec && segmented && zbytes <= WARP_SMEM_MAX &&
                           (uint64_t)cp.plan.max_k * 32 + 64 <= WRING;
     if (warp_fit && (forced_kernel() == K_WARP || (forced_kernel() == K_ANY && zbytes <= WARP_SMEM_DEFAULT))) {
@@ -662,23 +760,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const CachedPlan 
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
     }
-    // large arrays: one CTA per array, targets generated in-CTA, array in global memory,
-    // next group's values prefetched (pipe) or loaded per group (large)
-    if (forced_kernel() == K_PIPE && (uint64_t)cp.plan.max_k * 32 * PIPE_W + 2 * 32 * PIPE_W <= PRING) {
-        constexpr int W = PIPE_W;
-        const size_t psmem = sizeof(PipeShared<T, W>);
-        auto kern = !segmented ? shuffle_cta_pipe_kernel<T, W, 2>
-                               : (gen == 2 ? shuffle_cta_pipe_kernel<T, W, 1> : shuffle_cta_pipe_kernel<T, W, 0>);
-        const void *kp = (const void *)kern;
-        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-        const int grid = segmented ? grid_for(di, kp, 32 * W, psmem, num_arrays) : 1;
-        kern<<<grid, 32 * W, psmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
-                                          rk_first, segmented ? 1 : 0, gen);
-        CK(cudaGetLastError());
-        g_kernel = std::string("shuffle_cta_pipe_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
-                   std::to_string(W) + ">";
-        return BR_OK;
-    }
+    // large arrays: one CTA per array, targets generated in-CTA, array in global memory
     if (allow(K_LARGE) && (uint64_t)cp.plan.max_k * 32 * LARGE_W + 32 * LARGE_W <= large_ring(LARGE_W)) {
         constexpr int W = LARGE_W;
         const int grid = segmented ? (int)std::min<int64_t>(num_arrays, (int64_t)di.sms * 8) : 1;
@@ -742,14 +824,15 @@ int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std
     }
     if (!data) return fail(BR_E_INVALID, "null data pointer");
     if (!segmented && !state_dev) return fail(BR_E_INVALID, "null state pointer");
-    CachedPlan cp;
-    stt = get_plan(n, segs, naive, &cp);
+    PlanRef cp;
+    stt = get_plan(n, segs, naive, st, &cp);
     if (stt) return stt;
-    if (eb == 4)
-        return launch_shuffle<uint32_t>(data, num_arrays, n, cp, segmented, run_seed, base, words32,
-                                        (uint64_t *)state_dev, words64, rk_first, gen, di, st);
-    return launch_shuffle<uint64_t>(data, num_arrays, n, cp, segmented, run_seed, base, words32,
-                                    (uint64_t *)state_dev, words64, rk_first, gen, di, st);
+    const int r = eb == 4 ? launch_shuffle<uint32_t>(data, num_arrays, n, *cp, segmented, run_seed, base, words32,
+                                                     (uint64_t *)state_dev, words64, rk_first, gen, di, st)
+                          : launch_shuffle<uint64_t>(data, num_arrays, n, *cp, segmented, run_seed, base, words32,
+                                                     (uint64_t *)state_dev, words64, rk_first, gen, di, st);
+    cp->used(st);  // the plan outlives every kernel queued above (stream-ordered free)
+    return r;
 }
 
 }  // namespace
@@ -916,9 +999,34 @@ int br_pcg64_fill(uint64_t *out_dev, int64_t count, const br_pcg64 *st, uint64_t
 int br_state_upload(br_pcg64 *state_dev, const br_pcg64 *st, void *stream) {
     if (!state_dev || !st) return fail(BR_E_INVALID, "null state");
     const size_t bytes = host_is_chacha(st) ? sizeof(br_chacha) : sizeof(br_pcg64);
-    CK(cudaMemcpyAsync(state_dev, st, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    // through a per-thread ring of pinned 64-byte slots: the copy is a true async DMA (a
+    // pageable source would make the driver wait for the stream) and the caller's struct may
+    // go away at once.  A slot is reused only after the event of its previous copy (a host
+    // wait only if 64 uploads are still queued)
+    struct Ring {
+        br_chacha *slots = nullptr;
+        cudaEvent_t ev[64] = {};
+        int dev[64];
+        unsigned next = 0;
+    };
+    thread_local Ring ring;
+    if (!ring.slots) CK(cudaHostAlloc((void **)&ring.slots, 64 * sizeof(br_chacha), cudaHostAllocPortable));
+    const unsigned i = ring.next++ & 63u;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (ring.ev[i]) {
+        CK(cudaEventSynchronize(ring.ev[i]));
+        if (ring.dev[i] != dev) {  // events belong to a device
+            cudaEventDestroy(ring.ev[i]);
+            ring.ev[i] = nullptr;
+        }
+    }
+    if (!ring.ev[i]) CK(cudaEventCreateWithFlags(&ring.ev[i], cudaEventDisableTiming));
+    ring.dev[i] = dev;
+    memcpy(&ring.slots[i], st, bytes);
+    CK(cudaMemcpyAsync(state_dev, &ring.slots[i], bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    CK(cudaEventRecord(ring.ev[i], (cudaStream_t)stream));
     note_state_kind(state_dev, host_is_chacha(st));
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
     return BR_OK;
 }
 
@@ -1123,8 +1231,10 @@ int br_shuffle_naive_segmented(void *data, int eb, int64_t num_arrays, uint64_t 
 
 void br_release(void) {
     std::lock_guard<std::mutex> lk(g_mu);
-    for (auto &kv : g_plans) cudaFree(kv.second.dev);
-    g_plans.clear();
+    PlanCache &pc = plan_cache();
+    pc.map.clear();  // each plan is freed (stream-ordered) once no caller holds it
+    pc.lru.clear();
+    pc.bytes = 0;
 }
 
 }  // extern "C"

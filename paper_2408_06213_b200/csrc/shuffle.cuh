@@ -19,8 +19,7 @@
 //   shuffle_cta_large_kernel the same groups on arrays in global memory (HBM-resident);
 //   shuffle_mid_kernel / shuffle_large_gen+apply  warp-group forms for schedules with
 //                            large k; shuffle_resolve_kernel (closed-form, whole array)
-//                            serves single-array stream calls; shuffle_cta_pipe_kernel is a
-//                            measured alternative, run only when BR_SHUFFLE_KERNEL asks.
+//                            serves single-array stream calls.
 // Words: lane = batch, jump-ahead per lane, a CTA-wide vote on the rare rejection.
 #pragma once
 #include "chacha.cuh"
@@ -833,218 +832,6 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
     else if (CM != 1)
         shuffle_cta_large_body<T, W, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                             rk_first, segmented, gen, sh, chawin);
-}
-
-// -------------------------------------------------------------------------------------
-// arrays in global memory, software-pipelined: the next group's z[i], z[j] are loaded
-// while this group resolves, and patched from this group's writes when it is their turn
-// -------------------------------------------------------------------------------------
-// In the plain large kernel every group waits a full HBM round trip for its random z[j]
-// (about half of the stall samples, profiles/ncu_r1b.md).  Here group g+1's values are
-// loaded before group g writes.  Group g can only change them through its writes
-// z[j] = A for targets j below its range (it never writes positions of g+1's range
-// otherwise), so group g+1 looks each of its two addresses up in group g's lane-chain hash
-// (kept in the other half of a double buffer) and takes the writer's A where there is one.
-// Loads see either the old or the new value; the patch makes both right.
-// Measured on B200 (C5): 13.8 ms against 13.0 ms for the plain kernel -- hiding the read
-// latency does not help because C5 is bound by the THROUGHPUT of random 8-byte HBM accesses
-// (one random read and one random write per element: about 20 G/s each, against 23 G/s for
-// a bare random scatter, tools/micro/randgather.cu), not by their latency.  Opt-in only
-// (BR_SHUFFLE_KERNEL=pipe); kept and tested as the latency-hiding variant.
-static constexpr uint32_t PRING = 8192;  // u32 target ring: 2 groups + one generation step
-static constexpr int PHB = 11;           // 2048-slot hash per group
-static constexpr uint32_t PTAG_MAX = 1u << 22;
-
-template <typename T, int W>
-struct PipeBuf {
-    uint32_t ht[1 << PHB];  // (group tag << 9) | (lane + 1)
-    int16_t nxt[32 * W];
-    uint32_t jv[32 * W];
-    T AV[32 * W];
-    uint8_t wr[32 * W];  // the lane wrote z[j] = A (last toucher of a target below the group)
-};
-
-template <typename T, int W>
-struct PipeShared {
-    static constexpr uint32_t RSIZE = PRING;
-    using RType = uint32_t;
-    DevSeg segs[MAX_SEGS];
-    uint32_t ring[PRING];
-    PipeBuf<T, W> buf[2];
-    int16_t P[32 * W];
-    T VI[32 * W];
-    uint32_t fmin;
-    uint32_t frontier[2];
-};
-
-__device__ __forceinline__ uint32_t pipe_hash(uint32_t j) { return (j * 2654435761u) >> (32 - PHB); }
-
-template <typename T, int W>
-__device__ __forceinline__ T pipe_lookup(const PipeBuf<T, W> &pb, uint32_t ptag, uint32_t x, T v) {
-    const uint32_t head = pb.ht[pipe_hash(x)];
-    if ((head >> 9) != ptag) return v;
-    for (int t = (int)(head & 511u) - 1; t >= 0; t = pb.nxt[t])
-        if (pb.jv[t] == x && pb.wr[t]) return pb.AV[t];
-    return v;
-}
-
-template <typename T, int W>
-__device__ __forceinline__ void apply_group_pipe(T *z, PipeShared<T, W> &sh, uint32_t tag, uint32_t top, uint32_t lim,
-                                                 int L, T &vi, T &vj, bool patch, bool prefetch) {
-    constexpr int G = 32 * W;
-    PipeBuf<T, W> &cb = sh.buf[tag & 1];
-    const PipeBuf<T, W> &pb = sh.buf[(tag & 1) ^ 1];
-    const int64_t i64 = (int64_t)top - L;
-    const bool act = i64 >= (int64_t)lim;
-    const uint32_t i = act ? (uint32_t)i64 : 0;
-    const uint32_t j = act ? sh.ring[i & (PRING - 1)] : 0;
-    if (act && patch) {
-        vi = pipe_lookup(pb, tag - 1, i, vi);
-        vj = pipe_lookup(pb, tag - 1, j, vj);
-    }
-    const uint32_t lo_pos = top >= lim + (G - 1) ? top - (G - 1) : lim;
-    const bool inrange = act && j >= lo_pos && j < i;
-    const uint32_t h = pipe_hash(j);
-    int16_t link = -1;
-    if (act) {
-        const uint32_t old = atomicExch(&cb.ht[h], (tag << 9) | (uint32_t)(L + 1));
-        if ((old >> 9) == tag) link = (int16_t)((old & 511u) - 1);
-    }
-    cb.nxt[L] = link;
-    cb.jv[L] = j;
-    sh.P[L] = -1;
-    sh.VI[L] = vi;
-    __syncthreads();
-    int tl = -1;
-    bool later = false;
-    if (act) {
-        const uint32_t head = cb.ht[h];
-        for (int t = (int)(head & 511u) - 1; t >= 0; t = cb.nxt[t]) {
-            if (t != L && cb.jv[t] == j) {
-                if (t < L) tl = t > tl ? t : tl;
-                else later = true;
-            }
-        }
-    }
-    if (inrange && !later) sh.P[top - j] = (int16_t)L;
-    __syncthreads();
-    int p = sh.P[L];
-    p = p >= 0 ? p : L;
-    for (;;) {
-        const int q = sh.P[p];
-        const int np = q >= 0 ? q : p;
-        if (!__syncthreads_or(np != p)) break;
-        p = np;
-    }
-    const T A = sh.VI[p];
-    const bool writes_j = act && !later && j < lo_pos;
-    cb.AV[L] = A;
-    cb.wr[L] = writes_j ? 1 : 0;
-    __syncthreads();
-    const T B = tl >= 0 ? cb.AV[tl] : vj;
-    T nvi = T(0), nvj = T(0);
-    if (prefetch) {  // the next group's values, before this group's writes
-        const int64_t ni64 = (int64_t)top - G - L;
-        if (ni64 >= (int64_t)lim) {
-            const uint32_t ni = (uint32_t)ni64;
-            nvi = z[ni];
-            nvj = z[sh.ring[ni & (PRING - 1)]];
-        }
-    }
-    if (act) {
-        z[i] = B;
-        if (writes_j) z[j] = A;
-    }
-    vi = nvi;
-    vj = nvj;
-    __syncthreads();
-}
-
-template <typename T, int W, bool CHA>
-__device__ __forceinline__ void shuffle_cta_pipe_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
-                                                      uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
-                                                      uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
-                                                      int segmented, int gen, PipeShared<T, W> &sh,
-                                                      uint64_t *chawin) {
-    constexpr int G = 32 * W;
-    const int L = threadIdx.x;
-    for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
-    const uint32_t n = plan.n;
-    const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
-    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
-        T *z = data + a * (int64_t)n;
-        for (uint32_t q = L; q < (1u << PHB); q += G) {
-            sh.buf[0].ht[q] = 0;
-            sh.buf[1].ht[q] = 0;
-        }
-        __syncthreads();
-        u128 s0, inc;
-        bool lh;
-        ChaKey ck;
-        CtaGen<W> gs;
-        cta_gen_setup<CHA, W>(gs, s0, inc, lh, ck, segmented, gen, run_seed, base + a, state_io, n, L);
-        uint64_t *rkf = segmented ? nullptr : rk_first;
-        uint32_t tag = 0;
-        bool have = false;  // vi/vj hold this group's prefetched values
-        T vi = T(0), vj = T(0);
-        for (int64_t top = (int64_t)n - 1; top >= (int64_t)lim; top -= G) {
-            // targets of this group and the next one must be in the ring
-            const uint32_t need = top >= (int64_t)lim + (2 * G - 1) ? (uint32_t)top - (2 * G - 1) : lim;
-            while (gs.frontier > need && gs.B0 < plan.nbatches) large_gen_step<CHA, W>(gs, plan, sh, L, rkf, chawin, ck);
-            bool patch = have;
-            if (++tag == PTAG_MAX) {  // tag wrap: fresh tables, no prefetch to trust
-                for (uint32_t q = L; q < (1u << PHB); q += G) {
-                    sh.buf[0].ht[q] = 0;
-                    sh.buf[1].ht[q] = 0;
-                }
-                __syncthreads();
-                tag = 1;
-                patch = have = false;
-            }
-            if (!have) {
-                const int64_t i64 = top - L;
-                if (i64 >= (int64_t)lim) {
-                    vi = z[i64];
-                    vj = z[sh.ring[(uint32_t)i64 & (PRING - 1)]];
-                }
-            }
-            const bool pref = top >= (int64_t)lim + G;
-            apply_group_pipe(z, sh, tag, (uint32_t)top, lim, L, vi, vj, patch, pref);
-            have = pref;
-        }
-        while (gs.B0 < plan.nbatches) large_gen_step<CHA, W>(gs, plan, sh, L, rkf, chawin, ck);
-        const uint64_t words = (uint64_t)plan.nbatches + gs.D;
-        if (L == 0) {
-            if (segmented) {
-                if (words32) words32[a] = (uint32_t)words;
-            } else {
-                const u128 sf = CHA ? cha_add(s0, words) : gen_jump(s0, inc, words, lh);
-                state_io[0] = sf.hi;
-                state_io[1] = sf.lo;
-                if (words64) words64[0] = words;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-template <typename T, int W, int CM>
-__global__ void __launch_bounds__(32 * W) shuffle_cta_pipe_kernel(T *__restrict__ data, int64_t num_arrays,
-                                                                  DevPlan plan, uint64_t run_seed, int64_t base,
-                                                                  uint32_t *__restrict__ words32, uint64_t *state_io,
-                                                                  uint64_t *words64, uint64_t *rk_first,
-                                                                  int segmented, int gen) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    PipeShared<T, W> &sh = *reinterpret_cast<PipeShared<T, W> *>(smem_raw);
-    __shared__ __align__(16) uint64_t chawin[CM ? 8 * 32 * W : 2];
-    bool cha = CM == 1;
-    if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
-    if (CM != 0 && cha)
-        shuffle_cta_pipe_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
-                                             rk_first, segmented, gen, sh, chawin);
-    else if (CM != 1)
-        shuffle_cta_pipe_body<T, W, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
-                                           rk_first, segmented, gen, sh, chawin);
 }
 
 // Shared-memory-resident arrays with the same hashed CTA groups: payload moved by TMA bulk

@@ -222,115 +222,10 @@ __device__ __forceinline__ void warp_apply_group_exact(uint32_t z, uint32_t P, u
     __syncwarp();
 }
 
-// ---- 64-step groups: lane l owns steps l and l + 32 (two independent instruction streams
-// per lane, so each warp has twice the work between its dependent waits).  Same formulas as
-// warp_apply_group_exact with step indices s in [0, 64) and 64-bit lane masks.
-static constexpr uint32_t WRING64 = 512;  // two groups of 64 + one generation step (k <= 6)
-#ifndef BR_WTBL64
-#define BR_WTBL64 2048
-#endif
-static constexpr uint32_t WTBL64 = BR_WTBL64;
-
-__device__ __forceinline__ uint64_t ballot64(bool a, bool b) {
-    return (uint64_t)__ballot_sync(FULL, a) | ((uint64_t)__ballot_sync(FULL, b) << 32);
-}
-
-__device__ __forceinline__ void w64_targets(uint32_t ring, uint32_t tbl, uint32_t top, uint32_t lim, int lane,
-                                            uint32_t &ja, uint32_t &jb, bool &sha, bool &shb) {
-    const uint32_t sa = (uint32_t)lane, sb = sa + 32u;
-    const bool aa = sa <= top - lim, ab = sb <= top - lim;
-    ja = aa ? lds_u16(ring + 2u * ((top - sa) & (WRING64 - 1))) : 0u;
-    jb = ab ? lds_u16(ring + 2u * ((top - sb) & (WRING64 - 1))) : 0u;
-    const uint32_t ta = tbl + (ja & (WTBL64 - 1)), tb = tbl + (jb & (WTBL64 - 1));
-    if (aa) sts_s8(ta, (int)sa);
-    if (ab) sts_s8(tb, (int)sb);
-    __syncwarp();
-    sha = aa && lds_s8(ta) != (int)sa;
-    shb = ab && lds_s8(tb) != (int)sb;
-}
-
-__device__ __forceinline__ void w64_same(uint32_t top, uint32_t lim, int lane, uint32_t ja, uint32_t jb, bool sha,
-                                         bool shb, uint64_t &sma, uint64_t &smb) {
-    const uint32_t sa = (uint32_t)lane, sb = sa + 32u;
-    const bool aa = sa <= top - lim, ab = sb <= top - lim;
-    uint64_t pending = ballot64(sha, shb);
-    sma = 1ull << sa;
-    smb = 1ull << sb;
-    while (pending) {
-        const int f = __ffsll((long long)pending) - 1;
-        const uint32_t x = __shfl_sync(FULL, f < 32 ? ja : jb, f & 31);
-        const uint64_t S = ballot64(aa && ja == x, ab && jb == x);
-        if ((S >> sa) & 1ull) sma = S;
-        if ((S >> sb) & 1ull) smb = S;
-        pending &= ~S;
-    }
-}
-
-template <typename T>
-__device__ __forceinline__ T sel_t(bool c, T a, T b) { return c ? a : b; }
-
-template <typename T>
-__device__ __forceinline__ void w64_apply(uint32_t z, uint32_t P, uint32_t top, uint32_t lim, int lane, uint32_t ja,
-                                          uint32_t jb, uint64_t sma, uint64_t smb) {
-    constexpr uint32_t E = sizeof(T);
-    const uint32_t sa = (uint32_t)lane, sb = sa + 32u;
-    const bool aa = sa <= top - lim, ab = sb <= top - lim;
-    const uint32_t ia = top - sa, ib = top - sb;
-    const uint32_t lo = top - lim >= 63 ? top - 63 : lim;
-    T via = T(0), vja = T(0), vib = T(0), vjb = T(0);
-    if (aa) {
-        lds_v(z + E * ia, via);
-        lds_v(z + E * ja, vja);
-    }
-    if (ab) {
-        lds_v(z + E * ib, vib);
-        lds_v(z + E * jb, vjb);
-    }
-    const uint64_t bla = sma & ((1ull << sa) - 1ull), blb = smb & ((1ull << sb) - 1ull);
-    const uint64_t aba = sma & ~((2ull << sa) - 1ull), abb = smb & ~((2ull << sb) - 1ull);  // s = 63: 2 << 63 == 0
-    const bool inra = aa && ja >= lo && ja != ia;  // j = i_s' of the later step s' = top - j
-    const bool inrb = ab && jb >= lo && jb != ib;
-    T Aa = via, Ab = vib;
-    if (__any_sync(FULL, inra || inrb)) {
-        sts_s8(P + sa, -1);
-        sts_s8(P + sb, -1);
-        __syncwarp();
-        if (inra && (aba & ~(1ull << (top - ja))) == 0) sts_s8(P + (top - ja), (int)sa);
-        if (inrb && (abb & ~(1ull << (top - jb))) == 0) sts_s8(P + (top - jb), (int)sb);
-        __syncwarp();
-        const int pa = lds_s8(P + sa), pb = lds_s8(P + sb);
-        int ra = pa >= 0 ? pa : (int)sa, rb = pb >= 0 ? pb : (int)sb;
-        for (;;) {  // pointer jumping over 64 steps: step x's pointer is in lane x & 31, half x >> 5
-            const int a0 = __shfl_sync(FULL, ra, ra & 31), a1 = __shfl_sync(FULL, rb, ra & 31);
-            const int b0 = __shfl_sync(FULL, ra, rb & 31), b1 = __shfl_sync(FULL, rb, rb & 31);
-            const int na = ra < 32 ? a0 : a1, nb = rb < 32 ? b0 : b1;
-            if (!__any_sync(FULL, na != ra || nb != rb)) break;
-            ra = na;
-            rb = nb;
-        }
-        Aa = sel_t(ra < 32, shfl_t<T>(via, ra & 31), shfl_t<T>(vib, ra & 31));
-        Ab = sel_t(rb < 32, shfl_t<T>(via, rb & 31), shfl_t<T>(vib, rb & 31));
-        __syncwarp();
-    }
-    const int ta = bla ? 63 - __clzll((long long)bla) : (int)sa;  // T(s) < s: always in the first half
-    const int tb = blb ? 63 - __clzll((long long)blb) : (int)sb;
-    const T Bta = shfl_t<T>(Aa, ta & 31);
-    const T Btb = sel_t(tb < 32, shfl_t<T>(Aa, tb & 31), shfl_t<T>(Ab, tb & 31));
-    if (aa) {
-        sts_v(z + E * ia, bla ? Bta : vja);
-        if (!aba && ja < lo) sts_v(z + E * ja, Aa);
-    }
-    if (ab) {
-        sts_v(z + E * ib, blb ? Btb : vjb);
-        if (!abb && jb < lo) sts_v(z + E * jb, Ab);
-    }
-    __syncwarp();
-}
-
 // IDX: the warp shuffles a u16 index permutation of the array (2 bytes per element in shared
 // memory instead of sizeof(T)), then applies it to the payload through one of the CTA's
 // shared staging buffers: more arrays per SM (shuffle_idx_kernel).
-template <typename T, bool SEGMENTED, bool CHA, int GS, bool IDX = false>
+template <typename T, bool SEGMENTED, bool CHA, bool IDX = false>
 __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
                                                   uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
                                                   uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
@@ -341,7 +236,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
     using E = std::conditional_t<IDX, uint16_t, T>;  // element type of the array being permuted
     const int lane = threadIdx.x & 31;
     if (!IDX && use_tma && lane == 0) mbar_init(&bar, 1);
-    if (GS == 32) P[lane] = -1;  // warp_apply_group_exact's invariant
+    P[lane] = -1;  // warp_apply_group_exact's invariant
     __syncwarp();
     const uint32_t n = plan.n;
     const uint32_t bytes = n * (uint32_t)sizeof(T);
@@ -399,54 +294,19 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
         gs.frontier = n;
         uint64_t *rkf = SEGMENTED ? nullptr : rk_first;
         // the first targets are generated while the payload streams in
-        if (plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
+        if (plan.nbatches) warp_gen_step<CHA, WRING>(gs, plan, ring, lane, rkf, chawin, ck);
         if (!IDX && use_tma) {
             mbar_wait(&bar, parity);
             parity ^= 1u;
         }
         __syncwarp();
-        if (GS == 64 && n > lim) {
-            uint32_t top = n - 1, ja, jb;
-            uint64_t sma, smb;
-            const uint32_t need0 = top - lim >= 63 ? top - 63 : lim;
-            while (gs.frontier > need0 && gs.B0 < plan.nbatches)
-                warp_gen_step<CHA, WRING64>(gs, plan, ring, lane, rkf, chawin, ck);
-            __syncwarp();
-            const uint32_t zs = smem_base(z), rs = smem_base(ring), ps = smem_base(P), ts = smem_base(tbl);
-            bool sha, shb;
-            w64_targets(rs, ts, top, lim, lane, ja, jb, sha, shb);
-            w64_same(top, lim, lane, ja, jb, sha, shb, sma, smb);
-            auto group = [&](uint32_t t, uint32_t ca, uint32_t cb, uint64_t csa, uint64_t csb, uint32_t &na,
-                             uint32_t &nb, uint64_t &nsa, uint64_t &nsb) -> bool {
-                const bool last = t < lim + 64;
-                const uint32_t nt = t - 64;
-                bool sa = false, sb = false;
-                if (!last) {
-                    const uint32_t need = nt - lim >= 63 ? nt - 63 : lim;
-                    while (gs.frontier > need && gs.B0 < plan.nbatches)
-                        warp_gen_step<CHA, WRING64>(gs, plan, ring, lane, rkf, chawin, ck);
-                    __syncwarp();
-                    w64_targets(rs, ts, nt, lim, lane, na, nb, sa, sb);
-                }
-                w64_apply<E>(zs, ps, t, lim, lane, ca, cb, csa, csb);
-                if (!last) w64_same(nt, lim, lane, na, nb, sa, sb, nsa, nsb);
-                return last;
-            };
-            uint32_t ja2, jb2;
-            uint64_t sma2, smb2;
-            for (;;) {
-                if (group(top, ja, jb, sma, smb, ja2, jb2, sma2, smb2)) break;
-                top -= 64;
-                if (group(top, ja2, jb2, sma2, smb2, ja, jb, sma, smb)) break;
-                top -= 64;
-            }
-        } else if (n > lim) {
+        if (n > lim) {
             // software-pipelined: group g+1's targets and equality mask are prepared around
             // group g's swaps
             uint32_t top = n - 1, j;
             unsigned same;
             const uint32_t need0 = top - lim >= 31 ? top - 31 : lim;
-            while (gs.frontier > need0 && gs.B0 < plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
+            while (gs.frontier > need0 && gs.B0 < plan.nbatches) warp_gen_step<CHA, WRING>(gs, plan, ring, lane, rkf, chawin, ck);
             __syncwarp();
             const uint32_t zs = smem_base(z), rs = smem_base(ring), ps = smem_base(P), ts = smem_base(tbl);
             bool sh;
@@ -466,7 +326,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                     // the common case (targets already there) costs one compare
                     if (gs.frontier > need) {
                         do {
-                            warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
+                            warp_gen_step<CHA, WRING>(gs, plan, ring, lane, rkf, chawin, ck);
                         } while (gs.frontier > need && gs.B0 < plan.nbatches);
                     }
                     __syncwarp();
@@ -495,7 +355,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
             }
         }
         // finish the word accounting (a trailing rejection can follow the last position)
-        while (gs.B0 < plan.nbatches) warp_gen_step<CHA, (GS == 64 ? WRING64 : WRING)>(gs, plan, ring, lane, rkf, chawin, ck);
+        while (gs.B0 < plan.nbatches) warp_gen_step<CHA, WRING>(gs, plan, ring, lane, rkf, chawin, ck);
         if constexpr (IDX) {
             // take a free staging buffer, copy the payload in, write out[p] = payload[idx[p]]
             int sb = 0;
@@ -570,26 +430,26 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
 }
 
 // CM as in shuffle_mid_kernel: 0 = PCG64/Lehmer, 1 = ChaCha, 2 = from the stream state's tag
-template <typename T, bool SEGMENTED, int CM, int GS = 32>
+template <typename T, bool SEGMENTED, int CM>
 __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
                                                           uint64_t run_seed, int64_t base,
                                                           uint32_t *__restrict__ words32, uint64_t *state_io,
                                                           uint64_t *words64, uint64_t *rk_first, int use_tma,
                                                           int gen) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(16) uint16_t ring[GS == 64 ? WRING64 : WRING];
+    __shared__ __align__(16) uint16_t ring[WRING];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ int8_t P[GS];
-    __shared__ int8_t tbl[GS == 64 ? WTBL64 : WTBL + 32];
+    __shared__ int8_t P[32];
+    __shared__ int8_t tbl[WTBL + 32];
     __shared__ __align__(16) uint64_t chawin[CM ? 256 : 2];
     T *z = reinterpret_cast<T *>(smem_raw);
     bool cha = CM == 1;
     if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
-        shuffle_warp_body<T, SEGMENTED, CM != 0, GS>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+        shuffle_warp_body<T, SEGMENTED, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                                  rk_first, use_tma, gen, z, ring, P, tbl, bar, chawin);
     else if (CM != 1)
-        shuffle_warp_body<T, SEGMENTED, false, GS>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
+        shuffle_warp_body<T, SEGMENTED, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
                                                rk_first, use_tma, gen, z, ring, P, tbl, bar, chawin);
 }
 
@@ -631,11 +491,11 @@ __global__ void __launch_bounds__(768, 1) shuffle_idx_kernel(T *__restrict__ dat
     __syncthreads();
     uint64_t bar = 0;
     if constexpr (CM == 1)
-        shuffle_warp_body<T, true, true, 32, true>(data, num_arrays, plan, run_seed, base, words32, nullptr, nullptr,
+        shuffle_warp_body<T, true, true, true>(data, num_arrays, plan, run_seed, base, words32, nullptr, nullptr,
                                                    nullptr, use_tma, gen, idx, ring, P, tbl, bar, chawin, stage,
                                                    locks, nstage, selems);
     else
-        shuffle_warp_body<T, true, false, 32, true>(data, num_arrays, plan, run_seed, base, words32, nullptr,
+        shuffle_warp_body<T, true, false, true>(data, num_arrays, plan, run_seed, base, words32, nullptr,
                                                     nullptr, nullptr, use_tma, gen, idx, ring, P, tbl, bar, chawin,
                                                     stage, locks, nstage, selems);
 }

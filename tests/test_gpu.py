@@ -297,11 +297,9 @@ KERNEL_CASES = {  # forced kernel -> (name in last_kernel, lengths it can take)
     "resolve": ("shuffle_resolve_kernel", (2, 3, 64, 100, 1000, 4096, 4097, 10000)),
     "hash": ("shuffle_cta_hash_kernel", (2, 64, 1000, 4096, 10000, 20000)),
     "mid": ("shuffle_mid_kernel", (2, 64, 1000, 4096, 10000)),
-    "pipe": ("shuffle_cta_pipe_kernel", (2, 64, 1000, 4096, 70000, 300001)),
     "large": ("shuffle_cta_large_kernel", (2, 64, 1000, 4096, 70000)),
     "global": ("shuffle_large_gen_kernel", (2, 64, 1000, 4096, 70000)),
     "warp": ("shuffle_warp_kernel", (2, 33, 64, 1000, 4096, 6000, 12000)),
-    "warp64": ("shuffle_warp_kernel", (2, 33, 64, 65, 127, 1000, 4096, 6000, 12000)),
     "idx": ("shuffle_idx_kernel", (2, 33, 64, 65, 127, 1000, 4096, 4097, 6000, 12000)),
 }
 

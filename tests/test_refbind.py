@@ -182,7 +182,7 @@ def test_reference_exceptions(ref, dev):
         dev.partial_shuffle_batch(ref.make_source("pcg64", 1), list(range(52)), 52, 2, 100)
     with pytest.raises(ValueError):
         dev.shuffle_batched(ref.make_source("pcg64", 1), list(range(10)),
-                            ref.ShuffleSchedule(entries=((1 << 30, 2),), max_batch=2, word_bits=32))
+                            ref.ShuffleSchedule(entries=((1 << 16, 2),), max_batch=2, word_bits=32))
 
 
 @gpu
