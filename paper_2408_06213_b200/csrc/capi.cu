@@ -21,6 +21,7 @@
 #include "jump.cuh"
 #include "roll.cuh"
 #include "shuffle.cuh"
+#include "stage_shuffle.cuh"
 #include "warp_shuffle.cuh"
 
 using namespace br;
@@ -75,6 +76,13 @@ int ensure_device(int *dev_out, DeviceInfo *info_out) {
         CK(cudaMemcpyToSymbol(c_LA, t.LA, sizeof(t.LA)));
         CK(cudaMemcpyToSymbol(g_LSA, t.LSA, sizeof(t.LSA)));
         CK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+        // stream-ordered scratch (cudaMallocAsync) stays mapped in the pool between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = 16ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
         int coop = 0;
         CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
         d.coop = coop != 0;
@@ -588,15 +596,15 @@ constexpr uint32_t WARP_SMEM_DEFAULT = 16 * 1024; // warp kernel by default (mea
 #define RES_WS 16  // single-array stream calls: one CTA, as wide as its window allows
 #endif
 
-// BR_SHUFFLE_KERNEL=small|resolve|idx|warp|hash|mid|large|global restricts the dispatch below to one
+// BR_SHUFFLE_KERNEL=small|resolve|idx|warp|hash|mid|stage|large|global restricts the dispatch below to one
 // shuffle kernel where it is eligible (tests cover every kernel; A/B timing).  Unset: the
 // first eligible kernel in the order below.
-enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_LARGE, K_GLOBAL, K_WARP, K_IDX };
+enum { K_ANY = 0, K_SMALL, K_RESOLVE, K_HASH, K_MID, K_LARGE, K_GLOBAL, K_WARP, K_IDX, K_STAGE };
 int forced_kernel() {
     const char *e = getenv("BR_SHUFFLE_KERNEL");
     if (!e || !*e) return K_ANY;
-    static const char *names[] = {"", "small", "resolve", "hash", "mid", "large", "global", "warp", "idx"};
-    for (int i = 1; i <= K_IDX; ++i)
+    static const char *names[] = {"", "small", "resolve", "hash", "mid", "large", "global", "warp", "idx", "stage"};
+    for (int i = 1; i <= K_STAGE; ++i)
         if (!strcmp(e, names[i])) return i;
     return K_ANY;
 }
@@ -758,6 +766,30 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
                                      words64, rk_first, use_tma, gen);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_mid_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
+        return BR_OK;
+    }
+    // many arrays beyond shared memory: the stage pipeline (stage_shuffle.cuh), one CTA per
+    // array, random accesses in shared memory only.  PCG64/Lehmer streams, full plans.
+    const uint64_t sp_nb = (n + SP_B - 1) / SP_B;
+    const bool sp_fit = segmented && gen != 2 && cp.plan.lo <= 1 && sp_nb <= SP_MAXNB &&
+                        (uint64_t)cp.plan.max_k * SP_T + SP_B <= SP_RING;
+    if (sp_fit && (forced_kernel() == K_STAGE || (forced_kernel() == K_ANY && n > 65536))) {
+        const size_t smem = sizeof(SpShared<T>);
+        const void *kp = (const void *)shuffle_stage_kernel<T>;
+        CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int grid = grid_for(di, kp, SP_T, smem, num_arrays);
+        const size_t per = sp_scratch_bytes<T>((uint32_t)n);
+        unsigned char *scratch = nullptr;
+        CK(cudaMallocAsync((void **)&scratch, per * (size_t)grid, st));
+        T *dp = (T *)data;
+        DevPlan plan = cp.plan;
+        int g = gen;
+        size_t pc = per;
+        void *args[] = {&dp, &num_arrays, &plan, &run_seed, &base, &words32, &g, &scratch, &pc};
+        const cudaError_t le = cudaLaunchKernel(kp, dim3(grid), dim3(SP_T), args, smem, st);
+        CK(cudaFreeAsync(scratch, st));
+        if (le != cudaSuccess) return fail(BR_E_CUDA, std::string("stage kernel launch: ") + cudaGetErrorString(le));
+        g_kernel = std::string("shuffle_stage_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
         return BR_OK;
     }
     // large arrays: one CTA per array, targets generated in-CTA, array in global memory

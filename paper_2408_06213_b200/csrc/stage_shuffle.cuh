@@ -1,0 +1,368 @@
+// stage_shuffle.cuh -- many arrays too large for shared memory (C5: 256 x u64[2^20]):
+// Fisher-Yates as a pipeline of shared-memory stages, one CTA per array, no random access
+// to global memory.
+//
+// The array is cut into blocks of SP_B positions.  Steps run from the top (shuffle.py:100-134:
+// step s swaps z[s] and z[J[s]], J[s] <= s, s = n-1 down to 1), so block sg's steps happen after
+// every step of the blocks above it.  Stage sg (sg = NB-1 down to 0) holds block sg in shared
+// memory and
+//   1. applies, in time order, the steps of higher blocks that target it ("records" left by
+//      those stages: target offset, the step's position, the value it deposits).  For a target
+//      q the steps arrive as an exchange sequence: the first returns z0[q], each later one the
+//      value of the one before, and q keeps the last deposit.  The returned value is the step's
+//      final output (out[s] = the value at J[s] just before step s); it goes to the result slot
+//      of the record, which sits in the SOURCE block's result area;
+//   2. generates the targets of its own steps (CTA-wide, with the rejection realignment of
+//      large_gen_step: word alignment is exact for any number of rejections);
+//   3. runs its own steps in closed form (DESIGN.md section 2.4 restricted to the block):
+//      with FT(x) the first later step targeting x inside the block and NS(s) the next such
+//      step after s with s's target, the value at x before step x is Val(x) = Val(FT(x)) or the
+//      block contents after (1); an in-block step outputs Val(NS(s)) or the contents of its
+//      target; a step targeting a lower block leaves a record (target, s, Val(s)) for the stage
+//      of that block;
+//   4. writes its records grouped by target block (tiles), a tile table entry per lower block,
+//      its in-block outputs into its result area and a slot map (position -> result slot).
+// After stage 0 every result slot is filled; out[p] = result[slot[p]] is gathered block by
+// block through shared memory.  Global traffic is streaming (records, results, slot maps);
+// all random accesses are in shared memory.
+//
+// Exactness: stage sg sees the block exactly as the sequential loop would after all higher
+// steps (their deposits in time order, records carry s); its own steps are the sequential
+// loop's (closed form, checked exhaustively in tests/test_resolution.py and bit-exactly
+// against the oracle on the device).
+#pragma once
+#include "shuffle.cuh"
+
+namespace br {
+
+static constexpr uint32_t SP_B = 4096;     // positions per block (one stage)
+static constexpr int SP_W = 16;            // warps per CTA
+static constexpr int SP_T = 32 * SP_W;     // threads per CTA
+static constexpr uint32_t SP_C = 1024;     // records per chunk of step 1
+static constexpr uint32_t SP_RING = 8192;  // u32 target ring: a block + one generation step (k <= 7)
+static constexpr uint32_t SP_MAXNB = 1024; // blocks per array (n <= 4M)
+static constexpr uint32_t SP_NONE = 0xFFFFFFFFu;
+static constexpr uint16_t SP_NONE16 = 0xFFFF;
+
+template <typename T>
+struct SpShared {
+    static constexpr uint32_t RSIZE = SP_RING;
+    using RType = uint32_t;
+    DevSeg segs[MAX_SEGS];
+    uint32_t ring[SP_RING];  // targets by position (large_gen_step)
+    T mbox[SP_B];            // the block's contents
+    uint32_t head[SP_B];     // per-target chain heads (atomicExch), SP_NONE = empty
+    union {
+        struct {  // step 1: one chunk of records
+            uint32_t key[SP_C];  // the record's step position s (larger = earlier in time)
+            T val[SP_C];
+            uint16_t link[SP_C];
+            uint16_t q[SP_C];
+        } rec;
+        struct {  // step 3: the block's own steps
+            uint16_t F[SP_B];  // FT pointer, then the end of the FT chain (Val(x) = mbox[F[x]])
+            uint16_t link[SP_B];
+        } loc;
+    } u;
+    uint32_t vstart[SP_MAXNB];  // tiles: exclusive prefix of counts; step 4: per-target-block prefix
+    uint32_t tbase[SP_MAXNB];   // tiles: first record index; step 4: per-target-block counts
+    uint32_t wsum[SP_W + 1];
+    uint32_t frontier[2];
+    uint32_t fmin;
+    uint32_t nint;
+};
+
+// exclusive scan of a[0..len) in place (len <= 2 * SP_T); every thread gets the total
+__device__ __forceinline__ uint32_t sp_scan(uint32_t *a, uint32_t len, uint32_t *wsum, int L) {
+    const uint32_t i0 = 2 * L, i1 = 2 * L + 1;
+    const uint32_t v0 = i0 < len ? a[i0] : 0, v1 = i1 < len ? a[i1] : 0;
+    const uint32_t loc = v0 + v1;
+    uint32_t inc = loc;
+    const int lane = L & 31, w = L >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t x = lane < SP_W ? wsum[lane] : 0;
+        uint32_t y = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, y, d);
+            if (lane >= d) y += o;
+        }
+        if (lane < SP_W) wsum[lane] = y - x;  // exclusive warp offsets
+        if (lane == SP_W - 1) wsum[SP_W] = y;  // grand total
+    }
+    __syncthreads();
+    const uint32_t ex = wsum[w] + inc - loc;
+    const uint32_t total = wsum[SP_W];
+    if (i0 < len) a[i0] = ex;
+    if (i1 < len) a[i1] = ex + v0;
+    __syncthreads();
+    return total;
+}
+
+// per-CTA global scratch (bytes) for arrays of n elements of T
+template <typename T>
+__host__ __device__ constexpr size_t sp_scratch_bytes(uint32_t n) {
+    const size_t nb = (n + SP_B - 1) / SP_B;
+    const size_t a = ((size_t)n * 4 + 255) & ~(size_t)255;          // record (target offset | position << 16)
+    const size_t b = ((size_t)n * sizeof(T) + 255) & ~(size_t)255;  // record value
+    const size_t c = b;                                              // result slots
+    const size_t d = ((size_t)n * 2 + 255) & ~(size_t)255;          // slot map
+    const size_t e = (nb * nb * 4 + 255) & ~(size_t)255;            // tile table
+    return a + b + c + d + e;
+}
+
+template <typename T>
+__device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
+                                                   uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
+                                                   int gen, SpShared<T> &sh, unsigned char *__restrict__ scratch,
+                                                   size_t scratch_per_cta) {
+    constexpr int PER = SP_B / SP_T;  // positions per thread in steps 3-4
+    constexpr int RPER = SP_C / SP_T; // records per thread in step 1
+    const int L = threadIdx.x;
+    const uint32_t n = plan.n;
+    const uint32_t NB = (n + SP_B - 1) / SP_B;
+    const uint32_t lo = plan.lo;
+    unsigned char *w = scratch + (size_t)blockIdx.x * scratch_per_cta;
+    uint32_t *fwdq = reinterpret_cast<uint32_t *>(w);
+    w += ((size_t)n * 4 + 255) & ~(size_t)255;
+    T *fwdv = reinterpret_cast<T *>(w);
+    w += ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
+    T *res = reinterpret_cast<T *>(w);
+    w += ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
+    uint16_t *slot = reinterpret_cast<uint16_t *>(w);
+    w += ((size_t)n * 2 + 255) & ~(size_t)255;
+    uint32_t *desc = reinterpret_cast<uint32_t *>(w);
+
+    for (uint32_t q = L; q < plan.nseg; q += SP_T) sh.segs[q] = plan.segs[q];
+    for (uint32_t x = L; x < SP_B; x += SP_T) sh.head[x] = SP_NONE;
+    if (L == 0) sh.nint = 0;
+    __syncthreads();
+    for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        T *z = data + a * (int64_t)n;
+        u128 s0, inc;
+        bool lh;
+        ChaKey ck;
+        CtaGen<SP_W> gs;
+        cta_gen_setup<false, SP_W>(gs, s0, inc, lh, ck, 1, gen, run_seed, base + a, nullptr, n, L);
+        for (int sg = (int)NB - 1; sg >= 0; --sg) {
+            const uint32_t blo = (uint32_t)sg * SP_B;
+            const uint32_t bn = min(SP_B, n - blo);
+            const uint32_t slo = max(blo, lo);  // positions below slo have no step
+            // ---- the block as the higher blocks left it: z0, then their deposits in time order
+            for (uint32_t x = L; x < bn; x += SP_T) sh.mbox[x] = z[blo + x];
+            const uint32_t ntile = NB - 1 - (uint32_t)sg;  // tile j comes from block NB-1-j
+            for (uint32_t j = L; j < ntile; j += SP_T) {
+                const uint32_t sp = NB - 1 - j;
+                const uint32_t d = __ldcg(desc + (size_t)sp * NB + (uint32_t)sg);
+                sh.vstart[j] = d & 0xFFFFu;
+                sh.tbase[j] = sp * SP_B + (d >> 16);
+            }
+            __syncthreads();
+            const uint32_t R = sp_scan(sh.vstart, ntile, sh.wsum, L);
+            for (uint32_t c0 = 0; c0 < R; c0 += SP_C) {
+                const uint32_t cn = min(SP_C, R - c0);
+                uint32_t gi[RPER];
+#pragma unroll
+                for (int k = 0; k < RPER; ++k) {
+                    const uint32_t r = (uint32_t)L + (uint32_t)k * SP_T;
+                    gi[k] = SP_NONE;
+                    if (r < cn) {
+                        const uint32_t rr = c0 + r;
+                        uint32_t lo_j = 0, hi_j = ntile - 1;  // last tile starting at or before rr
+                        while (lo_j < hi_j) {
+                            const uint32_t mid = (lo_j + hi_j + 1) >> 1;
+                            if (sh.vstart[mid] <= rr) lo_j = mid;
+                            else hi_j = mid - 1;
+                        }
+                        const uint32_t idx = sh.tbase[lo_j] + (rr - sh.vstart[lo_j]);
+                        const uint32_t fq = __ldcg(fwdq + idx);
+                        const T v = __ldcg(fwdv + idx);
+                        const uint32_t q = fq & 0xFFFFu;
+                        sh.u.rec.key[r] = (NB - 1 - lo_j) * SP_B + (fq >> 16);
+                        sh.u.rec.val[r] = v;
+                        sh.u.rec.q[r] = (uint16_t)q;
+                        const uint32_t old = atomicExch(&sh.head[q], r);
+                        sh.u.rec.link[r] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
+                        gi[k] = idx;
+                    }
+                }
+                __syncthreads();
+                bool last[RPER];
+#pragma unroll
+                for (int k = 0; k < RPER; ++k) {
+                    last[k] = false;
+                    if (gi[k] != SP_NONE) {
+                        const uint32_t r = (uint32_t)L + (uint32_t)k * SP_T;
+                        const uint32_t K = sh.u.rec.key[r];
+                        const uint32_t q = sh.u.rec.q[r];
+                        uint32_t prev = SP_NONE, pk = SP_NONE;
+                        bool lst = true;
+                        for (uint32_t m = sh.head[q]; m != SP_NONE;) {
+                            const uint32_t km = sh.u.rec.key[m];
+                            if (km > K && km < pk) {
+                                pk = km;
+                                prev = m;
+                            }
+                            lst &= !(km < K);
+                            const uint16_t nx = sh.u.rec.link[m];
+                            m = nx == SP_NONE16 ? SP_NONE : nx;
+                        }
+                        __stcg(res + gi[k], prev != SP_NONE ? sh.u.rec.val[prev] : sh.mbox[q]);
+                        last[k] = lst;
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < RPER; ++k) {
+                    if (gi[k] != SP_NONE) {
+                        const uint32_t r = (uint32_t)L + (uint32_t)k * SP_T;
+                        const uint32_t q = sh.u.rec.q[r];
+                        if (last[k]) sh.mbox[q] = sh.u.rec.val[r];
+                        sh.head[q] = SP_NONE;
+                    }
+                }
+                __syncthreads();
+            }
+            // ---- the targets of this block's steps
+            while (gs.frontier > slo && gs.B0 < plan.nbatches)
+                large_gen_step<false, SP_W>(gs, plan, sh, L, nullptr, nullptr, ck);
+            __syncthreads();
+            // ---- this block's steps in closed form
+            uint32_t Jr[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                const uint32_t s = blo + i;
+                Jr[k] = SP_NONE;
+                if (i < bn && s >= slo) {
+                    const uint32_t J = sh.ring[s & (SP_RING - 1)];
+                    Jr[k] = J;
+                    if (J >= blo) {
+                        const uint32_t old = atomicExch(&sh.head[J - blo], i);
+                        sh.u.loc.link[i] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
+                    }
+                }
+            }
+            __syncthreads();
+            uint16_t ns[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                ns[k] = SP_NONE16;
+                if (i < bn) {
+                    uint32_t ft = SP_NONE;  // first in-block step after i targeting i
+                    for (uint32_t m = sh.head[i]; m != SP_NONE;) {
+                        if (m > i && m < ft) ft = m;
+                        const uint16_t nx = sh.u.loc.link[m];
+                        m = nx == SP_NONE16 ? SP_NONE : nx;
+                    }
+                    sh.u.loc.F[i] = ft == SP_NONE ? SP_NONE16 : (uint16_t)ft;
+                    if (Jr[k] != SP_NONE && Jr[k] >= blo) {  // next in-block step after i with i's target
+                        uint32_t nx2 = SP_NONE;
+                        for (uint32_t m = sh.head[Jr[k] - blo]; m != SP_NONE;) {
+                            if (m > i && m < nx2) nx2 = m;
+                            const uint16_t nx = sh.u.loc.link[m];
+                            m = nx == SP_NONE16 ? SP_NONE : nx;
+                        }
+                        ns[k] = nx2 == SP_NONE ? SP_NONE16 : (uint16_t)nx2;
+                    }
+                }
+            }
+            for (uint32_t t = L; t < (uint32_t)sg; t += SP_T) sh.tbase[t] = 0;  // per-target-block counts
+            __syncthreads();
+            uint16_t endp[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                uint32_t e = i;
+                if (i < bn)
+                    for (uint16_t f = sh.u.loc.F[e]; f != SP_NONE16; f = sh.u.loc.F[e]) e = f;
+                endp[k] = (uint16_t)e;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                if (i < bn) sh.u.loc.F[i] = endp[k];
+            }
+            __syncthreads();
+            // ---- outputs: in-block ones into the result area, records for lower blocks
+            T ov[PER];
+            uint32_t rk[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                rk[k] = 0;
+                if (i >= bn) continue;
+                const uint32_t J = Jr[k];
+                if (J == SP_NONE) {  // no step at this position (below lo): its final value
+                    ov[k] = sh.mbox[sh.u.loc.F[i]];
+                    rk[k] = atomicAdd(&sh.nint, 1u);
+                } else if (J >= blo) {
+                    ov[k] = sh.mbox[ns[k] != SP_NONE16 ? sh.u.loc.F[ns[k]] : J - blo];
+                    rk[k] = atomicAdd(&sh.nint, 1u);
+                    sh.head[J - blo] = SP_NONE;
+                } else {
+                    ov[k] = sh.mbox[sh.u.loc.F[i]];  // Val(s): the value leaving position s
+                    rk[k] = atomicAdd(&sh.tbase[J / SP_B], 1u);
+                }
+            }
+            __syncthreads();
+            for (uint32_t t = L; t < (uint32_t)sg; t += SP_T) sh.vstart[t] = sh.tbase[t];
+            __syncthreads();
+            const uint32_t next = sp_scan(sh.vstart, (uint32_t)sg, sh.wsum, L);
+            for (uint32_t t = L; t < (uint32_t)sg; t += SP_T)
+                __stcg(desc + (size_t)sg * NB + t, (sh.vstart[t] << 16) | sh.tbase[t]);
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                if (i >= bn) continue;
+                const uint32_t J = Jr[k];
+                uint32_t sl;
+                if (J == SP_NONE || J >= blo) {
+                    sl = next + rk[k];
+                    __stcg(res + blo + sl, ov[k]);
+                } else {
+                    const uint32_t tb = J / SP_B;
+                    sl = sh.vstart[tb] + rk[k];
+                    __stcg(fwdq + blo + sl, (J - tb * SP_B) | (i << 16));
+                    __stcg(fwdv + blo + sl, ov[k]);
+                }
+                __stcg(slot + blo + i, (uint16_t)sl);
+            }
+            if (L == 0) sh.nint = 0;
+            __syncthreads();
+        }
+        while (gs.B0 < plan.nbatches) large_gen_step<false, SP_W>(gs, plan, sh, L, nullptr, nullptr, ck);
+        if (L == 0 && words32) words32[a] = plan.nbatches + gs.D;
+        // ---- gather the outputs: out[p] = result[slot[p]], block by block through shared memory
+        for (uint32_t sg = 0; sg < NB; ++sg) {
+            const uint32_t blo = sg * SP_B;
+            const uint32_t bn = min(SP_B, n - blo);
+            for (uint32_t x = L; x < bn; x += SP_T) sh.mbox[x] = __ldcg(res + blo + x);
+            __syncthreads();
+            for (uint32_t x = L; x < bn; x += SP_T) z[blo + x] = sh.mbox[__ldcg(slot + blo + x)];
+            __syncthreads();
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SP_T) shuffle_stage_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
+                                                             uint64_t run_seed, int64_t base,
+                                                             uint32_t *__restrict__ words32, int gen,
+                                                             unsigned char *__restrict__ scratch,
+                                                             size_t scratch_per_cta) {
+    extern __shared__ __align__(16) unsigned char sp_smem[];
+    auto &sh = *reinterpret_cast<SpShared<T> *>(sp_smem);
+    shuffle_stage_body<T>(data, num_arrays, plan, run_seed, base, words32, gen, sh, scratch, scratch_per_cta);
+}
+
+}  // namespace br
