@@ -38,7 +38,7 @@ namespace br {
 static constexpr uint32_t SP_B = 4096;     // positions per block (one stage)
 static constexpr int SP_W = 16;            // warps per CTA
 static constexpr int SP_T = 32 * SP_W;     // threads per CTA
-static constexpr uint32_t SP_C = 1024;     // records per chunk of step 1
+static constexpr uint32_t SP_C = SP_B;     // records per chunk of step 1 (a whole tile always fits)
 static constexpr uint32_t SP_RING = 8192;  // u32 target ring: a block + one generation step (k <= 7)
 static constexpr uint32_t SP_MAXNB = 1024; // blocks per array (n <= 4M)
 static constexpr uint32_t SP_NONE = 0xFFFFFFFFu;
@@ -70,6 +70,7 @@ struct SpShared {
     uint32_t frontier[2];
     uint32_t fmin;
     uint32_t nint;
+    uint32_t chunk_end;
 };
 
 // exclusive scan of a[0..len) in place (len <= 2 * SP_T); every thread gets the total
@@ -166,8 +167,24 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
             }
             __syncthreads();
             const uint32_t R = sp_scan(sh.vstart, ntile, sh.wsum, L);
-            for (uint32_t c0 = 0; c0 < R; c0 += SP_C) {
-                const uint32_t cn = min(SP_C, R - c0);
+            // chunks of whole tiles (records of one tile are in no particular order; tiles are in
+            // time order), as many as fit SP_C records; records of one chunk are ordered by key
+            for (uint32_t jt = 0; jt < ntile;) {
+                if (L == 0) {  // last tile je with end(je) - start(jt) <= SP_C
+                    uint32_t a0 = jt, a1 = ntile - 1;
+                    while (a0 < a1) {
+                        const uint32_t mid = (a0 + a1 + 1) >> 1;
+                        const uint32_t end = mid + 1 < ntile ? sh.vstart[mid + 1] : R;
+                        if (end - sh.vstart[jt] <= SP_C) a0 = mid;
+                        else a1 = mid - 1;
+                    }
+                    sh.chunk_end = a0 + 1;
+                }
+                __syncthreads();
+                const uint32_t jn = sh.chunk_end;
+                const uint32_t c0 = sh.vstart[jt];
+                const uint32_t cn = (jn < ntile ? sh.vstart[jn] : R) - c0;
+                jt = jn;
                 uint32_t gi[RPER];
 #pragma unroll
                 for (int k = 0; k < RPER; ++k) {
