@@ -778,15 +778,37 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
         const void *kp = (const void *)shuffle_stage_kernel<T>;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int grid = grid_for(di, kp, SP_T, smem, num_arrays);
-        const size_t per = sp_scratch_bytes<T>((uint32_t)n);
+        const size_t cta = sp_cta_bytes<T>((uint32_t)n);
+        const size_t per_array = sp_array_bytes<T>((uint32_t)n);
+        // arrays per launch pair: every CTA busy, result slots of at most ~4 GB
+        const int64_t chunk = std::min<int64_t>(num_arrays, std::max<int64_t>(grid, (int64_t)((4ull << 30) / per_array)));
         unsigned char *scratch = nullptr;
-        CK(cudaMallocAsync((void **)&scratch, per * (size_t)grid, st));
-        T *dp = (T *)data;
-        DevPlan plan = cp.plan;
-        int g = gen;
-        size_t pc = per;
-        void *args[] = {&dp, &num_arrays, &plan, &run_seed, &base, &words32, &g, &scratch, &pc};
-        const cudaError_t le = cudaLaunchKernel(kp, dim3(grid), dim3(SP_T), args, smem, st);
+        const size_t cta_total = (cta * (size_t)grid + 255) & ~(size_t)255;
+        const size_t res_bytes = ((size_t)chunk * n * sizeof(T) + 255) & ~(size_t)255;
+        CK(cudaMallocAsync((void **)&scratch, cta_total + res_bytes + (size_t)chunk * n * 2, st));
+        T *res = (T *)(scratch + cta_total);
+        uint16_t *slot = (uint16_t *)(scratch + cta_total + res_bytes);
+        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+        const void *gk = (const void *)shuffle_stage_gather_kernel<T>;
+        const int ggrid = grid_for(di, gk, SPG_T, 0, chunk * (int64_t)((n + SP_B - 1) / SP_B));
+        cudaError_t le = cudaSuccess;
+        for (int64_t a0 = 0; a0 < num_arrays && le == cudaSuccess; a0 += chunk) {
+            int64_t na = std::min(chunk, num_arrays - a0);
+            T *dp = (T *)data + a0 * (int64_t)n;
+            DevPlan plan = cp.plan;
+            int g = gen;
+            size_t cb = cta;
+            int64_t b0 = base + a0;
+            uint32_t *w32 = words32 ? words32 + a0 : nullptr;
+            int tma = use_tma;
+            void *args[] = {&dp, &na, &plan, &run_seed, &b0, &w32, &g, &scratch, &cb, &res, &slot, &tma};
+            le = cudaLaunchKernel(kp, dim3((unsigned)std::min<int64_t>(grid, na)), dim3(SP_T), args, smem, st);
+            if (le == cudaSuccess) {
+                uint32_t nn = (uint32_t)n;
+                void *gargs[] = {&dp, &na, &nn, &res, &slot};
+                le = cudaLaunchKernel(gk, dim3(ggrid), dim3(SPG_T), gargs, 0, st);
+            }
+        }
         CK(cudaFreeAsync(scratch, st));
         if (le != cudaSuccess) return fail(BR_E_CUDA, std::string("stage kernel launch: ") + cudaGetErrorString(le));
         g_kernel = std::string("shuffle_stage_kernel<u") + std::to_string(8 * sizeof(T)) + ">";

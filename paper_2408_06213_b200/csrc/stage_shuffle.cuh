@@ -23,8 +23,10 @@
 //   4. writes its records grouped by target block (tiles), a tile table entry per lower block,
 //      its in-block outputs into its result area and a slot map (position -> result slot).
 // After stage 0 every result slot is filled; out[p] = result[slot[p]] is gathered block by
-// block through shared memory.  Global traffic is streaming (records, results, slot maps);
-// all random accesses are in shared memory.
+// block through shared memory by a second, fully parallel kernel (shuffle_stage_gather_kernel).
+// Global traffic is streaming (blocks, records, results, slot maps); all random accesses are
+// in shared memory.  The next block streams in (TMA bulk copy) while the current one is
+// worked on.
 //
 // Exactness: stage sg sees the block exactly as the sequential loop would after all higher
 // steps (their deposits in time order, records carry s); its own steps are the sequential
@@ -50,7 +52,7 @@ struct SpShared {
     using RType = uint32_t;
     DevSeg segs[MAX_SEGS];
     uint32_t ring[SP_RING];  // targets by position (large_gen_step)
-    T mbox[SP_B];            // the block's contents
+    T mbuf[2][SP_B];         // the block's contents; the next block streams into the other buffer
     uint32_t head[SP_B];     // per-target chain heads (atomicExch), SP_NONE = empty
     union {
         struct {  // step 1: one chunk of records
@@ -67,6 +69,7 @@ struct SpShared {
     uint32_t vstart[SP_MAXNB];  // tiles: exclusive prefix of counts; step 4: per-target-block prefix
     uint32_t tbase[SP_MAXNB];   // tiles: first record index; step 4: per-target-block counts
     uint32_t wsum[SP_W + 1];
+    uint64_t bar[2];
     uint32_t frontier[2];
     uint32_t fmin;
     uint32_t nint;
@@ -107,57 +110,89 @@ __device__ __forceinline__ uint32_t sp_scan(uint32_t *a, uint32_t len, uint32_t 
     return total;
 }
 
-// per-CTA global scratch (bytes) for arrays of n elements of T
+// global scratch: per CTA (records and tile table, reused array after array) and per array
+// (result slots and slot map, read by the gather kernel)
 template <typename T>
-__host__ __device__ constexpr size_t sp_scratch_bytes(uint32_t n) {
+__host__ __device__ constexpr size_t sp_cta_bytes(uint32_t n) {
     const size_t nb = (n + SP_B - 1) / SP_B;
-    const size_t a = ((size_t)n * 4 + 255) & ~(size_t)255;          // record (target offset | position << 16)
-    const size_t b = ((size_t)n * sizeof(T) + 255) & ~(size_t)255;  // record value
-    const size_t c = b;                                              // result slots
-    const size_t d = ((size_t)n * 2 + 255) & ~(size_t)255;          // slot map
-    const size_t e = (nb * nb * 4 + 255) & ~(size_t)255;            // tile table
-    return a + b + c + d + e;
+    return (((size_t)n * 4 + 255) & ~(size_t)255) +           // record (target offset | position << 16)
+           (((size_t)n * sizeof(T) + 255) & ~(size_t)255) +   // record value
+           ((nb * nb * 4 + 255) & ~(size_t)255);              // tile table
+}
+template <typename T>
+__host__ __device__ constexpr size_t sp_array_bytes(uint32_t n) {
+    return (size_t)n * (sizeof(T) + 2);  // result slots + slot map
 }
 
 template <typename T>
 __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
                                                    uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
-                                                   int gen, SpShared<T> &sh, unsigned char *__restrict__ scratch,
-                                                   size_t scratch_per_cta) {
-    constexpr int PER = SP_B / SP_T;  // positions per thread in steps 3-4
-    constexpr int RPER = SP_C / SP_T; // records per thread in step 1
+                                                   int gen, SpShared<T> &sh, unsigned char *__restrict__ cta_scratch,
+                                                   size_t cta_bytes, T *__restrict__ res_all,
+                                                   uint16_t *__restrict__ slot_all, int use_tma) {
+    constexpr int PER = SP_B / SP_T;   // positions per thread in steps 3-4
+    constexpr int RPER = SP_C / SP_T;  // records per thread in step 1
     const int L = threadIdx.x;
     const uint32_t n = plan.n;
     const uint32_t NB = (n + SP_B - 1) / SP_B;
     const uint32_t lo = plan.lo;
-    unsigned char *w = scratch + (size_t)blockIdx.x * scratch_per_cta;
+    unsigned char *w = cta_scratch + (size_t)blockIdx.x * cta_bytes;
     uint32_t *fwdq = reinterpret_cast<uint32_t *>(w);
     w += ((size_t)n * 4 + 255) & ~(size_t)255;
     T *fwdv = reinterpret_cast<T *>(w);
     w += ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
-    T *res = reinterpret_cast<T *>(w);
-    w += ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
-    uint16_t *slot = reinterpret_cast<uint16_t *>(w);
-    w += ((size_t)n * 2 + 255) & ~(size_t)255;
     uint32_t *desc = reinterpret_cast<uint32_t *>(w);
 
     for (uint32_t q = L; q < plan.nseg; q += SP_T) sh.segs[q] = plan.segs[q];
     for (uint32_t x = L; x < SP_B; x += SP_T) sh.head[x] = SP_NONE;
-    if (L == 0) sh.nint = 0;
+    if (L == 0) {
+        sh.nint = 0;
+        mbar_init(&sh.bar[0], 1);
+        mbar_init(&sh.bar[1], 1);
+    }
     __syncthreads();
+    uint32_t par0 = 0, par1 = 0;
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         T *z = data + a * (int64_t)n;
+        T *res = res_all + a * (int64_t)n;
+        uint16_t *slot = slot_all + a * (int64_t)n;
+        // block sg into buffer b: one bulk copy by thread 0 (completion on bar[b]) or plain loads
+        auto fetch = [&](int b, uint32_t sgf) {
+            const uint32_t blo = sgf * SP_B;
+            const uint32_t bn = min(SP_B, n - blo);
+            if (use_tma) {
+                if (L == 0) {
+                    fence_proxy_async();  // earlier generic accesses to the buffer come first
+                    mbar_arrive_expect_tx(&sh.bar[b], bn * (uint32_t)sizeof(T));
+                    bulk_load(sh.mbuf[b], z + blo, bn * (uint32_t)sizeof(T), &sh.bar[b]);
+                }
+            } else {
+                for (uint32_t x = L; x < bn; x += SP_T) sh.mbuf[b][x] = z[blo + x];
+            }
+        };
         u128 s0, inc;
         bool lh;
         ChaKey ck;
         CtaGen<SP_W> gs;
         cta_gen_setup<false, SP_W>(gs, s0, inc, lh, ck, 1, gen, run_seed, base + a, nullptr, n, L);
+        int cur = 0;
+        fetch(0, NB - 1);
         for (int sg = (int)NB - 1; sg >= 0; --sg) {
             const uint32_t blo = (uint32_t)sg * SP_B;
             const uint32_t bn = min(SP_B, n - blo);
             const uint32_t slo = max(blo, lo);  // positions below slo have no step
+            T *mbox = sh.mbuf[cur];
+            if (use_tma) {
+                if (cur == 0) {
+                    mbar_wait(&sh.bar[0], par0);
+                    par0 ^= 1u;
+                } else {
+                    mbar_wait(&sh.bar[1], par1);
+                    par1 ^= 1u;
+                }
+            }
+            if (sg > 0) fetch(cur ^ 1, (uint32_t)sg - 1);  // the next block streams in meanwhile
             // ---- the block as the higher blocks left it: z0, then their deposits in time order
-            for (uint32_t x = L; x < bn; x += SP_T) sh.mbox[x] = z[blo + x];
             const uint32_t ntile = NB - 1 - (uint32_t)sg;  // tile j comes from block NB-1-j
             for (uint32_t j = L; j < ntile; j += SP_T) {
                 const uint32_t sp = NB - 1 - j;
@@ -184,30 +219,49 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
                 const uint32_t jn = sh.chunk_end;
                 const uint32_t c0 = sh.vstart[jt];
                 const uint32_t cn = (jn < ntile ? sh.vstart[jn] : R) - c0;
-                jt = jn;
+                // thread L takes the RPER consecutive records c0 + RPER*L + k (one tile search)
                 uint32_t gi[RPER];
+                uint32_t jj = jt;
+                if ((uint32_t)(RPER * L) < cn) {
+                    uint32_t a0 = jt, a1 = jn - 1;
+                    const uint32_t rr = c0 + RPER * L;
+                    while (a0 < a1) {
+                        const uint32_t mid = (a0 + a1 + 1) >> 1;
+                        if (sh.vstart[mid] <= rr) a0 = mid;
+                        else a1 = mid - 1;
+                    }
+                    jj = a0;
+                }
 #pragma unroll
                 for (int k = 0; k < RPER; ++k) {
-                    const uint32_t r = (uint32_t)L + (uint32_t)k * SP_T;
+                    const uint32_t r = RPER * (uint32_t)L + (uint32_t)k;
                     gi[k] = SP_NONE;
                     if (r < cn) {
                         const uint32_t rr = c0 + r;
-                        uint32_t lo_j = 0, hi_j = ntile - 1;  // last tile starting at or before rr
-                        while (lo_j < hi_j) {
-                            const uint32_t mid = (lo_j + hi_j + 1) >> 1;
-                            if (sh.vstart[mid] <= rr) lo_j = mid;
-                            else hi_j = mid - 1;
-                        }
-                        const uint32_t idx = sh.tbase[lo_j] + (rr - sh.vstart[lo_j]);
-                        const uint32_t fq = __ldcg(fwdq + idx);
-                        const T v = __ldcg(fwdv + idx);
-                        const uint32_t q = fq & 0xFFFFu;
-                        sh.u.rec.key[r] = (NB - 1 - lo_j) * SP_B + (fq >> 16);
-                        sh.u.rec.val[r] = v;
-                        sh.u.rec.q[r] = (uint16_t)q;
-                        const uint32_t old = atomicExch(&sh.head[q], r);
-                        sh.u.rec.link[r] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
-                        gi[k] = idx;
+                        while (jj + 1 < jn && sh.vstart[jj + 1] <= rr) ++jj;
+                        gi[k] = sh.tbase[jj] + (rr - sh.vstart[jj]);
+                    }
+                }
+                uint32_t fq[RPER];
+                T fv[RPER];
+#pragma unroll
+                for (int k = 0; k < RPER; ++k) {
+                    if (gi[k] != SP_NONE) {
+                        fq[k] = __ldcg(fwdq + gi[k]);
+                        fv[k] = __ldcg(fwdv + gi[k]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < RPER; ++k) {
+                    if (gi[k] != SP_NONE) {
+                        const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;  // conflict-free slot
+                        const uint32_t sp = gi[k] / SP_B;  // source block (its records lie in its area)
+                        const uint32_t q = fq[k] & 0xFFFFu;
+                        sh.u.rec.key[si] = sp * SP_B + (fq[k] >> 16);
+                        sh.u.rec.val[si] = fv[k];
+                        sh.u.rec.q[si] = (uint16_t)q;
+                        const uint32_t old = atomicExch(&sh.head[q], si);
+                        sh.u.rec.link[si] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
                     }
                 }
                 __syncthreads();
@@ -216,9 +270,9 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
                 for (int k = 0; k < RPER; ++k) {
                     last[k] = false;
                     if (gi[k] != SP_NONE) {
-                        const uint32_t r = (uint32_t)L + (uint32_t)k * SP_T;
-                        const uint32_t K = sh.u.rec.key[r];
-                        const uint32_t q = sh.u.rec.q[r];
+                        const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
+                        const uint32_t K = sh.u.rec.key[si];
+                        const uint32_t q = sh.u.rec.q[si];
                         uint32_t prev = SP_NONE, pk = SP_NONE;
                         bool lst = true;
                         for (uint32_t m = sh.head[q]; m != SP_NONE;) {
@@ -231,7 +285,7 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
                             const uint16_t nx = sh.u.rec.link[m];
                             m = nx == SP_NONE16 ? SP_NONE : nx;
                         }
-                        __stcg(res + gi[k], prev != SP_NONE ? sh.u.rec.val[prev] : sh.mbox[q]);
+                        __stcg(res + gi[k], prev != SP_NONE ? sh.u.rec.val[prev] : mbox[q]);
                         last[k] = lst;
                     }
                 }
@@ -239,13 +293,14 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
 #pragma unroll
                 for (int k = 0; k < RPER; ++k) {
                     if (gi[k] != SP_NONE) {
-                        const uint32_t r = (uint32_t)L + (uint32_t)k * SP_T;
-                        const uint32_t q = sh.u.rec.q[r];
-                        if (last[k]) sh.mbox[q] = sh.u.rec.val[r];
+                        const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
+                        const uint32_t q = sh.u.rec.q[si];
+                        if (last[k]) mbox[q] = sh.u.rec.val[si];
                         sh.head[q] = SP_NONE;
                     }
                 }
                 __syncthreads();
+                jt = jn;
             }
             // ---- the targets of this block's steps
             while (gs.frontier > slo && gs.B0 < plan.nbatches)
@@ -320,14 +375,14 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
                 if (i >= bn) continue;
                 const uint32_t J = Jr[k];
                 if (J == SP_NONE) {  // no step at this position (below lo): its final value
-                    ov[k] = sh.mbox[sh.u.loc.F[i]];
+                    ov[k] = mbox[sh.u.loc.F[i]];
                     rk[k] = atomicAdd(&sh.nint, 1u);
                 } else if (J >= blo) {
-                    ov[k] = sh.mbox[ns[k] != SP_NONE16 ? sh.u.loc.F[ns[k]] : J - blo];
+                    ov[k] = mbox[ns[k] != SP_NONE16 ? sh.u.loc.F[ns[k]] : J - blo];
                     rk[k] = atomicAdd(&sh.nint, 1u);
                     sh.head[J - blo] = SP_NONE;
                 } else {
-                    ov[k] = sh.mbox[sh.u.loc.F[i]];  // Val(s): the value leaving position s
+                    ov[k] = mbox[sh.u.loc.F[i]];  // Val(s): the value leaving position s
                     rk[k] = atomicAdd(&sh.tbase[J / SP_B], 1u);
                 }
             }
@@ -356,18 +411,10 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
             }
             if (L == 0) sh.nint = 0;
             __syncthreads();
+            cur ^= 1;
         }
         while (gs.B0 < plan.nbatches) large_gen_step<false, SP_W>(gs, plan, sh, L, nullptr, nullptr, ck);
         if (L == 0 && words32) words32[a] = plan.nbatches + gs.D;
-        // ---- gather the outputs: out[p] = result[slot[p]], block by block through shared memory
-        for (uint32_t sg = 0; sg < NB; ++sg) {
-            const uint32_t blo = sg * SP_B;
-            const uint32_t bn = min(SP_B, n - blo);
-            for (uint32_t x = L; x < bn; x += SP_T) sh.mbox[x] = __ldcg(res + blo + x);
-            __syncthreads();
-            for (uint32_t x = L; x < bn; x += SP_T) z[blo + x] = sh.mbox[__ldcg(slot + blo + x)];
-            __syncthreads();
-        }
     }
 }
 
@@ -375,11 +422,54 @@ template <typename T>
 __global__ void __launch_bounds__(SP_T) shuffle_stage_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
                                                              uint64_t run_seed, int64_t base,
                                                              uint32_t *__restrict__ words32, int gen,
-                                                             unsigned char *__restrict__ scratch,
-                                                             size_t scratch_per_cta) {
+                                                             unsigned char *__restrict__ cta_scratch, size_t cta_bytes,
+                                                             T *__restrict__ res, uint16_t *__restrict__ slot,
+                                                             int use_tma) {
     extern __shared__ __align__(16) unsigned char sp_smem[];
     auto &sh = *reinterpret_cast<SpShared<T> *>(sp_smem);
-    shuffle_stage_body<T>(data, num_arrays, plan, run_seed, base, words32, gen, sh, scratch, scratch_per_cta);
+    shuffle_stage_body<T>(data, num_arrays, plan, run_seed, base, words32, gen, sh, cta_scratch, cta_bytes, res, slot,
+                          use_tma);
+}
+
+// out[p] = result[slot[p]] for every block of every array: one block per iteration through
+// shared memory (the slot map is a permutation of the block's result slots)
+static constexpr int SPG_T = 512;
+template <typename T>
+__global__ void __launch_bounds__(SPG_T) shuffle_stage_gather_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                     uint32_t n, const T *__restrict__ res,
+                                                                     const uint16_t *__restrict__ slot) {
+    __shared__ T buf[SP_B];
+    const uint32_t NB = (n + SP_B - 1) / SP_B;
+    const int64_t total = num_arrays * (int64_t)NB;
+    for (int64_t g = blockIdx.x; g < total; g += gridDim.x) {
+        const int64_t a = g / NB;
+        const uint32_t blo = (uint32_t)(g - a * NB) * SP_B;
+        const uint32_t bn = min(SP_B, n - blo);
+        const int64_t off = a * (int64_t)n + blo;
+        constexpr int PER = SP_B / SPG_T;
+        T v[PER];
+        uint16_t sl[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t x = threadIdx.x + k * SPG_T;
+            if (x < bn) {
+                v[k] = __ldcs(res + off + x);
+                sl[k] = __ldcs(slot + off + x);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t x = threadIdx.x + k * SPG_T;
+            if (x < bn) buf[x] = v[k];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t x = threadIdx.x + k * SPG_T;
+            if (x < bn) data[off + x] = buf[sl[k]];
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace br
