@@ -68,6 +68,7 @@ struct SpShared {
     } u;
     uint32_t vstart[SP_MAXNB];  // tiles: exclusive prefix of counts; step 4: per-target-block prefix
     uint32_t tbase[SP_MAXNB];   // tiles: first record index; step 4: per-target-block counts
+    uint32_t nd[SP_MAXNB];      // the next stage's tile table (prefetched during this stage)
     uint32_t wsum[SP_W + 1];
     uint64_t bar[2];
     uint32_t frontier[2];
@@ -124,6 +125,124 @@ __host__ __device__ constexpr size_t sp_array_bytes(uint32_t n) {
     return (size_t)n * (sizeof(T) + 2);  // result slots + slot map
 }
 
+// ---- target generation for one block: striped lanes, no per-stage jump
+// Slot (thread L, j) owns the batches b == L + SP_T*j (mod SP_G) and holds the generator state
+// whose output is word b + D of its next pending batch b.  A step covers the window
+// [B0, B0 + nact) (nact <= SP_G, so a slot has at most one batch in it); committed slots move
+// SP_G batches on (one precomputed affine jump), the others keep their state.  A rejected batch
+// f shifts every batch >= f by one word (shuffle.py:121-128): pending slots step once more.
+static constexpr int SP_GJ = 5;                 // slots per thread (k = 2: a block's 2048 batches in one step)
+static constexpr uint32_t SP_G = SP_GJ * SP_T;  // batches per step
+
+struct SpGen {
+    u128 s[SP_GJ];
+    uint32_t b[SP_GJ];   // pending batch of each slot
+    uint8_t seg[SP_GJ];  // its segment
+    u128 inc, AG, CG, M;
+    uint32_t B0, D;
+    bool lh;
+};
+
+__device__ __forceinline__ void sp_jump(u128 &s, u128 inc, uint32_t d, bool lh) {
+    while (d > (uint32_t)JUMP_SMALL) {
+        s = gen_jump_small(s, inc, JUMP_SMALL, lh);
+        d -= JUMP_SMALL;
+    }
+    if (d) s = gen_jump_small(s, inc, (int)d, lh);
+}
+
+template <typename T>
+__device__ __forceinline__ void sp_gen_init(SpGen &g, uint64_t seed, bool lh, int L) {
+    u128 s0, inc;
+    gen_seed(seed, s0, inc, lh);
+    g.inc = inc;
+    g.lh = lh;
+    g.M = gen_mult(lh);
+    gen_affine(SP_G, inc, lh, g.AG, g.CG);
+    const u128 s1 = gen_jump_small(s0, inc, L + 1, lh);  // output = word L
+#pragma unroll
+    for (int j = 0; j < SP_GJ; ++j) {
+        u128 x = s1;
+        sp_jump(x, inc, (uint32_t)(SP_T * j), lh);
+        g.s[j] = x;
+        g.b[j] = (uint32_t)L + (uint32_t)(SP_T * j);
+        g.seg[j] = 0;
+    }
+    g.B0 = 0;
+    g.D = 0;
+}
+
+// batch containing position p (plan.lo <= p < n)
+__device__ __forceinline__ uint32_t sp_batch_of(const DevSeg *segs, uint32_t nseg, uint32_t p) {
+    for (uint32_t q = 0; q < nseg; ++q) {
+        const DevSeg S = segs[q];
+        if (p >= S.start_n - S.count * S.k) return S.first_batch + (S.start_n - 1 - p) / S.k;
+    }
+    return 0;
+}
+
+// generate every batch up to and including b_need into the target ring
+template <typename T>
+__device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpShared<T> &sh, int L, uint32_t b_need) {
+    constexpr uint32_t RS = SP_RING;
+    while (g.B0 <= b_need) {
+        const uint32_t wend = min(g.B0 + SP_G, b_need + 1);  // window [B0, wend)
+        uint64_t t[SP_GJ];
+#pragma unroll
+        for (int j = 0; j < SP_GJ; ++j)
+            if (g.b[j] < wend) t[j] = __ldg(plan.thresh + g.b[j]);
+        uint32_t myfail = 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < SP_GJ; ++j) {
+            const uint32_t b = g.b[j];
+            if (b < wend) {
+                uint32_t q = g.seg[j];
+                while (q + 1 < plan.nseg && sh.segs[q + 1].first_batch <= b) ++q;
+                g.seg[j] = (uint8_t)q;
+                const DevSeg S = sh.segs[q];
+                const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
+                uint64_t r = gen_out(g.s[j], g.lh);
+                const uint32_t pos = nbb - 1;
+                if (plan.naive && S.k == 2) {
+                    uint32_t j1, j2;
+                    naive_pair(nbb, r, j1, j2);
+                    sh.ring[pos & (RS - 1)] = j1;
+                    sh.ring[(pos - 1) & (RS - 1)] = j2;
+                } else {
+                    for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (RS - 1)] = die(nbb - m, r);
+                }
+                if (r < t[j] && b < myfail) myfail = b;
+            }
+        }
+        if (!__syncthreads_or(myfail != 0xFFFFFFFFu)) {
+#pragma unroll
+            for (int j = 0; j < SP_GJ; ++j)
+                if (g.b[j] < wend) {
+                    g.b[j] += SP_G;
+                    g.s[j] = mad128(g.s[j], g.AG, g.CG);
+                }
+            g.B0 = wend;
+        } else {
+            if (L == 0) sh.fmin = 0xFFFFFFFFu;
+            __syncthreads();
+            if (myfail != 0xFFFFFFFFu) atomicMin(&sh.fmin, myfail);
+            __syncthreads();
+            const uint32_t f = sh.fmin;  // the first rejected batch: it and everything after take one word more
+#pragma unroll
+            for (int j = 0; j < SP_GJ; ++j) {
+                if (g.b[j] < f) {
+                    g.b[j] += SP_G;
+                    g.s[j] = mad128(g.s[j], g.AG, g.CG);
+                }
+                g.s[j] = mad128(g.s[j], g.M, g.inc);
+            }
+            g.B0 = f;
+            g.D += 1;
+            __syncthreads();
+        }
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
                                                    uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
@@ -170,11 +289,8 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
                 for (uint32_t x = L; x < bn; x += SP_T) sh.mbuf[b][x] = z[blo + x];
             }
         };
-        u128 s0, inc;
-        bool lh;
-        ChaKey ck;
-        CtaGen<SP_W> gs;
-        cta_gen_setup<false, SP_W>(gs, s0, inc, lh, ck, 1, gen, run_seed, base + a, nullptr, n, L);
+        SpGen g;
+        sp_gen_init<T>(g, array_seed(run_seed, (uint64_t)(base + a)), gen == 1, L);
         int cur = 0;
         fetch(0, NB - 1);
         for (int sg = (int)NB - 1; sg >= 0; --sg) {
@@ -182,6 +298,13 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
             const uint32_t bn = min(SP_B, n - blo);
             const uint32_t slo = max(blo, lo);  // positions below slo have no step
             T *mbox = sh.mbuf[cur];
+            // ---- tile table of this block (prefetched by the previous stage into nd)
+            const uint32_t ntile = NB - 1 - (uint32_t)sg;  // tile j comes from block NB-1-j
+            for (uint32_t j = L; j < ntile; j += SP_T) {
+                const uint32_t d = sh.nd[j];
+                sh.vstart[j] = d & 0xFFFFu;
+                sh.tbase[j] = (NB - 1 - j) * SP_B + (d >> 16);
+            }
             if (use_tma) {
                 if (cur == 0) {
                     mbar_wait(&sh.bar[0], par0);
@@ -191,18 +314,32 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
                     par1 ^= 1u;
                 }
             }
-            if (sg > 0) fetch(cur ^ 1, (uint32_t)sg - 1);  // the next block streams in meanwhile
-            // ---- the block as the higher blocks left it: z0, then their deposits in time order
-            const uint32_t ntile = NB - 1 - (uint32_t)sg;  // tile j comes from block NB-1-j
-            for (uint32_t j = L; j < ntile; j += SP_T) {
-                const uint32_t sp = NB - 1 - j;
-                const uint32_t d = __ldcg(desc + (size_t)sp * NB + (uint32_t)sg);
-                sh.vstart[j] = d & 0xFFFFu;
-                sh.tbase[j] = sp * SP_B + (d >> 16);
-            }
             __syncthreads();
+            if (sg > 0) fetch(cur ^ 1, (uint32_t)sg - 1);  // the next block streams in meanwhile
             const uint32_t R = sp_scan(sh.vstart, ntile, sh.wsum, L);
-            // chunks of whole tiles (records of one tile are in no particular order; tiles are in
+            // ---- the next stage's tile table (all but this stage's own tile, written at its end)
+            // and an L2 prefetch of its records
+            if (sg > 0) {
+                for (uint32_t j = L; j + 1 < NB - (uint32_t)sg; j += SP_T) {
+                    const uint32_t sp = NB - 1 - j;
+                    const uint32_t d = __ldcg(desc + (size_t)sp * NB + (uint32_t)(sg - 1));
+                    sh.nd[j] = d;
+                    const uint32_t cnt = d & 0xFFFFu;
+                    if (cnt) {
+                        const size_t first = (size_t)sp * SP_B + (d >> 16);
+                        const uintptr_t q0 = (uintptr_t)(fwdq + first) & ~(uintptr_t)15;
+                        const uintptr_t q1 = ((uintptr_t)(fwdq + first + cnt) + 15) & ~(uintptr_t)15;
+                        const uintptr_t v0 = (uintptr_t)(fwdv + first) & ~(uintptr_t)15;
+                        const uintptr_t v1 = ((uintptr_t)(fwdv + first + cnt) + 15) & ~(uintptr_t)15;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q0), "r"((uint32_t)(q1 - q0))
+                                     : "memory");
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v0), "r"((uint32_t)(v1 - v0))
+                                     : "memory");
+                    }
+                }
+            }
+            // ---- the block as the higher blocks left it: z0, then their deposits in time order.
+            // Chunks of whole tiles (records of one tile are in no particular order; tiles are in
             // time order), as many as fit SP_C records; records of one chunk are ordered by key
             for (uint32_t jt = 0; jt < ntile;) {
                 if (L == 0) {  // last tile je with end(je) - start(jt) <= SP_C
@@ -219,92 +356,94 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
                 const uint32_t jn = sh.chunk_end;
                 const uint32_t c0 = sh.vstart[jt];
                 const uint32_t cn = (jn < ntile ? sh.vstart[jn] : R) - c0;
-                // thread L takes the RPER consecutive records c0 + RPER*L + k (one tile search)
+                const bool act = (uint32_t)(RPER * L) < cn;  // thread L takes records RPER*L + k
                 uint32_t gi[RPER];
-                uint32_t jj = jt;
-                if ((uint32_t)(RPER * L) < cn) {
-                    uint32_t a0 = jt, a1 = jn - 1;
-                    const uint32_t rr = c0 + RPER * L;
-                    while (a0 < a1) {
-                        const uint32_t mid = (a0 + a1 + 1) >> 1;
-                        if (sh.vstart[mid] <= rr) a0 = mid;
-                        else a1 = mid - 1;
-                    }
-                    jj = a0;
-                }
-#pragma unroll
-                for (int k = 0; k < RPER; ++k) {
-                    const uint32_t r = RPER * (uint32_t)L + (uint32_t)k;
-                    gi[k] = SP_NONE;
-                    if (r < cn) {
-                        const uint32_t rr = c0 + r;
-                        while (jj + 1 < jn && sh.vstart[jj + 1] <= rr) ++jj;
-                        gi[k] = sh.tbase[jj] + (rr - sh.vstart[jj]);
-                    }
-                }
-                uint32_t fq[RPER];
-                T fv[RPER];
-#pragma unroll
-                for (int k = 0; k < RPER; ++k) {
-                    if (gi[k] != SP_NONE) {
-                        fq[k] = __ldcg(fwdq + gi[k]);
-                        fv[k] = __ldcg(fwdv + gi[k]);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < RPER; ++k) {
-                    if (gi[k] != SP_NONE) {
-                        const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;  // conflict-free slot
-                        const uint32_t sp = gi[k] / SP_B;  // source block (its records lie in its area)
-                        const uint32_t q = fq[k] & 0xFFFFu;
-                        sh.u.rec.key[si] = sp * SP_B + (fq[k] >> 16);
-                        sh.u.rec.val[si] = fv[k];
-                        sh.u.rec.q[si] = (uint16_t)q;
-                        const uint32_t old = atomicExch(&sh.head[q], si);
-                        sh.u.rec.link[si] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
-                    }
-                }
-                __syncthreads();
                 bool last[RPER];
-#pragma unroll
-                for (int k = 0; k < RPER; ++k) {
-                    last[k] = false;
-                    if (gi[k] != SP_NONE) {
-                        const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
-                        const uint32_t K = sh.u.rec.key[si];
-                        const uint32_t q = sh.u.rec.q[si];
-                        uint32_t prev = SP_NONE, pk = SP_NONE;
-                        bool lst = true;
-                        for (uint32_t m = sh.head[q]; m != SP_NONE;) {
-                            const uint32_t km = sh.u.rec.key[m];
-                            if (km > K && km < pk) {
-                                pk = km;
-                                prev = m;
-                            }
-                            lst &= !(km < K);
-                            const uint16_t nx = sh.u.rec.link[m];
-                            m = nx == SP_NONE16 ? SP_NONE : nx;
+                if (act) {
+                    uint32_t jj, a1 = jn - 1;
+                    {
+                        uint32_t a0 = jt;
+                        const uint32_t rr = c0 + RPER * L;
+                        while (a0 < a1) {
+                            const uint32_t mid = (a0 + a1 + 1) >> 1;
+                            if (sh.vstart[mid] <= rr) a0 = mid;
+                            else a1 = mid - 1;
                         }
-                        __stcg(res + gi[k], prev != SP_NONE ? sh.u.rec.val[prev] : mbox[q]);
-                        last[k] = lst;
+                        jj = a0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < RPER; ++k) {
+                        const uint32_t r = RPER * (uint32_t)L + (uint32_t)k;
+                        gi[k] = SP_NONE;
+                        if (r < cn) {
+                            const uint32_t rr = c0 + r;
+                            while (jj + 1 < jn && sh.vstart[jj + 1] <= rr) ++jj;
+                            gi[k] = sh.tbase[jj] + (rr - sh.vstart[jj]);
+                        }
+                    }
+                    uint32_t fq[RPER];
+                    T fv[RPER];
+#pragma unroll
+                    for (int k = 0; k < RPER; ++k)
+                        if (gi[k] != SP_NONE) {
+                            fq[k] = __ldcg(fwdq + gi[k]);
+                            fv[k] = __ldcg(fwdv + gi[k]);
+                        }
+#pragma unroll
+                    for (int k = 0; k < RPER; ++k)
+                        if (gi[k] != SP_NONE) {
+                            const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;  // conflict-free slot
+                            const uint32_t q = fq[k] & 0xFFFFu;
+                            // key = the step position s (the record lies in its source block's area)
+                            sh.u.rec.key[si] = (gi[k] / SP_B) * SP_B + (fq[k] >> 16);
+                            sh.u.rec.val[si] = fv[k];
+                            sh.u.rec.q[si] = (uint16_t)q;
+                            const uint32_t old = atomicExch(&sh.head[q], si);
+                            sh.u.rec.link[si] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
+                        }
+                }
+                __syncthreads();
+                if (act) {
+#pragma unroll
+                    for (int k = 0; k < RPER; ++k) {
+                        last[k] = false;
+                        if (gi[k] != SP_NONE) {
+                            const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
+                            const uint32_t K = sh.u.rec.key[si];
+                            const uint32_t q = sh.u.rec.q[si];
+                            uint32_t prev = SP_NONE, pk = SP_NONE;
+                            bool lst = true;
+                            for (uint32_t m = sh.head[q]; m != SP_NONE;) {
+                                const uint32_t km = sh.u.rec.key[m];
+                                if (km > K && km < pk) {
+                                    pk = km;
+                                    prev = m;
+                                }
+                                lst &= !(km < K);
+                                const uint16_t nx = sh.u.rec.link[m];
+                                m = nx == SP_NONE16 ? SP_NONE : nx;
+                            }
+                            __stcg(res + gi[k], prev != SP_NONE ? sh.u.rec.val[prev] : mbox[q]);
+                            last[k] = lst;
+                        }
                     }
                 }
                 __syncthreads();
+                if (act) {
 #pragma unroll
-                for (int k = 0; k < RPER; ++k) {
-                    if (gi[k] != SP_NONE) {
-                        const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
-                        const uint32_t q = sh.u.rec.q[si];
-                        if (last[k]) mbox[q] = sh.u.rec.val[si];
-                        sh.head[q] = SP_NONE;
-                    }
+                    for (int k = 0; k < RPER; ++k)
+                        if (gi[k] != SP_NONE) {
+                            const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
+                            const uint32_t q = sh.u.rec.q[si];
+                            if (last[k]) mbox[q] = sh.u.rec.val[si];
+                            sh.head[q] = SP_NONE;
+                        }
                 }
                 __syncthreads();
                 jt = jn;
             }
             // ---- the targets of this block's steps
-            while (gs.frontier > slo && gs.B0 < plan.nbatches)
-                large_gen_step<false, SP_W>(gs, plan, sh, L, nullptr, nullptr, ck);
+            sp_gen_block<T>(g, plan, sh, L, sp_batch_of(sh.segs, plan.nseg, slo));
             __syncthreads();
             // ---- this block's steps in closed form
             uint32_t Jr[PER];
@@ -392,6 +531,7 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
             const uint32_t next = sp_scan(sh.vstart, (uint32_t)sg, sh.wsum, L);
             for (uint32_t t = L; t < (uint32_t)sg; t += SP_T)
                 __stcg(desc + (size_t)sg * NB + t, (sh.vstart[t] << 16) | sh.tbase[t]);
+            if (L == 0 && sg > 0) sh.nd[NB - 1 - (uint32_t)sg] = (sh.vstart[sg - 1] << 16) | sh.tbase[sg - 1];
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
@@ -413,8 +553,7 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
             __syncthreads();
             cur ^= 1;
         }
-        while (gs.B0 < plan.nbatches) large_gen_step<false, SP_W>(gs, plan, sh, L, nullptr, nullptr, ck);
-        if (L == 0 && words32) words32[a] = plan.nbatches + gs.D;
+        if (L == 0 && words32) words32[a] = plan.nbatches + g.D;
     }
 }
 
