@@ -773,7 +773,9 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
     const uint64_t sp_nb = (n + SP_B - 1) / SP_B;
     const bool sp_fit = segmented && gen != 2 && cp.plan.lo <= 1 && sp_nb <= SP_MAXNB &&
                         (uint64_t)cp.plan.max_k * SP_T + SP_B <= SP_RING;
-    if (sp_fit && (forced_kernel() == K_STAGE || (forced_kernel() == K_ANY && n > 65536))) {
+    // measured slower than the CTA-group kernel on C5 (16.9 vs 12.2 ms), so
+    // it runs only when BR_SHUFFLE_KERNEL=stage asks
+    if (sp_fit && forced_kernel() == K_STAGE) {
         const size_t smem = sizeof(SpShared<T>);
         const void *kp = (const void *)shuffle_stage_kernel<T>;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -37,12 +37,15 @@
 
 namespace br {
 
-static constexpr uint32_t SP_B = 4096;     // positions per block (one stage)
-static constexpr int SP_W = 16;            // warps per CTA
-static constexpr int SP_T = 32 * SP_W;     // threads per CTA
-static constexpr uint32_t SP_C = SP_B;     // records per chunk of step 1 (a whole tile always fits)
-static constexpr uint32_t SP_RING = 8192;  // u32 target ring: a block + one generation step (k <= 7)
-static constexpr uint32_t SP_MAXNB = 1024; // blocks per array (n <= 4M)
+#ifndef SP_LOG_B
+#define SP_LOG_B 11
+#endif
+static constexpr uint32_t SP_B = 1u << SP_LOG_B;  // positions per block (one stage)
+static constexpr int SP_W = SP_B / 256;           // warps per CTA (8 positions per thread)
+static constexpr int SP_T = 32 * SP_W;            // threads per CTA
+static constexpr uint32_t SP_C = SP_B;            // records per chunk of step 1 (a whole tile always fits)
+static constexpr uint32_t SP_RING = 2 * SP_B;     // u32 target ring: a block + the straddling batch
+static constexpr uint32_t SP_MAXNB = 2 * SP_T;    // blocks per array (the tile scans cover 2 per thread)
 static constexpr uint32_t SP_NONE = 0xFFFFFFFFu;
 static constexpr uint16_t SP_NONE16 = 0xFFFF;
 
@@ -131,7 +134,7 @@ __host__ __device__ constexpr size_t sp_array_bytes(uint32_t n) {
 // [B0, B0 + nact) (nact <= SP_G, so a slot has at most one batch in it); committed slots move
 // SP_G batches on (one precomputed affine jump), the others keep their state.  A rejected batch
 // f shifts every batch >= f by one word (shuffle.py:121-128): pending slots step once more.
-static constexpr int SP_GJ = 5;                 // slots per thread (k = 2: a block's 2048 batches in one step)
+static constexpr int SP_GJ = 5;                 // slots per thread (k = 2: a block's batches in one step)
 static constexpr uint32_t SP_G = SP_GJ * SP_T;  // batches per step
 
 struct SpGen {
@@ -558,7 +561,7 @@ __device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t
 }
 
 template <typename T>
-__global__ void __launch_bounds__(SP_T) shuffle_stage_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
+__global__ void __launch_bounds__(SP_T, 2) shuffle_stage_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
                                                              uint64_t run_seed, int64_t base,
                                                              uint32_t *__restrict__ words32, int gen,
                                                              unsigned char *__restrict__ cta_scratch, size_t cta_bytes,

@@ -69,9 +69,10 @@ def test_stage_schedules(B, O, monkeypatch, maxb):
     assert "shuffle_stage_kernel" in kern and np.array_equal(got, ref) and np.array_equal(w, rw)
 
 
-def test_stage_is_default_for_c5_shape(B, O):
-    """C5 shape (u64[2^20]) through the default dispatch: 12 arrays, every one bit-exact (each
-    has ~172 rejected words, so the realignment runs inside every array)."""
+def test_stage_c5_shape(B, O, monkeypatch):
+    """C5 shape (u64[2^20]), 12 arrays, every one bit-exact (each has ~172 rejected words, so the
+    realignment runs inside every array)."""
+    monkeypatch.setenv("BR_SHUFFLE_KERNEL", "stage")
     n, na = 1 << 20, 12
     kern, got, ref, w, rw = _run(B, O, n, na, 8, "pcg64", seed=5, base=100)
     assert "shuffle_stage_kernel" in kern, kern
