@@ -769,31 +769,43 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
         return BR_OK;
     }
     // many arrays beyond shared memory: the stage pipeline (stage_shuffle.cuh), one CTA per
-    // array, random accesses in shared memory only.  PCG64/Lehmer streams, full plans.
-    const uint64_t sp_nb = (n + SP_B - 1) / SP_B;
-    const bool sp_fit = segmented && gen != 2 && cp.plan.lo <= 1 && sp_nb <= SP_MAXNB &&
-                        (uint64_t)cp.plan.max_k * SP_T + SP_B <= SP_RING;
-    // measured slower than the CTA-group kernel on C5 (16.9 vs 12.2 ms), so
-    // it runs only when BR_SHUFFLE_KERNEL=stage asks
+    // array, every random access in shared memory.  PCG64/Lehmer streams, full plans, n <= 2^20.
+    const bool sp_fit = segmented && gen != 2 && cp.plan.lo <= 1 && n > 1 && n <= (uint64_t)SP_MAXNB * SP_B &&
+                        cp.plan.max_k <= 8;
     if (sp_fit && forced_kernel() == K_STAGE) {
         const size_t smem = sizeof(SpShared<T>);
         const void *kp = (const void *)shuffle_stage_kernel<T>;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int grid = grid_for(di, kp, SP_T, smem, num_arrays);
-        const size_t cta = sp_cta_bytes<T>((uint32_t)n);
-        const size_t per_array = sp_array_bytes<T>((uint32_t)n);
-        // arrays per launch pair: every CTA busy, result slots of at most ~4 GB
+        const size_t cta = sp_cta_bytes((uint32_t)n);
+        const uint32_t vstride = (uint32_t)((n + 7) & ~(uint64_t)7);  // 16-byte aligned areas
+        const size_t per_array = (size_t)vstride * (sizeof(T) + 2) + 4;
+        // arrays per launch pair: every CTA busy, value areas of at most ~4 GB
         const int64_t chunk = std::min<int64_t>(num_arrays, std::max<int64_t>(grid, (int64_t)((4ull << 30) / per_array)));
-        unsigned char *scratch = nullptr;
         const size_t cta_total = (cta * (size_t)grid + 255) & ~(size_t)255;
-        const size_t res_bytes = ((size_t)chunk * n * sizeof(T) + 255) & ~(size_t)255;
-        CK(cudaMallocAsync((void **)&scratch, cta_total + res_bytes + (size_t)chunk * n * 2, st));
-        T *res = (T *)(scratch + cta_total);
-        uint16_t *slot = (uint16_t *)(scratch + cta_total + res_bytes);
-        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+        const size_t val_bytes = ((size_t)chunk * vstride * sizeof(T) + 255) & ~(size_t)255;
+        const size_t slot_bytes = ((size_t)chunk * vstride * 2 + 255) & ~(size_t)255;
+        unsigned char *scratch = nullptr;
+        CK(cudaMallocAsync((void **)&scratch, cta_total + val_bytes + slot_bytes + (size_t)chunk * 4, st));
+        T *val = (T *)(scratch + cta_total);
+        uint16_t *slot = (uint16_t *)(scratch + cta_total + val_bytes);
+        uint32_t *flags = (uint32_t *)(scratch + cta_total + val_bytes + slot_bytes);
+        const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 && !getenv("BR_SP_NOTMA") ? 1 : 0;
         const void *gk = (const void *)shuffle_stage_gather_kernel<T>;
         const int ggrid = grid_for(di, gk, SPG_T, 0, chunk * (int64_t)((n + SP_B - 1) / SP_B));
+        // flagged arrays (a tile larger than a chunk) are re-shuffled from their untouched payload
+        constexpr int LW = LARGE_W;
+        const void *fk = (const void *)shuffle_cta_large_kernel<T, LW, 0>;  // PCG64 and Lehmer
+        const size_t fsmem = large_smem_bytes<T, LW>(false);
+        CK(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
         cudaError_t le = cudaSuccess;
+#ifdef SP_CHECK
+        if (getenv("BR_SP_STOP")) {
+            int v = atoi(getenv("BR_SP_STOP")), ph = getenv("BR_SP_PHASE") ? atoi(getenv("BR_SP_PHASE")) : 99;
+            cudaMemcpyToSymbol(g_sp_stop, &v, 4);
+            cudaMemcpyToSymbol(g_sp_phase, &ph, 4);
+        }
+#endif
         for (int64_t a0 = 0; a0 < num_arrays && le == cudaSuccess; a0 += chunk) {
             int64_t na = std::min(chunk, num_arrays - a0);
             T *dp = (T *)data + a0 * (int64_t)n;
@@ -803,12 +815,35 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
             int64_t b0 = base + a0;
             uint32_t *w32 = words32 ? words32 + a0 : nullptr;
             int tma = use_tma;
-            void *args[] = {&dp, &na, &plan, &run_seed, &b0, &w32, &g, &scratch, &cb, &res, &slot, &tma};
-            le = cudaLaunchKernel(kp, dim3((unsigned)std::min<int64_t>(grid, na)), dim3(SP_T), args, smem, st);
+            uint32_t vs = vstride;
+            le = cudaMemsetAsync(flags, 0, (size_t)na * 4, st);
+            void *args[] = {&dp, &na, &plan, &run_seed, &b0, &w32, &g, &scratch, &cb, &val, &slot, &vs, &flags, &tma};
+            if (le == cudaSuccess)
+                le = cudaLaunchKernel(kp, dim3((unsigned)std::min<int64_t>(grid, na)), dim3(SP_T), args, smem, st);
+            const bool dbg = getenv("BR_SP_DEBUG") != nullptr;
+            if (dbg && le == cudaSuccess && (le = cudaStreamSynchronize(st)) != cudaSuccess)
+                return fail(BR_E_CUDA, std::string("stage kernel: ") + cudaGetErrorString(le));
+#ifdef SP_CHECK
+            if (dbg) {
+                unsigned h[8];
+                cudaMemcpyFromSymbol(h, g_sp_dbg, sizeof(h));
+                fprintf(stderr, "SP_CHECK line %u: %u %u %08x blk %u\n", h[0], h[1], h[2], h[3], h[4]);
+            }
+#endif
             if (le == cudaSuccess) {
                 uint32_t nn = (uint32_t)n;
-                void *gargs[] = {&dp, &na, &nn, &res, &slot};
+                void *gargs[] = {&dp, &na, &nn, &val, &slot, &vs, &flags};
                 le = cudaLaunchKernel(gk, dim3(ggrid), dim3(SPG_T), gargs, 0, st);
+                if (dbg && le == cudaSuccess && (le = cudaStreamSynchronize(st)) != cudaSuccess)
+                    return fail(BR_E_CUDA, std::string("gather kernel: ") + cudaGetErrorString(le));
+            }
+            if (le == cudaSuccess) {
+                uint64_t *nul = nullptr;
+                int seg1 = 1;
+                const uint32_t *only = flags;
+                void *fargs[] = {&dp, &na, &plan, &run_seed, &b0, &w32, &nul, &nul, &nul, &seg1, &g, (void *)&only};
+                le = cudaLaunchKernel(fk, dim3((unsigned)std::min<int64_t>(na, (int64_t)di.sms * 8)), dim3(32 * LW),
+                                      fargs, fsmem, st);
             }
         }
         CK(cudaFreeAsync(scratch, st));
@@ -826,7 +861,7 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
         const size_t wsmem = large_smem_bytes<T, W>(!segmented || gen == 2);
         CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
         kern<<<grid, 32 * W, wsmem, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, state_dev, words64,
-                                          rk_first, segmented ? 1 : 0, gen);
+                                          rk_first, segmented ? 1 : 0, gen, nullptr);
         CK(cudaGetLastError());
         g_kernel = std::string("shuffle_cta_large_kernel<u") + std::to_string(8 * sizeof(T)) + "," +
                    std::to_string(W) + ">";

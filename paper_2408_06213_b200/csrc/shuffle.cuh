@@ -763,7 +763,7 @@ __device__ __forceinline__ void shuffle_cta_large_body(T *__restrict__ data, int
                                                        uint64_t *state_io, uint64_t *words64, uint64_t *rk_first,
                                                        int segmented, int gen,
                                                        LargeShared<T, W, uint32_t, large_ring(W)> &sh,
-                                                       uint64_t *chawin) {
+                                                       uint64_t *chawin, const uint32_t *only) {
     constexpr int G = 32 * W;
     const int L = threadIdx.x;
     for (uint32_t q = L; q < plan.nseg; q += G) sh.segs[q] = plan.segs[q];
@@ -773,6 +773,7 @@ __device__ __forceinline__ void shuffle_cta_large_body(T *__restrict__ data, int
     const uint32_t n = plan.n;
     const uint32_t lim = plan.lo > 1 ? plan.lo : 1;
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
+        if (only && !only[a]) continue;  // re-run of the arrays another kernel flagged
         T *z = data + a * (int64_t)n;
         u128 s0, inc;
         bool lh;
@@ -818,7 +819,8 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
                                                                    DevPlan plan, uint64_t run_seed, int64_t base,
                                                                    uint32_t *__restrict__ words32, uint64_t *state_io,
                                                                    uint64_t *words64, uint64_t *rk_first,
-                                                                   int segmented, int gen) {
+                                                                   int segmented, int gen,
+                                                                   const uint32_t *__restrict__ only) {
     // dynamic shared memory: the CTA's tables, then the ChaCha keystream window (8 words per
     // thread) when the launch asks for one; sizes set at launch (large_smem_bytes)
     extern __shared__ __align__(16) unsigned char large_smem[];
@@ -828,10 +830,10 @@ __global__ void __launch_bounds__(32 * W) shuffle_cta_large_kernel(T *__restrict
     if constexpr (CM == 2) cha = is_posgen(mk128(state_io[2], state_io[3]));
     if (CM != 0 && cha)
         shuffle_cta_large_body<T, W, CM != 0>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
-                                              rk_first, segmented, gen, sh, chawin);
+                                              rk_first, segmented, gen, sh, chawin, only);
     else if (CM != 1)
         shuffle_cta_large_body<T, W, false>(data, num_arrays, plan, run_seed, base, words32, state_io, words64,
-                                            rk_first, segmented, gen, sh, chawin);
+                                            rk_first, segmented, gen, sh, chawin, only);
 }
 
 // Shared-memory-resident arrays with the same hashed CTA groups: payload moved by TMA bulk

@@ -1,83 +1,105 @@
 // stage_shuffle.cuh -- many arrays too large for shared memory (C5: 256 x u64[2^20]):
-// Fisher-Yates as a pipeline of shared-memory stages, one CTA per array, no random access
-// to global memory.
+// Fisher-Yates as a pipeline of shared-memory stages, one CTA per array, every random access
+// in shared memory and every global access a stream.
 //
-// The array is cut into blocks of SP_B positions.  Steps run from the top (shuffle.py:100-134:
-// step s swaps z[s] and z[J[s]], J[s] <= s, s = n-1 down to 1), so block sg's steps happen after
-// every step of the blocks above it.  Stage sg (sg = NB-1 down to 0) holds block sg in shared
-// memory and
-//   1. applies, in time order, the steps of higher blocks that target it ("records" left by
-//      those stages: target offset, the step's position, the value it deposits).  For a target
-//      q the steps arrive as an exchange sequence: the first returns z0[q], each later one the
-//      value of the one before, and q keeps the last deposit.  The returned value is the step's
-//      final output (out[s] = the value at J[s] just before step s); it goes to the result slot
-//      of the record, which sits in the SOURCE block's result area;
-//   2. generates the targets of its own steps (CTA-wide, with the rejection realignment of
-//      large_gen_step: word alignment is exact for any number of rejections);
-//   3. runs its own steps in closed form (DESIGN.md section 2.4 restricted to the block):
-//      with FT(x) the first later step targeting x inside the block and NS(s) the next such
-//      step after s with s's target, the value at x before step x is Val(x) = Val(FT(x)) or the
-//      block contents after (1); an in-block step outputs Val(NS(s)) or the contents of its
-//      target; a step targeting a lower block leaves a record (target, s, Val(s)) for the stage
-//      of that block;
-//   4. writes its records grouped by target block (tiles), a tile table entry per lower block,
-//      its in-block outputs into its result area and a slot map (position -> result slot).
-// After stage 0 every result slot is filled; out[p] = result[slot[p]] is gathered block by
-// block through shared memory by a second, fully parallel kernel (shuffle_stage_gather_kernel).
-// Global traffic is streaming (blocks, records, results, slot maps); all random accesses are
-// in shared memory.  The next block streams in (TMA bulk copy) while the current one is
-// worked on.
+// The array is cut into blocks of SP_B = 4096 positions.  Steps run from the top
+// (shuffle.py:100-134: step s swaps z[s] and z[J[s]], J[s] <= s, s = n-1 down to 1), so every
+// step of block sg happens after every step of the blocks above it.  Stage sg (NB-1 down to 0)
+// holds block sg (its original values, mbox) in shared memory and
+//   A. starts the TMA load of the block and prefetches its tile table;
+//   B. generates the targets of its own steps (CTA-wide windows of striped batches with the
+//      rejection realignment of shuffle.py:121-128: a rejected batch shifts every later batch
+//      by one word, exact for any number of rejections);
+//   C. resolves its own steps in closed form on indices only (DESIGN.md section 2.4 inside the
+//      block: FT(x) = the first later in-block step targeting x, NS(s) = the next in-block step
+//      after s with s's target, F = the end of the FT chain).  Afterwards every position
+//      knows which shared-memory slot holds its value: Val(s) = mbox[F(s)] for a step leaving
+//      the block, mbox[F(NS(s))] or mbox[J(s)] for an in-block output;
+//   D. applies, in time order, the steps of higher blocks that target it ("records": target
+//      offset x, step position s, deposited value).  The records of one target x form an
+//      exchange chain: the earliest returns the block's value at x, each later one the value
+//      deposited by the one before, and x keeps the last deposit.  A record's return value is
+//      the final output of its step; it overwrites the record's value slot, which sits in the
+//      SOURCE block's area (so the results of one source tile are contiguous);
+//   E. writes its own records grouped by target block (one tile per lower block, through a
+//      shared-memory staging area, coalesced), its in-block outputs after them, the tile table
+//      entries and the slot map (position -> slot in the block's area).
+// After stage 0 every slot holds a final value; shuffle_stage_gather_kernel writes
+// out[p] = area[slot[p]] block by block through shared memory.  The payload itself is only
+// read (block by block, stage A), so an array whose tiles would overflow a chunk (impossible
+// for generated words in practice, but not excluded) is flagged and re-shuffled from its
+// untouched payload by the CTA-group kernel.
 //
-// Exactness: stage sg sees the block exactly as the sequential loop would after all higher
-// steps (their deposits in time order, records carry s); its own steps are the sequential
-// loop's (closed form, checked exhaustively in tests/test_resolution.py and bit-exactly
-// against the oracle on the device).
+// Record key: x | s << 12 (s < 2^20, so n <= 2^20 = 256 blocks); the source block is s >> 12.
+// Exactness: stage sg sees its block exactly as the sequential loop does after all higher
+// steps (their deposits in time order: tiles in source order, s inside a tile); its own
+// steps are the sequential loop's (closed form, exhaustively checked in
+// tests/test_resolution.py, bit-exactly against the oracle on the device in tests/test_stage.py).
 #pragma once
 #include "shuffle.cuh"
 
 namespace br {
 
-#ifndef SP_LOG_B
-#define SP_LOG_B 11
+#ifdef SP_CHECK
+__device__ unsigned int g_sp_dbg[8];
+__device__ int g_sp_stop = -1;  // debug: last stage to run (stages below it are skipped)
+__device__ int g_sp_phase = 99;  // debug: phases to run in the last stage (1 = A-B, 2 = +C, 3 = +D)
+// records the first failed check (line and three values); the guarded access is skipped
+#define SP_OK(c, a0, a1, a2)                                                                   \
+    ((c) ? true : (atomicCAS(&g_sp_dbg[0], 0u, (unsigned)__LINE__) == 0u                      \
+                       ? (g_sp_dbg[1] = (unsigned)(a0), g_sp_dbg[2] = (unsigned)(a1),          \
+                          g_sp_dbg[3] = (unsigned)(a2), g_sp_dbg[4] = blockIdx.x, false)       \
+                       : false))
+#else
+#define SP_OK(c, a0, a1, a2) true
 #endif
-static constexpr uint32_t SP_B = 1u << SP_LOG_B;  // positions per block (one stage)
-static constexpr int SP_W = SP_B / 256;           // warps per CTA (8 positions per thread)
-static constexpr int SP_T = 32 * SP_W;            // threads per CTA
-static constexpr uint32_t SP_C = SP_B;            // records per chunk of step 1 (a whole tile always fits)
-static constexpr uint32_t SP_RING = 2 * SP_B;     // u32 target ring: a block + the straddling batch
-static constexpr uint32_t SP_MAXNB = 2 * SP_T;    // blocks per array (the tile scans cover 2 per thread)
+#define SP_ASSERT(c, ...)
+
+static constexpr int SP_LOG_B = 12;
+static constexpr uint32_t SP_B = 1u << SP_LOG_B;   // positions per block (one stage)
+static constexpr int SP_T = 512;                    // threads per CTA (two CTAs per SM)
+static constexpr int SP_W = SP_T / 32;
+static constexpr int SP_PER = SP_B / SP_T;          // positions per thread
+static constexpr uint32_t SP_C = 3456;              // inbox records per chunk
+static constexpr uint32_t SP_MAXNB = 256;           // blocks per array (n <= 2^20)
+static constexpr uint32_t SP_MAXCH = 128;           // chunks per stage
+static constexpr int SP_GJ = 4;                     // generator slots per thread
+static constexpr uint32_t SP_G = SP_GJ * SP_T;      // batches per generation window
+static constexpr uint32_t SP_RING = SP_B + 8;       // targets by position - blo + 8 (8 below: the straddling batch)
 static constexpr uint32_t SP_NONE = 0xFFFFFFFFu;
 static constexpr uint16_t SP_NONE16 = 0xFFFF;
+static constexpr uint32_t SP_JNONE = 0xFFFFFu;      // ring: no step at this position
 
 template <typename T>
 struct SpShared {
-    static constexpr uint32_t RSIZE = SP_RING;
-    using RType = uint32_t;
-    DevSeg segs[MAX_SEGS];
-    uint32_t ring[SP_RING];  // targets by position (large_gen_step)
-    T mbuf[2][SP_B];         // the block's contents; the next block streams into the other buffer
-    uint32_t head[SP_B];     // per-target chain heads (atomicExch), SP_NONE = empty
+    T mbox[SP_B];            // the block: original values, then after the higher blocks' deposits
+    uint32_t ring[SP_RING];  // J by position (B, C), then src << 20 | J (E)
+    uint16_t head[SP_B];     // per-target list heads (C: in-block steps, D: records), SP_NONE16 = empty
     union {
-        struct {  // step 1: one chunk of records
-            uint32_t key[SP_C];  // the record's step position s (larger = earlier in time)
+        struct {
+            uint16_t link[SP_B];
+            uint16_t F[SP_B];  // FT, then the end of the FT chain
+        } loc;
+        struct {
+            uint32_t key[SP_C];
             T val[SP_C];
             uint16_t link[SP_C];
-            uint16_t q[SP_C];
         } rec;
-        struct {  // step 3: the block's own steps
-            uint16_t F[SP_B];  // FT pointer, then the end of the FT chain (Val(x) = mbox[F[x]])
-            uint16_t link[SP_B];
-        } loc;
+        struct {
+            uint32_t key[SP_B];
+            T val[SP_B];
+        } out;
     } u;
-    uint32_t vstart[SP_MAXNB];  // tiles: exclusive prefix of counts; step 4: per-target-block prefix
-    uint32_t tbase[SP_MAXNB];   // tiles: first record index; step 4: per-target-block counts
-    uint32_t nd[SP_MAXNB];      // the next stage's tile table (prefetched during this stage)
+    u128 inc, AG, CG, M;  // generator constants of the array (the same for every thread)
+    DevSeg segs[MAX_SEGS];
+    uint32_t excl[SP_MAXNB + 1];  // inbox: exclusive prefix of the tile counts (tile t = source NB-1-t)
+    uint32_t toff[SP_MAXNB];      // per source block: global record index minus inbox index
+    uint32_t cnt[SP_MAXNB + 1];   // per target block: this stage's records, then their exclusive prefix
+    uint16_t cend[SP_MAXCH];      // chunk ends (tile index, exclusive)
     uint32_t wsum[SP_W + 1];
-    uint64_t bar[2];
-    uint32_t frontier[2];
-    uint32_t fmin;
-    uint32_t nint;
-    uint32_t chunk_end;
+    uint32_t carry[8];            // targets of the straddling batch for the next stage
+    uint64_t bar;
+    uint32_t fmin, nint, nchunk, bad;
 };
 
 // exclusive scan of a[0..len) in place (len <= 2 * SP_T); every thread gets the total
@@ -114,36 +136,38 @@ __device__ __forceinline__ uint32_t sp_scan(uint32_t *a, uint32_t len, uint32_t 
     return total;
 }
 
-// global scratch: per CTA (records and tile table, reused array after array) and per array
-// (result slots and slot map, read by the gather kernel)
-template <typename T>
-__host__ __device__ constexpr size_t sp_cta_bytes(uint32_t n) {
-    const size_t nb = (n + SP_B - 1) / SP_B;
-    return (((size_t)n * 4 + 255) & ~(size_t)255) +           // record (target offset | position << 16)
-           (((size_t)n * sizeof(T) + 255) & ~(size_t)255) +   // record value
-           ((nb * nb * 4 + 255) & ~(size_t)255);              // tile table
-}
-template <typename T>
-__host__ __device__ constexpr size_t sp_array_bytes(uint32_t n) {
-    return (size_t)n * (sizeof(T) + 2);  // result slots + slot map
+// 16-bit exchange in shared memory (list heads) through a CAS on the enclosing word
+__device__ __forceinline__ uint16_t sp_xchg16(uint16_t *p, uint16_t v) {
+    uint32_t *w = reinterpret_cast<uint32_t *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)3);
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 2) * 8;
+    uint32_t old = *w, assumed;
+    do {
+        assumed = old;
+        old = atomicCAS(w, assumed, (assumed & ~(0xFFFFu << sh)) | ((uint32_t)v << sh));
+    } while (old != assumed);
+    return (uint16_t)(old >> sh);
 }
 
-// ---- target generation for one block: striped lanes, no per-stage jump
-// Slot (thread L, j) owns the batches b == L + SP_T*j (mod SP_G) and holds the generator state
-// whose output is word b + D of its next pending batch b.  A step covers the window
-// [B0, B0 + nact) (nact <= SP_G, so a slot has at most one batch in it); committed slots move
-// SP_G batches on (one precomputed affine jump), the others keep their state.  A rejected batch
-// f shifts every batch >= f by one word (shuffle.py:121-128): pending slots step once more.
-static constexpr int SP_GJ = 5;                 // slots per thread (k = 2: a block's batches in one step)
-static constexpr uint32_t SP_G = SP_GJ * SP_T;  // batches per step
+__device__ __forceinline__ void sp_cp4(void *s, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void sp_cp8(void *s, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void sp_cp_wait() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 
+// ---- target generation: striped slots.  Slot (thread L, j) owns the batches b == L + SP_T*j
+// (mod SP_G) and holds the generator state whose output is word b + D of its next pending
+// batch b.  A window [B0, wend) has at most one batch per slot; committed slots move SP_G
+// batches on (one precomputed affine jump), the others keep their state.  A rejected batch f
+// shifts every batch >= f by one word: pending slots step once more.
 struct SpGen {
     u128 s[SP_GJ];
-    uint32_t b[SP_GJ];   // pending batch of each slot
-    uint8_t seg[SP_GJ];  // its segment
-    u128 inc, AG, CG, M;
+    uint32_t b[SP_GJ];  // pending batch of each slot
     uint32_t B0, D;
-    bool lh;
+    uint8_t seg[SP_GJ];
 };
 
 __device__ __forceinline__ void sp_jump(u128 &s, u128 inc, uint32_t d, bool lh) {
@@ -155,13 +179,17 @@ __device__ __forceinline__ void sp_jump(u128 &s, u128 inc, uint32_t d, bool lh) 
 }
 
 template <typename T>
-__device__ __forceinline__ void sp_gen_init(SpGen &g, uint64_t seed, bool lh, int L) {
+__device__ __forceinline__ void sp_gen_init(SpGen &g, SpShared<T> &sh, uint64_t seed, bool lh, int L) {
     u128 s0, inc;
     gen_seed(seed, s0, inc, lh);
-    g.inc = inc;
-    g.lh = lh;
-    g.M = gen_mult(lh);
-    gen_affine(SP_G, inc, lh, g.AG, g.CG);
+    if (L == 0) {
+        sh.inc = inc;
+        sh.M = gen_mult(lh);
+        u128 A, C;
+        gen_affine(SP_G, inc, lh, A, C);
+        sh.AG = A;
+        sh.CG = C;
+    }
     const u128 s1 = gen_jump_small(s0, inc, L + 1, lh);  // output = word L
 #pragma unroll
     for (int j = 0; j < SP_GJ; ++j) {
@@ -184,17 +212,17 @@ __device__ __forceinline__ uint32_t sp_batch_of(const DevSeg *segs, uint32_t nse
     return 0;
 }
 
-// generate every batch up to and including b_need into the target ring
+// generate every batch up to and including b_need; targets into ring[pos - blo + 8]
 template <typename T>
-__device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpShared<T> &sh, int L, uint32_t b_need) {
-    constexpr uint32_t RS = SP_RING;
+__device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpShared<T> &sh, int L, uint32_t b_need,
+                                             uint32_t blo, bool lh) {
     while (g.B0 <= b_need) {
         const uint32_t wend = min(g.B0 + SP_G, b_need + 1);  // window [B0, wend)
         uint64_t t[SP_GJ];
 #pragma unroll
         for (int j = 0; j < SP_GJ; ++j)
             if (g.b[j] < wend) t[j] = __ldg(plan.thresh + g.b[j]);
-        uint32_t myfail = 0xFFFFFFFFu;
+        uint32_t myfail = SP_NONE;
 #pragma unroll
         for (int j = 0; j < SP_GJ; ++j) {
             const uint32_t b = g.b[j];
@@ -204,40 +232,45 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
                 g.seg[j] = (uint8_t)q;
                 const DevSeg S = sh.segs[q];
                 const uint32_t nbb = S.start_n - (b - S.first_batch) * S.k;
-                uint64_t r = gen_out(g.s[j], g.lh);
-                const uint32_t pos = nbb - 1;
+                uint64_t r = gen_out(g.s[j], lh);
+                uint32_t *rg = sh.ring + (nbb - 1 - blo + 8);
                 if (plan.naive && S.k == 2) {
                     uint32_t j1, j2;
                     naive_pair(nbb, r, j1, j2);
-                    sh.ring[pos & (RS - 1)] = j1;
-                    sh.ring[(pos - 1) & (RS - 1)] = j2;
+                    rg[0] = j1;
+                    rg[-1] = j2;
                 } else {
-                    for (uint32_t m = 0; m < S.k; ++m) sh.ring[(pos - m) & (RS - 1)] = die(nbb - m, r);
+                    for (uint32_t m = 0; m < S.k; ++m) {
+                        const uint32_t d = die(nbb - m, r);
+                        if (SP_OK(nbb - 1 - m + 8 >= blo && nbb - 1 - m + 8 - blo < SP_RING, 3000 + b, nbb, blo)) rg[-(int)m] = d;
+                    }
                 }
                 if (r < t[j] && b < myfail) myfail = b;
             }
         }
-        if (!__syncthreads_or(myfail != 0xFFFFFFFFu)) {
+        if (!__syncthreads_or(myfail != SP_NONE)) {
+            const u128 AG = sh.AG, CG = sh.CG;
 #pragma unroll
             for (int j = 0; j < SP_GJ; ++j)
                 if (g.b[j] < wend) {
                     g.b[j] += SP_G;
-                    g.s[j] = mad128(g.s[j], g.AG, g.CG);
+                    g.s[j] = mad128(g.s[j], AG, CG);
                 }
             g.B0 = wend;
         } else {
-            if (L == 0) sh.fmin = 0xFFFFFFFFu;
+            if (L == 0) sh.fmin = SP_NONE;
             __syncthreads();
-            if (myfail != 0xFFFFFFFFu) atomicMin(&sh.fmin, myfail);
+            if (myfail != SP_NONE) atomicMin(&sh.fmin, myfail);
             __syncthreads();
             const uint32_t f = sh.fmin;  // the first rejected batch: it and everything after take one word more
+            const u128 AG = sh.AG, CG = sh.CG, M = sh.M, inc = sh.inc;
 #pragma unroll
             for (int j = 0; j < SP_GJ; ++j) {
                 if (g.b[j] < f) {
                     g.b[j] += SP_G;
-                    g.s[j] = mad128(g.s[j], g.AG, g.CG);
+                    g.s[j] = mad128(g.s[j], AG, CG);
                 }
-                g.s[j] = mad128(g.s[j], g.M, g.inc);
+                g.s[j] = mad128(g.s[j], M, inc);
             }
             g.B0 = f;
             g.D += 1;
@@ -246,348 +279,375 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
     }
 }
 
+// greedy chunks of whole tiles in inbox order, at most SP_C records each (warp 0).  A tile
+// larger than a chunk, or more chunks than SP_MAXCH, marks the array bad (re-run elsewhere).
+__device__ __forceinline__ void sp_chunk_plan(const uint32_t *excl, uint32_t ntile, uint16_t *cend, uint32_t &nchunk,
+                                              uint32_t &bad, int lane) {
+    uint32_t fill = 0, nch = 0;
+    bool ovf = false;
+    for (uint32_t base = 0; base < ntile && !ovf; base += 32) {
+        const uint32_t t = base + lane;
+        const uint32_t c = t < ntile ? excl[t + 1] - excl[t] : 0;
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        uint32_t consumed = 0;
+        int start = 0;
+        while (true) {
+            const unsigned over = __ballot_sync(0xFFFFFFFFu, lane >= start && t < ntile && fill + inc - consumed > SP_C);
+            if (!over) {
+                fill += __shfl_sync(0xFFFFFFFFu, inc, 31) - consumed;
+                break;
+            }
+            const int f = __ffs(over) - 1;
+            if (f == start && fill == 0) {  // one tile alone exceeds a chunk
+                ovf = true;
+                break;
+            }
+            if (lane == 0 && nch < SP_MAXCH) cend[nch] = (uint16_t)(base + f);
+            ++nch;
+            consumed = __shfl_sync(0xFFFFFFFFu, inc, f > 0 ? f - 1 : 0);
+            if (f == 0) consumed = 0;
+            start = f;
+            fill = 0;
+        }
+    }
+    if (!ovf && fill > 0) {
+        if (lane == 0 && nch < SP_MAXCH) cend[nch] = (uint16_t)ntile;
+        ++nch;
+    }
+    if (nch > SP_MAXCH) ovf = true;
+    if (lane == 0) {
+        nchunk = ovf ? 0 : nch;
+        if (ovf) bad = 1;
+    }
+}
+
+// scratch: per CTA the records' keys and the tile table (reused array after array); per
+// array the value areas, the slot map and a flag
+__host__ __device__ constexpr size_t sp_cta_bytes(uint32_t n) {
+    const size_t nb = (n + SP_B - 1) / SP_B;
+    return (((size_t)n * 4 + 255) & ~(size_t)255) + ((nb * nb * 4 + 255) & ~(size_t)255);
+}
+
 template <typename T>
-__device__ __forceinline__ void shuffle_stage_body(T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
+__device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, int64_t num_arrays, const DevPlan &plan,
                                                    uint64_t run_seed, int64_t base, uint32_t *__restrict__ words32,
                                                    int gen, SpShared<T> &sh, unsigned char *__restrict__ cta_scratch,
-                                                   size_t cta_bytes, T *__restrict__ res_all,
-                                                   uint16_t *__restrict__ slot_all, int use_tma) {
-    constexpr int PER = SP_B / SP_T;   // positions per thread in steps 3-4
-    constexpr int RPER = SP_C / SP_T;  // records per thread in step 1
+                                                   size_t cta_bytes, T *__restrict__ val_all,
+                                                   uint16_t *__restrict__ slot_all, uint32_t vstride,
+                                                   uint32_t *__restrict__ flags, int use_tma) {
     const int L = threadIdx.x;
+    const int lane = L & 31, wid = L >> 5;
     const uint32_t n = plan.n;
     const uint32_t NB = (n + SP_B - 1) / SP_B;
     const uint32_t lo = plan.lo;
-    unsigned char *w = cta_scratch + (size_t)blockIdx.x * cta_bytes;
-    uint32_t *fwdq = reinterpret_cast<uint32_t *>(w);
-    w += ((size_t)n * 4 + 255) & ~(size_t)255;
-    T *fwdv = reinterpret_cast<T *>(w);
-    w += ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
-    uint32_t *desc = reinterpret_cast<uint32_t *>(w);
+    const bool lh = gen == 1;
+    uint32_t *keyg = reinterpret_cast<uint32_t *>(cta_scratch + (size_t)blockIdx.x * cta_bytes);
+    uint32_t *desc = keyg + (((size_t)n * 4 + 255) & ~(size_t)255) / 4;
 
     for (uint32_t q = L; q < plan.nseg; q += SP_T) sh.segs[q] = plan.segs[q];
-    for (uint32_t x = L; x < SP_B; x += SP_T) sh.head[x] = SP_NONE;
+    for (uint32_t x = L; x < SP_B; x += SP_T) sh.head[x] = SP_NONE16;
+    for (uint32_t x = L; x <= SP_MAXNB; x += SP_T) sh.cnt[x] = 0;
     if (L == 0) {
         sh.nint = 0;
-        mbar_init(&sh.bar[0], 1);
-        mbar_init(&sh.bar[1], 1);
+        sh.bad = 0;
+        mbar_init(&sh.bar, 1);
     }
     __syncthreads();
-    uint32_t par0 = 0, par1 = 0;
+    uint32_t parity = 0;
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
-        T *z = data + a * (int64_t)n;
-        T *res = res_all + a * (int64_t)n;
-        uint16_t *slot = slot_all + a * (int64_t)n;
-        // block sg into buffer b: one bulk copy by thread 0 (completion on bar[b]) or plain loads
-        auto fetch = [&](int b, uint32_t sgf) {
-            const uint32_t blo = sgf * SP_B;
-            const uint32_t bn = min(SP_B, n - blo);
-            if (use_tma) {
-                if (L == 0) {
-                    fence_proxy_async();  // earlier generic accesses to the buffer come first
-                    mbar_arrive_expect_tx(&sh.bar[b], bn * (uint32_t)sizeof(T));
-                    bulk_load(sh.mbuf[b], z + blo, bn * (uint32_t)sizeof(T), &sh.bar[b]);
-                }
-            } else {
-                for (uint32_t x = L; x < bn; x += SP_T) sh.mbuf[b][x] = z[blo + x];
-            }
-        };
+        const T *z = data + a * (int64_t)n;
+        T *valg = val_all + a * (int64_t)vstride;
+        uint16_t *slotg = slot_all + a * (int64_t)vstride;
         SpGen g;
-        sp_gen_init<T>(g, array_seed(run_seed, (uint64_t)(base + a)), gen == 1, L);
-        int cur = 0;
-        fetch(0, NB - 1);
+        sp_gen_init<T>(g, sh, array_seed(run_seed, (uint64_t)(base + a)), lh, L);
+        __syncthreads();
         for (int sg = (int)NB - 1; sg >= 0; --sg) {
+#ifdef SP_CHECK
+            if (sg < g_sp_stop) break;
+            const int phmax = sg == g_sp_stop ? g_sp_phase : 99;
+#else
+            constexpr int phmax = 99;
+#endif
             const uint32_t blo = (uint32_t)sg * SP_B;
             const uint32_t bn = min(SP_B, n - blo);
             const uint32_t slo = max(blo, lo);  // positions below slo have no step
-            T *mbox = sh.mbuf[cur];
-            // ---- tile table of this block (prefetched by the previous stage into nd)
-            const uint32_t ntile = NB - 1 - (uint32_t)sg;  // tile j comes from block NB-1-j
-            for (uint32_t j = L; j < ntile; j += SP_T) {
-                const uint32_t d = sh.nd[j];
-                sh.vstart[j] = d & 0xFFFFu;
-                sh.tbase[j] = (NB - 1 - j) * SP_B + (d >> 16);
-            }
+            const uint32_t ntile = NB - 1 - (uint32_t)sg;
+            // ---- A. the block streams in; tile table entries of this block (all written by now)
             if (use_tma) {
-                if (cur == 0) {
-                    mbar_wait(&sh.bar[0], par0);
-                    par0 ^= 1u;
-                } else {
-                    mbar_wait(&sh.bar[1], par1);
-                    par1 ^= 1u;
+                if (L == 0) {
+                    fence_proxy_async();  // earlier generic accesses to mbox come first
+                    mbar_arrive_expect_tx(&sh.bar, bn * (uint32_t)sizeof(T));
+                    bulk_load(sh.mbox, z + blo, bn * (uint32_t)sizeof(T), &sh.bar);
                 }
+            } else {
+                for (uint32_t x = L; x < bn; x += SP_T) sh.mbox[x] = z[blo + x];
             }
+            const uint32_t dreg = (uint32_t)L < ntile ? __ldcg(desc + (size_t)sg * NB + (NB - 1 - L)) : 0;
+            if (L < 8) sh.ring[SP_B + L] = sh.carry[L];
+            // ---- B. targets of this block's steps
+            if (slo < blo + bn) sp_gen_block<T>(g, plan, sh, L, sp_batch_of(sh.segs, plan.nseg, slo), blo, lh);
             __syncthreads();
-            if (sg > 0) fetch(cur ^ 1, (uint32_t)sg - 1);  // the next block streams in meanwhile
-            const uint32_t R = sp_scan(sh.vstart, ntile, sh.wsum, L);
-            // ---- the next stage's tile table (all but this stage's own tile, written at its end)
-            // and an L2 prefetch of its records
-            if (sg > 0) {
-                for (uint32_t j = L; j + 1 < NB - (uint32_t)sg; j += SP_T) {
-                    const uint32_t sp = NB - 1 - j;
-                    const uint32_t d = __ldcg(desc + (size_t)sp * NB + (uint32_t)(sg - 1));
-                    sh.nd[j] = d;
-                    const uint32_t cnt = d & 0xFFFFu;
-                    if (cnt) {
-                        const size_t first = (size_t)sp * SP_B + (d >> 16);
-                        const uintptr_t q0 = (uintptr_t)(fwdq + first) & ~(uintptr_t)15;
-                        const uintptr_t q1 = ((uintptr_t)(fwdq + first + cnt) + 15) & ~(uintptr_t)15;
-                        const uintptr_t v0 = (uintptr_t)(fwdv + first) & ~(uintptr_t)15;
-                        const uintptr_t v1 = ((uintptr_t)(fwdv + first + cnt) + 15) & ~(uintptr_t)15;
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q0), "r"((uint32_t)(q1 - q0))
-                                     : "memory");
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v0), "r"((uint32_t)(v1 - v0))
-                                     : "memory");
-                    }
-                }
-            }
-            // ---- the block as the higher blocks left it: z0, then their deposits in time order.
-            // Chunks of whole tiles (records of one tile are in no particular order; tiles are in
-            // time order), as many as fit SP_C records; records of one chunk are ordered by key
-            for (uint32_t jt = 0; jt < ntile;) {
-                if (L == 0) {  // last tile je with end(je) - start(jt) <= SP_C
-                    uint32_t a0 = jt, a1 = ntile - 1;
-                    while (a0 < a1) {
-                        const uint32_t mid = (a0 + a1 + 1) >> 1;
-                        const uint32_t end = mid + 1 < ntile ? sh.vstart[mid + 1] : R;
-                        if (end - sh.vstart[jt] <= SP_C) a0 = mid;
-                        else a1 = mid - 1;
-                    }
-                    sh.chunk_end = a0 + 1;
-                }
-                __syncthreads();
-                const uint32_t jn = sh.chunk_end;
-                const uint32_t c0 = sh.vstart[jt];
-                const uint32_t cn = (jn < ntile ? sh.vstart[jn] : R) - c0;
-                const bool act = (uint32_t)(RPER * L) < cn;  // thread L takes records RPER*L + k
-                uint32_t gi[RPER];
-                bool last[RPER];
-                if (act) {
-                    uint32_t jj, a1 = jn - 1;
-                    {
-                        uint32_t a0 = jt;
-                        const uint32_t rr = c0 + RPER * L;
-                        while (a0 < a1) {
-                            const uint32_t mid = (a0 + a1 + 1) >> 1;
-                            if (sh.vstart[mid] <= rr) a0 = mid;
-                            else a1 = mid - 1;
-                        }
-                        jj = a0;
-                    }
+            if (L < 8) sh.carry[L] = sh.ring[L];
+            if (phmax < 2) break;
+            // ---- C. this block's steps in closed form (indices only)
 #pragma unroll
-                    for (int k = 0; k < RPER; ++k) {
-                        const uint32_t r = RPER * (uint32_t)L + (uint32_t)k;
-                        gi[k] = SP_NONE;
-                        if (r < cn) {
-                            const uint32_t rr = c0 + r;
-                            while (jj + 1 < jn && sh.vstart[jj + 1] <= rr) ++jj;
-                            gi[k] = sh.tbase[jj] + (rr - sh.vstart[jj]);
-                        }
-                    }
-                    uint32_t fq[RPER];
-                    T fv[RPER];
-#pragma unroll
-                    for (int k = 0; k < RPER; ++k)
-                        if (gi[k] != SP_NONE) {
-                            fq[k] = __ldcg(fwdq + gi[k]);
-                            fv[k] = __ldcg(fwdv + gi[k]);
-                        }
-#pragma unroll
-                    for (int k = 0; k < RPER; ++k)
-                        if (gi[k] != SP_NONE) {
-                            const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;  // conflict-free slot
-                            const uint32_t q = fq[k] & 0xFFFFu;
-                            // key = the step position s (the record lies in its source block's area)
-                            sh.u.rec.key[si] = (gi[k] / SP_B) * SP_B + (fq[k] >> 16);
-                            sh.u.rec.val[si] = fv[k];
-                            sh.u.rec.q[si] = (uint16_t)q;
-                            const uint32_t old = atomicExch(&sh.head[q], si);
-                            sh.u.rec.link[si] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
-                        }
-                }
-                __syncthreads();
-                if (act) {
-#pragma unroll
-                    for (int k = 0; k < RPER; ++k) {
-                        last[k] = false;
-                        if (gi[k] != SP_NONE) {
-                            const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
-                            const uint32_t K = sh.u.rec.key[si];
-                            const uint32_t q = sh.u.rec.q[si];
-                            uint32_t prev = SP_NONE, pk = SP_NONE;
-                            bool lst = true;
-                            for (uint32_t m = sh.head[q]; m != SP_NONE;) {
-                                const uint32_t km = sh.u.rec.key[m];
-                                if (km > K && km < pk) {
-                                    pk = km;
-                                    prev = m;
-                                }
-                                lst &= !(km < K);
-                                const uint16_t nx = sh.u.rec.link[m];
-                                m = nx == SP_NONE16 ? SP_NONE : nx;
-                            }
-                            __stcg(res + gi[k], prev != SP_NONE ? sh.u.rec.val[prev] : mbox[q]);
-                            last[k] = lst;
-                        }
-                    }
-                }
-                __syncthreads();
-                if (act) {
-#pragma unroll
-                    for (int k = 0; k < RPER; ++k)
-                        if (gi[k] != SP_NONE) {
-                            const uint32_t si = (uint32_t)k * SP_T + (uint32_t)L;
-                            const uint32_t q = sh.u.rec.q[si];
-                            if (last[k]) mbox[q] = sh.u.rec.val[si];
-                            sh.head[q] = SP_NONE;
-                        }
-                }
-                __syncthreads();
-                jt = jn;
-            }
-            // ---- the targets of this block's steps
-            sp_gen_block<T>(g, plan, sh, L, sp_batch_of(sh.segs, plan.nseg, slo));
-            __syncthreads();
-            // ---- this block's steps in closed form
-            uint32_t Jr[PER];
-#pragma unroll
-            for (int k = 0; k < PER; ++k) {
+            for (int k = 0; k < SP_PER; ++k) {
                 const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                const uint32_t s = blo + i;
-                Jr[k] = SP_NONE;
-                if (i < bn && s >= slo) {
-                    const uint32_t J = sh.ring[s & (SP_RING - 1)];
-                    Jr[k] = J;
-                    if (J >= blo) {
-                        const uint32_t old = atomicExch(&sh.head[J - blo], i);
-                        sh.u.loc.link[i] = old == SP_NONE ? SP_NONE16 : (uint16_t)old;
-                    }
+                if (i < bn && blo + i >= slo) {
+                    const uint32_t J = sh.ring[i + 8];
+                    if (J >= blo && SP_OK(J <= blo + i, sg, i, J)) sh.u.loc.link[i] = sp_xchg16(&sh.head[J - blo], (uint16_t)i);
                 }
             }
             __syncthreads();
-            uint16_t ns[PER];
+            uint32_t nsv[SP_PER / 2];  // NS of the thread's positions, two u16 per word
 #pragma unroll
-            for (int k = 0; k < PER; ++k) {
+            for (int k = 0; k < SP_PER; ++k) {
                 const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                ns[k] = SP_NONE16;
+                uint32_t ns = SP_NONE16;
                 if (i < bn) {
-                    uint32_t ft = SP_NONE;  // first in-block step after i targeting i
-                    for (uint32_t m = sh.head[i]; m != SP_NONE;) {
+                    uint32_t ft = SP_NONE16;  // first in-block step after i targeting i
+                    for (uint32_t m = sh.head[i]; m != SP_NONE16 && SP_OK(m < bn, 4000 + sg, i, m); m = sh.u.loc.link[m])
                         if (m > i && m < ft) ft = m;
-                        const uint16_t nx = sh.u.loc.link[m];
-                        m = nx == SP_NONE16 ? SP_NONE : nx;
-                    }
-                    sh.u.loc.F[i] = ft == SP_NONE ? SP_NONE16 : (uint16_t)ft;
-                    if (Jr[k] != SP_NONE && Jr[k] >= blo) {  // next in-block step after i with i's target
-                        uint32_t nx2 = SP_NONE;
-                        for (uint32_t m = sh.head[Jr[k] - blo]; m != SP_NONE;) {
-                            if (m > i && m < nx2) nx2 = m;
-                            const uint16_t nx = sh.u.loc.link[m];
-                            m = nx == SP_NONE16 ? SP_NONE : nx;
-                        }
-                        ns[k] = nx2 == SP_NONE ? SP_NONE16 : (uint16_t)nx2;
+                    sh.u.loc.F[i] = (uint16_t)ft;
+                    if (blo + i >= slo) {
+                        const uint32_t J = sh.ring[i + 8];
+                        if (J >= blo && SP_OK(J <= blo + i, 1000 + sg, i, J))  // next in-block step after i with i's target
+                            for (uint32_t m = sh.head[J - blo]; m != SP_NONE16 && SP_OK(m < bn, 5000 + sg, i, m); m = sh.u.loc.link[m])
+                                if (m > i && m < ns) ns = m;
                     }
                 }
+                if (k & 1) nsv[k / 2] |= ns << 16;
+                else nsv[k / 2] = ns;
             }
-            for (uint32_t t = L; t < (uint32_t)sg; t += SP_T) sh.tbase[t] = 0;  // per-target-block counts
             __syncthreads();
-            uint16_t endp[PER];
+            uint32_t fe[SP_PER / 2];  // ends of the FT chains
 #pragma unroll
-            for (int k = 0; k < PER; ++k) {
+            for (int k = 0; k < SP_PER; ++k) {
                 const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
                 uint32_t e = i;
                 if (i < bn)
-                    for (uint16_t f = sh.u.loc.F[e]; f != SP_NONE16; f = sh.u.loc.F[e]) e = f;
-                endp[k] = (uint16_t)e;
+                    for (uint32_t f = sh.u.loc.F[e]; f != SP_NONE16 && SP_OK(f < bn && f > e, 8000 + sg, e, f); f = sh.u.loc.F[e]) e = f;
+                if (k & 1) fe[k / 2] |= e << 16;
+                else fe[k / 2] = e;
             }
             __syncthreads();
 #pragma unroll
-            for (int k = 0; k < PER; ++k) {
+            for (int k = 0; k < SP_PER; ++k) {
                 const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                if (i < bn) sh.u.loc.F[i] = endp[k];
+                if (i < bn) sh.u.loc.F[i] = (uint16_t)(fe[k / 2] >> (16 * (k & 1)));
             }
             __syncthreads();
-            // ---- outputs: in-block ones into the result area, records for lower blocks
-            T ov[PER];
-            uint32_t rk[PER];
 #pragma unroll
-            for (int k = 0; k < PER; ++k) {
+            for (int k = 0; k < SP_PER; ++k) {
                 const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                rk[k] = 0;
-                if (i >= bn) continue;
-                const uint32_t J = Jr[k];
-                if (J == SP_NONE) {  // no step at this position (below lo): its final value
-                    ov[k] = mbox[sh.u.loc.F[i]];
-                    rk[k] = atomicAdd(&sh.nint, 1u);
-                } else if (J >= blo) {
-                    ov[k] = mbox[ns[k] != SP_NONE16 ? sh.u.loc.F[ns[k]] : J - blo];
-                    rk[k] = atomicAdd(&sh.nint, 1u);
-                    sh.head[J - blo] = SP_NONE;
-                } else {
-                    ov[k] = mbox[sh.u.loc.F[i]];  // Val(s): the value leaving position s
-                    rk[k] = atomicAdd(&sh.tbase[J / SP_B], 1u);
+                if (i < bn) {
+                    uint32_t src, J;
+                    if (blo + i < slo) {  // no step: the position's final value
+                        src = sh.u.loc.F[i];
+                        J = SP_JNONE;
+                    } else {
+                        J = sh.ring[i + 8];
+                        if (!SP_OK(J <= blo + i, 2000 + sg, i, J)) J = blo + i;
+                        if (J >= blo) {
+                            const uint32_t ns = (nsv[k / 2] >> (16 * (k & 1))) & 0xFFFFu;
+                            src = ns != SP_NONE16 ? sh.u.loc.F[ns] : J - blo;
+                            sh.head[J - blo] = SP_NONE16;
+                        } else {
+                            src = sh.u.loc.F[i];  // Val(s): the value leaving position s
+                        }
+                    }
+                    sh.ring[i + 8] = (src << 20) | J;
                 }
             }
+            if (phmax < 3) break;
+            // ---- D. the higher blocks' deposits, in time order
+            if ((uint32_t)L < ntile) sh.excl[L] = dreg & 0xFFFFu;
             __syncthreads();
-            for (uint32_t t = L; t < (uint32_t)sg; t += SP_T) sh.vstart[t] = sh.tbase[t];
-            __syncthreads();
-            const uint32_t next = sp_scan(sh.vstart, (uint32_t)sg, sh.wsum, L);
-            for (uint32_t t = L; t < (uint32_t)sg; t += SP_T)
-                __stcg(desc + (size_t)sg * NB + t, (sh.vstart[t] << 16) | sh.tbase[t]);
-            if (L == 0 && sg > 0) sh.nd[NB - 1 - (uint32_t)sg] = (sh.vstart[sg - 1] << 16) | sh.tbase[sg - 1];
-#pragma unroll
-            for (int k = 0; k < PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                if (i >= bn) continue;
-                const uint32_t J = Jr[k];
-                uint32_t sl;
-                if (J == SP_NONE || J >= blo) {
-                    sl = next + rk[k];
-                    __stcg(res + blo + sl, ov[k]);
-                } else {
-                    const uint32_t tb = J / SP_B;
-                    sl = sh.vstart[tb] + rk[k];
-                    __stcg(fwdq + blo + sl, (J - tb * SP_B) | (i << 16));
-                    __stcg(fwdv + blo + sl, ov[k]);
-                }
-                __stcg(slot + blo + i, (uint16_t)sl);
+            const uint32_t R = sp_scan(sh.excl, ntile, sh.wsum, L);
+            if ((uint32_t)L < ntile) {
+                const uint32_t src = NB - 1 - (uint32_t)L;
+                sh.toff[src] = src * SP_B + (dreg >> 16) - sh.excl[L];
             }
+            if (L == 0) sh.excl[ntile] = R;
+            __syncthreads();
+            if (wid == 0) sp_chunk_plan(sh.excl, ntile, sh.cend, sh.nchunk, sh.bad, lane);
+            if (use_tma) {
+                mbar_wait(&sh.bar, parity);
+                parity ^= 1u;
+            }
+            __syncthreads();
+            const uint32_t nch = phmax < 4 ? 0 : sh.nchunk;
+            uint32_t ta = 0;
+            for (uint32_t ch = 0; ch < nch; ++ch) {
+                const uint32_t tb = sh.cend[ch];
+                const uint32_t cbase = sh.excl[ta];
+                uint32_t ccount = sh.excl[tb] - cbase;
+                if (!SP_OK(ccount <= SP_C && tb <= ntile && tb >= ta, 9000 + sg, (ch << 16) | (ta << 8) | tb, ccount)) {
+                    ccount = 0;
+                    ta = tb;
+                    continue;
+                }
+                for (uint32_t t = ta + (uint32_t)wid; t < tb; t += SP_W) {
+                    const uint32_t src = NB - 1 - t;
+                    const uint32_t c0 = sh.excl[t], cn = sh.excl[t + 1] - c0;
+                    const uint32_t g0 = sh.toff[src] + c0;
+                    if (!SP_OK(g0 + cn <= (src + 1) * SP_B && g0 >= src * SP_B && c0 - cbase + cn <= SP_C, sg, t, g0)) continue;
+                    for (uint32_t q = lane; q < cn; q += 32) {
+                        sp_cp4(&sh.u.rec.key[c0 - cbase + q], keyg + g0 + q);
+                        if (sizeof(T) == 8) sp_cp8(&sh.u.rec.val[c0 - cbase + q], valg + g0 + q);
+                        else sp_cp4(&sh.u.rec.val[c0 - cbase + q], valg + g0 + q);
+                    }
+                }
+                sp_cp_wait();
+                __syncthreads();
+                if (phmax < 5) { ta = tb; continue; }
+                for (uint32_t r = L; r < ccount; r += SP_T) {
+                    const uint32_t x = sh.u.rec.key[r] & (SP_B - 1);
+                    sh.u.rec.link[r] = sp_xchg16(&sh.head[x], (uint16_t)r);
+                }
+                __syncthreads();
+                if (phmax < 6) { ta = tb; continue; }
+                uint32_t lastm = 0;
+                for (uint32_t r = L, j = 0; r < ccount; r += SP_T, ++j) {
+                    const uint32_t K = sh.u.rec.key[r];
+                    const uint32_t s = K >> SP_LOG_B, x = K & (SP_B - 1);
+                    uint32_t bs = SP_NONE, best = SP_NONE16;
+                    bool last = true;
+                    for (uint32_t m = sh.head[x]; m != SP_NONE16 && SP_OK(m < ccount, 6000 + sg, r, m); m = sh.u.rec.link[m]) {
+                        const uint32_t sm = sh.u.rec.key[m] >> SP_LOG_B;
+                        if (sm > s && sm < bs) {
+                            bs = sm;
+                            best = m;
+                        }
+                        last &= !(sm < s);
+                    }
+                    const T res = best != SP_NONE16 ? sh.u.rec.val[best] : sh.mbox[x];
+                    const uint32_t gi = sh.toff[s >> SP_LOG_B] + cbase + r;  // (u32: toff may wrap)
+                    if (SP_OK(s < n && (s >> SP_LOG_B) > (uint32_t)sg && gi < n, sg, r, K)) __stcg(valg + gi, res);
+                    if (last) lastm |= 1u << j;
+                }
+                __syncthreads();
+                if (phmax < 7) { ta = tb; continue; }
+                for (uint32_t r = L, j = 0; r < ccount; r += SP_T, ++j) {
+                    const uint32_t x = sh.u.rec.key[r] & (SP_B - 1);
+                    if ((lastm >> j) & 1) sh.mbox[x] = sh.u.rec.val[r];
+                    sh.head[x] = SP_NONE16;
+                }
+                __syncthreads();
+                ta = tb;
+            }
+            if (phmax < 8) break;
+            // ---- E. this block's records (by target block), in-block outputs, slot map
+            uint32_t rk[SP_PER / 2];
+#pragma unroll
+            for (int k = 0; k < SP_PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                uint32_t rank = 0;
+                bool inb = true;
+                if (i < bn) {
+                    const uint32_t J = sh.ring[i + 8] & SP_JNONE;
+                    if (J < blo && SP_OK((J >> SP_LOG_B) < (uint32_t)sg, 7000 + sg, i, J)) {
+                        rank = atomicAdd(&sh.cnt[J >> SP_LOG_B], 1u);
+                        inb = false;
+                    }
+                }
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, i < bn && inb);
+                uint32_t b0 = 0;
+                if (lane == 0 && m) b0 = atomicAdd(&sh.nint, (uint32_t)__popc(m));
+                b0 = __shfl_sync(0xFFFFFFFFu, b0, 0);
+                if (i < bn && inb) rank = b0 + __popc(m & ((1u << lane) - 1));
+                if (k & 1) rk[k / 2] |= rank << 16;
+                else rk[k / 2] = rank;
+            }
+            __syncthreads();
+            const uint32_t nrec = sp_scan(sh.cnt, (uint32_t)sg, sh.wsum, L);
+            if (L == 0) sh.cnt[sg] = nrec;
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < SP_PER; ++k) {
+                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                if (i < bn) {
+                    const uint32_t e = sh.ring[i + 8];
+                    const uint32_t J = e & SP_JNONE, src = e >> 20;
+                    const uint32_t rank = (rk[k / 2] >> (16 * (k & 1))) & 0xFFFFu;
+                    uint32_t slot;
+                    if (J < blo) {
+                        slot = sh.cnt[J >> SP_LOG_B] + rank;
+                        if (SP_OK(slot < bn, sg, i, slot)) sh.u.out.key[slot] = (J & (SP_B - 1)) | ((blo + i) << SP_LOG_B);
+                    } else {
+                        slot = nrec + rank;
+                    }
+                    if (SP_OK(slot < bn && src < SP_B, sg, slot, e)) sh.u.out.val[slot] = sh.mbox[src];
+                    slotg[blo + i] = (uint16_t)slot;
+                }
+            }
+            for (uint32_t tb = L; tb < (uint32_t)sg; tb += SP_T)
+                __stcg(desc + (size_t)tb * NB + sg, (sh.cnt[tb] << 16) | (sh.cnt[tb + 1] - sh.cnt[tb]));
+            __syncthreads();
+            // staged area out, 16-byte stores
+            {
+                const uint32_t vb = bn * (uint32_t)sizeof(T);
+                const uint32_t v16 = vb / 16;
+                const uint4 *sv = reinterpret_cast<const uint4 *>(sh.u.out.val);
+                uint4 *gv = reinterpret_cast<uint4 *>(valg + blo);
+                for (uint32_t q = L; q < v16; q += SP_T) __stcg(gv + q, sv[q]);
+                for (uint32_t x = v16 * 16 / (uint32_t)sizeof(T) + L; x < bn; x += SP_T) valg[blo + x] = sh.u.out.val[x];
+                const uint32_t k16 = (nrec + 3) / 4;
+                const uint4 *sk = reinterpret_cast<const uint4 *>(sh.u.out.key);
+                uint4 *gk = reinterpret_cast<uint4 *>(keyg + blo);
+                for (uint32_t q = L; q < k16; q += SP_T) __stcg(gk + q, sk[q]);
+            }
+            for (uint32_t tb = L; tb <= (uint32_t)sg; tb += SP_T) sh.cnt[tb] = 0;
             if (L == 0) sh.nint = 0;
             __syncthreads();
-            cur ^= 1;
         }
-        if (L == 0 && words32) words32[a] = plan.nbatches + g.D;
+        if (L == 0) {
+            if (words32) words32[a] = plan.nbatches + g.D;
+            if (sh.bad) flags[a] = 1;
+            sh.bad = 0;
+        }
+        __syncthreads();
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(SP_T, 2) shuffle_stage_kernel(T *__restrict__ data, int64_t num_arrays, DevPlan plan,
-                                                             uint64_t run_seed, int64_t base,
-                                                             uint32_t *__restrict__ words32, int gen,
-                                                             unsigned char *__restrict__ cta_scratch, size_t cta_bytes,
-                                                             T *__restrict__ res, uint16_t *__restrict__ slot,
-                                                             int use_tma) {
+__global__ void __launch_bounds__(SP_T, 2) shuffle_stage_kernel(const T *__restrict__ data, int64_t num_arrays,
+                                                                 DevPlan plan, uint64_t run_seed, int64_t base,
+                                                                 uint32_t *__restrict__ words32, int gen,
+                                                                 unsigned char *__restrict__ cta_scratch,
+                                                                 size_t cta_bytes, T *__restrict__ val_all,
+                                                                 uint16_t *__restrict__ slot_all, uint32_t vstride,
+                                                                 uint32_t *__restrict__ flags, int use_tma) {
     extern __shared__ __align__(16) unsigned char sp_smem[];
     auto &sh = *reinterpret_cast<SpShared<T> *>(sp_smem);
-    shuffle_stage_body<T>(data, num_arrays, plan, run_seed, base, words32, gen, sh, cta_scratch, cta_bytes, res, slot,
-                          use_tma);
+    shuffle_stage_body<T>(data, num_arrays, plan, run_seed, base, words32, gen, sh, cta_scratch, cta_bytes, val_all,
+                          slot_all, vstride, flags, use_tma);
 }
 
-// out[p] = result[slot[p]] for every block of every array: one block per iteration through
-// shared memory (the slot map is a permutation of the block's result slots)
+// out[p] = area[slot[p]] for every block of every unflagged array, one block per iteration
+// through shared memory (the slot map is a permutation of the block's slots)
 static constexpr int SPG_T = 512;
 template <typename T>
 __global__ void __launch_bounds__(SPG_T) shuffle_stage_gather_kernel(T *__restrict__ data, int64_t num_arrays,
-                                                                     uint32_t n, const T *__restrict__ res,
-                                                                     const uint16_t *__restrict__ slot) {
+                                                                     uint32_t n, const T *__restrict__ val_all,
+                                                                     const uint16_t *__restrict__ slot_all,
+                                                                     uint32_t vstride,
+                                                                     const uint32_t *__restrict__ flags) {
     __shared__ T buf[SP_B];
     const uint32_t NB = (n + SP_B - 1) / SP_B;
     const int64_t total = num_arrays * (int64_t)NB;
     for (int64_t g = blockIdx.x; g < total; g += gridDim.x) {
         const int64_t a = g / NB;
+        if (flags[a]) continue;
         const uint32_t blo = (uint32_t)(g - a * NB) * SP_B;
         const uint32_t bn = min(SP_B, n - blo);
         const int64_t off = a * (int64_t)n + blo;
+        const int64_t voff = a * (int64_t)vstride + blo;
         constexpr int PER = SP_B / SPG_T;
         T v[PER];
         uint16_t sl[PER];
@@ -595,8 +655,8 @@ __global__ void __launch_bounds__(SPG_T) shuffle_stage_gather_kernel(T *__restri
         for (int k = 0; k < PER; ++k) {
             const uint32_t x = threadIdx.x + k * SPG_T;
             if (x < bn) {
-                v[k] = __ldcs(res + off + x);
-                sl[k] = __ldcs(slot + off + x);
+                v[k] = __ldcs(val_all + voff + x);
+                sl[k] = __ldcs(slot_all + voff + x);
             }
         }
 #pragma unroll
@@ -608,7 +668,7 @@ __global__ void __launch_bounds__(SPG_T) shuffle_stage_gather_kernel(T *__restri
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const uint32_t x = threadIdx.x + k * SPG_T;
-            if (x < bn) data[off + x] = buf[sl[k]];
+            if (x < bn) __stcs(data + off + x, buf[sl[k]]);
         }
         __syncthreads();
     }
