@@ -719,7 +719,9 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
         if args.config == "c2":
-            v, reps, dt = cpu_c2(cores, target_s=8.0)
+            # the same procedure as the reference arm (--impl reference): W warm-up and K timed
+            # full-config steps, so the two CPU numbers measure the same thing
+            v, reps, dt = cpu_c2(cores, steps=args.steps, warmup=args.warmup)
             line["cpu_baseline"] = {
                 "value": v, "unit": "rolls/s", "cores": cores, "kind": "port",
                 "sample": f"{reps} x the full C2 config ({NB_C2} batches on one continuing stream; the reference's "

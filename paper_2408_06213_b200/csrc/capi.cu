@@ -769,10 +769,11 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
         return BR_OK;
     }
     // many arrays beyond shared memory: the stage pipeline (stage_shuffle.cuh), one CTA per
-    // array, every random access in shared memory.  PCG64/Lehmer streams, full plans, n <= 2^20.
+    // array, every random access in shared memory.  PCG64/Lehmer streams, full plans, n <= 2^20
+    // (C5: 9.2 ms against 12.2 for the CTA-group kernel on the array in global memory).
     const bool sp_fit = segmented && gen != 2 && cp.plan.lo <= 1 && n > 1 && n <= (uint64_t)SP_MAXNB * SP_B &&
                         cp.plan.max_k <= 8;
-    if (sp_fit && forced_kernel() == K_STAGE) {
+    if (sp_fit && (forced_kernel() == K_STAGE || forced_kernel() == K_ANY)) {
         const size_t smem = sizeof(SpShared<T>);
         const void *kp = (const void *)shuffle_stage_kernel<T>;
         CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -350,7 +350,8 @@ DISPATCH = [  # (n, item bytes, arrays, kernel the default dispatch picks; DESIG
     (8192, 4, 1024, "shuffle_idx_kernel"),
     (12000, 4, 512, "shuffle_cta_hash_kernel"),
     (20000, 4, 256, "shuffle_cta_hash_kernel"),
-    (70000, 8, 8, "shuffle_cta_large_kernel"),
+    (70000, 8, 8, "shuffle_stage_kernel"),
+    (300001, 4, 4, "shuffle_stage_kernel"),
 ]
 
 
@@ -546,7 +547,7 @@ def test_c5_sample_vs_golden_and_oracle(B, O, golden):
     payload = O.pcg64_fill(O.pcg64(5), 0, n * na)  # C5 payload convention: words of pcg64(5)
     dev = torch.from_numpy(payload.view(np.int64).copy()).cuda()
     _, words = B.shuffle_many(dev, n, 5, return_words=True)
-    assert "shuffle_cta_large" in B.last_kernel()
+    assert "shuffle_stage_kernel" in B.last_kernel()
     got = dev.cpu().numpy().view(np.uint64)
     ref = payload.copy()
     rw = O.shuffle_segmented(ref, n, 5)

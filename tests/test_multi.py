@@ -113,3 +113,50 @@ def test_sharded_roll_stream_cascading_shifts(tmp_path, O):
     assert all(bool(p["rec"]) for p in parts[1:])
     assert np.array_equal(np.concatenate([p["rolls"] for p in parts]), rolls)
     assert np.array_equal(np.concatenate([p["words"] for p in parts]), words)
+
+
+# ------------------------------------------------------------- single-process sections (multi.py)
+def _oracle_sections(O, bounds, nb, S):
+    """resolve_sections driven by the oracle as the section roller (the GPU tests drive it with
+    the device kernels): the concatenated sections equal one sequential stream."""
+    from paper_2408_06213_b200 import multi, shard
+
+    state, inc = shard.seeded_state(O.array_seed(7, 1))
+    res = {}
+
+    def roll(r, shift):
+        first, count = shard.even_split(nb, S, r)
+        st, _ = shard.advanced_state(state, inc, first + shift)
+        rolls, words, _, _ = O.roll_batches(O.pcg64_from_state(st, inc), bounds[2 * first: 2 * (first + count)], 2)
+        res[r] = (rolls, words)
+        return int(words.astype(np.int64).sum()) - count
+
+    extras = [roll(r, 0) for r in range(S)]
+    shifts = multi.resolve_sections(extras, roll)
+    return res, shifts
+
+
+def test_resolve_sections_single_process(O):
+    nb = 6000
+    for S, cascade in ((2, False), (3, True), (5, True)):
+        bounds = _roll_bounds(nb, cascade)
+        res, shifts = _oracle_sections(O, bounds, nb, S)
+        rolls, words, _, _ = O.roll_batches(O.pcg64(O.array_seed(7, 1)), bounds, 2)
+        assert shifts[0] == 0 and shifts[1] > 0
+        assert np.array_equal(np.concatenate([res[r][0] for r in range(S)]), rolls)
+        assert np.array_equal(np.concatenate([res[r][1] for r in range(S)]), words)
+
+
+def test_resolve_sections_fixed_point_rounds():
+    """A re-roll that changes the section's own extras moves every later section again."""
+    from paper_2408_06213_b200 import multi
+
+    calls = []
+
+    def reroll(r, d):
+        calls.append((r, d))
+        return {1: 5, 2: 0, 3: 1}.get(r, 0) if d else 0
+
+    shifts = multi.resolve_sections([3, 0, 0, 0], reroll)
+    assert shifts == [0, 3, 8, 8]
+    assert (1, 3) in calls and (2, 8) in calls and (3, 8) in calls
