@@ -60,7 +60,6 @@ static constexpr uint32_t SP_B = 1u << SP_LOG_B;   // positions per block (one s
 static constexpr int SP_T = 512;                    // threads per CTA (two CTAs per SM)
 static constexpr int SP_W = SP_T / 32;
 static constexpr int SP_PER = SP_B / SP_T;          // positions per thread
-static constexpr uint32_t SP_C = 3456;              // inbox records per chunk
 static constexpr uint32_t SP_MAXNB = 256;           // blocks per array (n <= 2^20)
 static constexpr uint32_t SP_MAXCH = 128;           // chunks per stage
 static constexpr int SP_GJ = 4;                     // generator slots per thread
@@ -70,20 +69,28 @@ static constexpr uint32_t SP_NONE = 0xFFFFFFFFu;
 static constexpr uint16_t SP_NONE16 = 0xFFFF;
 static constexpr uint32_t SP_JNONE = 0xFFFFFu;      // ring: no step at this position
 
+// inbox records per chunk: key, value and bucket entry per record in the 48 KB union
+template <typename T>
+__host__ __device__ constexpr uint32_t sp_cap() {
+    return sizeof(T) == 8 ? 3072u : 4096u;
+}
+
 template <typename T>
 struct SpShared {
     T mbox[SP_B];            // the block: original values, then after the higher blocks' deposits
     uint32_t ring[SP_RING];  // J by position (B, C), then src << 20 | J (E)
-    uint16_t head[SP_B];     // per-target list heads (C: in-block steps, D: records), SP_NONE16 = empty
+    uint32_t xcnt[SP_B / 2]; // D: records per target offset (two u16 per word), then bucket starts
     union {
         struct {
+            uint32_t ft[SP_B];    // first later in-block step targeting x (atomicMin)
+            uint32_t head[SP_B];  // per-target lists of in-block steps
             uint16_t link[SP_B];
-            uint16_t F[SP_B];  // FT, then the end of the FT chain
+            uint16_t F[SP_B];     // the end of the FT chain
         } loc;
         struct {
-            uint32_t key[SP_C];
-            T val[SP_C];
-            uint16_t link[SP_C];
+            uint32_t key[sp_cap<T>()];
+            T val[sp_cap<T>()];
+            uint32_t bkt[sp_cap<T>()];  // records bucketed by target offset: s << 12 | chunk index
         } rec;
         struct {
             uint32_t key[SP_B];
@@ -136,17 +143,47 @@ __device__ __forceinline__ uint32_t sp_scan(uint32_t *a, uint32_t len, uint32_t 
     return total;
 }
 
-// 16-bit exchange in shared memory (list heads) through a CAS on the enclosing word
-__device__ __forceinline__ uint16_t sp_xchg16(uint16_t *p, uint16_t v) {
-    uint32_t *w = reinterpret_cast<uint32_t *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)3);
-    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 2) * 8;
-    uint32_t old = *w, assumed;
-    do {
-        assumed = old;
-        old = atomicCAS(w, assumed, (assumed & ~(0xFFFFu << sh)) | ((uint32_t)v << sh));
-    } while (old != assumed);
-    return (uint16_t)(old >> sh);
+// exclusive scan, in place, of the SP_B u16 counters packed two per word in xc (8 per thread)
+__device__ __forceinline__ void sp_scan_x(uint32_t *xc, uint32_t *wsum, int L) {
+    static_assert(SP_T * 8 == SP_B, "eight counters per thread");
+    const uint4 w = reinterpret_cast<const uint4 *>(xc)[L];
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    uint32_t tot = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tot += (wv[q] & 0xFFFFu) + (wv[q] >> 16);
+    uint32_t inc = tot;
+    const int lane = L & 31, wp = L >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) wsum[wp] = inc;
+    __syncthreads();
+    if (wp == 0) {
+        const uint32_t x = lane < SP_W ? wsum[lane] : 0;
+        uint32_t y = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, y, d);
+            if (lane >= d) y += o;
+        }
+        if (lane < SP_W) wsum[lane] = y - x;
+    }
+    __syncthreads();
+    uint32_t run = wsum[wp] + inc - tot;
+    uint32_t ov[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t lo = run;
+        run += wv[q] & 0xFFFFu;
+        ov[q] = lo | (run << 16);
+        run += wv[q] >> 16;
+    }
+    reinterpret_cast<uint4 *>(xc)[L] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+    __syncthreads();
 }
+
 
 __device__ __forceinline__ void sp_cp4(void *s, const void *g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(s)), "l"(g) : "memory");
@@ -282,7 +319,7 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
 // greedy chunks of whole tiles in inbox order, at most SP_C records each (warp 0).  A tile
 // larger than a chunk, or more chunks than SP_MAXCH, marks the array bad (re-run elsewhere).
 __device__ __forceinline__ void sp_chunk_plan(const uint32_t *excl, uint32_t ntile, uint16_t *cend, uint32_t &nchunk,
-                                              uint32_t &bad, int lane) {
+                                              uint32_t &bad, int lane, const uint32_t SP_C) {
     uint32_t fill = 0, nch = 0;
     bool ovf = false;
     for (uint32_t base = 0; base < ntile && !ovf; base += 32) {
@@ -350,7 +387,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
     uint32_t *desc = keyg + (((size_t)n * 4 + 255) & ~(size_t)255) / 4;
 
     for (uint32_t q = L; q < plan.nseg; q += SP_T) sh.segs[q] = plan.segs[q];
-    for (uint32_t x = L; x < SP_B; x += SP_T) sh.head[x] = SP_NONE16;
+    for (uint32_t x = L; x < SP_B / 2; x += SP_T) sh.xcnt[x] = 0;
     for (uint32_t x = L; x <= SP_MAXNB; x += SP_T) sh.cnt[x] = 0;
     if (L == 0) {
         sh.nint = 0;
@@ -394,74 +431,86 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             __syncthreads();
             if (L < 8) sh.carry[L] = sh.ring[L];
             if (phmax < 2) break;
-            // ---- C. this block's steps in closed form (indices only)
+            // ---- C. this block's steps in closed form (indices only).  Steps with an in-block
+            // target are rare above block 0 (about 2048/sg of the block's 4096), so the lists, the FT
+            // minima and the chain walks run only when there is one; otherwise every position is
+            // its own source.
+            int nin = 0;
 #pragma unroll
             for (int k = 0; k < SP_PER; ++k) {
                 const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                if (i < bn && blo + i >= slo) {
-                    const uint32_t J = sh.ring[i + 8];
-                    if (J >= blo && SP_OK(J <= blo + i, sg, i, J)) sh.u.loc.link[i] = sp_xchg16(&sh.head[J - blo], (uint16_t)i);
-                }
+                if (i < bn && blo + i >= slo && sh.ring[i + 8] >= blo) ++nin;
             }
-            __syncthreads();
-            uint32_t nsv[SP_PER / 2];  // NS of the thread's positions, two u16 per word
-#pragma unroll
-            for (int k = 0; k < SP_PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                uint32_t ns = SP_NONE16;
-                if (i < bn) {
-                    uint32_t ft = SP_NONE16;  // first in-block step after i targeting i
-                    for (uint32_t m = sh.head[i]; m != SP_NONE16 && SP_OK(m < bn, 4000 + sg, i, m); m = sh.u.loc.link[m])
-                        if (m > i && m < ft) ft = m;
-                    sh.u.loc.F[i] = (uint16_t)ft;
-                    if (blo + i >= slo) {
-                        const uint32_t J = sh.ring[i + 8];
-                        if (J >= blo && SP_OK(J <= blo + i, 1000 + sg, i, J))  // next in-block step after i with i's target
-                            for (uint32_t m = sh.head[J - blo]; m != SP_NONE16 && SP_OK(m < bn, 5000 + sg, i, m); m = sh.u.loc.link[m])
-                                if (m > i && m < ns) ns = m;
+            if (__syncthreads_or(nin)) {
+                {
+                    const uint4 none4 = make_uint4(SP_NONE, SP_NONE, SP_NONE, SP_NONE);
+                    uint4 *ft4 = reinterpret_cast<uint4 *>(sh.u.loc.ft), *hd4 = reinterpret_cast<uint4 *>(sh.u.loc.head);
+                    for (uint32_t q = L; q < SP_B / 4; q += SP_T) {
+                        ft4[q] = none4;
+                        hd4[q] = none4;
                     }
                 }
-                if (k & 1) nsv[k / 2] |= ns << 16;
-                else nsv[k / 2] = ns;
-            }
-            __syncthreads();
-            uint32_t fe[SP_PER / 2];  // ends of the FT chains
+                __syncthreads();
 #pragma unroll
-            for (int k = 0; k < SP_PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                uint32_t e = i;
-                if (i < bn)
-                    for (uint32_t f = sh.u.loc.F[e]; f != SP_NONE16 && SP_OK(f < bn && f > e, 8000 + sg, e, f); f = sh.u.loc.F[e]) e = f;
-                if (k & 1) fe[k / 2] |= e << 16;
-                else fe[k / 2] = e;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < SP_PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                if (i < bn) sh.u.loc.F[i] = (uint16_t)(fe[k / 2] >> (16 * (k & 1)));
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < SP_PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                if (i < bn) {
-                    uint32_t src, J;
-                    if (blo + i < slo) {  // no step: the position's final value
-                        src = sh.u.loc.F[i];
-                        J = SP_JNONE;
-                    } else {
-                        J = sh.ring[i + 8];
-                        if (!SP_OK(J <= blo + i, 2000 + sg, i, J)) J = blo + i;
-                        if (J >= blo) {
-                            const uint32_t ns = (nsv[k / 2] >> (16 * (k & 1))) & 0xFFFFu;
-                            src = ns != SP_NONE16 ? sh.u.loc.F[ns] : J - blo;
-                            sh.head[J - blo] = SP_NONE16;
-                        } else {
-                            src = sh.u.loc.F[i];  // Val(s): the value leaving position s
+                for (int k = 0; k < SP_PER; ++k) {
+                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                    if (i < bn && blo + i >= slo) {
+                        const uint32_t J = sh.ring[i + 8];
+                        if (J >= blo && SP_OK(J <= blo + i, sg, i, J)) {
+                            const uint32_t y = J - blo;
+                            if (i > y) atomicMin(&sh.u.loc.ft[y], i);
+                            sh.u.loc.link[i] = (uint16_t)atomicExch(&sh.u.loc.head[y], i);
                         }
                     }
-                    sh.ring[i + 8] = (src << 20) | J;
+                }
+                __syncthreads();
+                uint32_t nsv[SP_PER / 2];  // NS of the thread's in-block steps, two u16 per word
+#pragma unroll
+                for (int k = 0; k < SP_PER; ++k) {
+                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                    uint32_t ns = SP_NONE16;
+                    if (i < bn) {
+                        uint32_t e = i;  // the end of i's FT chain
+                        for (uint32_t f = sh.u.loc.ft[e]; f != SP_NONE && SP_OK(f < bn && f > e, 8000 + sg, e, f); f = sh.u.loc.ft[e]) e = f;
+                        sh.u.loc.F[i] = (uint16_t)e;
+                        if (blo + i >= slo) {
+                            const uint32_t J = sh.ring[i + 8];
+                            if (J >= blo)  // the next in-block step after i with i's target
+                                for (uint32_t m = sh.u.loc.head[J - blo]; m != SP_NONE16 && m != SP_NONE && SP_OK(m < bn, 5000 + sg, i, m);
+                                     m = sh.u.loc.link[m])
+                                    if (m > i && m < ns) ns = m;
+                        }
+                    }
+                    if (k & 1) nsv[k / 2] |= ns << 16;
+                    else nsv[k / 2] = ns;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < SP_PER; ++k) {
+                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                    if (i < bn) {
+                        uint32_t src, J;
+                        if (blo + i < slo) {  // no step: the position's final value
+                            src = sh.u.loc.F[i];
+                            J = SP_JNONE;
+                        } else {
+                            J = sh.ring[i + 8];
+                            if (!SP_OK(J <= blo + i, 2000 + sg, i, J)) J = blo + i;
+                            if (J >= blo) {
+                                const uint32_t ns = (nsv[k / 2] >> (16 * (k & 1))) & 0xFFFFu;
+                                src = ns != SP_NONE16 ? sh.u.loc.F[ns] : J - blo;
+                            } else {
+                                src = sh.u.loc.F[i];  // Val(s): the value leaving position s
+                            }
+                        }
+                        sh.ring[i + 8] = (src << 20) | J;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < SP_PER; ++k) {
+                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+                    if (i < bn) sh.ring[i + 8] = (i << 20) | (blo + i < slo ? SP_JNONE : sh.ring[i + 8]);
                 }
             }
             if (phmax < 3) break;
@@ -475,7 +524,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             }
             if (L == 0) sh.excl[ntile] = R;
             __syncthreads();
-            if (wid == 0) sp_chunk_plan(sh.excl, ntile, sh.cend, sh.nchunk, sh.bad, lane);
+            if (wid == 0) sp_chunk_plan(sh.excl, ntile, sh.cend, sh.nchunk, sh.bad, lane, sp_cap<T>());
             if (use_tma) {
                 mbar_wait(&sh.bar, parity);
                 parity ^= 1u;
@@ -487,7 +536,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 const uint32_t tb = sh.cend[ch];
                 const uint32_t cbase = sh.excl[ta];
                 uint32_t ccount = sh.excl[tb] - cbase;
-                if (!SP_OK(ccount <= SP_C && tb <= ntile && tb >= ta, 9000 + sg, (ch << 16) | (ta << 8) | tb, ccount)) {
+                if (!SP_OK(ccount <= sp_cap<T>() && tb <= ntile && tb >= ta, 9000 + sg, (ch << 16) | (ta << 8) | tb, ccount)) {
                     ccount = 0;
                     ta = tb;
                     continue;
@@ -496,7 +545,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                     const uint32_t src = NB - 1 - t;
                     const uint32_t c0 = sh.excl[t], cn = sh.excl[t + 1] - c0;
                     const uint32_t g0 = sh.toff[src] + c0;
-                    if (!SP_OK(g0 + cn <= (src + 1) * SP_B && g0 >= src * SP_B && c0 - cbase + cn <= SP_C, sg, t, g0)) continue;
+                    if (!SP_OK(g0 + cn <= (src + 1) * SP_B && g0 >= src * SP_B && c0 - cbase + cn <= sp_cap<T>(), sg, t, g0)) continue;
                     for (uint32_t q = lane; q < cn; q += 32) {
                         sp_cp4(&sh.u.rec.key[c0 - cbase + q], keyg + g0 + q);
                         if (sizeof(T) == 8) sp_cp8(&sh.u.rec.val[c0 - cbase + q], valg + g0 + q);
@@ -506,38 +555,67 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 sp_cp_wait();
                 __syncthreads();
                 if (phmax < 5) { ta = tb; continue; }
-                for (uint32_t r = L; r < ccount; r += SP_T) {
-                    const uint32_t x = sh.u.rec.key[r] & (SP_B - 1);
-                    sh.u.rec.link[r] = sp_xchg16(&sh.head[x], (uint16_t)r);
+                // records bucketed by target offset x (counting sort), then each record finds its
+                // predecessor at x (the least later-in-order step s' > s) by scanning its bucket
+                constexpr uint32_t RPT = (sp_cap<T>() + SP_T - 1) / SP_T;
+                uint32_t arr[(RPT + 1) / 2];  // arrival index of each record within its bucket
+#pragma unroll
+                for (uint32_t j = 0; j < RPT; ++j) {
+                    const uint32_t r = (uint32_t)L + j * SP_T;
+                    uint32_t av = 0;
+                    if (r < ccount) {
+                        const uint32_t x = sh.u.rec.key[r] & (SP_B - 1), hs = (x & 1) * 16;
+                        av = (atomicAdd(&sh.xcnt[x >> 1], 1u << hs) >> hs) & 0xFFFFu;
+                    }
+                    if (j & 1) arr[j / 2] |= av << 16;
+                    else arr[j / 2] = av;
+                }
+                __syncthreads();
+                sp_scan_x(sh.xcnt, sh.wsum, L);
+#pragma unroll
+                for (uint32_t j = 0; j < RPT; ++j) {
+                    const uint32_t r = (uint32_t)L + j * SP_T;
+                    if (r < ccount) {
+                        const uint32_t K = sh.u.rec.key[r];
+                        const uint32_t x = K & (SP_B - 1);
+                        const uint32_t st = (sh.xcnt[x >> 1] >> ((x & 1) * 16)) & 0xFFFFu;
+                        sh.u.rec.bkt[st + ((arr[j / 2] >> (16 * (j & 1))) & 0xFFFFu)] = (K & ~(SP_B - 1)) | r;
+                    }
                 }
                 __syncthreads();
                 if (phmax < 6) { ta = tb; continue; }
                 uint32_t lastm = 0;
-                for (uint32_t r = L, j = 0; r < ccount; r += SP_T, ++j) {
-                    const uint32_t K = sh.u.rec.key[r];
-                    const uint32_t s = K >> SP_LOG_B, x = K & (SP_B - 1);
-                    uint32_t bs = SP_NONE, best = SP_NONE16;
-                    bool last = true;
-                    for (uint32_t m = sh.head[x]; m != SP_NONE16 && SP_OK(m < ccount, 6000 + sg, r, m); m = sh.u.rec.link[m]) {
-                        const uint32_t sm = sh.u.rec.key[m] >> SP_LOG_B;
-                        if (sm > s && sm < bs) {
-                            bs = sm;
-                            best = m;
+#pragma unroll
+                for (uint32_t j = 0; j < RPT; ++j) {
+                    const uint32_t r = (uint32_t)L + j * SP_T;
+                    if (r < ccount) {
+                        const uint32_t K = sh.u.rec.key[r];
+                        const uint32_t s = K >> SP_LOG_B, x = K & (SP_B - 1);
+                        const uint32_t sw = sh.xcnt[x >> 1];
+                        const uint32_t st = (sw >> ((x & 1) * 16)) & 0xFFFFu;
+                        const uint32_t en = (x & 1) ? (x == SP_B - 1 ? ccount : sh.xcnt[(x >> 1) + 1] & 0xFFFFu) : sw >> 16;
+                        const uint32_t hiK = K | (SP_B - 1), loK = K & ~(SP_B - 1);
+                        uint32_t best = SP_NONE;
+                        bool last = true;
+                        for (uint32_t q = st; q < en; ++q) {
+                            const uint32_t e = sh.u.rec.bkt[q];
+                            if (e > hiK && e < best) best = e;
+                            last &= !(e < loK);
                         }
-                        last &= !(sm < s);
+                        const T res = best != SP_NONE ? sh.u.rec.val[best & (SP_B - 1)] : sh.mbox[x];
+                        const uint32_t gi = sh.toff[s >> SP_LOG_B] + cbase + r;  // (u32: toff may wrap)
+                        if (SP_OK(s < n && (s >> SP_LOG_B) > (uint32_t)sg && gi < n, sg, r, K)) __stcg(valg + gi, res);
+                        if (last) lastm |= 1u << j;
                     }
-                    const T res = best != SP_NONE16 ? sh.u.rec.val[best] : sh.mbox[x];
-                    const uint32_t gi = sh.toff[s >> SP_LOG_B] + cbase + r;  // (u32: toff may wrap)
-                    if (SP_OK(s < n && (s >> SP_LOG_B) > (uint32_t)sg && gi < n, sg, r, K)) __stcg(valg + gi, res);
-                    if (last) lastm |= 1u << j;
                 }
                 __syncthreads();
                 if (phmax < 7) { ta = tb; continue; }
-                for (uint32_t r = L, j = 0; r < ccount; r += SP_T, ++j) {
-                    const uint32_t x = sh.u.rec.key[r] & (SP_B - 1);
-                    if ((lastm >> j) & 1) sh.mbox[x] = sh.u.rec.val[r];
-                    sh.head[x] = SP_NONE16;
+#pragma unroll
+                for (uint32_t j = 0; j < RPT; ++j) {
+                    const uint32_t r = (uint32_t)L + j * SP_T;
+                    if ((lastm >> j) & 1) sh.mbox[sh.u.rec.key[r] & (SP_B - 1)] = sh.u.rec.val[r];
                 }
+                reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);
                 __syncthreads();
                 ta = tb;
             }
