@@ -68,6 +68,7 @@ static constexpr uint32_t SP_RING = SP_B + 8;       // targets by position - blo
 static constexpr uint32_t SP_NONE = 0xFFFFFFFFu;
 static constexpr uint16_t SP_NONE16 = 0xFFFF;
 static constexpr uint32_t SP_JNONE = 0xFFFFFu;      // ring: no step at this position
+static constexpr uint32_t SP_TGT = 0x80000000u;     // ring flag (C): the position is an in-block step's target
 
 // inbox records per chunk: key, value and bucket entry per record in the 48 KB union
 template <typename T>
@@ -193,6 +194,12 @@ __device__ __forceinline__ void sp_cp8(void *s, const void *g) {
 }
 __device__ __forceinline__ void sp_cp_wait() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// the end of the FT chain from e (C): FT values are later in-block steps, so the walk ends
+__device__ __forceinline__ uint32_t sp_chase(const uint32_t *ft, uint32_t e) {
+    for (uint32_t f = ft[e]; f != SP_NONE; f = ft[e]) e = f;
+    return e;
 }
 
 // ---- target generation: striped slots.  Slot (thread L, j) owns the batches b == L + SP_T*j
@@ -385,6 +392,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
     const bool lh = gen == 1;
     uint32_t *keyg = reinterpret_cast<uint32_t *>(cta_scratch + (size_t)blockIdx.x * cta_bytes);
     uint32_t *desc = keyg + (((size_t)n * 4 + 255) & ~(size_t)255) / 4;
+    uint16_t *src16 = reinterpret_cast<uint16_t *>(sh.xcnt);  // C -> E (D is done): each position's source slot
 
     for (uint32_t q = L; q < plan.nseg; q += SP_T) sh.segs[q] = plan.segs[q];
     for (uint32_t x = L; x < SP_B / 2; x += SP_T) sh.xcnt[x] = 0;
@@ -404,12 +412,6 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
         sp_gen_init<T>(g, sh, array_seed(run_seed, (uint64_t)(base + a)), lh, L);
         __syncthreads();
         for (int sg = (int)NB - 1; sg >= 0; --sg) {
-#ifdef SP_CHECK
-            if (sg < g_sp_stop) break;
-            const int phmax = sg == g_sp_stop ? g_sp_phase : 99;
-#else
-            constexpr int phmax = 99;
-#endif
             const uint32_t blo = (uint32_t)sg * SP_B;
             const uint32_t bn = min(SP_B, n - blo);
             const uint32_t slo = max(blo, lo);  // positions below slo have no step
@@ -426,94 +428,11 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             }
             const uint32_t dreg = (uint32_t)L < ntile ? __ldcg(desc + (size_t)sg * NB + (NB - 1 - L)) : 0;
             if (L < 8) sh.ring[SP_B + L] = sh.carry[L];
+            if (blo + (uint32_t)L < slo) sh.ring[L + 8] = SP_JNONE;  // no step (block 0 below plan.lo)
             // ---- B. targets of this block's steps
             if (slo < blo + bn) sp_gen_block<T>(g, plan, sh, L, sp_batch_of(sh.segs, plan.nseg, slo), blo, lh);
             __syncthreads();
             if (L < 8) sh.carry[L] = sh.ring[L];
-            if (phmax < 2) break;
-            // ---- C. this block's steps in closed form (indices only).  Steps with an in-block
-            // target are rare above block 0 (about 2048/sg of the block's 4096), so the lists, the FT
-            // minima and the chain walks run only when there is one; otherwise every position is
-            // its own source.
-            int nin = 0;
-#pragma unroll
-            for (int k = 0; k < SP_PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                if (i < bn && blo + i >= slo && sh.ring[i + 8] >= blo) ++nin;
-            }
-            if (__syncthreads_or(nin)) {
-                {
-                    const uint4 none4 = make_uint4(SP_NONE, SP_NONE, SP_NONE, SP_NONE);
-                    uint4 *ft4 = reinterpret_cast<uint4 *>(sh.u.loc.ft), *hd4 = reinterpret_cast<uint4 *>(sh.u.loc.head);
-                    for (uint32_t q = L; q < SP_B / 4; q += SP_T) {
-                        ft4[q] = none4;
-                        hd4[q] = none4;
-                    }
-                }
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < SP_PER; ++k) {
-                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                    if (i < bn && blo + i >= slo) {
-                        const uint32_t J = sh.ring[i + 8];
-                        if (J >= blo && SP_OK(J <= blo + i, sg, i, J)) {
-                            const uint32_t y = J - blo;
-                            if (i > y) atomicMin(&sh.u.loc.ft[y], i);
-                            sh.u.loc.link[i] = (uint16_t)atomicExch(&sh.u.loc.head[y], i);
-                        }
-                    }
-                }
-                __syncthreads();
-                uint32_t nsv[SP_PER / 2];  // NS of the thread's in-block steps, two u16 per word
-#pragma unroll
-                for (int k = 0; k < SP_PER; ++k) {
-                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                    uint32_t ns = SP_NONE16;
-                    if (i < bn) {
-                        uint32_t e = i;  // the end of i's FT chain
-                        for (uint32_t f = sh.u.loc.ft[e]; f != SP_NONE && SP_OK(f < bn && f > e, 8000 + sg, e, f); f = sh.u.loc.ft[e]) e = f;
-                        sh.u.loc.F[i] = (uint16_t)e;
-                        if (blo + i >= slo) {
-                            const uint32_t J = sh.ring[i + 8];
-                            if (J >= blo)  // the next in-block step after i with i's target
-                                for (uint32_t m = sh.u.loc.head[J - blo]; m != SP_NONE16 && m != SP_NONE && SP_OK(m < bn, 5000 + sg, i, m);
-                                     m = sh.u.loc.link[m])
-                                    if (m > i && m < ns) ns = m;
-                        }
-                    }
-                    if (k & 1) nsv[k / 2] |= ns << 16;
-                    else nsv[k / 2] = ns;
-                }
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < SP_PER; ++k) {
-                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                    if (i < bn) {
-                        uint32_t src, J;
-                        if (blo + i < slo) {  // no step: the position's final value
-                            src = sh.u.loc.F[i];
-                            J = SP_JNONE;
-                        } else {
-                            J = sh.ring[i + 8];
-                            if (!SP_OK(J <= blo + i, 2000 + sg, i, J)) J = blo + i;
-                            if (J >= blo) {
-                                const uint32_t ns = (nsv[k / 2] >> (16 * (k & 1))) & 0xFFFFu;
-                                src = ns != SP_NONE16 ? sh.u.loc.F[ns] : J - blo;
-                            } else {
-                                src = sh.u.loc.F[i];  // Val(s): the value leaving position s
-                            }
-                        }
-                        sh.ring[i + 8] = (src << 20) | J;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < SP_PER; ++k) {
-                    const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
-                    if (i < bn) sh.ring[i + 8] = (i << 20) | (blo + i < slo ? SP_JNONE : sh.ring[i + 8]);
-                }
-            }
-            if (phmax < 3) break;
             // ---- D. the higher blocks' deposits, in time order
             if ((uint32_t)L < ntile) sh.excl[L] = dreg & 0xFFFFu;
             __syncthreads();
@@ -530,7 +449,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 parity ^= 1u;
             }
             __syncthreads();
-            const uint32_t nch = phmax < 4 ? 0 : sh.nchunk;
+            const uint32_t nch = sh.nchunk;
             uint32_t ta = 0;
             for (uint32_t ch = 0; ch < nch; ++ch) {
                 const uint32_t tb = sh.cend[ch];
@@ -554,7 +473,6 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 }
                 sp_cp_wait();
                 __syncthreads();
-                if (phmax < 5) { ta = tb; continue; }
                 // records bucketed by target offset x (counting sort), then each record finds its
                 // predecessor at x (the least later-in-order step s' > s) by scanning its bucket
                 constexpr uint32_t RPT = (sp_cap<T>() + SP_T - 1) / SP_T;
@@ -583,7 +501,6 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                     }
                 }
                 __syncthreads();
-                if (phmax < 6) { ta = tb; continue; }
                 uint32_t lastm = 0;
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
@@ -609,7 +526,6 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                     }
                 }
                 __syncthreads();
-                if (phmax < 7) { ta = tb; continue; }
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
                     const uint32_t r = (uint32_t)L + j * SP_T;
@@ -619,17 +535,73 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 __syncthreads();
                 ta = tb;
             }
-            if (phmax < 8) break;
+            // ---- C. this block's own steps in closed form (indices only).  Steps with an
+            // in-block target are rare above block 0 (about 2048/sg of the block's 4096), so only
+            // the entries they touch are initialised: FT minima and lists at their targets and at
+            // themselves, and a flag on every targeted position (ring bit 31).  A position that no
+            // in-block step targets, and that has none itself, is its own source.
+            uint32_t nin = 0;
+#pragma unroll
+            for (int q = 0; q < SP_PER; ++q) {
+                const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
+                if (i < bn) {
+                    const uint32_t J = sh.ring[i + 8] & ~SP_TGT;
+                    if (J >= blo && J != SP_JNONE) {
+                        const uint32_t y = J - blo;
+                        sh.u.loc.ft[y] = SP_NONE;
+                        sh.u.loc.head[y] = SP_NONE;
+                        sh.u.loc.ft[i] = SP_NONE;
+                        atomicOr(&sh.ring[y + 8], SP_TGT);
+                        ++nin;
+                    }
+                }
+            }
+            const bool inblk = __syncthreads_or(nin) != 0;
+            if (inblk) {
+#pragma unroll
+                for (int q = 0; q < SP_PER; ++q) {
+                    const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
+                    if (i < bn) {
+                        const uint32_t J = sh.ring[i + 8] & ~SP_TGT;
+                        if (J >= blo && J != SP_JNONE) {
+                            const uint32_t y = J - blo;
+                            if (i > y) atomicMin(&sh.u.loc.ft[y], i);
+                            sh.u.loc.link[i] = (uint16_t)atomicExch(&sh.u.loc.head[y], i);
+                        }
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < SP_PER; ++q) {
+                    const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
+                    if (i < bn) {
+                        const uint32_t w = sh.ring[i + 8];
+                        const uint32_t J = w & ~SP_TGT;
+                        uint32_t src = i;
+                        if (J >= blo && J != SP_JNONE) {  // in-block output: the next step with i's target
+                            uint32_t ns = SP_NONE;
+                            for (uint32_t m = sh.u.loc.head[J - blo]; m != SP_NONE && m != SP_NONE16; m = sh.u.loc.link[m])
+                                if (m > i && m < ns) ns = m;
+                            if (ns != SP_NONE) src = sp_chase(sh.u.loc.ft, ns);
+                            else src = J - blo;
+                        } else if (w & SP_TGT) {  // the value leaving position i (or its final value)
+                            src = sp_chase(sh.u.loc.ft, i);
+                        }
+                        src16[i] = (uint16_t)src;
+                    }
+                }
+            }
+            __syncthreads();
             // ---- E. this block's records (by target block), in-block outputs, slot map
             uint32_t rk[SP_PER / 2];
 #pragma unroll
-            for (int k = 0; k < SP_PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+            for (int q = 0; q < SP_PER; ++q) {
+                const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
                 uint32_t rank = 0;
                 bool inb = true;
                 if (i < bn) {
-                    const uint32_t J = sh.ring[i + 8] & SP_JNONE;
-                    if (J < blo && SP_OK((J >> SP_LOG_B) < (uint32_t)sg, 7000 + sg, i, J)) {
+                    const uint32_t J = sh.ring[i + 8] & ~SP_TGT;
+                    if (J < blo) {
                         rank = atomicAdd(&sh.cnt[J >> SP_LOG_B], 1u);
                         inb = false;
                     }
@@ -639,28 +611,28 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 if (lane == 0 && m) b0 = atomicAdd(&sh.nint, (uint32_t)__popc(m));
                 b0 = __shfl_sync(0xFFFFFFFFu, b0, 0);
                 if (i < bn && inb) rank = b0 + __popc(m & ((1u << lane) - 1));
-                if (k & 1) rk[k / 2] |= rank << 16;
-                else rk[k / 2] = rank;
+                if (q & 1) rk[q / 2] |= rank << 16;
+                else rk[q / 2] = rank;
             }
             __syncthreads();
             const uint32_t nrec = sp_scan(sh.cnt, (uint32_t)sg, sh.wsum, L);
             if (L == 0) sh.cnt[sg] = nrec;
             __syncthreads();
 #pragma unroll
-            for (int k = 0; k < SP_PER; ++k) {
-                const uint32_t i = (uint32_t)L + (uint32_t)k * SP_T;
+            for (int q = 0; q < SP_PER; ++q) {
+                const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
                 if (i < bn) {
-                    const uint32_t e = sh.ring[i + 8];
-                    const uint32_t J = e & SP_JNONE, src = e >> 20;
-                    const uint32_t rank = (rk[k / 2] >> (16 * (k & 1))) & 0xFFFFu;
+                    const uint32_t J = sh.ring[i + 8] & ~SP_TGT;
+                    const uint32_t src = inblk ? src16[i] : i;
+                    const uint32_t rank = (rk[q / 2] >> (16 * (q & 1))) & 0xFFFFu;
                     uint32_t slot;
                     if (J < blo) {
                         slot = sh.cnt[J >> SP_LOG_B] + rank;
-                        if (SP_OK(slot < bn, sg, i, slot)) sh.u.out.key[slot] = (J & (SP_B - 1)) | ((blo + i) << SP_LOG_B);
+                        sh.u.out.key[slot] = (J & (SP_B - 1)) | ((blo + i) << SP_LOG_B);
                     } else {
                         slot = nrec + rank;
                     }
-                    if (SP_OK(slot < bn && src < SP_B, sg, slot, e)) sh.u.out.val[slot] = sh.mbox[src];
+                    sh.u.out.val[slot] = sh.mbox[src];
                     slotg[blo + i] = (uint16_t)slot;
                 }
             }
@@ -682,6 +654,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             }
             for (uint32_t tb = L; tb <= (uint32_t)sg; tb += SP_T) sh.cnt[tb] = 0;
             if (L == 0) sh.nint = 0;
+            reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);  // src16 -> the next stage's counters
             __syncthreads();
         }
         if (L == 0) {
