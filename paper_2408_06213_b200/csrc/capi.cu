@@ -628,6 +628,15 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
     const uint32_t stride = (uint32_t)(n | 1u);
     const int tpb = 64;  // 2 warps: many small blocks per SM overlap their load/compute/store phases
     const size_t small_smem = (size_t)tpb * stride * sizeof(T);
+    // n <= 64: u8 index permutations in a transposed (conflict-free) layout, payload applied per warp
+    if (allow(K_SMALL) && segmented && cp.plan.max_k <= 8 && n <= 64 && !getenv("BR_SMALL_ROWS")) {
+        auto kern = gen == 2 ? shuffle_small_idx_kernel<T, true> : shuffle_small_idx_kernel<T, false>;
+        const int64_t blocks = (num_arrays + SMI_T - 1) / SMI_T;
+        kern<<<(unsigned)blocks, SMI_T, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, gen);
+        CK(cudaGetLastError());
+        g_kernel = std::string("shuffle_small_idx_kernel<u") + std::to_string(8 * sizeof(T)) + ">";
+        return BR_OK;
+    }
     if (allow(K_SMALL) && segmented && cp.plan.max_k <= 8 && small_smem <= SMALL_SMEM_MAX / 2) {
         auto kern = gen == 2 ? shuffle_small_kernel<T, true> : shuffle_small_kernel<T, false>;
         CK(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));

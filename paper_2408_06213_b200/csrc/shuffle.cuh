@@ -226,6 +226,155 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
     small_copy<T>(buf, g, (uint32_t)tcount * n, n, stride, t0, magic, lane, false, vec_ok != 0);
 }
 
+// One thread per array on a u8 INDEX permutation (n <= 64).  Each thread shuffles the
+// identity 0..n-1 as bytes, the same dice and swaps as shuffle_small_kernel, in a TRANSPOSED
+// layout: byte j of lane l sits in word (j/4)*32 + l, i.e. every lane owns one bank, so the
+// random swaps are conflict-free (the row layout measured ~3.5-way conflicts, the bound of
+// shuffle_small_kernel).  The warp then turns its 32 permutations into rows (odd stride) and
+// applies them to the payload one array at a time: lane l loads items l and l+32 (coalesced),
+// fetches item row[p] from its owner lane with shuffles, and stores positions l and l+32.
+// The payload never enters shared memory.
+static constexpr int SMI_T = 256;
+static constexpr int SMI_WW = 32 * 17;  // words per warp: 16 transposed words x 32 lanes, or 32 rows of 17
+
+__device__ __forceinline__ uint32_t smi_pos(uint32_t j) { return ((j & ~3u) << 5) | (j & 3u); }
+
+template <typename T>
+__device__ __forceinline__ T smi_shfl(T v, int src) {
+    if constexpr (sizeof(T) == 8) {
+        const uint64_t x = (uint64_t)v;
+        const uint32_t lo = __shfl_sync(0xFFFFFFFFu, (uint32_t)x, src), hi = __shfl_sync(0xFFFFFFFFu, (uint32_t)(x >> 32), src);
+        return (T)(((uint64_t)hi << 32) | lo);
+    } else {
+        return (T)__shfl_sync(0xFFFFFFFFu, (uint32_t)v, src);
+    }
+}
+
+template <int K, bool CHA>
+__device__ __forceinline__ void smi_segment(uint8_t *zt, uint32_t nb, uint32_t count, const uint64_t *thresh, u128 &s,
+                                            u128 inc, uint32_t &words, bool lh, const ChaKey &ck, ChaCursor &cur,
+                                            bool naive) {
+    for (uint32_t c = 0; c < count; ++c, nb -= K) {
+        const uint64_t t = __ldg(thresh + c);
+        uint32_t d[K];
+        uint64_t r;
+        do {
+            if constexpr (CHA) {
+                s = cha_add(s, 1);
+                r = cha_out_cached(ck, cur, s);
+            } else {
+                s = mad128_wide(s, gen_mult(lh), inc);  // 17 SASS instead of mad128's 25
+                r = gen_out(s, lh);
+            }
+            ++words;
+            if (K == 2 && naive) {
+                naive_pair(nb, r, d[0], d[K - 1]);
+            } else {
+#pragma unroll
+                for (int m = 0; m < K; ++m) d[m] = die(nb - m, r);
+            }
+        } while (r < t);  // reject: re-draw the whole batch (shuffle.py:121-128)
+#pragma unroll
+        for (int m = 0; m < K; ++m) {
+            uint8_t *pi = zt + smi_pos(nb - 1 - m), *pj = zt + (d[m] + (d[m] & ~3u) * 31u);
+            const uint8_t x = *pi, y = *pj;
+            *pi = y;
+            *pj = x;
+        }
+    }
+}
+
+template <bool CHA>
+__device__ __forceinline__ void smi_segment_any(uint8_t *zt, uint32_t k, uint32_t nb, uint32_t count,
+                                                const uint64_t *thresh, u128 &s, u128 inc, uint32_t &words, bool lh,
+                                                const ChaKey &ck, ChaCursor &cur, bool naive) {
+    switch (k) {
+        case 1: smi_segment<1, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 2: smi_segment<2, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 3: smi_segment<3, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 4: smi_segment<4, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 5: smi_segment<5, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 6: smi_segment<6, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        case 7: smi_segment<7, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+        default: smi_segment<8, CHA>(zt, nb, count, thresh, s, inc, words, lh, ck, cur, naive); break;
+    }
+}
+
+template <typename T, bool CHA>
+__global__ void __launch_bounds__(SMI_T, 4) shuffle_small_idx_kernel(T *__restrict__ data, int64_t num_arrays,
+                                                                 DevPlan plan, uint64_t run_seed, int64_t base,
+                                                                 uint32_t *__restrict__ words_out, int gen) {
+    __shared__ __align__(16) uint32_t wr[SMI_T / 32][SMI_WW];
+    __shared__ DevSeg segs[MAX_SEGS];
+    const uint32_t n = plan.n;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t *W = wr[wid];
+    const int64_t a = (int64_t)blockIdx.x * SMI_T + tid;
+    if (tid < (int)plan.nseg) segs[tid] = plan.segs[tid];
+#pragma unroll
+    for (int w = 0; w < 16; ++w) W[w * 32 + lane] = 0x03020100u + 0x04040404u * (uint32_t)w;
+    __syncthreads();
+    if (a < num_arrays) {
+        u128 s, inc;
+        const bool lh = gen == 1;
+        ChaKey ck;
+        ChaCursor cur;
+        cur.valid = false;
+        const uint64_t seed = array_seed(run_seed, (uint64_t)(base + a));
+        if constexpr (CHA) {
+            chacha_seed(seed, ck);
+            s = mk128(0, 0);
+            inc = mk128(ck.nonce, CHACHA_TAG);
+        } else {
+            gen_seed(seed, s, inc, lh);
+        }
+        uint8_t *zt = reinterpret_cast<uint8_t *>(W) + lane * 4;
+        uint32_t words = 0;
+        for (uint32_t sg = 0; sg < plan.nseg; ++sg) {
+            const DevSeg S = segs[sg];
+            smi_segment_any<CHA>(zt, S.k, S.start_n, S.count, plan.thresh + S.first_batch, s, inc, words, lh, ck, cur,
+                                 plan.naive != 0);
+        }
+        if (words_out) words_out[a] = words;
+    }
+    __syncwarp();
+    {  // transposed -> rows: lane l's permutation at W[17 l ..]
+        uint32_t mine[16];
+#pragma unroll
+        for (int w = 0; w < 16; ++w) mine[w] = W[w * 32 + lane];
+        __syncwarp();
+#pragma unroll
+        for (int w = 0; w < 16; ++w) W[17 * lane + w] = mine[w];
+        __syncwarp();
+    }
+    const int64_t aw = (int64_t)blockIdx.x * SMI_T + wid * 32;
+    const int cnt = (int)min((int64_t)32, num_arrays - aw);
+    const uint32_t l0 = (uint32_t)lane, l1 = (uint32_t)lane + 32;
+    constexpr int U = 8;
+    for (int t0 = 0; t0 < cnt; t0 += U) {
+        T v0[U], v1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const T *g = data + (aw + t0 + u) * (int64_t)n;
+            const bool ok = t0 + u < cnt;
+            v0[u] = ok && l0 < n ? g[l0] : T(0);
+            v1[u] = ok && l1 < n ? g[l1] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint8_t *row = reinterpret_cast<const uint8_t *>(W + 17 * (t0 + u));
+            const uint32_t x0 = row[l0], x1 = row[l1];  // (bytes past n are never used)
+            const T a0 = smi_shfl(v0[u], (int)(x0 & 31)), b0 = smi_shfl(v1[u], (int)(x0 & 31));
+            const T a1 = smi_shfl(v0[u], (int)(x1 & 31)), b1 = smi_shfl(v1[u], (int)(x1 & 31));
+            if (t0 + u < cnt) {
+                T *g = data + (aw + t0 + u) * (int64_t)n;
+                if (l0 < n) g[l0] = (x0 & 32) ? b0 : a0;
+                if (l1 < n) g[l1] = (x1 & 32) ? b1 : a1;
+            }
+        }
+    }
+}
+
 // -------------------------------------------------------------------------------------
 // one warp per array
 // -------------------------------------------------------------------------------------

@@ -262,7 +262,7 @@ def test_c3_every_array(B, O, golden, golden_arrays):
     n, na = 64, 1 << 20
     data = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
     _, words = B.shuffle_many(data, n, 1234, return_words=True)
-    assert "shuffle_small_kernel" in B.last_kernel()
+    assert "shuffle_small" in B.last_kernel()
     got = u32(data)
     ref = np.tile(np.arange(n, dtype=np.uint32), na)
     ref_words = O.shuffle_segmented(ref, n, 1234)
@@ -293,7 +293,7 @@ def test_c4_sample(B, O, golden):
 
 
 KERNEL_CASES = {  # forced kernel -> (name in last_kernel, lengths it can take)
-    "small": ("shuffle_small_kernel", (2, 5, 64, 100)),
+    "small": ("shuffle_small", (2, 5, 33, 64, 100)),
     "resolve": ("shuffle_resolve_kernel", (2, 3, 64, 100, 1000, 4096, 4097, 10000)),
     "hash": ("shuffle_cta_hash_kernel", (2, 64, 1000, 4096, 10000, 20000)),
     "mid": ("shuffle_mid_kernel", (2, 64, 1000, 4096, 10000)),
@@ -342,7 +342,7 @@ def test_every_shuffle_kernel(B, O, monkeypatch, kernel, gen):
 
 
 DISPATCH = [  # (n, item bytes, arrays, kernel the default dispatch picks)
-    (64, 4, 2048, "shuffle_small_kernel"),
+    (64, 4, 2048, "shuffle_small_idx_kernel"),
     (1000, 4, 2048, "shuffle_warp_kernel"),
     (2048, 4, 2048, "shuffle_warp_kernel"),
     (4096, 4, 4096, "shuffle_idx_kernel"),
