@@ -613,7 +613,7 @@ int forced_kernel() {
 int idx_stages() {
     const char *e = getenv("BR_IDX_STAGES");
     const int v = e ? atoi(e) : 2;
-    return v < 1 ? 1 : (v > 8 ? 8 : v);
+    return v >= 8 ? 8 : (v >= 4 ? 4 : (v >= 2 ? 2 : 1));  // a power of two: ticket slots are tk % 32
 }
 
 inline bool allow(int k) {

@@ -20,9 +20,6 @@
 
 namespace br {
 
-#ifndef BR_IDX_SLEEP
-#define BR_IDX_SLEEP 256  // ns a warp sleeps after finding every staging buffer taken
-#endif
 // 256 entries hold the current and next group and one generation step for k <= 6 (the
 // default schedule); with the 1 KB target table that keeps 12 arrays of 16 KB per SM
 static constexpr uint32_t WRING = 256;
@@ -357,16 +354,18 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
         // finish the word accounting (a trailing rejection can follow the last position)
         while (gs.B0 < plan.nbatches) warp_gen_step<CHA, WRING>(gs, plan, ring, lane, rkf, chawin, ck);
         if constexpr (IDX) {
-            // take a free staging buffer, copy the payload in, write out[p] = payload[idx[p]]
+            // take a staging buffer in ticket order (FIFO hand-off): ticket t uses buffer
+            // t % nstage; the holder of ticket t - nstage hands it over by arriving on the
+            // mbarrier of ticket slot t % 32 (at most 24 + 8 tickets are outstanding, so a
+            // slot's barrier is never two phases behind its waiter), and the waiter sleeps in
+            // mbarrier.try_wait instead of polling a lock
+            uint64_t *slotbar = reinterpret_cast<uint64_t *>(locks + 32);
             int sb = 0;
+            uint32_t tk = 0;
             if (lane == 0) {
-                for (;;) {
-                    if (atomicCAS(&locks[sb], 0u, 1u) == 0u) break;
-                    if (++sb == nstage) {
-                        sb = 0;
-                        __nanosleep(BR_IDX_SLEEP);  // a spinning warp takes issue slots from the shuffling ones
-                    }
-                }
+                tk = atomicAdd(&locks[0], 1u);
+                sb = (int)(tk % (uint32_t)nstage);
+                mbar_wait(slotbar + (tk & 31u), (tk >> 5) & 1u);  // (tickets 0..nstage-1: handed over at start)
             }
             sb = __shfl_sync(FULL, sb, 0);
             __syncwarp();
@@ -401,10 +400,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                 for (uint32_t p = lane; p < n; p += 32) g[p] = buf[z[p]];
             }
             __syncwarp();
-            if (lane == 0) {
-                __threadfence_block();
-                atomicExch(&locks[sb], 0u);
-            }
+            if (lane == 0) mbar_arrive(slotbar + ((tk + (uint32_t)nstage) & 31u));
         } else if (use_tma) {
             if (lane == 0) {
                 fence_proxy_async();
@@ -458,7 +454,7 @@ __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, 
 // of one array each, shared by the CTA's warps under a lock) + 16 B of locks + per warp
 // { u16 index array, target ring, equality table, Pred bytes, ChaCha window }.
 constexpr uint32_t idx_warp_fixed(int cm) { return 2 * WRING + WTBL + 32 + 32 + (cm ? 256 * 8 : 0); }
-constexpr uint32_t IDX_CTL_BYTES = 128;  // 8 locks, 8 phases, 8 mbarriers
+constexpr uint32_t IDX_CTL_BYTES = 384;  // ticket, 8 load phases, 8 load mbarriers, 32 ticket-slot mbarriers
 
 
 template <typename T, int CM>
@@ -484,9 +480,13 @@ __global__ void __launch_bounds__(768, 1) shuffle_idx_kernel(T *__restrict__ dat
     int8_t *P = tbl + WTBL + 32;  // the table's last 32 bytes: inactive lanes' private slots
     uint64_t *chawin = reinterpret_cast<uint64_t *>(P + 32);
     if (threadIdx.x < (unsigned)nstage) {
-        locks[threadIdx.x] = 0u;
+        locks[threadIdx.x] = 0u;  // locks[0]: the staging-buffer ticket counter
         locks[8 + threadIdx.x] = 0u;
-        mbar_init(reinterpret_cast<uint64_t *>(locks + 16) + threadIdx.x, 1);
+        mbar_init(reinterpret_cast<uint64_t *>(locks + 16) + threadIdx.x, 1);  // bulk load done
+    }
+    if (threadIdx.x < 32) {  // ticket hand-off; the first nstage tickets are handed their buffers now
+        mbar_init(reinterpret_cast<uint64_t *>(locks + 32) + threadIdx.x, 1);
+        if (threadIdx.x < (unsigned)nstage) mbar_arrive(reinterpret_cast<uint64_t *>(locks + 32) + threadIdx.x);
     }
     __syncthreads();
     uint64_t bar = 0;
