@@ -20,8 +20,11 @@
  *     br_last_error() gives the thread-local message of the last failure.
  *   - Generator state that evolves across calls lives in device memory (br_pcg64 in
  *     *_dev buffers) so that back-to-back calls need no host round trip.
- *   - Word width is 64 bits (PCG64 XSL-RR 128/64, wordsource.py:71-89); shuffled arrays
- *     have n < 2^32 elements of 4 or 8 bytes.
+ *   - Word width is 64 bits (PCG64 XSL-RR 128/64, wordsource.py:71-89); items are 4 or 8
+ *     bytes.  The stream forms take any n (shuffle.py:175-190: the single rolls above
+ *     2^32 - 1 run in a 64-bit head kernel, the rest on the 32-bit kernels); the segmented
+ *     forms take n < 2^32 (BR_E_UNSUPPORTED otherwise) and the naive ones raise
+ *     BR_E_BOUND_OVERFLOW once the pair product passes 2^64 (shuffle.py:240-241).
  *   - There is no CPU fallback: without a CUDA device every device entry point returns
  *     BR_E_CUDA.
  */

@@ -22,6 +22,7 @@
 #include "roll.cuh"
 #include "shuffle.cuh"
 #include "stage_shuffle.cuh"
+#include "head64.cuh"
 #include "warp_shuffle.cuh"
 
 using namespace br;
@@ -911,12 +912,50 @@ int shuffle_common(void *data, int eb, int64_t num_arrays, uint64_t n, const std
     if (gen < 0 || gen > 2) return fail(BR_E_UNSUPPORTED, "generator must be 0 (pcg64), 1 (lehmer) or 2 (chacha)");
     if (eb != 4 && eb != 8) return fail(BR_E_UNSUPPORTED, "elem_bytes must be 4 or 8");
     if (num_arrays < 0) return fail(BR_E_INVALID, "num_arrays < 0");
-    if (n >= (1ull << 32)) return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements");
     int dev;
     DeviceInfo di;
     int stt = ensure_device(&dev, &di);
     if (stt) return stt;
     cudaStream_t st = (cudaStream_t)stream;
+    // arrays of 2^32 or more elements (shuffle.py:175-190): the single-roll head above
+    // 2^32 - 1 runs in shuffle_head64_kernel on the stream, the rest below it continues here
+    // (BR_HEAD64_STOP lowers the split for tests on small arrays)
+    uint64_t hstop = (1ull << 32) - 1;
+    if (const char *e = getenv("BR_HEAD64_STOP")) hstop = std::min<uint64_t>(hstop, strtoull(e, nullptr, 10));
+    if (n > hstop && !naive && hstop >= 1) {
+        if (segmented) return fail(BR_E_UNSUPPORTED, "segmented arrays of 2^32 or more elements (shuffle each through the stream form)");
+        if (segs.empty() || segs[0].k != 1 || segs[0].start_n != n || segs[0].count < n - hstop)
+            return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements need single rolls above 2^32 - 1");
+        if (!data) return fail(BR_E_INVALID, "null data pointer");
+        if (!state_dev) return fail(BR_E_INVALID, "null state pointer");
+        std::vector<br_segment> rest(segs);
+        rest[0].start_n = hstop;
+        rest[0].count -= n - hstop;
+        if (rest[0].count == 0) rest.erase(rest.begin());
+        uint64_t *hw = nullptr;
+        CK(cudaMallocAsync((void **)&hw, sizeof(uint64_t), st));
+        if (eb == 4)
+            shuffle_head64_kernel<uint32_t><<<1, H64_T, 0, st>>>((uint32_t *)data, n, hstop, (uint64_t *)state_dev, hw,
+                                                                 rk_first);
+        else
+            shuffle_head64_kernel<uint64_t><<<1, H64_T, 0, st>>>((uint64_t *)data, n, hstop, (uint64_t *)state_dev, hw,
+                                                                 rk_first);
+        cudaError_t le = cudaGetLastError();
+        int r = le == cudaSuccess ? BR_OK : fail(BR_E_CUDA, std::string("head kernel: ") + cudaGetErrorString(le));
+        if (r == BR_OK) {
+            r = shuffle_common(data, eb, 1, hstop, rest, false, 0, 0, nullptr, state_dev, words64, nullptr, gen, stream,
+                               false);
+            const std::string rest_kernel = g_kernel;
+            if (r == BR_OK && words64) add_words_kernel<<<1, 1, 0, st>>>(words64, hw);
+            g_kernel = "shuffle_head64_kernel+" + rest_kernel;
+        }
+        cudaFreeAsync(hw, st);
+        return r;
+    }
+    if (n >= (1ull << 32)) {
+        if (naive && n > (1ull << 32)) return fail(BR_E_BOUND_OVERFLOW, "pair product exceeds 2**64");
+        return fail(BR_E_UNSUPPORTED, "arrays of 2^32 or more elements");
+    }
     if (segs.empty() || num_arrays == 0) {  // n < 2: nothing to do, no words consumed
         if (segmented && words32 && num_arrays > 0) CK(cudaMemsetAsync(words32, 0, num_arrays * sizeof(uint32_t), st));
         if (!segmented && words64) CK(cudaMemsetAsync(words64, 0, sizeof(uint64_t), st));
