@@ -37,6 +37,7 @@
 // tests/test_resolution.py, bit-exactly against the oracle on the device in tests/test_stage.py).
 #pragma once
 #include "shuffle.cuh"
+#include <type_traits>
 
 namespace br {
 
@@ -54,6 +55,16 @@ __device__ int g_sp_phase = 99;  // debug: phases to run in the last stage (1 = 
 #define SP_OK(c, a0, a1, a2) true
 #endif
 #define SP_ASSERT(c, ...)
+#ifdef SP_PROF  // per-phase clock64 totals of CTA 0, printed at the end (profiling build)
+#define SP_TICK(k)                        \
+    if (L == 0) {                         \
+        const long long t_ = clock64();   \
+        sp_acc[k] += t_ - sp_t;           \
+        sp_t = t_;                        \
+    }
+#else
+#define SP_TICK(k)
+#endif
 
 static constexpr int SP_LOG_B = 12;
 static constexpr uint32_t SP_B = 1u << SP_LOG_B;   // positions per block (one stage)
@@ -61,7 +72,6 @@ static constexpr int SP_T = 512;                    // threads per CTA (two CTAs
 static constexpr int SP_W = SP_T / 32;
 static constexpr int SP_PER = SP_B / SP_T;          // positions per thread
 static constexpr uint32_t SP_MAXNB = 256;           // blocks per array (n <= 2^20)
-static constexpr uint32_t SP_MAXCH = 128;           // chunks per stage
 static constexpr int SP_GJ = 4;                     // generator slots per thread
 static constexpr uint32_t SP_G = SP_GJ * SP_T;      // batches per generation window
 static constexpr uint32_t SP_RING = SP_B + 8;       // targets by position - blo + 8 (8 below: the straddling batch)
@@ -100,14 +110,14 @@ struct SpShared {
     } u;
     u128 inc, AG, CG, M;  // generator constants of the array (the same for every thread)
     DevSeg segs[MAX_SEGS];
+    uint64_t ub[MAX_SEGS];  // ff(start_n, k) of each segment (0: 2^64)
     uint32_t excl[SP_MAXNB + 1];  // inbox: exclusive prefix of the tile counts (tile t = source NB-1-t)
     uint32_t toff[SP_MAXNB];      // per source block: global record index minus inbox index
     uint32_t cnt[SP_MAXNB + 1];   // per target block: this stage's records, then their exclusive prefix
-    uint16_t cend[SP_MAXCH];      // chunk ends (tile index, exclusive)
     uint32_t wsum[SP_W + 1];
     uint32_t carry[8];            // targets of the straddling batch for the next stage
     uint64_t bar;
-    uint32_t fmin, nint, nchunk, bad;
+    uint32_t fmin, nint, bad;
 };
 
 // exclusive scan of a[0..len) in place (len <= 2 * SP_T); every thread gets the total
@@ -142,6 +152,31 @@ __device__ __forceinline__ uint32_t sp_scan(uint32_t *a, uint32_t len, uint32_t 
     if (i1 < len) a[i1] = ex + v0;
     __syncthreads();
     return total;
+}
+
+// exclusive scan of a[0..len) in place by one warp (len <= 256); returns the total
+__device__ __forceinline__ uint32_t sp_scan_w(uint32_t *a, uint32_t len, int lane) {
+    uint32_t v[8], tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t i = (uint32_t)lane * 8 + q;
+        v[q] = i < len ? a[i] : 0;
+        tot += v[q];
+    }
+    uint32_t inc = tot;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    uint32_t ex = inc - tot;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t i = (uint32_t)lane * 8 + q;
+        if (i < len) a[i] = ex;
+        ex += v[q];
+    }
+    return __shfl_sync(0xFFFFFFFFu, inc, 31);
 }
 
 // exclusive scan, in place, of the SP_B u16 counters packed two per word in xc (8 per thread)
@@ -262,10 +297,6 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
                                              uint32_t blo, bool lh) {
     while (g.B0 <= b_need) {
         const uint32_t wend = min(g.B0 + SP_G, b_need + 1);  // window [B0, wend)
-        uint64_t t[SP_GJ];
-#pragma unroll
-        for (int j = 0; j < SP_GJ; ++j)
-            if (g.b[j] < wend) t[j] = __ldg(plan.thresh + g.b[j]);
         uint32_t myfail = SP_NONE;
 #pragma unroll
         for (int j = 0; j < SP_GJ; ++j) {
@@ -284,12 +315,25 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
                     rg[0] = j1;
                     rg[-1] = j2;
                 } else {
-                    for (uint32_t m = 0; m < S.k; ++m) {
-                        const uint32_t d = die(nbb - m, r);
-                        if (SP_OK(nbb - 1 - m + 8 >= blo && nbb - 1 - m + 8 - blo < SP_RING, 3000 + b, nbb, blo)) rg[-(int)m] = d;
+                    auto dice = [&](auto K) {
+#pragma unroll
+                        for (int m = 0; m < decltype(K)::value; ++m) rg[-m] = die(nbb - m, r);
+                    };
+                    switch (S.k) {
+                        case 1: dice(std::integral_constant<int, 1>{}); break;
+                        case 2: dice(std::integral_constant<int, 2>{}); break;
+                        case 3: dice(std::integral_constant<int, 3>{}); break;
+                        case 4: dice(std::integral_constant<int, 4>{}); break;
+                        case 5: dice(std::integral_constant<int, 5>{}); break;
+                        case 6: dice(std::integral_constant<int, 6>{}); break;
+                        case 7: dice(std::integral_constant<int, 7>{}); break;
+                        default: dice(std::integral_constant<int, 8>{}); break;
                     }
                 }
-                if (r < t[j] && b < myfail) myfail = b;
+                // the exact threshold (2^64 mod ff(n_b, k) < ff(n_b, k) <= the segment's first
+                // product) is read only below that bound: the reference's carried bound u
+                const uint64_t ub = sh.ub[q];
+                if ((ub == 0 || r < ub) && r < __ldg(plan.thresh + b) && b < myfail) myfail = b;
             }
         }
         if (!__syncthreads_or(myfail != SP_NONE)) {
@@ -323,52 +367,6 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
     }
 }
 
-// greedy chunks of whole tiles in inbox order, at most SP_C records each (warp 0).  A tile
-// larger than a chunk, or more chunks than SP_MAXCH, marks the array bad (re-run elsewhere).
-__device__ __forceinline__ void sp_chunk_plan(const uint32_t *excl, uint32_t ntile, uint16_t *cend, uint32_t &nchunk,
-                                              uint32_t &bad, int lane, const uint32_t SP_C) {
-    uint32_t fill = 0, nch = 0;
-    bool ovf = false;
-    for (uint32_t base = 0; base < ntile && !ovf; base += 32) {
-        const uint32_t t = base + lane;
-        const uint32_t c = t < ntile ? excl[t + 1] - excl[t] : 0;
-        uint32_t inc = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-            if (lane >= d) inc += o;
-        }
-        uint32_t consumed = 0;
-        int start = 0;
-        while (true) {
-            const unsigned over = __ballot_sync(0xFFFFFFFFu, lane >= start && t < ntile && fill + inc - consumed > SP_C);
-            if (!over) {
-                fill += __shfl_sync(0xFFFFFFFFu, inc, 31) - consumed;
-                break;
-            }
-            const int f = __ffs(over) - 1;
-            if (f == start && fill == 0) {  // one tile alone exceeds a chunk
-                ovf = true;
-                break;
-            }
-            if (lane == 0 && nch < SP_MAXCH) cend[nch] = (uint16_t)(base + f);
-            ++nch;
-            consumed = __shfl_sync(0xFFFFFFFFu, inc, f > 0 ? f - 1 : 0);
-            if (f == 0) consumed = 0;
-            start = f;
-            fill = 0;
-        }
-    }
-    if (!ovf && fill > 0) {
-        if (lane == 0 && nch < SP_MAXCH) cend[nch] = (uint16_t)ntile;
-        ++nch;
-    }
-    if (nch > SP_MAXCH) ovf = true;
-    if (lane == 0) {
-        nchunk = ovf ? 0 : nch;
-        if (ovf) bad = 1;
-    }
-}
 
 // scratch: per CTA the records' keys and the tile table (reused array after array); per
 // array the value areas, the slot map and a flag
@@ -394,7 +392,13 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
     uint32_t *desc = keyg + (((size_t)n * 4 + 255) & ~(size_t)255) / 4;
     uint16_t *src16 = reinterpret_cast<uint16_t *>(sh.xcnt);  // C -> E (D is done): each position's source slot
 
-    for (uint32_t q = L; q < plan.nseg; q += SP_T) sh.segs[q] = plan.segs[q];
+    for (uint32_t q = L; q < plan.nseg; q += SP_T) {
+        const DevSeg S = plan.segs[q];
+        sh.segs[q] = S;
+        unsigned __int128 f = 1;
+        for (uint32_t m = 0; m < S.k; ++m) f *= (uint64_t)(S.start_n - m);
+        sh.ub[q] = f >> 64 ? 0ull : (uint64_t)f;  // (plans hold products <= 2^64)
+    }
     for (uint32_t x = L; x < SP_B / 2; x += SP_T) sh.xcnt[x] = 0;
     for (uint32_t x = L; x <= SP_MAXNB; x += SP_T) sh.cnt[x] = 0;
     if (L == 0) {
@@ -404,6 +408,9 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
     }
     __syncthreads();
     uint32_t parity = 0;
+#ifdef SP_PROF
+    long long sp_acc[10] = {0}, sp_t = clock64();
+#endif
     for (int64_t a = blockIdx.x; a < num_arrays; a += gridDim.x) {
         const T *z = data + a * (int64_t)n;
         T *valg = val_all + a * (int64_t)vstride;
@@ -411,6 +418,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
         SpGen g;
         sp_gen_init<T>(g, sh, array_seed(run_seed, (uint64_t)(base + a)), lh, L);
         __syncthreads();
+        uint32_t dreg = 0;  // this stage's tile-table row entry (tile L), loaded at the end of the stage above
         for (int sg = (int)NB - 1; sg >= 0; --sg) {
             const uint32_t blo = (uint32_t)sg * SP_B;
             const uint32_t bn = min(SP_B, n - blo);
@@ -426,53 +434,75 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             } else {
                 for (uint32_t x = L; x < bn; x += SP_T) sh.mbox[x] = z[blo + x];
             }
-            const uint32_t dreg = (uint32_t)L < ntile ? __ldcg(desc + (size_t)sg * NB + (NB - 1 - L)) : 0;
             if (L < 8) sh.ring[SP_B + L] = sh.carry[L];
             if (blo + (uint32_t)L < slo) sh.ring[L + 8] = SP_JNONE;  // no step (block 0 below plan.lo)
-            // ---- B. targets of this block's steps
-            if (slo < blo + bn) sp_gen_block<T>(g, plan, sh, L, sp_batch_of(sh.segs, plan.nseg, slo), blo, lh);
-            __syncthreads();
-            if (L < 8) sh.carry[L] = sh.ring[L];
-            // ---- D. the higher blocks' deposits, in time order
-            if ((uint32_t)L < ntile) sh.excl[L] = dreg & 0xFFFFu;
-            __syncthreads();
-            const uint32_t R = sp_scan(sh.excl, ntile, sh.wsum, L);
+            // ---- D setup: the inbox tiles' prefix and chunks (warp 0), then chunk 0's records
+            // are requested before the generation step so that they land behind it
             if ((uint32_t)L < ntile) {
-                const uint32_t src = NB - 1 - (uint32_t)L;
-                sh.toff[src] = src * SP_B + (dreg >> 16) - sh.excl[L];
-            }
-            if (L == 0) sh.excl[ntile] = R;
-            __syncthreads();
-            if (wid == 0) sp_chunk_plan(sh.excl, ntile, sh.cend, sh.nchunk, sh.bad, lane, sp_cap<T>());
-            if (use_tma) {
-                mbar_wait(&sh.bar, parity);
-                parity ^= 1u;
+                sh.excl[L] = dreg & 0xFFFFu;
+                sh.toff[NB - 1 - (uint32_t)L] = dreg >> 16;
             }
             __syncthreads();
-            const uint32_t nch = sh.nchunk;
-            uint32_t ta = 0;
-            for (uint32_t ch = 0; ch < nch; ++ch) {
-                const uint32_t tb = sh.cend[ch];
-                const uint32_t cbase = sh.excl[ta];
-                uint32_t ccount = sh.excl[tb] - cbase;
-                if (!SP_OK(ccount <= sp_cap<T>() && tb <= ntile && tb >= ta, 9000 + sg, (ch << 16) | (ta << 8) | tb, ccount)) {
-                    ccount = 0;
-                    ta = tb;
-                    continue;
+            if (wid == 0) {
+                const uint32_t R = sp_scan_w(sh.excl, ntile, lane);
+                for (uint32_t t = lane; t < ntile; t += 32) {  // global record index minus inbox index
+                    const uint32_t src = NB - 1 - t;
+                    sh.toff[src] = src * SP_B + sh.toff[src] - sh.excl[t];
                 }
+                if (lane == 0) sh.excl[ntile] = R;
+            }
+            __syncthreads();
+            // chunks: the longest run of whole tiles from ta within sp_cap records (a tile larger
+            // than a chunk marks the array for the fallback kernel)
+            auto chunk_end = [&](uint32_t ta) {
+                const uint32_t lim = sh.excl[ta] + sp_cap<T>();
+                uint32_t l = ta, h = ntile;
+                while (l < h) {
+                    const uint32_t m = (l + h + 1) >> 1;
+                    if (sh.excl[m] <= lim) l = m;
+                    else h = m - 1;
+                }
+                return l;
+            };
+            auto issue_chunk = [&](uint32_t ta, uint32_t tb) {
+                const uint32_t cbase = sh.excl[ta];
                 for (uint32_t t = ta + (uint32_t)wid; t < tb; t += SP_W) {
                     const uint32_t src = NB - 1 - t;
                     const uint32_t c0 = sh.excl[t], cn = sh.excl[t + 1] - c0;
                     const uint32_t g0 = sh.toff[src] + c0;
-                    if (!SP_OK(g0 + cn <= (src + 1) * SP_B && g0 >= src * SP_B && c0 - cbase + cn <= sp_cap<T>(), sg, t, g0)) continue;
                     for (uint32_t q = lane; q < cn; q += 32) {
                         sp_cp4(&sh.u.rec.key[c0 - cbase + q], keyg + g0 + q);
                         if (sizeof(T) == 8) sp_cp8(&sh.u.rec.val[c0 - cbase + q], valg + g0 + q);
                         else sp_cp4(&sh.u.rec.val[c0 - cbase + q], valg + g0 + q);
                     }
                 }
-                sp_cp_wait();
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            const uint32_t tb0 = ntile ? chunk_end(0) : 0;
+            if (tb0) issue_chunk(0, tb0);
+            // ---- B. targets of this block's steps
+            if (slo < blo + bn) sp_gen_block<T>(g, plan, sh, L, sp_batch_of(sh.segs, plan.nseg, slo), blo, lh);
+            __syncthreads();
+            SP_TICK(0)
+            if (L < 8) sh.carry[L] = sh.ring[L];
+            if (use_tma) {
+                mbar_wait(&sh.bar, parity);
+                parity ^= 1u;
+            }
+            SP_TICK(1)
+            uint32_t ta = 0;
+            for (uint32_t ch = 0; ta < ntile; ++ch) {
+                const uint32_t tb = ch == 0 ? tb0 : chunk_end(ta);
+                if (tb == ta) {  // one tile alone exceeds a chunk
+                    if (L == 0) sh.bad = 1;
+                    break;
+                }
+                const uint32_t cbase = sh.excl[ta];
+                const uint32_t ccount = sh.excl[tb] - cbase;
+                if (ch > 0) issue_chunk(ta, tb);
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
                 __syncthreads();
+                SP_TICK(2)
                 // records bucketed by target offset x (counting sort), then each record finds its
                 // predecessor at x (the least later-in-order step s' > s) by scanning its bucket
                 constexpr uint32_t RPT = (sp_cap<T>() + SP_T - 1) / SP_T;
@@ -490,6 +520,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 }
                 __syncthreads();
                 sp_scan_x(sh.xcnt, sh.wsum, L);
+                SP_TICK(3)
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
                     const uint32_t r = (uint32_t)L + j * SP_T;
@@ -501,6 +532,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                     }
                 }
                 __syncthreads();
+                SP_TICK(4)
                 uint32_t lastm = 0;
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
@@ -533,6 +565,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 }
                 reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);
                 __syncthreads();
+                SP_TICK(5)
                 ta = tb;
             }
             // ---- C. this block's own steps in closed form (indices only).  Steps with an
@@ -556,6 +589,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                     }
                 }
             }
+            SP_TICK(6)
             const bool inblk = __syncthreads_or(nin) != 0;
             if (inblk) {
 #pragma unroll
@@ -592,6 +626,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 }
             }
             __syncthreads();
+            SP_TICK(7)
             // ---- E. this block's records (by target block), in-block outputs, slot map
             uint32_t rk[SP_PER / 2];
 #pragma unroll
@@ -615,9 +650,12 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 else rk[q / 2] = rank;
             }
             __syncthreads();
-            const uint32_t nrec = sp_scan(sh.cnt, (uint32_t)sg, sh.wsum, L);
-            if (L == 0) sh.cnt[sg] = nrec;
+            if (wid == 0) {
+                const uint32_t tot = sp_scan_w(sh.cnt, (uint32_t)sg, lane);
+                if (lane == 0) sh.cnt[sg] = tot;
+            }
             __syncthreads();
+            const uint32_t nrec = sh.cnt[sg];
 #pragma unroll
             for (int q = 0; q < SP_PER; ++q) {
                 const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
@@ -656,7 +694,15 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             if (L == 0) sh.nint = 0;
             reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);  // src16 -> the next stage's counters
             __syncthreads();
+            // the next stage's tile-table row: complete now (this stage wrote the last entry)
+            dreg = sg > 0 && (uint32_t)L < ntile + 1 ? __ldcg(desc + (size_t)(sg - 1) * NB + (NB - 1 - L)) : 0;
+            SP_TICK(8)
         }
+#ifdef SP_PROF
+        if (L == 0 && blockIdx.x == 0)
+            printf("SP_PROF cycles: gen %lld dsetup %lld load %lld count %lld scatter %lld resolve %lld C0 %lld C %lld E %lld\n",
+                   sp_acc[0], sp_acc[1], sp_acc[2], sp_acc[3], sp_acc[4], sp_acc[5], sp_acc[6], sp_acc[7], sp_acc[8]);
+#endif
         if (L == 0) {
             if (words32) words32[a] = plan.nbatches + g.D;
             if (sh.bad) flags[a] = 1;
