@@ -235,9 +235,15 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
 // fetches item row[p] from its owner lane with shuffles, and stores positions l and l+32.
 // The payload never enters shared memory.
 static constexpr int SMI_T = 256;
+#ifndef SMI_MINB
+#define SMI_MINB 4
+#endif
+#ifndef SMI_U
+#define SMI_U 8
+#endif
 static constexpr int SMI_WW = 32 * 17;  // words per warp: 16 transposed words x 32 lanes, or 32 rows of 17
 
-__device__ __forceinline__ uint32_t smi_pos(uint32_t j) { return ((j & ~3u) << 5) | (j & 3u); }
+__device__ __forceinline__ uint32_t smi_pos(uint32_t j) { return j + (j >> 2) * 124u; }  // (j/4)*128 + j%4
 
 template <typename T>
 __device__ __forceinline__ T smi_shfl(T v, int src) {
@@ -276,7 +282,7 @@ __device__ __forceinline__ void smi_segment(uint8_t *zt, uint32_t nb, uint32_t c
         } while (r < t);  // reject: re-draw the whole batch (shuffle.py:121-128)
 #pragma unroll
         for (int m = 0; m < K; ++m) {
-            uint8_t *pi = zt + smi_pos(nb - 1 - m), *pj = zt + (d[m] + (d[m] & ~3u) * 31u);
+            uint8_t *pi = zt + smi_pos(nb - 1 - m), *pj = zt + smi_pos(d[m]);
             const uint8_t x = *pi, y = *pj;
             *pi = y;
             *pj = x;
@@ -301,7 +307,7 @@ __device__ __forceinline__ void smi_segment_any(uint8_t *zt, uint32_t k, uint32_
 }
 
 template <typename T, bool CHA>
-__global__ void __launch_bounds__(SMI_T, 4) shuffle_small_idx_kernel(T *__restrict__ data, int64_t num_arrays,
+__global__ void __launch_bounds__(SMI_T, SMI_MINB) shuffle_small_idx_kernel(T *__restrict__ data, int64_t num_arrays,
                                                                  DevPlan plan, uint64_t run_seed, int64_t base,
                                                                  uint32_t *__restrict__ words_out, int gen) {
     __shared__ __align__(16) uint32_t wr[SMI_T / 32][SMI_WW];
@@ -350,15 +356,17 @@ __global__ void __launch_bounds__(SMI_T, 4) shuffle_small_idx_kernel(T *__restri
     const int64_t aw = (int64_t)blockIdx.x * SMI_T + wid * 32;
     const int cnt = (int)min((int64_t)32, num_arrays - aw);
     const uint32_t l0 = (uint32_t)lane, l1 = (uint32_t)lane + 32;
-    constexpr int U = 8;
-    for (int t0 = 0; t0 < cnt; t0 += U) {
+    constexpr int U = SMI_U;
+    const bool in0 = l0 < n, in1 = l1 < n;
+    T *gw = data + aw * (int64_t)n;  // the warp's 32 arrays, contiguous
+    for (int t0 = 0; t0 < cnt; t0 += U, gw += (int64_t)U * n) {
         T v0[U], v1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const T *g = data + (aw + t0 + u) * (int64_t)n;
+            const T *g = gw + u * n;
             const bool ok = t0 + u < cnt;
-            v0[u] = ok && l0 < n ? g[l0] : T(0);
-            v1[u] = ok && l1 < n ? g[l1] : T(0);
+            v0[u] = ok && in0 ? g[l0] : T(0);
+            v1[u] = ok && in1 ? g[l1] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -366,10 +374,10 @@ __global__ void __launch_bounds__(SMI_T, 4) shuffle_small_idx_kernel(T *__restri
             const uint32_t x0 = row[l0], x1 = row[l1];  // (bytes past n are never used)
             const T a0 = smi_shfl(v0[u], (int)(x0 & 31)), b0 = smi_shfl(v1[u], (int)(x0 & 31));
             const T a1 = smi_shfl(v0[u], (int)(x1 & 31)), b1 = smi_shfl(v1[u], (int)(x1 & 31));
+            T *g = gw + u * n;
             if (t0 + u < cnt) {
-                T *g = data + (aw + t0 + u) * (int64_t)n;
-                if (l0 < n) g[l0] = (x0 & 32) ? b0 : a0;
-                if (l1 < n) g[l1] = (x1 & 32) ? b1 : a1;
+                if (in0) g[l0] = (x0 & 32) ? b0 : a0;
+                if (in1) g[l1] = (x1 & 32) ? b1 : a1;
             }
         }
     }
