@@ -319,6 +319,16 @@ __global__ void __launch_bounds__(SMI_T, SMI_MINB) shuffle_small_idx_kernel(T *_
     if (tid < (int)plan.nseg) segs[tid] = plan.segs[tid];
 #pragma unroll
     for (int w = 0; w < 16; ++w) W[w * 32 + lane] = 0x03020100u + 0x04040404u * (uint32_t)w;
+    {  // the warp's payload span (32 arrays) is pulled into L2 while the permutations are built
+        const int64_t aw0 = (int64_t)blockIdx.x * SMI_T + wid * 32;
+        const int64_t cnt0 = min((int64_t)32, num_arrays - aw0);
+        if (cnt0 > 0) {
+            const char *p0 = reinterpret_cast<const char *>(data + aw0 * (int64_t)n);
+            const uint64_t span = (uint64_t)cnt0 * n * sizeof(T);
+            for (uint64_t off = (uint64_t)lane * 128; off < span; off += 32 * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + off));
+        }
+    }
     __syncthreads();
     if (a < num_arrays) {
         u128 s, inc;
