@@ -900,7 +900,10 @@ def test_abi_error_paths(B):
     zp, stp, wp = (C.c_void_p(t.data_ptr()) for t in (z, st, w64))
     regs = B.DEFAULT_SCHEDULE._regimes()
     assert L.br_shuffle_stream(zp, 2, 64, stp, regs, len(regs), 0, None, sp) == N.BR_E_UNSUPPORTED  # elem size
-    assert L.br_shuffle_stream(zp, 4, 1 << 32, stp, regs, len(regs), 0, None, sp) != N.BR_OK  # n >= 2^32
+    # n >= 2^32: the stream form takes it (tests/test_head64.py); the segmented form does not,
+    # and the naive form overflows its pair product (shuffle.py:240-241); no launch happens
+    assert L.br_shuffle_segmented(zp, 4, 1, 1 << 32, 1, 0, regs, len(regs), 0, None, sp) == N.BR_E_UNSUPPORTED
+    assert L.br_shuffle_naive_stream(zp, 4, (1 << 32) + 1, stp, None, sp) == N.BR_E_BOUND_OVERFLOW
     assert L.br_shuffle_stream(None, 4, 64, stp, regs, len(regs), 0, None, sp) == N.BR_E_INVALID
     assert L.br_shuffle_stream(zp, 4, 64, None, regs, len(regs), 0, None, sp) == N.BR_E_INVALID
     assert L.br_shuffle_segmented(zp, 4, 1, 64, 1, 0, regs, len(regs), 3, None, sp) == N.BR_E_UNSUPPORTED  # generator
