@@ -509,6 +509,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 uint32_t arr[(RPT + 1) / 2];  // arrival index of each record within its bucket
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
+                    if (j * SP_T >= ccount) break;  // (uniform: the chunk's records end)
                     const uint32_t r = (uint32_t)L + j * SP_T;
                     uint32_t av = 0;
                     if (r < ccount) {
@@ -523,6 +524,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 SP_TICK(3)
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
+                    if (j * SP_T >= ccount) break;  // (uniform: the chunk's records end)
                     const uint32_t r = (uint32_t)L + j * SP_T;
                     if (r < ccount) {
                         const uint32_t K = sh.u.rec.key[r];
@@ -536,6 +538,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 uint32_t lastm = 0;
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
+                    if (j * SP_T >= ccount) break;  // (uniform: the chunk's records end)
                     const uint32_t r = (uint32_t)L + j * SP_T;
                     if (r < ccount) {
                         const uint32_t K = sh.u.rec.key[r];
@@ -560,6 +563,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                 __syncthreads();
 #pragma unroll
                 for (uint32_t j = 0; j < RPT; ++j) {
+                    if (j * SP_T >= ccount) break;  // (uniform: the chunk's records end)
                     const uint32_t r = (uint32_t)L + j * SP_T;
                     if ((lastm >> j) & 1) sh.mbox[sh.u.rec.key[r] & (SP_B - 1)] = sh.u.rec.val[r];
                 }
