@@ -73,7 +73,7 @@ static constexpr int SP_W = SP_T / 32;
 static constexpr int SP_PER = SP_B / SP_T;          // positions per thread
 static constexpr uint32_t SP_MAXNB = 256;           // blocks per array (n <= 2^20)
 #ifndef SP_GJ_N
-#define SP_GJ_N 1  // 512-batch windows: a rejection re-runs at most 512 (C5: 7.66 ms against 8.09 with 4)
+#define SP_GJ_N 1  // 512-batch windows: a rejection re-runs at most 512 (C5: 7.66 ms against 8.09 with 4; 4 slots with 512-batch windows where rejections are frequent: 8.23, register spills)
 #endif
 static constexpr int SP_GJ = SP_GJ_N;                     // generator slots per thread
 static constexpr uint32_t SP_G = SP_GJ * SP_T;      // batches per generation window
@@ -345,7 +345,7 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
             for (int j = 0; j < SP_GJ; ++j)
                 if (g.b[j] < wend) {
                     g.b[j] += SP_G;
-                    g.s[j] = mad128(g.s[j], AG, CG);
+                    g.s[j] = mad128_wide(g.s[j], AG, CG);
                 }
             g.B0 = wend;
         } else {
@@ -359,9 +359,9 @@ __device__ __forceinline__ void sp_gen_block(SpGen &g, const DevPlan &plan, SpSh
             for (int j = 0; j < SP_GJ; ++j) {
                 if (g.b[j] < f) {
                     g.b[j] += SP_G;
-                    g.s[j] = mad128(g.s[j], AG, CG);
+                    g.s[j] = mad128_wide(g.s[j], AG, CG);
                 }
-                g.s[j] = mad128(g.s[j], M, inc);
+                g.s[j] = mad128_wide(g.s[j], M, inc);
             }
             g.B0 = f;
             g.D += 1;
