@@ -580,13 +580,20 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             // the entries they touch are initialised: FT minima and lists at their targets and at
             // themselves, and a flag on every targeted position (ring bit 31).  A position that no
             // in-block step targets, and that has none itself, is its own source.
+            // (the same pass ranks E's outputs: records by target block, in-block outputs in order)
             uint32_t nin = 0;
+            uint32_t rk[SP_PER / 2];
 #pragma unroll
             for (int q = 0; q < SP_PER; ++q) {
                 const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
+                uint32_t rank = 0;
+                bool inb = true;
                 if (i < bn) {
                     const uint32_t J = sh.ring[i + 8] & ~SP_TGT;
-                    if (J >= blo && J != SP_JNONE) {
+                    if (J < blo) {
+                        rank = atomicAdd(&sh.cnt[J >> SP_LOG_B], 1u);
+                        inb = false;
+                    } else if (J != SP_JNONE) {
                         const uint32_t y = J - blo;
                         sh.u.loc.ft[y] = SP_NONE;
                         sh.u.loc.head[y] = SP_NONE;
@@ -595,6 +602,13 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                         ++nin;
                     }
                 }
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, i < bn && inb);
+                uint32_t b0 = 0;
+                if (lane == 0 && m) b0 = atomicAdd(&sh.nint, (uint32_t)__popc(m));
+                b0 = __shfl_sync(0xFFFFFFFFu, b0, 0);
+                if (i < bn && inb) rank = b0 + __popc(m & ((1u << lane) - 1));
+                if (q & 1) rk[q / 2] |= rank << 16;
+                else rk[q / 2] = rank;
             }
             SP_TICK(6)
             const bool inblk = __syncthreads_or(nin) != 0;
@@ -635,28 +649,6 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             __syncthreads();
             SP_TICK(7)
             // ---- E. this block's records (by target block), in-block outputs, slot map
-            uint32_t rk[SP_PER / 2];
-#pragma unroll
-            for (int q = 0; q < SP_PER; ++q) {
-                const uint32_t i = (uint32_t)L + (uint32_t)q * SP_T;
-                uint32_t rank = 0;
-                bool inb = true;
-                if (i < bn) {
-                    const uint32_t J = sh.ring[i + 8] & ~SP_TGT;
-                    if (J < blo) {
-                        rank = atomicAdd(&sh.cnt[J >> SP_LOG_B], 1u);
-                        inb = false;
-                    }
-                }
-                const unsigned m = __ballot_sync(0xFFFFFFFFu, i < bn && inb);
-                uint32_t b0 = 0;
-                if (lane == 0 && m) b0 = atomicAdd(&sh.nint, (uint32_t)__popc(m));
-                b0 = __shfl_sync(0xFFFFFFFFu, b0, 0);
-                if (i < bn && inb) rank = b0 + __popc(m & ((1u << lane) - 1));
-                if (q & 1) rk[q / 2] |= rank << 16;
-                else rk[q / 2] = rank;
-            }
-            __syncthreads();
             if (wid == 0) {
                 const uint32_t tot = sp_scan_w(sh.cnt, (uint32_t)sg, lane);
                 if (lane == 0) sh.cnt[sg] = tot;
