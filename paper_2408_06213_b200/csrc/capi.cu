@@ -631,7 +631,8 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
     const size_t small_smem = (size_t)tpb * stride * sizeof(T);
     // n <= 64: u8 index permutations in a transposed (conflict-free) layout, payload applied per warp
     if (allow(K_SMALL) && segmented && cp.plan.max_k <= 8 && n <= 64 && !getenv("BR_SMALL_ROWS")) {
-        auto kern = gen == 2 ? shuffle_small_idx_kernel<T, true> : shuffle_small_idx_kernel<T, false>;
+        auto kern = n == 64 ? (gen == 2 ? shuffle_small_idx_kernel<T, true, 64> : shuffle_small_idx_kernel<T, false, 64>)
+                            : (gen == 2 ? shuffle_small_idx_kernel<T, true> : shuffle_small_idx_kernel<T, false>);
         const int64_t blocks = (num_arrays + SMI_T - 1) / SMI_T;
         kern<<<(unsigned)blocks, SMI_T, 0, st>>>((T *)data, num_arrays, cp.plan, run_seed, base, words32, gen);
         CK(cudaGetLastError());

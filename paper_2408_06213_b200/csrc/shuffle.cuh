@@ -306,7 +306,7 @@ __device__ __forceinline__ void smi_segment_any(uint8_t *zt, uint32_t k, uint32_
     }
 }
 
-template <typename T, bool CHA>
+template <typename T, bool CHA, int NF = 0>  // NF: n known at compile time (0: runtime)
 __global__ void __launch_bounds__(SMI_T, SMI_MINB) shuffle_small_idx_kernel(T *__restrict__ data, int64_t num_arrays,
                                                                  DevPlan plan, uint64_t run_seed, int64_t base,
                                                                  uint32_t *__restrict__ words_out, int gen) {
@@ -367,6 +367,29 @@ __global__ void __launch_bounds__(SMI_T, SMI_MINB) shuffle_small_idx_kernel(T *_
     const int cnt = (int)min((int64_t)32, num_arrays - aw);
     const uint32_t l0 = (uint32_t)lane, l1 = (uint32_t)lane + 32;
     constexpr int U = SMI_U;
+    if (NF == 64 && cnt == 32) {  // the C3 shape: constant offsets, no predicates
+        constexpr int UF = 4;
+        T *gw = data + aw * 64;
+#pragma unroll 1
+        for (int t0 = 0; t0 < 32; t0 += UF, gw += UF * 64) {
+            T v0[UF], v1[UF];
+#pragma unroll
+            for (int u = 0; u < UF; ++u) {
+                v0[u] = gw[u * 64 + l0];
+                v1[u] = gw[u * 64 + l1];
+            }
+#pragma unroll
+            for (int u = 0; u < UF; ++u) {
+                const uint8_t *row = reinterpret_cast<const uint8_t *>(W + 17 * (t0 + u));
+                const uint32_t x0 = row[l0], x1 = row[l1];
+                const T a0 = smi_shfl(v0[u], (int)(x0 & 31)), b0 = smi_shfl(v1[u], (int)(x0 & 31));
+                const T a1 = smi_shfl(v0[u], (int)(x1 & 31)), b1 = smi_shfl(v1[u], (int)(x1 & 31));
+                gw[u * 64 + l0] = (x0 & 32) ? b0 : a0;
+                gw[u * 64 + l1] = (x1 & 32) ? b1 : a1;
+            }
+        }
+        return;
+    }
     const bool in0 = l0 < n, in1 = l1 < n;
     T *gw = data + aw * (int64_t)n;  // the warp's 32 arrays, contiguous
     for (int t0 = 0; t0 < cnt; t0 += U, gw += (int64_t)U * n) {
