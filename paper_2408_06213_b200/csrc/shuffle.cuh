@@ -234,6 +234,11 @@ __global__ void __launch_bounds__(128) shuffle_small_kernel(T *__restrict__ data
 // applies them to the payload one array at a time: lane l loads items l and l+32 (coalesced),
 // fetches item row[p] from its owner lane with shuffles, and stores positions l and l+32.
 // The payload never enters shared memory.
+template <typename T>
+struct alignas(2 * sizeof(T)) SmiPair {
+    T a, b;
+};
+
 static constexpr int SMI_T = 256;
 #ifndef SMI_MINB
 #define SMI_MINB 4
@@ -256,15 +261,36 @@ __device__ __forceinline__ T smi_shfl(T v, int src) {
     }
 }
 
+// The K swaps of a batch at remaining length nb = 4a + R (za: row a of the lane's column):
+// position nb-1-m = 4a + e, e = R-1-m, lies floor(e/4) rows away at byte e mod 4.
+template <int K, int R>
+__device__ __forceinline__ void smi_swaps(uint8_t *zt, uint8_t *za, const uint32_t (&d)[K]) {
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+        const int e = R - 1 - m;
+        const int row = (e >= 0) ? e / 4 : -((3 - e) / 4), byte = e - 4 * row;
+        uint8_t *pi = za + (row * 128 + byte), *pj = zt + smi_pos(d[m]);
+        const uint8_t x = *pi, y = *pj;
+        *pi = y;
+        *pj = x;
+    }
+}
+
 template <int K, bool CHA>
 __device__ __forceinline__ void smi_segment(uint8_t *zt, uint32_t nb, uint32_t count, const uint64_t *thresh, u128 &s,
                                             u128 inc, uint32_t &words, bool lh, const ChaKey &ck, ChaCursor &cur,
                                             bool naive) {
+    // ub, the product of the segment's first K bounds, bounds every later batch's product and so
+    // its threshold: the exact threshold is read only below it (the carried bound of
+    // shuffle.py:118-128); n <= 64 and K <= 8 keep it below 2^48
+    uint64_t ub = 1;
+#pragma unroll
+    for (int m = 0; m < K; ++m) ub *= (uint64_t)(nb - m);
+    words += count;
     for (uint32_t c = 0; c < count; ++c, nb -= K) {
-        const uint64_t t = __ldg(thresh + c);
         uint32_t d[K];
         uint64_t r;
-        do {
+        auto draw = [&]() {
             if constexpr (CHA) {
                 s = cha_add(s, 1);
                 r = cha_out_cached(ck, cur, s);
@@ -272,20 +298,28 @@ __device__ __forceinline__ void smi_segment(uint8_t *zt, uint32_t nb, uint32_t c
                 s = mad128_wide(s, gen_mult(lh), inc);  // 17 SASS instead of mad128's 25
                 r = gen_out(s, lh);
             }
-            ++words;
             if (K == 2 && naive) {
                 naive_pair(nb, r, d[0], d[K - 1]);
             } else {
 #pragma unroll
                 for (int m = 0; m < K; ++m) d[m] = die(nb - m, r);
             }
-        } while (r < t);  // reject: re-draw the whole batch (shuffle.py:121-128)
-#pragma unroll
-        for (int m = 0; m < K; ++m) {
-            uint8_t *pi = zt + smi_pos(nb - 1 - m), *pj = zt + smi_pos(d[m]);
-            const uint8_t x = *pi, y = *pj;
-            *pi = y;
-            *pj = x;
+        };
+        draw();
+        if (r < ub) {
+            const uint64_t t = __ldg(thresh + c);
+            while (r < t) {  // reject: re-draw the whole batch (shuffle.py:121-128)
+                draw();
+                ++words;
+            }
+        }
+        // nb = 4a + R: the batch's own positions are constant offsets from row a once R is known
+        uint8_t *za = zt + (nb >> 2) * 128u;
+        switch (nb & 3u) {
+            case 0: smi_swaps<K, 0>(zt, za, d); break;
+            case 1: smi_swaps<K, 1>(zt, za, d); break;
+            case 2: smi_swaps<K, 2>(zt, za, d); break;
+            default: smi_swaps<K, 3>(zt, za, d); break;
         }
     }
 }
@@ -318,7 +352,8 @@ __global__ void __launch_bounds__(SMI_T, SMI_MINB) shuffle_small_idx_kernel(T *_
     const int64_t a = (int64_t)blockIdx.x * SMI_T + tid;
     if (tid < (int)plan.nseg) segs[tid] = plan.segs[tid];
 #pragma unroll
-    for (int w = 0; w < 16; ++w) W[w * 32 + lane] = 0x03020100u + 0x04040404u * (uint32_t)w;
+    for (int w = 0; w < 16; ++w)  // NF == 64: token j names its owner lane j / 2 and half j & 1 (bit 5)
+        W[w * 32 + lane] = NF == 64 ? 0x21012000u + 0x02020202u * (uint32_t)w : 0x03020100u + 0x04040404u * (uint32_t)w;
     {  // the warp's payload span (32 arrays) is pulled into L2 while the permutations are built
         const int64_t aw0 = (int64_t)blockIdx.x * SMI_T + wid * 32;
         const int64_t cnt0 = min((int64_t)32, num_arrays - aw0);
@@ -367,26 +402,36 @@ __global__ void __launch_bounds__(SMI_T, SMI_MINB) shuffle_small_idx_kernel(T *_
     const int cnt = (int)min((int64_t)32, num_arrays - aw);
     const uint32_t l0 = (uint32_t)lane, l1 = (uint32_t)lane + 32;
     constexpr int U = SMI_U;
-    if (NF == 64 && cnt == 32) {  // the C3 shape: constant offsets, no predicates
-        constexpr int UF = 4;
-        T *gw = data + aw * 64;
+    if (NF == 64 && cnt == 32 && (reinterpret_cast<uintptr_t>(data) & (2 * sizeof(T) - 1)) == 0) {
+        // the C3 shape: lane l moves items 2l, 2l+1 as one vector; SHFL reads the token's low 5 bits
+        using P = SmiPair<T>;
+        constexpr int UF = sizeof(T) == 4 ? 4 : 2;  // arrays per step, loaded one step ahead
+        P *gw = reinterpret_cast<P *>(data + aw * 64) + lane;
+        P v[2][UF];
+        auto load = [&](P (&b)[UF], int t0) {
+#pragma unroll
+            for (int u = 0; u < UF; ++u) b[u] = gw[(t0 + u) * 32];
+        };
+        auto apply = [&](P (&b)[UF], int t0) {
+#pragma unroll
+            for (int u = 0; u < UF; ++u) {
+                const uint32_t xx = reinterpret_cast<const uint16_t *>(W + 17 * (t0 + u))[lane];
+                const uint32_t x0 = xx, x1 = xx >> 8;
+                const T a0 = smi_shfl(b[u].a, (int)x0), b0 = smi_shfl(b[u].b, (int)x0);
+                const T a1 = smi_shfl(b[u].a, (int)x1), b1 = smi_shfl(b[u].b, (int)x1);
+                P o;
+                o.a = (x0 & 32) ? b0 : a0;
+                o.b = (x1 & 32) ? b1 : a1;
+                gw[(t0 + u) * 32] = o;
+            }
+        };
+        load(v[0], 0);
 #pragma unroll 1
-        for (int t0 = 0; t0 < 32; t0 += UF, gw += UF * 64) {
-            T v0[UF], v1[UF];
-#pragma unroll
-            for (int u = 0; u < UF; ++u) {
-                v0[u] = gw[u * 64 + l0];
-                v1[u] = gw[u * 64 + l1];
-            }
-#pragma unroll
-            for (int u = 0; u < UF; ++u) {
-                const uint8_t *row = reinterpret_cast<const uint8_t *>(W + 17 * (t0 + u));
-                const uint32_t x0 = row[l0], x1 = row[l1];
-                const T a0 = smi_shfl(v0[u], (int)(x0 & 31)), b0 = smi_shfl(v1[u], (int)(x0 & 31));
-                const T a1 = smi_shfl(v0[u], (int)(x1 & 31)), b1 = smi_shfl(v1[u], (int)(x1 & 31));
-                gw[u * 64 + l0] = (x0 & 32) ? b0 : a0;
-                gw[u * 64 + l1] = (x1 & 32) ? b1 : a1;
-            }
+        for (int t0 = 0; t0 < 32; t0 += 2 * UF) {
+            load(v[1], t0 + UF);
+            apply(v[0], t0);
+            if (t0 + 2 * UF < 32) load(v[0], t0 + 2 * UF);
+            apply(v[1], t0 + UF);
         }
         return;
     }
@@ -404,7 +449,11 @@ __global__ void __launch_bounds__(SMI_T, SMI_MINB) shuffle_small_idx_kernel(T *_
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint8_t *row = reinterpret_cast<const uint8_t *>(W + 17 * (t0 + u));
-            const uint32_t x0 = row[l0], x1 = row[l1];  // (bytes past n are never used)
+            uint32_t x0 = row[l0], x1 = row[l1];  // (bytes past n are never used)
+            if (NF == 64) {  // undo the (lane, half) token form
+                x0 = ((x0 & 31) << 1) | (x0 >> 5);
+                x1 = ((x1 & 31) << 1) | (x1 >> 5);
+            }
             const T a0 = smi_shfl(v0[u], (int)(x0 & 31)), b0 = smi_shfl(v1[u], (int)(x0 & 31));
             const T a1 = smi_shfl(v0[u], (int)(x1 & 31)), b1 = smi_shfl(v1[u], (int)(x1 & 31));
             T *g = gw + u * n;
