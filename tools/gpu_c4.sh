@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu.py -x -q -p no:cacheprovider -k "idx or c4 or dispatch or KERNEL or forced" 2>&1 | tail -3
-REPS=10 timeout 300 python tools/shuffle_time.py c4 default 2>&1 | tail -1
+# C4: staging-buffer count sweep of the index kernel (warps per SM follow from shared memory)
+for s in 2 4 8; do echo stages=$s; BR_SHUFFLE_KERNEL=idx BR_IDX_STAGES=$s REPS=10 python tools/shuffle_time.py c4 idx; done
