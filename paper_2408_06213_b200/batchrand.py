@@ -738,6 +738,16 @@ def _shuffle_stream(source, z, regimes, unbatched: bool, segments=None, want_rk=
         return _shuffle_stream_host(source, host[0], host[1], regimes, unbatched, segments, want_rk, naive, torch)
     st = _state_struct(source)
     dev, fin = _device_payload(z, torch)
+    if _is_fixed(source) and dev.data_ptr() == getattr(z, "data_ptr", lambda: 0)():
+        # a replayed sequence can be over-read: shuffle a copy of the caller's CUDA tensor and
+        # copy back only on success, so SourceExhausted leaves the payload unchanged
+        target, dev = dev, dev.clone()
+        fin0 = fin
+
+        def fin(d):
+            target.copy_(d)
+            return fin0(target)
+
     n = dev.numel()
     scratch = _call_scratch(torch)
     ds = DeviceStream.__new__(DeviceStream)

@@ -994,6 +994,17 @@ def test_fixed_sequence_source(B, O):
     with pytest.raises(B.SourceExhausted):
         B.shuffle_batched(s, z)
     assert z == list(range(1000)) and s.cursor == 100
+    # the same with a caller's CUDA tensor (large enough to skip the host staging path)
+    s = B.FixedSequenceSource(words[:100], 64)
+    zt = torch.arange(20000, dtype=torch.int32, device="cuda")
+    with pytest.raises(B.SourceExhausted):
+        B.shuffle_batched(s, zt)
+    assert torch.equal(zt, torch.arange(20000, dtype=torch.int32, device="cuda")) and s.cursor == 100
+    s = B.FixedSequenceSource(words, 64)
+    zt = torch.arange(3000, dtype=torch.int32, device="cuda")
+    B.shuffle_batched(s, zt)
+    o = O.fixed(words)
+    assert np.array_equal(u32(zt), O.shuffle_batched(o, np.arange(3000, dtype=np.uint32))) and s.cursor == o.cursor
     with pytest.raises(TypeError):
         B.shuffle_batched(B.FixedSequenceSource([1, 2, 3], 16), [1, 2, 3], B.ShuffleSchedule(((1 << 4, 2),), 2, 16))
     with pytest.raises(TypeError):
