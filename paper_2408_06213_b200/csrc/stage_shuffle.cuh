@@ -68,7 +68,10 @@ __device__ int g_sp_phase = 99;  // debug: phases to run in the last stage (1 = 
 
 static constexpr int SP_LOG_B = 12;
 static constexpr uint32_t SP_B = 1u << SP_LOG_B;   // positions per block (one stage)
-static constexpr int SP_T = 512;                    // threads per CTA (two CTAs per SM)
+#ifndef SP_T_N
+#define SP_T_N 512  // 1024 (one CTA per SM): 148 arrays 4.92 ms against 5.65, but 256 arrays take two waves, 9.63 ms against 7.55
+#endif
+static constexpr int SP_T = SP_T_N;                 // threads per CTA (512: two CTAs per SM)
 static constexpr int SP_W = SP_T / 32;
 static constexpr int SP_PER = SP_B / SP_T;          // positions per thread
 static constexpr uint32_t SP_MAXNB = 256;           // blocks per array (n <= 2^20)
@@ -184,12 +187,19 @@ __device__ __forceinline__ uint32_t sp_scan_w(uint32_t *a, uint32_t len, int lan
 
 // exclusive scan, in place, of the SP_B u16 counters packed two per word in xc (8 per thread)
 __device__ __forceinline__ void sp_scan_x(uint32_t *xc, uint32_t *wsum, int L) {
-    static_assert(SP_T * 8 == SP_B, "eight counters per thread");
-    const uint4 w = reinterpret_cast<const uint4 *>(xc)[L];
-    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    constexpr int NWD = (int)(SP_B / SP_T / 2);  // words (two counters each) per thread
+    static_assert(NWD == 4 || NWD == 2, "eight or four counters per thread");
+    uint32_t wv[NWD];
+    if constexpr (NWD == 4) {
+        const uint4 w = reinterpret_cast<const uint4 *>(xc)[L];
+        wv[0] = w.x, wv[1] = w.y, wv[2] = w.z, wv[3] = w.w;
+    } else {
+        const uint2 w = reinterpret_cast<const uint2 *>(xc)[L];
+        wv[0] = w.x, wv[1] = w.y;
+    }
     uint32_t tot = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tot += (wv[q] & 0xFFFFu) + (wv[q] >> 16);
+    for (int q = 0; q < NWD; ++q) tot += (wv[q] & 0xFFFFu) + (wv[q] >> 16);
     uint32_t inc = tot;
     const int lane = L & 31, wp = L >> 5;
 #pragma unroll
@@ -211,15 +221,16 @@ __device__ __forceinline__ void sp_scan_x(uint32_t *xc, uint32_t *wsum, int L) {
     }
     __syncthreads();
     uint32_t run = wsum[wp] + inc - tot;
-    uint32_t ov[4];
+    uint32_t ov[NWD];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NWD; ++q) {
         const uint32_t lo = run;
         run += wv[q] & 0xFFFFu;
         ov[q] = lo | (run << 16);
         run += wv[q] >> 16;
     }
-    reinterpret_cast<uint4 *>(xc)[L] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+    if constexpr (NWD == 4) reinterpret_cast<uint4 *>(xc)[L] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+    else reinterpret_cast<uint2 *>(xc)[L] = make_uint2(ov[0], ov[1]);
     __syncthreads();
 }
 
@@ -570,7 +581,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
                     const uint32_t r = (uint32_t)L + j * SP_T;
                     if ((lastm >> j) & 1) sh.mbox[sh.u.rec.key[r] & (SP_B - 1)] = sh.u.rec.val[r];
                 }
-                reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);
+                if ((uint32_t)L < SP_B / 8) reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);
                 __syncthreads();
                 SP_TICK(5)
                 ta = tb;
@@ -691,7 +702,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
             }
             for (uint32_t tb = L; tb <= (uint32_t)sg; tb += SP_T) sh.cnt[tb] = 0;
             if (L == 0) sh.nint = 0;
-            reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);  // src16 -> the next stage's counters
+            if ((uint32_t)L < SP_B / 8) reinterpret_cast<uint4 *>(sh.xcnt)[L] = make_uint4(0, 0, 0, 0);  // src16 -> the next stage's counters
             __syncthreads();
             // the next stage's tile-table row: complete now (this stage wrote the last entry)
             dreg = sg > 0 && (uint32_t)L < ntile + 1 ? __ldcg(desc + (size_t)(sg - 1) * NB + (NB - 1 - L)) : 0;
@@ -712,7 +723,7 @@ __device__ __forceinline__ void shuffle_stage_body(const T *__restrict__ data, i
 }
 
 template <typename T>
-__global__ void __launch_bounds__(SP_T, 2) shuffle_stage_kernel(const T *__restrict__ data, int64_t num_arrays,
+__global__ void __launch_bounds__(SP_T, 1024 / SP_T) shuffle_stage_kernel(const T *__restrict__ data, int64_t num_arrays,
                                                                  DevPlan plan, uint64_t run_seed, int64_t base,
                                                                  uint32_t *__restrict__ words32, int gen,
                                                                  unsigned char *__restrict__ cta_scratch,
