@@ -355,17 +355,19 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
         while (gs.B0 < plan.nbatches) warp_gen_step<CHA, WRING>(gs, plan, ring, lane, rkf, chawin, ck);
         if constexpr (IDX) {
             // take a staging buffer in ticket order (FIFO hand-off): ticket t uses buffer
-            // t % nstage; the holder of ticket t - nstage hands it over by arriving on the
-            // mbarrier of ticket slot t % 32 (at most 24 + 8 tickets are outstanding, so a
-            // slot's barrier is never two phases behind its waiter), and the waiter sleeps in
-            // mbarrier.try_wait instead of polling a lock
+            // t % nstage and is number t / nstage in that buffer's queue; its predecessor in the
+            // queue hands the buffer over by arriving on the mbarrier of the queue's slot
+            // (t / nstage) % 32.  A queue's waiters are consecutive and at most one per warp
+            // (<= 24), so a slot's barrier is never two phases away from its waiter; the
+            // waiter sleeps in mbarrier.try_wait instead of polling a lock
             uint64_t *slotbar = reinterpret_cast<uint64_t *>(locks + 32);
             int sb = 0;
             uint32_t tk = 0;
             if (lane == 0) {
                 tk = atomicAdd(&locks[0], 1u);
                 sb = (int)(tk % (uint32_t)nstage);
-                mbar_wait(slotbar + (tk & 31u), (tk >> 5) & 1u);  // (tickets 0..nstage-1: handed over at start)
+                const uint32_t sq = tk / (uint32_t)nstage;  // position in the buffer's own queue
+                mbar_wait(slotbar + (uint32_t)sb * 32u + (sq & 31u), (sq >> 5) & 1u);  // (the first holder: handed over at start)
             }
             sb = __shfl_sync(FULL, sb, 0);
             __syncwarp();
@@ -400,7 +402,7 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                 for (uint32_t p = lane; p < n; p += 32) g[p] = buf[z[p]];
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(slotbar + ((tk + (uint32_t)nstage) & 31u));
+            if (lane == 0) mbar_arrive(slotbar + (uint32_t)sb * 32u + ((tk / (uint32_t)nstage + 1u) & 31u));
         } else if (use_tma) {
             if (lane == 0) {
                 fence_proxy_async();
@@ -454,7 +456,11 @@ __global__ void __launch_bounds__(32) shuffle_warp_kernel(T *__restrict__ data, 
 // of one array each, shared by the CTA's warps under a lock) + 16 B of locks + per warp
 // { u16 index array, target ring, equality table, Pred bytes, ChaCha window }.
 constexpr uint32_t idx_warp_fixed(int cm) { return 2 * WRING + WTBL + 32 + 32 + (cm ? 256 * 8 : 0); }
-constexpr uint32_t IDX_CTL_BYTES = 384;  // ticket, 8 load phases, 8 load mbarriers, 32 ticket-slot mbarriers
+// ticket, 8 load phases, 8 load mbarriers, then 32 ticket-slot mbarriers PER BUFFER (8 buffers): a
+// buffer's waiters are consecutive in its own queue, so 32 slots cover any 24 warps.  (One ring of
+// 32 slots over all buffers let ticket t + 32 pass while t still waited once 17 or more warps
+// queued on one buffer: two holders of one buffer.)
+constexpr uint32_t IDX_CTL_BYTES = 128 + 8 * 32 * 8;
 
 
 template <typename T, int CM>
@@ -484,9 +490,10 @@ __global__ void __launch_bounds__(768, 1) shuffle_idx_kernel(T *__restrict__ dat
         locks[8 + threadIdx.x] = 0u;
         mbar_init(reinterpret_cast<uint64_t *>(locks + 16) + threadIdx.x, 1);  // bulk load done
     }
-    if (threadIdx.x < 32) {  // ticket hand-off; the first nstage tickets are handed their buffers now
-        mbar_init(reinterpret_cast<uint64_t *>(locks + 32) + threadIdx.x, 1);
-        if (threadIdx.x < (unsigned)nstage) mbar_arrive(reinterpret_cast<uint64_t *>(locks + 32) + threadIdx.x);
+    for (uint32_t i = threadIdx.x; i < (uint32_t)nstage * 32u; i += blockDim.x) {
+        // ticket hand-off; the first ticket of each buffer is handed its buffer now
+        mbar_init(reinterpret_cast<uint64_t *>(locks + 32) + i, 1);
+        if ((i & 31u) == 0) mbar_arrive(reinterpret_cast<uint64_t *>(locks + 32) + i);
     }
     __syncthreads();
     uint64_t bar = 0;
