@@ -721,7 +721,8 @@ int launch_shuffle(void *data, int64_t num_arrays, uint64_t n, const PlanStore &
                 CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 const int64_t ctas = (num_arrays + nw - 1) / nw;
                 const int grid = (int)std::min<int64_t>(ctas, di.sms);
-                const int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+                int use_tma = (((uintptr_t)data | (n * sizeof(T))) & 15) == 0 ? 1 : 0;
+                if (const char *he = getenv("BR_IDX_HOLD_US")) use_tma |= std::min(1000, std::max(0, atoi(he))) << 8;  // test knob
                 T *dp = (T *)data;
                 DevPlan plan = cp.plan;
                 int ns = nstage;

@@ -232,6 +232,10 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
                                                   int nstage = 0, uint32_t stage_elems = 0) {
     using E = std::conditional_t<IDX, uint16_t, T>;  // element type of the array being permuted
     const int lane = threadIdx.x & 31;
+    // test knob (BR_IDX_HOLD_US, bits 8.. of use_tma): the holder of staging buffer 0 sleeps that
+    // long, which piles the warps up on one buffer's queue (tests/test_gpu.py ticket stress)
+    const int hold_us = use_tma >> 8;
+    use_tma &= 1;
     if (!IDX && use_tma && lane == 0) mbar_init(&bar, 1);
     P[lane] = -1;  // warp_apply_group_exact's invariant
     __syncwarp();
@@ -372,6 +376,8 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
             sb = __shfl_sync(FULL, sb, 0);
             __syncwarp();
             T *buf = stage + (size_t)sb * stage_elems;
+            if (hold_us && sb == 0)
+                for (int h = 0; h < hold_us; ++h) __nanosleep(1000);
             if (use_tma) {  // one bulk copy; the stage's mbarrier phase lives next to its lock
                 uint64_t *sbar = reinterpret_cast<uint64_t *>(locks + 16) + sb;
                 const uint32_t ph = locks[8 + sb];

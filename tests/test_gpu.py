@@ -370,6 +370,25 @@ def test_default_dispatch(B, O, n, eb, na, kernel):
         assert np.array_equal(got[a], ref) and int(u32(w)[a]) == int(rw[0]), (n, eb, a)
 
 
+def test_idx_staging_queue_under_pressure(B, O, monkeypatch):
+    """The index kernel's staging hand-off with its queues saturated: the holder of buffer 0 sleeps
+    (BR_IDX_HOLD_US), so nearly every warp of a CTA ends up waiting on that one buffer.  A single
+    ring of 32 ticket slots over both buffers let a second warp into a held buffer here."""
+    monkeypatch.setenv("BR_SHUFFLE_KERNEL", "idx")
+    monkeypatch.setenv("BR_IDX_HOLD_US", "40")
+    n, na = 2048, 148 * 24 * 5
+    dev = torch.arange(n, dtype=torch.int32, device="cuda").repeat(na)
+    B.shuffle_many(dev, n, 31337, array_index_base=1)
+    torch.cuda.synchronize()
+    assert "shuffle_idx_kernel" in B.last_kernel()
+    got = u32(dev).reshape(na, n)
+    assert np.array_equal(np.sort(got, axis=1), np.tile(np.arange(n, dtype=np.uint32), (na, 1)))
+    for a in list(range(0, na, 997)) + [na - 1]:
+        ref = np.arange(n, dtype=np.uint32)
+        O.shuffle_segmented(ref, n, 31337, array_index_base=1 + a)
+        assert np.array_equal(got[a], ref), a
+
+
 @pytest.mark.parametrize("kernel", ["idx", "warp", "hash", "small", "large"])
 def test_unaligned_payload(B, O, monkeypatch, kernel):
     """Payload starting 4 bytes past a 16-byte boundary: the kernels fall back from bulk (TMA)
