@@ -366,21 +366,22 @@ __device__ __forceinline__ void shuffle_warp_body(T *__restrict__ data, int64_t 
             // waiter sleeps in mbarrier.try_wait instead of polling a lock
             uint64_t *slotbar = reinterpret_cast<uint64_t *>(locks + 32);
             int sb = 0;
-            uint32_t tk = 0;
+            uint32_t tk = 0, ph = 0;
             if (lane == 0) {
                 tk = atomicAdd(&locks[0], 1u);
                 sb = (int)(tk % (uint32_t)nstage);
                 const uint32_t sq = tk / (uint32_t)nstage;  // position in the buffer's own queue
                 mbar_wait(slotbar + (uint32_t)sb * 32u + (sq & 31u), (sq >> 5) & 1u);  // (the first holder: handed over at start)
+                ph = locks[8 + sb];  // the buffer's load phase, read once by the lane that flips it
             }
             sb = __shfl_sync(FULL, sb, 0);
+            ph = __shfl_sync(FULL, ph, 0);
             __syncwarp();
             T *buf = stage + (size_t)sb * stage_elems;
             if (hold_us && sb == 0)
                 for (int h = 0; h < hold_us; ++h) __nanosleep(1000);
             if (use_tma) {  // one bulk copy; the stage's mbarrier phase lives next to its lock
                 uint64_t *sbar = reinterpret_cast<uint64_t *>(locks + 16) + sb;
-                const uint32_t ph = locks[8 + sb];
                 if (lane == 0) {
                     fence_proxy_async();  // the previous holder's generic reads of buf come first
                     mbar_arrive_expect_tx(sbar, bytes);
