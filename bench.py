@@ -405,8 +405,11 @@ def cpu_c2(cores, steps=None, warmup=1, target_s=None):
     wds = np.empty(NB_C2, dtype=np.uint8)
     rolls.fill(0)
     wds.fill(0)  # pages touched before timing
-    for _ in range(warmup):
-        O.roll_batches_mt(src, bounds, 2, nthreads=cores, out=(rolls, wds))
+    t_w = time.perf_counter()
+    w = 0
+    while w < warmup or time.perf_counter() - t_w < 0.5:  # W steps and at least 0.5 s: the host
+        O.roll_batches_mt(src, bounds, 2, nthreads=cores, out=(rolls, wds))  # threads and clocks have ramped
+        w += 1
     reps, t = 0, time.perf_counter()
     while True:
         O.roll_batches_mt(src, bounds, 2, nthreads=cores, out=(rolls, wds))
